@@ -1,0 +1,11 @@
+"""B200-native drop-in for the reference auto-labeler hot path (icelabel.process_tile)."""
+from .types import (CLASS_COLORS, MASK_FIXED, MASK_OTSU, ROSS_SEA_SUMMER, ClassId, ColorRange,
+                    FilterConfig, FilterOutput, LabelMask, SceneRaster, SegmentationScheme, Tile,
+                    TileResult, get_preset)
+from .ops import (apply_filter, autolabel, check_windows, detect_mask, process_tile, process_tiles,
+                  segment, segment_batch)
+
+__all__ = ["CLASS_COLORS", "MASK_FIXED", "MASK_OTSU", "ROSS_SEA_SUMMER", "ClassId", "ColorRange",
+           "FilterConfig", "FilterOutput", "LabelMask", "SceneRaster", "SegmentationScheme", "Tile",
+           "TileResult", "get_preset", "apply_filter", "autolabel", "check_windows", "detect_mask",
+           "process_tile", "process_tiles", "segment", "segment_batch"]

@@ -1,0 +1,147 @@
+"""K1 / K1s on the GPU, bit-exact against the reference (golden digests) and the oracle.
+
+Golden digests were produced by the reference itself (tests/golden/make_golden.py); the
+oracle (oracle/autolabel_ref.c, pinned by tests/test_oracle_golden.py) covers inputs
+beyond the golden set.  Calls go through the C ABI (libicelabel_b200.so).
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import autolabel as orc
+from paper_2403_13135_b200 import icelabel as il
+from paper_2403_13135_b200.icelabel import synth
+from tests.golden.cases import all_cases
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "autolabel_golden.json")))
+CASES = {c["name"]: c for c in all_cases()}
+SAT_ONLY = il.SegmentationScheme("sat-only", (
+    il.ColorRange(il.ClassId.THICK_ICE, (0, 100, 205), (179, 255, 255)),
+    il.ColorRange(il.ClassId.THIN_ICE, (0, 100, 31), (179, 255, 204)),
+    il.ColorRange(il.ClassId.OPEN_WATER, (0, 100, 0), (179, 255, 30))))
+SCHEMES = {"ross-sea-summer": il.ROSS_SEA_SUMMER, "sat-only": SAT_ONLY}
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("rec", GOLDEN["cases"], ids=lambda r: r["name"])
+def test_matches_reference_golden(rec):
+    rgb = CASES[rec["name"]]["make"]()
+    cfg = il.FilterConfig(**rec.get("cfg", {}))
+    scheme = SCHEMES[rec.get("scheme", "ross-sea-summer")]
+    if rec["op"] == "process_tile":
+        res = il.process_tile(il.Tile(il.SceneRaster(rgb, "t"), "t", 0, 0), cfg, scheme)
+        assert res.error == rec["error"]
+        if not rec["error"]:
+            assert sha(res.label) == rec["label_sha"]
+            assert sha(res.filtered) == rec["filtered_sha"]
+            assert res.affected_fraction == rec["affected_fraction"]
+    elif rec["op"] == "apply_filter":
+        try:
+            fo = il.apply_filter(il.SceneRaster(rgb), cfg)
+            err = ""
+        except ValueError as exc:
+            err = f"ValueError: {exc}"
+        assert err == rec["error"]
+        if not err:
+            assert sha(fo.filtered.data) == rec["filtered_sha"]
+            assert sha(fo.cloud_shadow_mask) == rec["mask_sha"]
+            assert fo.affected_fraction == rec["affected_fraction"]
+    else:
+        try:
+            lm = il.segment(il.SceneRaster(rgb), scheme)
+            err = ""
+        except ValueError as exc:
+            err = f"ValueError: {exc}"
+        assert err == rec["error"]
+        if not err:
+            assert sha(lm.data) == rec["label_sha"]
+
+
+def _batch_vs_oracle(tiles, cfg=None):
+    cfg = cfg or il.FilterConfig()
+    dev = torch.from_numpy(np.stack(tiles)).cuda()
+    res = il.autolabel(dev, cfg, want_mask=True)
+    filt = res["filtered"].cpu().numpy()
+    lab = res["label"].cpu().numpy()
+    mask = res["mask"].cpu().numpy()
+    aff = res["affected"].cpu().numpy()
+    cnt = res["counts"].cpu().numpy()
+    un = res["unmatched"].cpu().numpy()
+    ocfg = orc.make_cfg(**{k: getattr(cfg, k) for k in cfg.__dataclass_fields__})
+    for i, t in enumerate(tiles):
+        f, m, a = orc.apply_filter(t, ocfg)
+        lbl, first = orc.segment(f)
+        assert np.array_equal(filt[i], f), i
+        assert np.array_equal(mask[i], m), i
+        assert aff[i] == a, i
+        assert np.array_equal(lab[i], lbl), i
+        assert un[i] == first, i
+        assert cnt[i].tolist() == np.bincount(lbl.ravel(), minlength=256)[:3].tolist(), i
+
+
+def test_batch_tgray_tint_rand_vs_oracle():
+    tiles = [rgb for rgb, _ in synth.corpus(7, 24, 0.5)]
+    tiles += [synth.tint(t, 7, i) for i, t in enumerate(tiles[:8])]
+    tiles += [synth.random_tile(100 + i) for i in range(4)]
+    _batch_vs_oracle(tiles)
+
+
+@pytest.mark.parametrize("size", [21, 37, 64, 129])
+def test_ragged_sizes_vs_oracle(size):
+    rng = np.random.default_rng(size)
+    smooth = np.repeat(np.repeat(rng.integers(0, 256, (size // 8 + 1, size // 8 + 1, 3)), 8, 0), 8, 1)
+    tiles = [rng.integers(0, 256, (size, size, 3), dtype=np.uint8),
+             smooth[:size, :size].astype(np.uint8)]
+    _batch_vs_oracle(tiles)
+
+
+def test_config_variants_vs_oracle():
+    tiles = [rgb for rgb, _ in synth.corpus(11, 4, 1.0, size=96)]
+    tiles.append(synth.random_tile(5, size=96))
+    for cfg in (il.FilterConfig(noise_median_k=5), il.FilterConfig(bg_median_k=9, bg_dilate_k=5),
+                il.FilterConfig(mask_mode="fixed", fixed_t=20), il.FilterConfig(diff_truncate=True)):
+        _batch_vs_oracle(tiles, cfg)
+
+
+def test_hsv_exhaustive_vs_oracle():
+    allrgb = np.arange(1 << 24, dtype=np.uint32)
+    rgb = np.stack([(allrgb >> 16) & 255, (allrgb >> 8) & 255, allrgb & 255], -1).astype(np.uint8)
+    dev = torch.from_numpy(rgb).cuda()
+    out = torch.empty_like(dev)
+    from paper_2403_13135_b200 import _native
+    _native.call("ice_rgb_to_hsv", dev.data_ptr(), 1 << 24, out.data_ptr(), _native.stream_handle())
+    assert np.array_equal(out.cpu().numpy(), orc.rgb_to_hsv(rgb))
+
+
+def test_segment_batch_counts_and_unmatched():
+    rng = np.random.default_rng(3)
+    tiles = rng.integers(0, 256, (8, 33, 47, 3), dtype=np.uint8)
+    res = il.segment_batch(torch.from_numpy(tiles).cuda(), SAT_ONLY)
+    lab = res["label"].cpu().numpy()
+    for i in range(8):
+        want, first = orc.segment(tiles[i], ((0, (0, 100, 205), (179, 255, 255)),
+                                             (1, (0, 100, 31), (179, 255, 204)),
+                                             (2, (0, 100, 0), (179, 255, 30))))
+        assert np.array_equal(lab[i], want)
+        assert int(res["unmatched"][i]) == first
+        assert res["counts"][i].tolist() == np.bincount(want.ravel(), minlength=256)[:3].tolist()
+
+
+def test_empty_batch_and_window_errors():
+    out = il.autolabel(torch.empty((0, 32, 32, 3), dtype=torch.uint8, device="cuda"))
+    assert out["label"].shape == (0, 32, 32)
+    with pytest.raises(ValueError, match=r"window 21 exceeds image extent \(16, 16\)"):
+        il.autolabel(torch.zeros((1, 16, 16, 3), dtype=torch.uint8, device="cuda"))
+    res = il.process_tile(il.Tile(il.SceneRaster(np.zeros((5, 5, 3), np.uint8)), "s", 0, 0),
+                          il.FilterConfig(), il.ROSS_SEA_SUMMER)
+    assert res.error == "ValueError: window 7 exceeds image extent (5, 5)"
