@@ -82,6 +82,35 @@ int ice_rgb_to_hsv(const uint8_t *rgb, int64_t npx, uint8_t *hsv, void *stream);
  * master weights / grads / Adam state fp32.
  * --------------------------------------------------------------------------------- */
 
+/* Implicit-GEMM convolution on tcgen05 (model.py:68-69 Conv2d(k=3, padding=1), and the
+ * 1x1 / im2col-stem case with ksize = 1).  NHWC bf16 activations, KRSC bf16 weights
+ * [cout][ksize][ksize][c1 + c2].  The input is the channel concatenation [x1 | x2]
+ * (model.py:129 torch.cat([skip, x], 1)); x2 may be NULL with c2 = 0.  All channel
+ * counts must be multiples of 64, h and w powers of two.
+ *   y = act(conv(x, w) + bias) * drop_scale[n][cout]; act = ReLU if relu != 0;
+ *   bias, drop_scale may be NULL. */
+int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2,
+                   int32_t n, int32_t h, int32_t w, int32_t ksize, const uint16_t *wgt,
+                   const float *bias, int32_t cout, int32_t relu, const float *drop_scale,
+                   uint16_t *y, void *stream);
+
+/* Data gradient of ice_conv_fprop w.r.t. its input (autograd of model.py:68-69, 129).
+ * dx is written split into dx1 (first c1 channels) and dx2 (last c2; may be NULL), each
+ *   dx_i = (conv_transpose(dy, w)_i + add_i) * drop_scale_i[n][c] * [relu_ref_i > 0]
+ * i.e. the fused backward of "ReLU -> Dropout2d" for the tensor that fed the conv, plus an
+ * optional second gradient contribution (the skip path).  Optional pointers may be NULL. */
+int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32_t h, int32_t w,
+                   int32_t ksize, const uint16_t *wgt, int32_t c1, int32_t c2,
+                   uint16_t *dx1, const uint16_t *relu_ref1, const float *drop_scale1,
+                   const uint16_t *add1, uint16_t *dx2, const uint16_t *relu_ref2,
+                   const float *drop_scale2, const uint16_t *add2, void *stream);
+
+/* Weight gradient: dw[cout][ksize][ksize][c1 + c2] (fp32) += sum over pixels of
+ * dy[p][cout] * x[p + tap][c].  dw must be zeroed by the caller before the first call. */
+int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2,
+                   const uint16_t *dy, int32_t cout, int32_t n, int32_t h, int32_t w,
+                   int32_t ksize, float *dw, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -48,6 +48,9 @@ SIGNATURES = {
                       _V, _V, _V, _V, _V, _V, _V],
     "ice_segment": [_V, _I64, _I32, _I32, ctypes.POINTER(IceScheme), _V, _V, _V, _V],
     "ice_rgb_to_hsv": [_V, _I64, _V, _V],
+    "ice_conv_fprop": [_V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, _V, _I32, _I32, _V, _V, _V],
+    "ice_conv_dgrad": [_V, _I32, _I32, _I32, _I32, _I32, _V, _I32, _I32, _V, _V, _V, _V, _V, _V, _V, _V, _V],
+    "ice_conv_wgrad": [_V, _I32, _V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, _V],
 }
 
 _lib = None

@@ -1,0 +1,544 @@
+// conv_tc.cu -- NHWC bf16 implicit-GEMM convolutions on 5th-gen tensor cores (tcgen05).
+//
+// One warp-specialised kernel template serves fprop, dgrad and wgrad of the U-Net's
+// convolutions (icetrain/model.py:64-88):
+//   warp 0      TMA producer: per K-block, tap-shifted boxes of the NHWC activation
+//               (4-D tensor map (C, W, H, N); out-of-image rows/cols arrive zero-filled,
+//               which IS the conv's zero padding) and the weight slab;
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (128 x BN x 16 per op);
+//   warps 2..5  epilogue: tcgen05.ld of the fp32 accumulator, fused bias / ReLU /
+//               Dropout2d / ReLU-backward / gradient-sum, bf16 NHWC store (or fp32
+//               red.add for weight gradients).
+// The concatenation cat([skip, x], 1) of model.py:129 is never materialised: channel
+// blocks below c1 come from the skip tensor's map, the rest from the other map.
+//
+// GEMM views (m = output row in TMEM lanes, n = TMEM column, k = reduction):
+//   fprop  D[pixel][cout]     = sum_{tap,cin}  X[pixel+tap][cin]  * W[cout][tap][cin]   A,B K-major
+//   dgrad  D[pixel][cin]      = sum_{tap,cout} dY[pixel-tap][cout]* W[cout][tap][cin]   A K-major, B MN-major
+//   wgrad  D[cout][(tap,cin)] = sum_{pixel}    dY[pixel][cout]    * X[pixel+tap][cin]   A,B MN-major
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "icelabel_b200.h"
+#include "tc_common.cuh"
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = one 128-byte swizzle row
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int NTHREADS = 192;
+
+struct PixTile {  // a box of Wt x Ht x Nt pixels, and how many boxes tile (W, H, N)
+    int Wt, Ht, Nt, tw, th, tn;
+    __device__ __forceinline__ void origin(int t, int &n0, int &h0, int &w0) const {
+        int wi = t % tw;
+        t /= tw;
+        int hi = t % th;
+        int ni = t / th;
+        w0 = wi * Wt;
+        h0 = hi * Ht;
+        n0 = ni * Nt;
+    }
+    __device__ __forceinline__ void pixel(int row, int n0, int h0, int w0, int &n, int &h, int &w) const {
+        w = w0 + row % Wt;
+        int r = row / Wt;
+        h = h0 + r % Ht;
+        n = n0 + r / Ht;
+    }
+};
+
+struct Taps {
+    int n;
+    int8_t dy[9], dx[9];
+};
+
+// ------------------------------------------------------------------------------------
+struct FpropProb {
+    static constexpr bool A_MN = false, B_MN = false;
+    CUtensorMap xa, xb, wm;
+    PixTile pt;
+    Taps taps;
+    int N, H, W, c1, c2, cout;
+    const float *bias;
+    const float *drop;  // [N][cout] or null
+    int relu;
+    bf16 *y;
+
+    __device__ void kb_range(int, int &kb0, int &nkb) const {
+        kb0 = 0;
+        nkb = taps.n * ((c1 + c2) / BK);
+    }
+    __device__ void prefetch() const {
+        tc::tma_prefetch_desc(&xa);
+        if (c2) tc::tma_prefetch_desc(&xb);
+        tc::tma_prefetch_desc(&wm);
+    }
+    template <int BN>
+    __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt) const {
+        const int cch = (c1 + c2) / BK;
+        const int t = kb / cch, c = (kb % cch) * BK;
+        int n0, h0, w0;
+        pt.origin(mt, n0, h0, w0);
+        if (c < c1) tc::tma_load_4d(sa, &xa, bar, c, w0 + taps.dx[t], h0 + taps.dy[t], n0);
+        else tc::tma_load_4d(sa, &xb, bar, c - c1, w0 + taps.dx[t], h0 + taps.dy[t], n0);
+        tc::tma_load_3d(sb, &wm, bar, c, t, nt * BN);
+    }
+    template <int BN>
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt) const {
+        int n0, h0, w0, n, h, w;
+        pt.origin(mt, n0, h0, w0);
+        pt.pixel(row, n0, h0, w0, n, h, w);
+        const bool valid = n < N;
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 32; ++cc) {
+            float v[32];
+            tc::tmem_ld32(tmem + cc * 32, v);
+            if (!valid) continue;
+            const int col0 = nt * BN + cc * 32;
+            uint4 *dst = reinterpret_cast<uint4 *>(y + ((size_t)((size_t)n * H + h) * W + w) * cout + col0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t pk[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    int j = q * 8 + e * 2;
+                    float a = v[j] + (bias ? __ldg(bias + col0 + j) : 0.f);
+                    float b = v[j + 1] + (bias ? __ldg(bias + col0 + j + 1) : 0.f);
+                    if (relu) {
+                        a = fmaxf(a, 0.f);
+                        b = fmaxf(b, 0.f);
+                    }
+                    if (drop) {
+                        a *= __ldg(drop + (size_t)n * cout + col0 + j);
+                        b *= __ldg(drop + (size_t)n * cout + col0 + j + 1);
+                    }
+                    pk[e] = tc::pack_bf16(a, b);
+                }
+                dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+        }
+    }
+};
+
+// ------------------------------------------------------------------------------------
+struct DgradProb {
+    static constexpr bool A_MN = false, B_MN = true;
+    CUtensorMap dym, wm;  // dY (box 64 x pixel tile), weights (box 64 cin x 1 x 64 cout)
+    PixTile pt;
+    Taps taps;
+    int N, H, W, c1, c2, cout;
+    bf16 *out1, *out2;
+    const bf16 *ref1, *ref2, *add1, *add2;
+    const float *drop1, *drop2;
+
+    __device__ void kb_range(int, int &kb0, int &nkb) const {
+        kb0 = 0;
+        nkb = taps.n * (cout / BK);
+    }
+    __device__ void prefetch() const {
+        tc::tma_prefetch_desc(&dym);
+        tc::tma_prefetch_desc(&wm);
+    }
+    template <int BN>
+    __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt) const {
+        const int cch = cout / BK;
+        const int t = kb / cch, c = (kb % cch) * BK;
+        int n0, h0, w0;
+        pt.origin(mt, n0, h0, w0);
+        tc::tma_load_4d(sa, &dym, bar, c, w0 - taps.dx[t], h0 - taps.dy[t], n0);
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j) tc::tma_load_3d(sb + j * 8192, &wm, bar, nt * BN + j * 64, t, c);
+    }
+    template <int BN>
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt) const {
+        int n0, h0, w0, n, h, w;
+        pt.origin(mt, n0, h0, w0);
+        pt.pixel(row, n0, h0, w0, n, h, w);
+        const bool valid = n < N;
+        const size_t pix = ((size_t)n * H + h) * W + w;
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 32; ++cc) {
+            float v[32];
+            tc::tmem_ld32(tmem + cc * 32, v);
+            if (!valid) continue;
+            int col = nt * BN + cc * 32;
+            bf16 *out;
+            const bf16 *ref, *add;
+            const float *drop;
+            int cs;
+            if (col < c1) {
+                out = out1; ref = ref1; add = add1; drop = drop1; cs = c1;
+            } else {
+                col -= c1;
+                out = out2; ref = ref2; add = add2; drop = drop2; cs = c2;
+            }
+            if (!out) continue;
+            const size_t off = pix * cs + col;
+            float extra[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) extra[j] = 0.f;
+            if (add) {
+                const uint4 *ap = reinterpret_cast<const uint4 *>(add + off);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 u = ap[q];
+                    const bf16 *b = reinterpret_cast<const bf16 *>(&u);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) extra[q * 8 + e] = __bfloat162float(b[e]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += extra[j];
+            if (ref) {
+                const uint4 *rp = reinterpret_cast<const uint4 *>(ref + off);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 u = rp[q];
+                    const bf16 *b = reinterpret_cast<const bf16 *>(&u);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (!(__bfloat162float(b[e]) > 0.f)) v[q * 8 + e] = 0.f;
+                }
+            }
+            if (drop) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] *= __ldg(drop + (size_t)n * cs + col + j);
+            }
+            uint4 *dst = reinterpret_cast<uint4 *>(out + off);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                dst[q] = make_uint4(tc::pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), tc::pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
+                                    tc::pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), tc::pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+            }
+        }
+    }
+};
+
+// ------------------------------------------------------------------------------------
+struct WgradProb {
+    static constexpr bool A_MN = true, B_MN = true;
+    CUtensorMap dym, xa, xb;  // boxes of 64 channels x 64 pixels
+    PixTile pk;               // the 64-pixel K-block geometry
+    Taps taps;
+    int N, H, W, c1, c2, cout;
+    int total_kb, kb_per_split;
+    float *dw;  // [cout][taps][c1+c2]
+
+    __device__ void kb_range(int z, int &kb0, int &nkb) const {
+        kb0 = z * kb_per_split;
+        nkb = min(total_kb - kb0, kb_per_split);
+    }
+    __device__ void prefetch() const {
+        tc::tma_prefetch_desc(&dym);
+        tc::tma_prefetch_desc(&xa);
+        if (c2) tc::tma_prefetch_desc(&xb);
+    }
+    template <int BN>
+    __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt) const {
+        int n0, h0, w0;
+        pk.origin(kb, n0, h0, w0);
+        tc::tma_load_4d(sa, &dym, bar, mt * BM, w0, h0, n0);
+        tc::tma_load_4d(sa + 8192, &dym, bar, mt * BM + 64, w0, h0, n0);
+        const int ct = c1 + c2;
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j) {
+            const int col = nt * BN + j * 64;
+            const int t = col / ct, c = col - t * ct;
+            if (c < c1) tc::tma_load_4d(sb + j * 8192, &xa, bar, c, w0 + taps.dx[t], h0 + taps.dy[t], n0);
+            else tc::tma_load_4d(sb + j * 8192, &xb, bar, c - c1, w0 + taps.dx[t], h0 + taps.dy[t], n0);
+        }
+    }
+    template <int BN>
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt) const {
+        const int m = mt * BM + row;
+        const int ld = taps.n * (c1 + c2);
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 32; ++cc) {
+            float v[32];
+            tc::tmem_ld32(tmem + cc * 32, v);
+            if (m >= cout) continue;
+            float *dst = dw + (size_t)m * ld + nt * BN + cc * 32;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) tc::red_add_v4(dst + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+    }
+};
+
+// ------------------------------------------------------------------------------------
+template <int BN, int STAGES>
+constexpr int smem_bytes() {
+    return 1024 + STAGES * (A_BYTES + BN * BK * 2) + (2 * STAGES + 1) * 8 + 16;
+}
+
+template <int BN, int STAGES, class P>
+__global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__ P p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int B_BYTES = BN * BK * 2;
+    uint8_t *sa = base;
+    uint8_t *sb = base + STAGES * A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sb + STAGES * B_BYTES);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(tfull + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mt = blockIdx.x, nt = blockIdx.y;
+    int kb0, nkb;
+    p.kb_range(blockIdx.z, kb0, nkb);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(tfull, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) p.prefetch();
+    if (warp == 1) tc::tmem_alloc<BN>(tslot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (nkb > 0) {
+        if (warp == 0) {
+            if (lane == 0) {
+                for (int i = 0; i < nkb; ++i) {
+                    const int s = i % STAGES;
+                    const uint32_t ph = (i / STAGES) & 1;
+                    tc::mbar_wait(&empty[s], ph ^ 1);
+                    tc::mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+                    p.template load<BN>(kb0 + i, sa + s * A_BYTES, sb + s * B_BYTES, &full[s], mt, nt);
+                }
+            }
+        } else if (warp == 1) {
+            if (lane == 0) {
+                constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, P::A_MN, P::B_MN);
+                for (int i = 0; i < nkb; ++i) {
+                    const int s = i % STAGES;
+                    const uint32_t ph = (i / STAGES) & 1;
+                    tc::mbar_wait(&full[s], ph);
+                    tc::tc_fence_after();
+                    const uint32_t a0 = tc::smem_u32(sa + s * A_BYTES);
+                    const uint32_t b0 = tc::smem_u32(sb + s * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = P::A_MN ? tc::sw128_desc(a0 + k * 2048, 8192, 1024)
+                                                    : tc::sw128_desc(a0 + k * 32, 16, 1024);
+                        const uint64_t bd = P::B_MN ? tc::sw128_desc(b0 + k * 2048, 8192, 1024)
+                                                    : tc::sw128_desc(b0 + k * 32, 16, 1024);
+                        tc::umma_f16(tmem, ad, bd, idesc, (i | k) != 0 ? 1u : 0u);
+                    }
+                    tc::umma_commit(&empty[s]);
+                }
+                tc::umma_commit(tfull);
+            }
+            __syncwarp();
+        } else {
+            tc::mbar_wait(tfull, 0);
+            tc::tc_fence_after();
+            const int sub = warp & 3;
+            p.template epilogue<BN>(tmem + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc<BN>(tmem);
+}
+
+// ------------------------------------------------------------------------------------
+// host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// NHWC activation viewed as 4-D (C, W, H, N); box = 64 channels x a pixel box
+bool map_act(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, const PixTile &pt) {
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)pt.Wt, (cuuint32_t)pt.Ht, (cuuint32_t)pt.Nt};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(ptr), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// KRSC weights viewed as 3-D (Cin, taps, Cout); box = 64 cin x 1 tap x rows
+bool map_wgt(CUtensorMap *m, const void *ptr, int cout, int taps, int cin, int rows) {
+    cuuint64_t dims[3] = {(cuuint64_t)cin, (cuuint64_t)taps, (cuuint64_t)cout};
+    cuuint64_t strides[2] = {(cuuint64_t)cin * 2, (cuuint64_t)taps * cin * 2};
+    cuuint32_t box[3] = {64, 1, (cuuint32_t)rows};
+    cuuint32_t es[3] = {1, 1, 1};
+    return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(ptr), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+PixTile pix_tile(int N, int H, int W, int npx) {
+    PixTile t;
+    t.Wt = W < npx ? W : npx;
+    int rest = npx / t.Wt;
+    t.Ht = H < rest ? H : rest;
+    t.Nt = rest / t.Ht;
+    t.tw = W / t.Wt;
+    t.th = H / t.Ht;
+    t.tn = (N + t.Nt - 1) / t.Nt;
+    return t;
+}
+
+bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+Taps make_taps(int ksize) {
+    Taps t;
+    memset(&t, 0, sizeof t);
+    if (ksize == 1) {
+        t.n = 1;
+    } else {
+        t.n = 9;
+        for (int i = 0; i < 9; ++i) {
+            t.dy[i] = (int8_t)(i / 3 - 1);
+            t.dx[i] = (int8_t)(i % 3 - 1);
+        }
+    }
+    return t;
+}
+
+template <int BN, int STAGES, class P>
+int launch(const P &p, dim3 grid, cudaStream_t st) {
+    constexpr int smem = smem_bytes<BN, STAGES>();
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(conv_gemm<BN, STAGES, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return (int)e;
+        attr = true;
+    }
+    conv_gemm<BN, STAGES, P><<<grid, NTHREADS, smem, st>>>(p);
+    return (int)cudaGetLastError();
+}
+
+int pick_bn(int ntot, long long m_tiles) {
+    // largest tile that still gives >= one wave of CTAs; 64 as the floor
+    const int cands[3] = {256, 128, 64};
+    for (int i = 0; i < 3; ++i) {
+        int bn = cands[i];
+        if (ntot % bn) continue;
+        if (m_tiles * (ntot / bn) >= 148 || bn == 64) return bn;
+    }
+    return 64;
+}
+
+bool shape_ok(int N, int H, int W) { return N > 0 && pow2(H) && pow2(W); }
+
+}  // namespace
+
+extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2, int32_t n, int32_t h,
+                              int32_t w, int32_t ksize, const uint16_t *wgt, const float *bias, int32_t cout,
+                              int32_t relu, const float *drop_scale, uint16_t *y, void *stream) {
+    if (!encode_fn()) return ICE_ENODRIVER;
+    if (!x1 || !wgt || !y || c1 <= 0 || c1 % 64 || c2 < 0 || c2 % 64 || (c2 && !x2) || cout <= 0 || cout % 64 ||
+        (ksize != 1 && ksize != 3) || !shape_ok(n, h, w))
+        return ICE_EINVAL;
+    FpropProb p;
+    memset(&p, 0, sizeof p);
+    p.pt = pix_tile(n, h, w, BM);
+    p.taps = make_taps(ksize);
+    p.N = n; p.H = h; p.W = w; p.c1 = c1; p.c2 = c2; p.cout = cout;
+    p.bias = bias; p.drop = drop_scale; p.relu = relu; p.y = reinterpret_cast<bf16 *>(y);
+    const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
+    const int bn = pick_bn(cout, mtiles);
+    if (!map_act(&p.xa, x1, n, h, w, c1, p.pt)) return ICE_EINVAL;
+    if (c2 && !map_act(&p.xb, x2, n, h, w, c2, p.pt)) return ICE_EINVAL;
+    if (!map_wgt(&p.wm, wgt, cout, p.taps.n, c1 + c2, bn)) return ICE_EINVAL;
+    dim3 grid((unsigned)mtiles, cout / bn, 1);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (bn == 256) return launch<256, 4>(p, grid, st);
+    if (bn == 128) return launch<128, 6>(p, grid, st);
+    return launch<64, 8>(p, grid, st);
+}
+
+extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32_t h, int32_t w, int32_t ksize,
+                              const uint16_t *wgt, int32_t c1, int32_t c2, uint16_t *dx1, const uint16_t *relu_ref1,
+                              const float *drop_scale1, const uint16_t *add1, uint16_t *dx2,
+                              const uint16_t *relu_ref2, const float *drop_scale2, const uint16_t *add2,
+                              void *stream) {
+    if (!encode_fn()) return ICE_ENODRIVER;
+    if (!dy || !wgt || c1 <= 0 || c1 % 64 || c2 < 0 || c2 % 64 || cout <= 0 || cout % 64 ||
+        (ksize != 1 && ksize != 3) || !shape_ok(n, h, w))
+        return ICE_EINVAL;
+    DgradProb p;
+    memset(&p, 0, sizeof p);
+    p.pt = pix_tile(n, h, w, BM);
+    p.taps = make_taps(ksize);
+    p.N = n; p.H = h; p.W = w; p.c1 = c1; p.c2 = c2; p.cout = cout;
+    p.out1 = reinterpret_cast<bf16 *>(dx1); p.out2 = reinterpret_cast<bf16 *>(dx2);
+    p.ref1 = reinterpret_cast<const bf16 *>(relu_ref1); p.ref2 = reinterpret_cast<const bf16 *>(relu_ref2);
+    p.add1 = reinterpret_cast<const bf16 *>(add1); p.add2 = reinterpret_cast<const bf16 *>(add2);
+    p.drop1 = drop_scale1; p.drop2 = drop_scale2;
+    const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
+    const int ct = c1 + c2;
+    int bn = pick_bn(ct, mtiles);
+    // a column tile must not straddle the dx1 / dx2 split
+    while (bn > 64 && (c1 % bn)) bn >>= 1;
+    if (!map_act(&p.dym, dy, n, h, w, cout, p.pt)) return ICE_EINVAL;
+    if (!map_wgt(&p.wm, wgt, cout, p.taps.n, ct, 64)) return ICE_EINVAL;
+    dim3 grid((unsigned)mtiles, ct / bn, 1);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (bn == 256) return launch<256, 4>(p, grid, st);
+    if (bn == 128) return launch<128, 6>(p, grid, st);
+    return launch<64, 8>(p, grid, st);
+}
+
+extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2, const uint16_t *dy,
+                              int32_t cout, int32_t n, int32_t h, int32_t w, int32_t ksize, float *dw,
+                              void *stream) {
+    if (!encode_fn()) return ICE_ENODRIVER;
+    if (!x1 || !dy || !dw || c1 <= 0 || c1 % 64 || c2 < 0 || c2 % 64 || (c2 && !x2) || cout <= 0 || cout % 64 ||
+        (ksize != 1 && ksize != 3) || !shape_ok(n, h, w))
+        return ICE_EINVAL;
+    WgradProb p;
+    memset(&p, 0, sizeof p);
+    p.pk = pix_tile(n, h, w, BK);
+    p.taps = make_taps(ksize);
+    p.N = n; p.H = h; p.W = w; p.c1 = c1; p.c2 = c2; p.cout = cout;
+    p.dw = dw;
+    const int ncols = p.taps.n * (c1 + c2);
+    const int mtiles = (cout + BM - 1) / BM;
+    int bn = 64;
+    if (ncols % 256 == 0) bn = 256;
+    else if (ncols % 128 == 0) bn = 128;
+    const int ntiles = ncols / bn;
+    p.total_kb = p.pk.tw * p.pk.th * p.pk.tn;
+    const long long tiles = (long long)mtiles * ntiles;
+    int splits = (int)((2 * 148 + tiles - 1) / tiles);
+    if (splits > p.total_kb) splits = p.total_kb;
+    if (splits < 1) splits = 1;
+    p.kb_per_split = (p.total_kb + splits - 1) / splits;
+    splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
+    if (!map_act(&p.dym, dy, n, h, w, cout, p.pk)) return ICE_EINVAL;
+    if (!map_act(&p.xa, x1, n, h, w, c1, p.pk)) return ICE_EINVAL;
+    if (c2 && !map_act(&p.xb, x2, n, h, w, c2, p.pk)) return ICE_EINVAL;
+    dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (bn == 256) return launch<256, 4>(p, grid, st);
+    if (bn == 128) return launch<128, 6>(p, grid, st);
+    return launch<64, 8>(p, grid, st);
+}
