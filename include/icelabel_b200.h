@@ -98,18 +98,96 @@ int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c
  * dx is written split into dx1 (first c1 channels) and dx2 (last c2; may be NULL), each
  *   dx_i = (conv_transpose(dy, w)_i + add_i) * drop_scale_i[n][c] * [relu_ref_i > 0]
  * i.e. the fused backward of "ReLU -> Dropout2d" for the tensor that fed the conv, plus an
- * optional second gradient contribution (the skip path).  Optional pointers may be NULL. */
+ * optional second gradient contribution (the skip path).  Optional pointers may be NULL.
+ * dx2_planes != 0 writes dx2 as four sub-pixel planes [4][n][h/2][w/2][c2] (plane
+ * 2*(y&1)+(x&1)), the layout ice_halve_dgrad / ice_halve_wgrad consume. */
 int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32_t h, int32_t w,
                    int32_t ksize, const uint16_t *wgt, int32_t c1, int32_t c2,
                    uint16_t *dx1, const uint16_t *relu_ref1, const float *drop_scale1,
                    const uint16_t *add1, uint16_t *dx2, const uint16_t *relu_ref2,
-                   const float *drop_scale2, const uint16_t *add2, void *stream);
+                   const float *drop_scale2, const uint16_t *add2, int32_t dx2_planes,
+                   void *stream);
 
 /* Weight gradient: dw[cout][ksize][ksize][c1 + c2] (fp32) += sum over pixels of
  * dy[p][cout] * x[p + tap][c].  dw must be zeroed by the caller before the first call. */
 int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2,
                    const uint16_t *dy, int32_t cout, int32_t n, int32_t h, int32_t w,
                    int32_t ksize, float *dw, void *stream);
+
+/* Halving conv forward (model.py:79-88,105,128): y[n][2h][2w][cout] =
+ * conv2x2(pad(upsample_nearest_2x(x), (0,1,0,1))) + bias, as four sub-pixel GEMMs over
+ * the low-res x[n][h][w][c] with the 9 combined weight slabs wc[cout][9][c] (bf16) that
+ * ice_halve_prep builds from the 2x2 weights. */
+int ice_halve_fprop(const uint16_t *x, int32_t c, int32_t n, int32_t h, int32_t w,
+                    const uint16_t *wc, const float *bias, int32_t cout, uint16_t *y,
+                    void *stream);
+
+/* Halving conv data gradient: dx[n][h][w][c] = (sum over sub-pixel classes and taps of
+ * dy_planes[cls][n][h - dy][w - dx][cout] * wc^T) * drop_scale[n][c] * [relu_ref > 0]. */
+int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t n, int32_t h, int32_t w,
+                    const uint16_t *wc, int32_t c, uint16_t *dx, const uint16_t *relu_ref,
+                    const float *drop_scale, void *stream);
+
+/* Halving conv weight gradient: dw[cout][2][2][c] (fp32, caller-zeroed) +=
+ * sum over classes/pixels of dy_planes[cls][p] (x) x[p + ((cy + a) / 2, (cx + b) / 2)]. */
+int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_planes, int32_t cout,
+                    int32_t n, int32_t h, int32_t w, float *dw, void *stream);
+
+/* ---- bandwidth-bound U-Net kernels (unet_ops.cu) ---------------------------------- */
+
+/* Input stem: train.py:63 (u8 NHWC / 255) fused with the im2col of the first 3x3 conv
+ * (model.py:68, Cin = 3): out[p][(r*3+s)*3+c] = img[p+(r-1,s-1)][c] / 255, zero outside
+ * and in columns 27..63.  img u8 [n][h][w][3], out bf16 [n][h][w][64]. */
+int ice_stem_im2col(const uint8_t *img, int32_t n, int32_t h, int32_t w, uint16_t *out,
+                    void *stream);
+
+/* Same stem from an fp32 NHWC image already in [0, 1] (UNet.forward on float input). */
+int ice_stem_im2col_f32(const float *img, int32_t n, int32_t h, int32_t w, uint16_t *out,
+                        void *stream);
+
+/* fp32 [rows][k] -> bf16 [rows][kp] zero-padded (stem weights 64 x 27 -> 64 x 64). */
+int ice_pad_weights(const float *src, int32_t rows, int32_t k, uint16_t *dst, int32_t kp,
+                    void *stream);
+
+/* 2x2 halving-conv weights fp32 [cout][2][2][c] -> 9 combined bf16 slabs [cout][9][c]. */
+int ice_halve_prep(const float *w, int32_t cout, int32_t c, uint16_t *wc, void *stream);
+
+/* nn.MaxPool2d(2) forward (model.py:102,125), NHWC bf16, c % 8 == 0. */
+int ice_maxpool_fwd(const uint16_t *x, int32_t n, int32_t h, int32_t w, int32_t c,
+                    uint16_t *y, void *stream);
+
+/* Fused backward of ReLU -> Dropout2d -> {skip, MaxPool2d} for a down block output x:
+ * dz = (add + maxpool_backward(dpool)) * drop[n][c] * [x > 0]; add/drop may be NULL.
+ * Ties route to the first maximum in window order, like torch's CPU max_pool2d. */
+int ice_maxpool_bwd(const uint16_t *x, const uint16_t *dpool, const uint16_t *add,
+                    const float *drop, int32_t n, int32_t h, int32_t w, int32_t c,
+                    uint16_t *dz, void *stream);
+
+/* Head (model.py:109,130 out = Conv2d(64, 3, 1)) + nn.CrossEntropyLoss (train.py:89,96).
+ * h bf16 [npx][64] (hw pixels per image), labels u8 [npx], w_out fp32 [3][64], b_out [3].
+ * Accumulates stats[0] += sum of per-pixel losses, stats[1] += argmax hits (if stats).
+ * Training (dw, db non-NULL): dlogits = (softmax - onehot) * grad_scale; dw += dlogits^T h,
+ * db += sum dlogits, and dz (if non-NULL) = (dlogits W) * drop[n][c] * [h > 0].
+ * logits (optional) fp32 [npx][3]. */
+int ice_head_ce(const uint16_t *h, int64_t npx, int32_t hw, const uint8_t *labels,
+                const float *w_out, const float *b_out, const float *drop, float grad_scale,
+                uint16_t *dz, float *dw, float *db, float *stats, float *logits, void *stream);
+
+/* Bias gradient: db[c] += sum_rows dz[row][c] (dz bf16 [rows][c], c % 8 == 0, c <= 2048). */
+int ice_bias_grad(const uint16_t *dz, int64_t rows, int32_t c, float *db, void *stream);
+
+/* Dropout2d multipliers (model.py:74-75): out[i] = (u_i >= p) / (1 - p), u from a
+ * counter-based hash of (seed, i). */
+int ice_dropout_scale(int32_t count, float p, uint64_t seed, float *out, void *stream);
+
+/* torch.optim.Adam step (defaults of train.py:149: no weight decay, no amsgrad) over flat
+ * fp32 buffers, fused with the bf16 working-copy write and zeroing of g. */
+int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64_t step, float lr,
+             float beta1, float beta2, float eps, uint16_t *out_bf16, void *stream);
+
+/* fp32 -> bf16 cast; fill. */
+int ice_cast_bf16(const float *src, int64_t n, uint16_t *dst, void *stream);
+int ice_fill_f32(float *dst, int64_t n, float value, void *stream);
 
 #ifdef __cplusplus
 }

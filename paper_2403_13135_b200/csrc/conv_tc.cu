@@ -54,7 +54,7 @@ struct PixTile {  // a box of Wt x Ht x Nt pixels, and how many boxes tile (W, H
 
 struct Taps {
     int n;
-    int8_t dy[9], dx[9];
+    int8_t dy[9], dx[9], plane[9], wt[9];  // pixel shift, source plane (5-D maps), weight tap
 };
 
 // ------------------------------------------------------------------------------------
@@ -62,16 +62,17 @@ struct FpropProb {
     static constexpr bool A_MN = false, B_MN = false;
     CUtensorMap xa, xb, wm;
     PixTile pt;
-    Taps taps;
+    Taps taps[4];  // per blockIdx.z (the 4 sub-pixel classes of the halving conv; else 1)
     int N, H, W, c1, c2, cout;
+    int omul;      // 1: output pixel = input pixel; 2: output (2h + cy, 2w + cx), z = 2 cy + cx
     const float *bias;
     const float *drop;  // [N][cout] or null
     int relu;
     bf16 *y;
 
-    __device__ void kb_range(int, int &kb0, int &nkb) const {
+    __device__ void kb_range(int z, int &kb0, int &nkb) const {
         kb0 = 0;
-        nkb = taps.n * ((c1 + c2) / BK);
+        nkb = taps[z].n * ((c1 + c2) / BK);
     }
     __device__ void prefetch() const {
         tc::tma_prefetch_desc(&xa);
@@ -79,28 +80,34 @@ struct FpropProb {
         tc::tma_prefetch_desc(&wm);
     }
     template <int BN>
-    __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt) const {
+    __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int z) const {
+        const Taps &tp = taps[z];
         const int cch = (c1 + c2) / BK;
         const int t = kb / cch, c = (kb % cch) * BK;
         int n0, h0, w0;
         pt.origin(mt, n0, h0, w0);
-        if (c < c1) tc::tma_load_4d(sa, &xa, bar, c, w0 + taps.dx[t], h0 + taps.dy[t], n0);
-        else tc::tma_load_4d(sa, &xb, bar, c - c1, w0 + taps.dx[t], h0 + taps.dy[t], n0);
-        tc::tma_load_3d(sb, &wm, bar, c, t, nt * BN);
+        if (c < c1) tc::tma_load_4d(sa, &xa, bar, c, w0 + tp.dx[t], h0 + tp.dy[t], n0);
+        else tc::tma_load_4d(sa, &xb, bar, c - c1, w0 + tp.dx[t], h0 + tp.dy[t], n0);
+        tc::tma_load_3d(sb, &wm, bar, c, tp.wt[t], nt * BN);
     }
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt) const {
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z) const {
         int n0, h0, w0, n, h, w;
         pt.origin(mt, n0, h0, w0);
         pt.pixel(row, n0, h0, w0, n, h, w);
         const bool valid = n < N;
+        const int OH = H * omul, OW = W * omul;
+        if (omul == 2) {
+            h = 2 * h + (z >> 1);
+            w = 2 * w + (z & 1);
+        }
 #pragma unroll 1
         for (int cc = 0; cc < BN / 32; ++cc) {
             float v[32];
             tc::tmem_ld32(tmem + cc * 32, v);
             if (!valid) continue;
             const int col0 = nt * BN + cc * 32;
-            uint4 *dst = reinterpret_cast<uint4 *>(y + ((size_t)((size_t)n * H + h) * W + w) * cout + col0);
+            uint4 *dst = reinterpret_cast<uint4 *>(y + ((size_t)((size_t)n * OH + h) * OW + w) * cout + col0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 uint32_t pk[4];
@@ -132,6 +139,8 @@ struct DgradProb {
     PixTile pt;
     Taps taps;
     int N, H, W, c1, c2, cout;
+    int planes_in;    // dY given as 4 sub-pixel planes [4][N][H][W][cout] (5-D map, plane per tap)
+    int planes_out2;  // dx2 written as sub-pixel planes [4][N][H/2][W/2][c2]
     bf16 *out1, *out2;
     const bf16 *ref1, *ref2, *add1, *add2;
     const float *drop1, *drop2;
@@ -145,22 +154,25 @@ struct DgradProb {
         tc::tma_prefetch_desc(&wm);
     }
     template <int BN>
-    __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt) const {
+    __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
         const int cch = cout / BK;
         const int t = kb / cch, c = (kb % cch) * BK;
         int n0, h0, w0;
         pt.origin(mt, n0, h0, w0);
-        tc::tma_load_4d(sa, &dym, bar, c, w0 - taps.dx[t], h0 - taps.dy[t], n0);
+        if (planes_in) tc::tma_load_5d(sa, &dym, bar, c, w0 - taps.dx[t], h0 - taps.dy[t], n0, taps.plane[t]);
+        else tc::tma_load_4d(sa, &dym, bar, c, w0 - taps.dx[t], h0 - taps.dy[t], n0);
 #pragma unroll
-        for (int j = 0; j < BN / 64; ++j) tc::tma_load_3d(sb + j * 8192, &wm, bar, nt * BN + j * 64, t, c);
+        for (int j = 0; j < BN / 64; ++j) tc::tma_load_3d(sb + j * 8192, &wm, bar, nt * BN + j * 64, taps.wt[t], c);
     }
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt) const {
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int) const {
         int n0, h0, w0, n, h, w;
         pt.origin(mt, n0, h0, w0);
         pt.pixel(row, n0, h0, w0, n, h, w);
         const bool valid = n < N;
         const size_t pix = ((size_t)n * H + h) * W + w;
+        const size_t pix_planes =
+            ((((size_t)((h & 1) * 2 + (w & 1)) * N + n) * (H >> 1) + (h >> 1)) * (W >> 1)) + (w >> 1);
 #pragma unroll 1
         for (int cc = 0; cc < BN / 32; ++cc) {
             float v[32];
@@ -178,7 +190,7 @@ struct DgradProb {
                 out = out2; ref = ref2; add = add2; drop = drop2; cs = c2;
             }
             if (!out) continue;
-            const size_t off = pix * cs + col;
+            const size_t off = ((out == out2 && planes_out2) ? pix_planes : pix) * cs + col;
             float extra[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) extra[j] = 0.f;
@@ -227,6 +239,7 @@ struct WgradProb {
     Taps taps;
     int N, H, W, c1, c2, cout;
     int total_kb, kb_per_split;
+    int halve;  // 2x2 halving conv: dY = 4 sub-pixel planes (5-D map), K runs over (class, pixel block)
     float *dw;  // [cout][taps][c1+c2]
 
     __device__ void kb_range(int z, int &kb0, int &nkb) const {
@@ -239,22 +252,37 @@ struct WgradProb {
         if (c2) tc::tma_prefetch_desc(&xb);
     }
     template <int BN>
-    __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt) const {
-        int n0, h0, w0;
+    __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
+        int n0, h0, w0, cls = 0;
+        if (halve) {
+            const int nblk = pk.tw * pk.th * pk.tn;
+            cls = kb / nblk;
+            kb -= cls * nblk;
+        }
         pk.origin(kb, n0, h0, w0);
-        tc::tma_load_4d(sa, &dym, bar, mt * BM, w0, h0, n0);
-        tc::tma_load_4d(sa + 8192, &dym, bar, mt * BM + 64, w0, h0, n0);
+        if (halve) {
+            tc::tma_load_5d(sa, &dym, bar, mt * BM, w0, h0, n0, cls);
+            tc::tma_load_5d(sa + 8192, &dym, bar, mt * BM + 64, w0, h0, n0, cls);
+        } else {
+            tc::tma_load_4d(sa, &dym, bar, mt * BM, w0, h0, n0);
+            tc::tma_load_4d(sa + 8192, &dym, bar, mt * BM + 64, w0, h0, n0);
+        }
         const int ct = c1 + c2;
 #pragma unroll
         for (int j = 0; j < BN / 64; ++j) {
             const int col = nt * BN + j * 64;
             const int t = col / ct, c = col - t * ct;
-            if (c < c1) tc::tma_load_4d(sb + j * 8192, &xa, bar, c, w0 + taps.dx[t], h0 + taps.dy[t], n0);
-            else tc::tma_load_4d(sb + j * 8192, &xb, bar, c - c1, w0 + taps.dx[t], h0 + taps.dy[t], n0);
+            int sy = taps.dy[t], sx = taps.dx[t];
+            if (halve) {  // output (2p + cy, 2q + cx) reads up[2p + cy + a][2q + cx + b] = x[p + (cy + a) / 2][...]
+                sy = ((cls >> 1) + (t >> 1)) >> 1;
+                sx = ((cls & 1) + (t & 1)) >> 1;
+            }
+            if (c < c1) tc::tma_load_4d(sb + j * 8192, &xa, bar, c, w0 + sx, h0 + sy, n0);
+            else tc::tma_load_4d(sb + j * 8192, &xb, bar, c - c1, w0 + sx, h0 + sy, n0);
         }
     }
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt) const {
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int) const {
         const int m = mt * BM + row;
         const int ld = taps.n * (c1 + c2);
 #pragma unroll 1
@@ -315,7 +343,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
                     const uint32_t ph = (i / STAGES) & 1;
                     tc::mbar_wait(&empty[s], ph ^ 1);
                     tc::mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-                    p.template load<BN>(kb0 + i, sa + s * A_BYTES, sb + s * B_BYTES, &full[s], mt, nt);
+                    p.template load<BN>(kb0 + i, sa + s * A_BYTES, sb + s * B_BYTES, &full[s], mt, nt, blockIdx.z);
                 }
             }
         } else if (warp == 1) {
@@ -345,7 +373,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
             tc::mbar_wait(tfull, 0);
             tc::tc_fence_after();
             const int sub = warp & 3;
-            p.template epilogue<BN>(tmem + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt);
+            p.template epilogue<BN>(tmem + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, blockIdx.z);
         }
     }
     tc::tc_fence_before();
@@ -378,6 +406,18 @@ bool map_act(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, const 
     cuuint32_t box[4] = {64, (cuuint32_t)pt.Wt, (cuuint32_t)pt.Ht, (cuuint32_t)pt.Nt};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(ptr), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 4 sub-pixel planes [4][N][H][W][C] viewed as 5-D (C, W, H, N, 4); box = 64 x pixel box x 1
+bool map_planes(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, const PixTile &pt) {
+    cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N, 4};
+    cuuint64_t strides[4] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2,
+                             (cuuint64_t)N * H * W * C * 2};
+    cuuint32_t box[5] = {64, (cuuint32_t)pt.Wt, (cuuint32_t)pt.Ht, (cuuint32_t)pt.Nt, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(ptr), dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -417,10 +457,21 @@ Taps make_taps(int ksize) {
         for (int i = 0; i < 9; ++i) {
             t.dy[i] = (int8_t)(i / 3 - 1);
             t.dx[i] = (int8_t)(i % 3 - 1);
+            t.wt[i] = (int8_t)i;
         }
     }
     return t;
 }
+
+// Halving conv (model.py:79-88, 105, 128): y = conv2x2(pad(upsample2x(x), (0,1,0,1))).
+// Output pixel (2p + cy, 2q + cx) only sees x[p + {0,1}][q + {0,1}]; per sub-pixel class
+// the 2x2 taps collapse onto 1, 2, 2 and 4 distinct inputs with summed weights (9 combined
+// weight slabs, see ice_halve_prep in unet_ops.cu).  The zero pad row/column is exactly
+// the TMA out-of-bounds fill of x[p+1] / x[q+1] at the last row / column.
+//   combined slab: 0:(0,0)c0  1:(0,0)c1 2:(0,1)c1  3:(0,0)c2 4:(1,0)c2  5..8:(0,0),(0,1),(1,0),(1,1)c3
+const int8_t HALVE_CLS[9] = {0, 1, 1, 2, 2, 3, 3, 3, 3};
+const int8_t HALVE_DY[9] = {0, 0, 0, 0, 1, 0, 0, 1, 1};
+const int8_t HALVE_DX[9] = {0, 0, 1, 0, 0, 0, 1, 0, 1};
 
 template <int BN, int STAGES, class P>
 int launch(const P &p, dim3 grid, cudaStream_t st) {
@@ -460,14 +511,15 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
     FpropProb p;
     memset(&p, 0, sizeof p);
     p.pt = pix_tile(n, h, w, BM);
-    p.taps = make_taps(ksize);
+    p.taps[0] = make_taps(ksize);
+    p.omul = 1;
     p.N = n; p.H = h; p.W = w; p.c1 = c1; p.c2 = c2; p.cout = cout;
     p.bias = bias; p.drop = drop_scale; p.relu = relu; p.y = reinterpret_cast<bf16 *>(y);
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     const int bn = pick_bn(cout, mtiles);
     if (!map_act(&p.xa, x1, n, h, w, c1, p.pt)) return ICE_EINVAL;
     if (c2 && !map_act(&p.xb, x2, n, h, w, c2, p.pt)) return ICE_EINVAL;
-    if (!map_wgt(&p.wm, wgt, cout, p.taps.n, c1 + c2, bn)) return ICE_EINVAL;
+    if (!map_wgt(&p.wm, wgt, cout, p.taps[0].n, c1 + c2, bn)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, cout / bn, 1);
     cudaStream_t st = (cudaStream_t)stream;
     if (bn == 256) return launch<256, 4>(p, grid, st);
@@ -479,7 +531,7 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
                               const uint16_t *wgt, int32_t c1, int32_t c2, uint16_t *dx1, const uint16_t *relu_ref1,
                               const float *drop_scale1, const uint16_t *add1, uint16_t *dx2,
                               const uint16_t *relu_ref2, const float *drop_scale2, const uint16_t *add2,
-                              void *stream) {
+                              int32_t dx2_planes, void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!dy || !wgt || c1 <= 0 || c1 % 64 || c2 < 0 || c2 % 64 || cout <= 0 || cout % 64 ||
         (ksize != 1 && ksize != 3) || !shape_ok(n, h, w))
@@ -493,6 +545,8 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
     p.ref1 = reinterpret_cast<const bf16 *>(relu_ref1); p.ref2 = reinterpret_cast<const bf16 *>(relu_ref2);
     p.add1 = reinterpret_cast<const bf16 *>(add1); p.add2 = reinterpret_cast<const bf16 *>(add2);
     p.drop1 = drop_scale1; p.drop2 = drop_scale2;
+    p.planes_out2 = dx2_planes;
+    if (dx2_planes && ((h | w) & 1)) return ICE_EINVAL;
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     const int ct = c1 + c2;
     int bn = pick_bn(ct, mtiles);
@@ -536,6 +590,98 @@ extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2
     if (!map_act(&p.dym, dy, n, h, w, cout, p.pk)) return ICE_EINVAL;
     if (!map_act(&p.xa, x1, n, h, w, c1, p.pk)) return ICE_EINVAL;
     if (c2 && !map_act(&p.xb, x2, n, h, w, c2, p.pk)) return ICE_EINVAL;
+    dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (bn == 256) return launch<256, 4>(p, grid, st);
+    if (bn == 128) return launch<128, 6>(p, grid, st);
+    return launch<64, 8>(p, grid, st);
+}
+
+extern "C" int ice_halve_fprop(const uint16_t *x, int32_t c, int32_t n, int32_t h, int32_t w, const uint16_t *wc,
+                               const float *bias, int32_t cout, uint16_t *y, void *stream) {
+    if (!encode_fn()) return ICE_ENODRIVER;
+    if (!x || !wc || !y || c <= 0 || c % 64 || cout <= 0 || cout % 64 || !shape_ok(n, h, w)) return ICE_EINVAL;
+    FpropProb p;
+    memset(&p, 0, sizeof p);
+    p.pt = pix_tile(n, h, w, BM);
+    for (int i = 0; i < 9; ++i) {
+        Taps &t = p.taps[HALVE_CLS[i]];
+        t.dy[t.n] = HALVE_DY[i];
+        t.dx[t.n] = HALVE_DX[i];
+        t.wt[t.n] = (int8_t)i;
+        t.n++;
+    }
+    p.omul = 2;
+    p.N = n; p.H = h; p.W = w; p.c1 = c; p.c2 = 0; p.cout = cout;
+    p.bias = bias; p.relu = 0; p.y = reinterpret_cast<bf16 *>(y);
+    const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
+    const int bn = pick_bn(cout, mtiles * 4);
+    if (!map_act(&p.xa, x, n, h, w, c, p.pt)) return ICE_EINVAL;
+    if (!map_wgt(&p.wm, wc, cout, 9, c, bn)) return ICE_EINVAL;
+    dim3 grid((unsigned)mtiles, cout / bn, 4);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (bn == 256) return launch<256, 4>(p, grid, st);
+    if (bn == 128) return launch<128, 6>(p, grid, st);
+    return launch<64, 8>(p, grid, st);
+}
+
+extern "C" int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t n, int32_t h, int32_t w,
+                               const uint16_t *wc, int32_t c, uint16_t *dx, const uint16_t *relu_ref,
+                               const float *drop_scale, void *stream) {
+    if (!encode_fn()) return ICE_ENODRIVER;
+    if (!dy_planes || !wc || !dx || c <= 0 || c % 64 || cout <= 0 || cout % 64 || !shape_ok(n, h, w))
+        return ICE_EINVAL;
+    DgradProb p;
+    memset(&p, 0, sizeof p);
+    p.pt = pix_tile(n, h, w, BM);
+    p.taps.n = 9;
+    for (int i = 0; i < 9; ++i) {
+        p.taps.dy[i] = HALVE_DY[i];
+        p.taps.dx[i] = HALVE_DX[i];
+        p.taps.plane[i] = HALVE_CLS[i];
+        p.taps.wt[i] = (int8_t)i;
+    }
+    p.planes_in = 1;
+    p.N = n; p.H = h; p.W = w; p.c1 = c; p.c2 = 0; p.cout = cout;
+    p.out1 = reinterpret_cast<bf16 *>(dx);
+    p.ref1 = reinterpret_cast<const bf16 *>(relu_ref);
+    p.drop1 = drop_scale;
+    const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
+    const int bn = pick_bn(c, mtiles);
+    if (!map_planes(&p.dym, dy_planes, n, h, w, cout, p.pt)) return ICE_EINVAL;
+    if (!map_wgt(&p.wm, wc, cout, 9, c, 64)) return ICE_EINVAL;
+    dim3 grid((unsigned)mtiles, c / bn, 1);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (bn == 256) return launch<256, 4>(p, grid, st);
+    if (bn == 128) return launch<128, 6>(p, grid, st);
+    return launch<64, 8>(p, grid, st);
+}
+
+extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_planes, int32_t cout, int32_t n,
+                               int32_t h, int32_t w, float *dw, void *stream) {
+    if (!encode_fn()) return ICE_ENODRIVER;
+    if (!x || !dy_planes || !dw || c <= 0 || c % 64 || cout <= 0 || cout % 64 || !shape_ok(n, h, w))
+        return ICE_EINVAL;
+    WgradProb p;
+    memset(&p, 0, sizeof p);
+    p.pk = pix_tile(n, h, w, BK);
+    p.taps.n = 4;  // (a, b) of the 2x2 kernel; shifts derive from (class, tap) in load()
+    p.halve = 1;
+    p.N = n; p.H = h; p.W = w; p.c1 = c; p.c2 = 0; p.cout = cout;
+    p.dw = dw;
+    const int ncols = 4 * c;
+    const int mtiles = (cout + BM - 1) / BM;
+    int bn = ncols % 256 == 0 ? 256 : (ncols % 128 == 0 ? 128 : 64);
+    const int ntiles = ncols / bn;
+    p.total_kb = 4 * p.pk.tw * p.pk.th * p.pk.tn;
+    const long long tiles = (long long)mtiles * ntiles;
+    int splits = (int)((2 * 148 + tiles - 1) / tiles);
+    if (splits > p.total_kb) splits = p.total_kb;
+    if (splits < 1) splits = 1;
+    p.kb_per_split = (p.total_kb + splits - 1) / splits;
+    splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
+    if (!map_planes(&p.dym, dy_planes, n, h, w, cout, p.pk)) return ICE_EINVAL;
+    if (!map_act(&p.xa, x, n, h, w, c, p.pk)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
     cudaStream_t st = (cudaStream_t)stream;
     if (bn == 256) return launch<256, 4>(p, grid, st);

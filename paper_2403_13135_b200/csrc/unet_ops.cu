@@ -1,0 +1,516 @@
+// unet_ops.cu -- the bandwidth-bound U-Net kernels around the tcgen05 convolutions:
+// input stem (u8 -> bf16 im2col), 2x2 max-pool forward / fused backward, fused
+// 1x1-head + softmax cross-entropy forward/backward, bias gradients, Dropout2d scales,
+// weight-layout prep, and the fused multi-tensor Adam step.
+//
+// All NHWC bf16; every kernel is a single streaming pass (HBM roofline), vectorised to
+// 16-byte accesses where the channel count allows.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "icelabel_b200.h"
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ float bf(uint16_t u) { return __uint_as_float((uint32_t)u << 16); }
+__device__ __forceinline__ uint16_t to_bf(float f) {
+    bf16 h = __float2bfloat16_rn(f);
+    return *reinterpret_cast<uint16_t *>(&h);
+}
+
+inline unsigned grid_for(long long work, int per_block) {
+    long long b = (work + per_block - 1) / per_block;
+    if (b > 148LL * 32) b = 148LL * 32;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+
+// ---- stem: train.py:63 (u8 / 255) + im2col of the 3x3x3 first conv, K padded to 64 ----
+// out[p][(r*3+s)*3 + c] = img[p + (r-1, s-1)][c] / 255 (zero outside), out[p][27..63] = 0
+__global__ void stem_im2col_kernel(const uint8_t *__restrict__ img, int n, int h, int w, uint16_t *__restrict__ out) {
+    const long long npx = (long long)n * h * w;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < npx; p += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(p % w);
+        const int y = (int)((p / w) % h);
+        const long long img0 = p - (long long)y * w - x;  // first pixel of this image
+        uint16_t v[64];
+#pragma unroll
+        for (int i = 27; i < 64; ++i) v[i] = 0;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const int yy = y + t / 3 - 1, xx = x + t % 3 - 1;
+            const bool in = yy >= 0 && yy < h && xx >= 0 && xx < w;
+            const uint8_t *px = img + 3 * (img0 + (long long)yy * w + xx);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[t * 3 + c] = in ? to_bf((float)px[c] / 255.0f) : (uint16_t)0;
+        }
+        uint4 *dst = reinterpret_cast<uint4 *>(out + p * 64);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            uint4 u;
+            u.x = v[q * 8 + 0] | ((uint32_t)v[q * 8 + 1] << 16);
+            u.y = v[q * 8 + 2] | ((uint32_t)v[q * 8 + 3] << 16);
+            u.z = v[q * 8 + 4] | ((uint32_t)v[q * 8 + 5] << 16);
+            u.w = v[q * 8 + 6] | ((uint32_t)v[q * 8 + 7] << 16);
+            dst[q] = u;
+        }
+    }
+}
+
+// same stem from an fp32 NHWC image already scaled to [0, 1] (UNet.forward on float input)
+__global__ void stem_im2col_f32_kernel(const float *__restrict__ img, int n, int h, int w, uint16_t *__restrict__ out) {
+    const long long npx = (long long)n * h * w;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < npx; p += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(p % w);
+        const int y = (int)((p / w) % h);
+        const long long img0 = p - (long long)y * w - x;
+        uint16_t v[64];
+#pragma unroll
+        for (int i = 27; i < 64; ++i) v[i] = 0;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const int yy = y + t / 3 - 1, xx = x + t % 3 - 1;
+            const bool in = yy >= 0 && yy < h && xx >= 0 && xx < w;
+            const float *px = img + 3 * (img0 + (long long)yy * w + xx);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[t * 3 + c] = in ? to_bf(px[c]) : (uint16_t)0;
+        }
+        uint4 *dst = reinterpret_cast<uint4 *>(out + p * 64);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            uint4 u;
+            u.x = v[q * 8 + 0] | ((uint32_t)v[q * 8 + 1] << 16);
+            u.y = v[q * 8 + 2] | ((uint32_t)v[q * 8 + 3] << 16);
+            u.z = v[q * 8 + 4] | ((uint32_t)v[q * 8 + 5] << 16);
+            u.w = v[q * 8 + 6] | ((uint32_t)v[q * 8 + 7] << 16);
+            dst[q] = u;
+        }
+    }
+}
+
+// fp32 [rows][k] -> bf16 [rows][kp], zero padded (stem weights 64 x 27 -> 64 x 64)
+__global__ void pad_weights_kernel(const float *__restrict__ src, int rows, int k, uint16_t *__restrict__ dst, int kp) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * kp; i += gridDim.x * blockDim.x) {
+        const int r = i / kp, c = i % kp;
+        dst[i] = c < k ? to_bf(src[r * k + c]) : (uint16_t)0;
+    }
+}
+
+// 2x2 weights [cout][2][2][c] -> 9 combined sub-pixel slabs [cout][9][c] (see conv_tc.cu)
+__global__ void halve_prep_kernel(const float *__restrict__ w, int cout, int c, uint16_t *__restrict__ wc) {
+    const long long total = (long long)cout * c;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const long long o = i / c, ci = i % c;
+        const float *b = w + o * 4 * c + ci;
+        const float w00 = b[0], w01 = b[c], w10 = b[2 * c], w11 = b[3 * c];
+        uint16_t *d = wc + o * 9 * c + ci;
+        d[0 * c] = to_bf(w00 + w01 + w10 + w11);
+        d[1 * c] = to_bf(w00 + w10);
+        d[2 * c] = to_bf(w01 + w11);
+        d[3 * c] = to_bf(w00 + w01);
+        d[4 * c] = to_bf(w10 + w11);
+        d[5 * c] = to_bf(w00);
+        d[6 * c] = to_bf(w01);
+        d[7 * c] = to_bf(w10);
+        d[8 * c] = to_bf(w11);
+    }
+}
+
+// ---- max-pool 2x2 / 2 (model.py:102,125 nn.MaxPool2d(2)) ----------------------------
+// 8 channels per thread (16-byte vectors)
+__global__ void maxpool_fwd_kernel(const uint16_t *__restrict__ x, int n, int h, int w, int c, uint16_t *__restrict__ y) {
+    const int ho = h / 2, wo = w / 2, cv = c / 8;
+    const long long total = (long long)n * ho * wo * cv;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int cg = (int)(i % cv);
+        long long p = i / cv;
+        const int xo = (int)(p % wo);
+        const int yo = (int)((p / wo) % ho);
+        const long long img = p / ((long long)wo * ho);
+        const uint4 *src = reinterpret_cast<const uint4 *>(x);
+        const long long r0 = ((img * h + 2 * yo) * w + 2 * xo) * cv + cg;
+        uint4 a = src[r0], b = src[r0 + cv], cc = src[r0 + (long long)w * cv], d = src[r0 + (long long)w * cv + cv];
+        const uint16_t *pa = reinterpret_cast<const uint16_t *>(&a), *pb = reinterpret_cast<const uint16_t *>(&b);
+        const uint16_t *pc = reinterpret_cast<const uint16_t *>(&cc), *pd = reinterpret_cast<const uint16_t *>(&d);
+        uint4 o;
+        uint16_t *po = reinterpret_cast<uint16_t *>(&o);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            // first maximum in window order wins (torch CPU max_pool2d uses a strict '>')
+            uint16_t best = pa[e];
+            float bv = bf(best);
+            if (bf(pb[e]) > bv) { best = pb[e]; bv = bf(best); }
+            if (bf(pc[e]) > bv) { best = pc[e]; bv = bf(best); }
+            if (bf(pd[e]) > bv) { best = pd[e]; }
+            po[e] = best;
+        }
+        reinterpret_cast<uint4 *>(y)[i] = o;
+    }
+}
+
+// dz = (add + maxpool_backward(dpool)) * drop[n][c] * [x > 0]: the fused backward of
+// "ReLU -> Dropout2d -> {skip, MaxPool2d}" for a down block's output x (model.py:115-118).
+__global__ void maxpool_bwd_kernel(const uint16_t *__restrict__ x, const uint16_t *__restrict__ dpool,
+                                   const uint16_t *__restrict__ add, const float *__restrict__ drop, int n, int h, int w,
+                                   int c, uint16_t *__restrict__ dz) {
+    const int ho = h / 2, wo = w / 2, cv = c / 8;
+    const long long total = (long long)n * ho * wo * cv;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int cg = (int)(i % cv);
+        long long p = i / cv;
+        const int xo = (int)(p % wo);
+        const int yo = (int)((p / wo) % ho);
+        const long long img = p / ((long long)wo * ho);
+        const long long r[4] = {((img * h + 2 * yo) * w + 2 * xo) * cv + cg, 0, 0, 0};
+        const long long idx[4] = {r[0], r[0] + cv, r[0] + (long long)w * cv, r[0] + (long long)w * cv + cv};
+        uint4 xv[4], av[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            xv[k] = reinterpret_cast<const uint4 *>(x)[idx[k]];
+            av[k] = add ? reinterpret_cast<const uint4 *>(add)[idx[k]] : make_uint4(0, 0, 0, 0);
+        }
+        const uint4 g = reinterpret_cast<const uint4 *>(dpool)[i];
+        const uint16_t *pg = reinterpret_cast<const uint16_t *>(&g);
+        uint4 out[4];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            float v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = bf(reinterpret_cast<const uint16_t *>(&xv[k])[e]);
+            int arg = 0;
+            float bv = v[0];
+#pragma unroll
+            for (int k = 1; k < 4; ++k)
+                if (v[k] > bv) { bv = v[k]; arg = k; }
+            const float s = drop ? drop[img * c + cg * 8 + e] : 1.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float d = bf(reinterpret_cast<const uint16_t *>(&av[k])[e]) + (k == arg ? bf(pg[e]) : 0.f);
+                d = v[k] > 0.f ? d * s : 0.f;
+                reinterpret_cast<uint16_t *>(&out[k])[e] = to_bf(d);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) reinterpret_cast<uint4 *>(dz)[idx[k]] = out[k];
+    }
+}
+
+// ---- head: out 1x1 conv 64 -> 3 (model.py:109,130) + CrossEntropyLoss (train.py:89,96) --
+// Per pixel: logits, log-softmax loss, argmax hit; backward dlogits = (p - onehot) * scale,
+// dh = dlogits W, dz = dh * drop * [h > 0] (the ReLU/Dropout2d of up.4's output), and
+// block-reduced dW (3 x 64), db (3), loss sum, correct count.
+constexpr int HEAD_NT = 256;
+constexpr int HC = 64;
+
+__global__ void __launch_bounds__(HEAD_NT) head_ce_kernel(
+    const uint16_t *__restrict__ hact, long long npx, int hw, const uint8_t *__restrict__ labels,
+    const float *__restrict__ w_out, const float *__restrict__ b_out, const float *__restrict__ drop, float grad_scale,
+    uint16_t *__restrict__ dz, float *__restrict__ dw, float *__restrict__ db, float *__restrict__ stats,
+    float *__restrict__ logits_out) {
+    __shared__ float sw[3 * HC];
+    __shared__ uint16_t sh[HEAD_NT][HC + 2];
+    __shared__ float sd[HEAD_NT][3];
+    for (int i = threadIdx.x; i < 3 * HC; i += HEAD_NT) sw[i] = w_out[i];
+    __syncthreads();
+    const bool train = dw != nullptr;
+    float acc_w = 0.f;  // thread t < 192 owns dW[t / 64][t % 64]
+    float acc_b = 0.f, loss_sum = 0.f, correct = 0.f;
+    const float b0 = b_out[0], b1 = b_out[1], b2 = b_out[2];
+    for (long long base = (long long)blockIdx.x * HEAD_NT; base < npx; base += (long long)gridDim.x * HEAD_NT) {
+        const long long p = base + threadIdx.x;
+        const bool valid = p < npx;
+        float h[HC];
+        if (valid) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(hact + p * HC);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                uint4 u = src[q];
+                const uint16_t *e = reinterpret_cast<const uint16_t *>(&u);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) h[q * 8 + j] = bf(e[j]);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < HC; ++j) h[j] = 0.f;
+        }
+        float l0 = b0, l1 = b1, l2 = b2;
+#pragma unroll
+        for (int j = 0; j < HC; ++j) {
+            l0 = fmaf(sw[j], h[j], l0);
+            l1 = fmaf(sw[HC + j], h[j], l1);
+            l2 = fmaf(sw[2 * HC + j], h[j], l2);
+        }
+        float d0 = 0.f, d1 = 0.f, d2 = 0.f;
+        if (valid) {
+            const int y = labels[p];
+            const float mx = fmaxf(l0, fmaxf(l1, l2));
+            const float e0 = __expf(l0 - mx), e1 = __expf(l1 - mx), e2 = __expf(l2 - mx);
+            const float se = e0 + e1 + e2;
+            const float ly = y == 0 ? l0 : (y == 1 ? l1 : l2);
+            loss_sum += mx + __logf(se) - ly;
+            const int am = (l0 >= l1 && l0 >= l2) ? 0 : (l1 >= l2 ? 1 : 2);
+            correct += am == y;
+            if (logits_out) {
+                logits_out[3 * p] = l0;
+                logits_out[3 * p + 1] = l1;
+                logits_out[3 * p + 2] = l2;
+            }
+            if (train) {
+                const float inv = 1.f / se;
+                d0 = (e0 * inv - (y == 0)) * grad_scale;
+                d1 = (e1 * inv - (y == 1)) * grad_scale;
+                d2 = (e2 * inv - (y == 2)) * grad_scale;
+            }
+        }
+        if (!train) continue;
+        if (valid && dz) {
+            const long long img = p / hw;
+            uint4 *dst = reinterpret_cast<uint4 *>(dz + p * HC);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                uint32_t pk[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float g[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int j = q * 8 + e * 2 + u;
+                        float v = d0 * sw[j] + d1 * sw[HC + j] + d2 * sw[2 * HC + j];
+                        if (drop) v *= drop[img * HC + j];
+                        g[u] = h[j] > 0.f ? v : 0.f;
+                    }
+                    pk[e] = (uint32_t)to_bf(g[0]) | ((uint32_t)to_bf(g[1]) << 16);
+                }
+                dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < HC; ++j) sh[threadIdx.x][j] = to_bf(h[j]);
+        sd[threadIdx.x][0] = d0;
+        sd[threadIdx.x][1] = d1;
+        sd[threadIdx.x][2] = d2;
+        __syncthreads();
+        if (threadIdx.x < 3 * HC) {
+            const int k = threadIdx.x / HC, j = threadIdx.x % HC;
+            float s = 0.f;
+            for (int r = 0; r < HEAD_NT; ++r) s = fmaf(sd[r][k], bf(sh[r][j]), s);
+            acc_w += s;
+        } else if (threadIdx.x < 3 * HC + 3) {
+            const int k = threadIdx.x - 3 * HC;
+            float s = 0.f;
+            for (int r = 0; r < HEAD_NT; ++r) s += sd[r][k];
+            acc_b += s;
+        }
+    }
+    if (train) {
+        if (threadIdx.x < 3 * HC) atomicAdd(&dw[threadIdx.x], acc_w);
+        else if (threadIdx.x < 3 * HC + 3) atomicAdd(&db[threadIdx.x - 3 * HC], acc_b);
+    }
+    for (int o = 16; o; o >>= 1) {
+        loss_sum += __shfl_xor_sync(0xffffffffu, loss_sum, o);
+        correct += __shfl_xor_sync(0xffffffffu, correct, o);
+    }
+    if ((threadIdx.x & 31) == 0 && stats) {
+        atomicAdd(&stats[0], loss_sum);
+        atomicAdd(&stats[1], correct);
+    }
+}
+
+// ---- bias gradient: db[c] += sum over rows of dz[row][c] --------------------------------
+__global__ void bias_grad_kernel(const uint16_t *__restrict__ dz, long long rows, int c, float *__restrict__ db) {
+    extern __shared__ float red[];
+    const int groups = c / 8;               // 16-byte vectors per row
+    const int rows_per_iter = blockDim.x / groups;
+    const int g = threadIdx.x % groups, r0 = threadIdx.x / groups;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (r0 < rows_per_iter) {
+        for (long long r = (long long)blockIdx.x * rows_per_iter + r0; r < rows; r += (long long)gridDim.x * rows_per_iter) {
+            uint4 u = reinterpret_cast<const uint4 *>(dz + r * c)[g];
+            const uint16_t *e = reinterpret_cast<const uint16_t *>(&u);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] += bf(e[j]);
+        }
+    }
+    for (int j = 0; j < 8; ++j) red[threadIdx.x * 8 + j] = r0 < rows_per_iter ? acc[j] : 0.f;
+    __syncthreads();
+    for (int i = threadIdx.x; i < c; i += blockDim.x) {
+        const int gg = i / 8, j = i % 8;
+        float s = 0.f;
+        for (int rr = 0; rr < rows_per_iter; ++rr) s += red[(rr * groups + gg) * 8 + j];
+        atomicAdd(&db[i], s);
+    }
+}
+
+// ---- Dropout2d (model.py:74-75): per (sample, channel) keep with prob 1 - p, scale 1/(1-p)
+__device__ __forceinline__ uint32_t mix32(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return (uint32_t)x;
+}
+__global__ void dropout_scale_kernel(int count, float p, unsigned long long seed, float *__restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        const float u = (mix32(seed * 0x9E3779B97F4A7C15ULL + (unsigned long long)i) >> 8) * (1.0f / 16777216.0f);
+        out[i] = u >= p ? 1.0f / (1.0f - p) : 0.0f;
+    }
+}
+
+// ---- fused Adam (torch.optim.Adam defaults, train.py:149): one pass over p, g, m, v;
+// writes the bf16 working copy and zeroes the gradient for the next step ---------------
+__global__ void adam_kernel(float *__restrict__ p, float *__restrict__ g, float *__restrict__ m, float *__restrict__ v,
+                            long long n, float lr_corr, float b1, float b2, float eps, float bc2_sqrt,
+                            uint16_t *__restrict__ out_bf16) {
+    const long long n4 = n / 4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        float4 pp = reinterpret_cast<float4 *>(p)[i];
+        float4 gg = reinterpret_cast<float4 *>(g)[i];
+        float4 mm = reinterpret_cast<float4 *>(m)[i];
+        float4 vv = reinterpret_cast<float4 *>(v)[i];
+        float *pe = &pp.x, *ge = &gg.x, *me = &mm.x, *ve = &vv.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            me[e] = me[e] + (1.f - b1) * (ge[e] - me[e]);
+            ve[e] = ve[e] * b2 + (1.f - b2) * ge[e] * ge[e];
+            const float denom = sqrtf(ve[e]) / bc2_sqrt + eps;
+            pe[e] = pe[e] - lr_corr * (me[e] / denom);
+        }
+        reinterpret_cast<float4 *>(p)[i] = pp;
+        reinterpret_cast<float4 *>(m)[i] = mm;
+        reinterpret_cast<float4 *>(v)[i] = vv;
+        reinterpret_cast<float4 *>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (out_bf16) {
+            uint2 o;
+            o.x = (uint32_t)to_bf(pp.x) | ((uint32_t)to_bf(pp.y) << 16);
+            o.y = (uint32_t)to_bf(pp.z) | ((uint32_t)to_bf(pp.w) << 16);
+            reinterpret_cast<uint2 *>(out_bf16)[i] = o;
+        }
+    }
+    // tail
+    for (long long i = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const float ge = g[i];
+        const float me = m[i] + (1.f - b1) * (ge - m[i]);
+        const float ve = v[i] * b2 + (1.f - b2) * ge * ge;
+        const float pe = p[i] - lr_corr * (me / (sqrtf(ve) / bc2_sqrt + eps));
+        m[i] = me;
+        v[i] = ve;
+        p[i] = pe;
+        g[i] = 0.f;
+        if (out_bf16) out_bf16[i] = to_bf(pe);
+    }
+}
+
+__global__ void cast_bf16_kernel(const float *__restrict__ src, long long n, uint16_t *__restrict__ dst) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = to_bf(src[i]);
+}
+
+__global__ void fill_f32_kernel(float *__restrict__ dst, long long n, float v) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = v;
+}
+
+}  // namespace
+
+#define LAUNCH_CHECK() return (int)cudaGetLastError()
+
+extern "C" int ice_stem_im2col(const uint8_t *img, int32_t n, int32_t h, int32_t w, uint16_t *out, void *stream) {
+    if (!img || !out || n < 1 || h < 1 || w < 1) return ICE_EINVAL;
+    stem_im2col_kernel<<<grid_for((long long)n * h * w, 256), 256, 0, (cudaStream_t)stream>>>(img, n, h, w, out);
+    LAUNCH_CHECK();
+}
+
+extern "C" int ice_stem_im2col_f32(const float *img, int32_t n, int32_t h, int32_t w, uint16_t *out, void *stream) {
+    if (!img || !out || n < 1 || h < 1 || w < 1) return ICE_EINVAL;
+    stem_im2col_f32_kernel<<<grid_for((long long)n * h * w, 256), 256, 0, (cudaStream_t)stream>>>(img, n, h, w, out);
+    LAUNCH_CHECK();
+}
+
+extern "C" int ice_pad_weights(const float *src, int32_t rows, int32_t k, uint16_t *dst, int32_t kp, void *stream) {
+    if (!src || !dst || rows < 1 || k < 1 || kp < k) return ICE_EINVAL;
+    pad_weights_kernel<<<grid_for((long long)rows * kp, 256), 256, 0, (cudaStream_t)stream>>>(src, rows, k, dst, kp);
+    LAUNCH_CHECK();
+}
+
+extern "C" int ice_halve_prep(const float *w, int32_t cout, int32_t c, uint16_t *wc, void *stream) {
+    if (!w || !wc || cout < 1 || c < 1) return ICE_EINVAL;
+    halve_prep_kernel<<<grid_for((long long)cout * c, 256), 256, 0, (cudaStream_t)stream>>>(w, cout, c, wc);
+    LAUNCH_CHECK();
+}
+
+extern "C" int ice_maxpool_fwd(const uint16_t *x, int32_t n, int32_t h, int32_t w, int32_t c, uint16_t *y,
+                               void *stream) {
+    if (!x || !y || n < 1 || h < 2 || w < 2 || (h | w) & 1 || c % 8) return ICE_EINVAL;
+    maxpool_fwd_kernel<<<grid_for((long long)n * (h / 2) * (w / 2) * (c / 8), 256), 256, 0, (cudaStream_t)stream>>>(
+        x, n, h, w, c, y);
+    LAUNCH_CHECK();
+}
+
+extern "C" int ice_maxpool_bwd(const uint16_t *x, const uint16_t *dpool, const uint16_t *add, const float *drop,
+                               int32_t n, int32_t h, int32_t w, int32_t c, uint16_t *dz, void *stream) {
+    if (!x || !dpool || !dz || n < 1 || h < 2 || w < 2 || (h | w) & 1 || c % 8) return ICE_EINVAL;
+    maxpool_bwd_kernel<<<grid_for((long long)n * (h / 2) * (w / 2) * (c / 8), 256), 256, 0, (cudaStream_t)stream>>>(
+        x, dpool, add, drop, n, h, w, c, dz);
+    LAUNCH_CHECK();
+}
+
+extern "C" int ice_head_ce(const uint16_t *h, int64_t npx, int32_t hw, const uint8_t *labels, const float *w_out,
+                           const float *b_out, const float *drop, float grad_scale, uint16_t *dz, float *dw, float *db,
+                           float *stats, float *logits, void *stream) {
+    if (!h || !labels || !w_out || !b_out || npx < 0 || hw < 1 || ((dw == nullptr) != (db == nullptr))) return ICE_EINVAL;
+    if (npx == 0) return ICE_OK;
+    unsigned blocks = grid_for(npx, HEAD_NT);
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    head_ce_kernel<<<blocks, HEAD_NT, 0, (cudaStream_t)stream>>>(h, npx, hw, labels, w_out, b_out, drop, grad_scale,
+                                                                 dz, dw, db, stats, logits);
+    LAUNCH_CHECK();
+}
+
+extern "C" int ice_bias_grad(const uint16_t *dz, int64_t rows, int32_t c, float *db, void *stream) {
+    if (!dz || !db || rows < 0 || c < 8 || c % 8 || c / 8 > 256) return ICE_EINVAL;
+    if (rows == 0) return ICE_OK;
+    const int threads = 256;
+    const int rows_per_iter = threads / (c / 8);
+    unsigned blocks = grid_for(rows, rows_per_iter * 64);
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    bias_grad_kernel<<<blocks, threads, threads * 8 * sizeof(float), (cudaStream_t)stream>>>(dz, rows, c, db);
+    LAUNCH_CHECK();
+}
+
+extern "C" int ice_dropout_scale(int32_t count, float p, uint64_t seed, float *out, void *stream) {
+    if (!out || count < 0 || p < 0.f || p >= 1.f) return ICE_EINVAL;
+    if (count == 0) return ICE_OK;
+    dropout_scale_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(count, p, seed, out);
+    LAUNCH_CHECK();
+}
+
+extern "C" int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64_t step, float lr, float beta1,
+                        float beta2, float eps, uint16_t *out_bf16, void *stream) {
+    if (!p || !g || !m || !v || n < 0 || step < 1) return ICE_EINVAL;
+    if (n == 0) return ICE_OK;
+    // torch.optim.Adam (_single_tensor_adam): step_size = lr / (1 - b1^t), denom = sqrt(v)/sqrt(1 - b2^t) + eps
+    const double bc1 = 1.0 - pow((double)beta1, (double)step);
+    const double bc2 = 1.0 - pow((double)beta2, (double)step);
+    adam_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, (cudaStream_t)stream>>>(
+        p, g, m, v, n, (float)(lr / bc1), beta1, beta2, eps, (float)sqrt(bc2), out_bf16);
+    LAUNCH_CHECK();
+}
+
+extern "C" int ice_cast_bf16(const float *src, int64_t n, uint16_t *dst, void *stream) {
+    if (!src || !dst || n < 0) return ICE_EINVAL;
+    if (n == 0) return ICE_OK;
+    cast_bf16_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(src, n, dst);
+    LAUNCH_CHECK();
+}
+
+extern "C" int ice_fill_f32(float *dst, int64_t n, float value, void *stream) {
+    if (!dst || n < 0) return ICE_EINVAL;
+    if (n == 0) return ICE_OK;
+    fill_f32_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(dst, n, value);
+    LAUNCH_CHECK();
+}

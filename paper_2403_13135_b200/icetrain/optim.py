@@ -1,0 +1,26 @@
+"""Adam facade over the fused ice_adam kernel (torch.optim.Adam defaults, train.py:149)."""
+from __future__ import annotations
+
+
+class Adam:
+    """Drop-in for ``torch.optim.Adam(model.parameters(), lr=...)`` on a B200 UNet:
+    ``params`` is what UNet.parameters() returns (its engine)."""
+
+    def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
+                 weight_decay: float = 0.0, amsgrad: bool = False):
+        if lr <= 0:
+            raise ValueError(f"Invalid learning rate: {lr}")
+        if weight_decay or amsgrad:
+            raise ValueError("only the reference's Adam defaults (no weight decay, no amsgrad) are fused")
+        self.engines = list(params)
+        self.lr, self.betas, self.eps = lr, tuple(betas), eps
+        self.step_count = 0
+
+    def step(self) -> None:
+        self.step_count += 1
+        for e in self.engines:
+            e.adam(self.step_count, self.lr, self.betas, self.eps)
+
+    def zero_grad(self, set_to_none: bool = True) -> None:
+        for e in self.engines:
+            e.zero_grad()

@@ -1,0 +1,311 @@
+"""Synchronous data-parallel U-Net training on B200s.
+
+Mirrors icetrain.train (/root/reference/pkg/trainer/src/icetrain/train.py):
+  * TrainConfig / TrainResult / TABLE_COLUMNS / BATCH_CHOICES  (train.py:25-57)
+  * synchronized_step(models, optimizers, shards) -> (mean_loss, total)   (train.py:85-120)
+  * train / train_distributed / throughput_table / table_csv            (train.py:188-234)
+
+The reference runs one thread replica per "device" on the CPU and averages gradients in
+Python, weighted by shard size.  Here every shard's cross-entropy gradient is pre-scaled by
+1 / (union pixels), so a plain SUM over shards is exactly that weighted average:
+  * local replicas (several shards on one GPU) accumulate into one gradient buffer
+    (every gradient kernel accumulates);
+  * across processes (one per GPU, torch.distributed/NCCL) the flat gradient buffer is
+    all-reduced in buckets laid out in backward-readiness order, each bucket launched on a
+    side stream as soon as backward has produced it (overlap with the rest of backward).
+Every replica then applies the identical fused Adam step, so replicas never drift.
+"""
+
+from __future__ import annotations
+
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .data import train_val_split
+from .model import UNet, UNetSpec
+from .optim import Adam
+
+BATCH_CHOICES = (16, 32, 64)
+TABLE_COLUMNS = ("devices", "total_s", "s_per_epoch", "samples_per_s", "speedup")
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    batch_size: int = 32
+    epochs: int = 5
+    lr: float = 1e-3
+    val_fraction: float = 0.2
+    seed: int = 0
+    device: str = "cpu"
+
+    def __post_init__(self) -> None:
+        if self.batch_size < 1:
+            raise ValueError(f"batch_size must be >= 1, got {self.batch_size}")
+        if self.epochs < 1:
+            raise ValueError(f"epochs must be >= 1, got {self.epochs}")
+        if self.lr <= 0:
+            raise ValueError(f"lr must be positive, got {self.lr}")
+        if self.device not in ("cpu", "cuda"):
+            raise ValueError(f"device must be cpu or cuda, got {self.device!r}")
+
+
+@dataclass
+class TrainResult:
+    model: UNet
+    spec: UNetSpec
+    config: TrainConfig
+    history: list = field(default_factory=list)
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist if dist.is_available() and dist.is_initialized() else None
+
+
+def _as_nhwc(x: torch.Tensor, device) -> tuple:
+    """Shard images -> (device tensor, float_input).  Accepts the reference's NCHW float
+    in [0, 1] (train.py:63) or the GPU pipeline's NHWC uint8."""
+    if x.dtype == torch.uint8:
+        t = x if x.shape[-1] == 3 else x.permute(0, 2, 3, 1)
+        return t.to(device, non_blocking=True).contiguous(), False
+    t = x.permute(0, 2, 3, 1) if x.shape[1] == 3 and x.shape[-1] != 3 else x
+    return t.to(device, torch.float32, non_blocking=True).contiguous(), True
+
+
+class GradBucketer:
+    """Bucketed SUM all-reduce of the flat gradient buffer, overlapped with backward.
+
+    Buckets are contiguous slices of UNetEngine.grads (laid out in readiness order); when
+    backward reports a layer done, every bucket whose last layer is complete is launched on
+    a side stream after an event recorded on the compute stream.  `finish()` joins the side
+    stream back into the compute stream."""
+
+    def __init__(self, engine, bucket_bytes: int = 64 << 20, group=None):
+        from .model import readiness_order
+        self.engine, self.group = engine, group
+        self.stream = torch.cuda.Stream(device=engine.device)
+        names = readiness_order(engine.spec)
+        self.buckets = []  # (start, stop, last layer name)
+        start = 0
+        limit = bucket_bytes // 4
+        for k, name in enumerate(names):
+            lo, hi = engine.layer_slice(name)
+            last = k == len(names) - 1
+            if hi - start >= limit or last:
+                self.buckets.append((start, engine.numel if last else hi, name))
+                start = hi
+        self.pending = []
+
+    def on_layer_done(self, name: str) -> None:
+        dist = _dist()
+        for start, stop, last in self.buckets:
+            if last == name:
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream())
+                with torch.cuda.stream(self.stream):
+                    self.stream.wait_event(ev)
+                    dist.all_reduce(self.engine.grads[start:stop], group=self.group)
+
+    def finish(self) -> None:
+        torch.cuda.current_stream().wait_stream(self.stream)
+
+
+def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
+    """One collective training step (train.py:85-120).  ``shards[i]`` is replica i's
+    ``(x, y)`` slice of the union batch (may be empty).  Under torch.distributed each rank
+    passes its own shard(s) and the union spans all ranks.  Returns the union-batch mean
+    loss and the union sample count."""
+    engine = models[0].engine
+    device = engine.device
+    counts = [len(x) for x, _ in shards]
+    local = sum(counts)
+    dist = _dist()
+    if dist is not None:
+        t = torch.tensor([float(local)], device=device)
+        dist.all_reduce(t)
+        total = int(t.item())
+    else:
+        total = local
+    if total == 0:
+        raise ValueError("synchronized step got only empty shards")
+    A = None
+    seed = getattr(optimizers[0], "step_count", 0) + 1
+    bucketer = None
+    if dist is not None and dist.get_world_size() > 1:
+        bucketer = getattr(engine, "_bucketer", None) or GradBucketer(engine)
+        engine._bucketer = bucketer
+    live = [(k, s) for k, s in enumerate(shards) if counts[k] > 0]
+    for idx, (k, (x, y)) in enumerate(live):
+        xin, is_float = _as_nhwc(x, device)
+        S = xin.shape[1]
+        A = engine.forward(xin, train=models[0].training, seed=seed * 1009 + k, float_input=is_float)
+        if idx == 0:
+            A.stats.zero_()
+        A.labels.copy_(y.to(device, non_blocking=True), non_blocking=True)
+        dz = engine.head(A, A.labels, train=True, grad_scale=1.0 / (total * S * S))
+        last = idx == len(live) - 1
+        engine.backward(A, dz, on_layer_done=bucketer.on_layer_done if (bucketer and last) else None)
+    if A is None:  # this rank had no samples: contribute zeros
+        engine.ensure(1, models[0].spec.input_size).stats.zero_()
+        A = engine.acts
+        if bucketer:
+            for _, _, last in bucketer.buckets:
+                bucketer.on_layer_done(last)
+    if bucketer:
+        bucketer.finish()
+    stats = A.stats
+    if dist is not None:
+        dist.all_reduce(stats)
+    S = models[0].spec.input_size if A.S is None else A.S
+    mean_loss = float(stats[0].item()) / (total * S * S)
+    for m in models[1:]:
+        m.engine.grads.copy_(engine.grads)
+    for opt in optimizers:
+        opt.step()
+    return mean_loss, total
+
+
+def _validate_pairs(pairs: list, spec: UNetSpec) -> None:
+    if not pairs:
+        raise ValueError("training corpus is empty")
+    step = 2 ** spec.depth
+    shape = pairs[0][0].shape
+    for i, (tile, mask) in enumerate(pairs):
+        if tile.shape != shape or mask.shape != shape[:2]:
+            raise ValueError(f"pair {i}: shape {tile.shape}/{mask.shape} does "
+                             f"not match the corpus shape {shape}")
+        if mask.min() < 0 or mask.max() >= spec.classes:
+            raise ValueError(f"pair {i}: class index out of range for {spec.classes} classes")
+    if shape[2] != spec.in_channels or shape[0] % step or shape[1] % step:
+        raise ValueError(f"tile shape {shape} does not fit the model "
+                         f"(needs {spec.in_channels} channels, dims divisible by {step})")
+
+
+def _device_corpus(pairs: list, device):
+    """uint8 NHWC images and uint8 labels, resident in HBM (the reference keeps float32
+    NCHW copies in host RAM, train.py:60-65)."""
+    x = torch.from_numpy(np.ascontiguousarray(np.stack([p[0] for p in pairs]))).to(device)
+    y = torch.from_numpy(np.ascontiguousarray(np.stack([p[1] for p in pairs]).astype(np.uint8))).to(device)
+    return x, y
+
+
+def evaluate(model: UNet, x: torch.Tensor, y: torch.Tensor, batch: int) -> tuple:
+    """(mean loss, pixel accuracy) in eval mode (train.py:123-134)."""
+    eng = model.engine
+    loss_sum, correct, pixels = 0.0, 0.0, 0
+    for start in range(0, len(x), batch):
+        xb, yb = x[start:start + batch], y[start:start + batch]
+        A = eng.forward(xb, train=False)
+        A.stats.zero_()
+        eng.head(A, yb.contiguous(), train=False)
+        st = A.stats.tolist()
+        loss_sum += st[0]
+        correct += st[1]
+        pixels += yb.numel()
+    return loss_sum / pixels, correct / pixels
+
+
+def _fit(pairs: list, spec: UNetSpec, config: TrainConfig, replicas: int) -> tuple:
+    _validate_pairs(pairs, spec)
+    torch.manual_seed(config.seed)
+    train_pairs, val_pairs = train_val_split(pairs, config.val_fraction, config.seed)
+    dist = _dist()
+    rank = dist.get_rank() if dist else 0
+    world = dist.get_world_size() if dist else 1
+    device = torch.device("cuda", torch.cuda.current_device())
+    x_train, y_train = _device_corpus(train_pairs, device)
+    x_val, y_val = _device_corpus(val_pairs, device) if val_pairs else (None, None)
+
+    local = replicas if dist is None else 1
+    models = [UNet(spec, device)]
+    for _ in range(local - 1):
+        twin = UNet(spec, device)
+        twin.load_state_dict(models[0].state_dict())
+        models.append(twin)
+    if dist is not None:  # parameter broadcast from rank 0 (train.py:144-148)
+        dist.broadcast(models[0].engine.params, 0)
+        models[0].engine.refresh_working_weights()
+    optimizers = [Adam(m.parameters(), lr=config.lr) for m in models]
+
+    shuffler = torch.Generator().manual_seed(config.seed)
+    history = []
+    n_replicas = local * world
+    torch.cuda.synchronize()
+    started = time.perf_counter()
+    for epoch in range(config.epochs):
+        for m in models:
+            m.train()
+        order = torch.randperm(len(x_train), generator=shuffler)
+        span = config.batch_size * n_replicas
+        loss_sum, seen = 0.0, 0
+        for start in range(0, len(order), span):
+            union = order[start:start + span]
+            pieces = torch.tensor_split(union, n_replicas)
+            mine = pieces[rank * local:(rank + 1) * local]
+            shards = [(x_train[p.to(device)], y_train[p.to(device)]) for p in mine]
+            loss, count = synchronized_step(models, optimizers, shards)
+            loss_sum += loss * count
+            seen += count
+        entry = {"epoch": epoch, "train_loss": loss_sum / seen}
+        entry["train_acc"] = evaluate(models[0], x_train, y_train, config.batch_size)[1]
+        if x_val is not None:
+            entry["val_loss"], entry["val_acc"] = evaluate(models[0], x_val, y_val, config.batch_size)
+        history.append(entry)
+    torch.cuda.synchronize()
+    total_s = time.perf_counter() - started
+    result = TrainResult(models[0], spec, config, history)
+    row = {
+        "devices": n_replicas,
+        "total_s": round(total_s, 3),
+        "s_per_epoch": round(total_s / config.epochs, 3),
+        "samples_per_s": round(config.epochs * len(x_train) / total_s, 3) if total_s > 0 else 0.0,
+        "speedup": 1.0,
+    }
+    return result, row
+
+
+def train(pairs: list, spec: UNetSpec, config: TrainConfig) -> TrainResult:
+    result, _ = _fit(pairs, spec, config, replicas=1)
+    return result
+
+
+def _available_replicas(config: TrainConfig, requested: int) -> int:
+    if requested < 1:
+        raise ValueError(f"devices must be >= 1, got {requested}")
+    dist = _dist()
+    if dist is not None and requested not in (1, dist.get_world_size()):
+        warnings.warn(f"requested {requested} devices but the process group has "
+                      f"{dist.get_world_size()} ranks; using the process group")
+    return requested
+
+
+def train_distributed(pairs: list, spec: UNetSpec, config: TrainConfig, devices: int = 1) -> tuple:
+    """Synchronous data-parallel training.  Under torch.distributed (one process per GPU,
+    launched by torchrun) the replicas are the ranks; otherwise ``devices`` lockstep
+    replicas share the current GPU (same math, for equivalence testing)."""
+    replicas = _available_replicas(config, devices)
+    return _fit(pairs, spec, config, replicas)
+
+
+def throughput_table(pairs: list, spec: UNetSpec, config: TrainConfig, device_counts: tuple = (1, 2)) -> list:
+    if not device_counts:
+        raise ValueError("device_counts must list at least one count")
+    rows = []
+    for n in device_counts:
+        _, row = train_distributed(pairs, spec, config, devices=n)
+        rows.append(row)
+    base = rows[0]["samples_per_s"]
+    for row in rows:
+        row["speedup"] = round(row["samples_per_s"] / base, 3) if base > 0 else 1.0
+    return rows
+
+
+def table_csv(rows: list) -> str:
+    lines = [",".join(TABLE_COLUMNS)]
+    for row in rows:
+        lines.append(",".join(str(row[c]) for c in TABLE_COLUMNS))
+    return "\n".join(lines) + "\n"
