@@ -88,10 +88,31 @@ def load():
     return _lib
 
 
+class _Counter:
+    """Launch accounting: every ice_* entry point enqueues exactly one kernel.  When
+    `events` is a list, each call is bracketed by CUDA events on the current stream
+    (bench.py's per-kernel breakdown); otherwise only the count is kept."""
+    launches = 0
+    events = None
+
+
+counter = _Counter()
+
+
 def call(name: str, *args) -> None:
+    ev = counter.events
+    if ev is not None:
+        import torch
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
     rc = getattr(load(), name)(*args)
     if rc != ICE_OK:
         raise NativeError(name, rc)
+    counter.launches += 1
+    if ev is not None:
+        e1.record()
+        ev.append((name, args, e0, e1))
 
 
 def ptr(t) -> int:

@@ -114,6 +114,22 @@ class GradBucketer:
         torch.cuda.current_stream().wait_stream(self.stream)
 
 
+def device_step(model, optimizer, x, y, union_count: int, bucketer=None) -> None:
+    """One data-parallel step with everything already on the device and no host sync:
+    forward, fused CE head, backward (bucketed gradient all-reduce overlapped when a
+    bucketer is given), fused Adam.  x: u8 NHWC [n, S, S, 3], y: u8 [n, S, S].
+    The step's loss sum / hit count accumulate in model.engine.stats."""
+    engine = model.engine
+    step = optimizer.step_count + 1
+    S = x.shape[1]
+    A = engine.forward(x, train=model.training, seed=step)
+    dz = engine.head(A, y, train=True, grad_scale=1.0 / (union_count * S * S))
+    engine.backward(A, dz, on_layer_done=bucketer.on_layer_done if bucketer else None)
+    if bucketer:
+        bucketer.finish()
+    optimizer.step()
+
+
 def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
     """One collective training step (train.py:85-120).  ``shards[i]`` is replica i's
     ``(x, y)`` slice of the union batch (may be empty).  Under torch.distributed each rank
