@@ -90,6 +90,21 @@ struct FpropProb {
         else tc::tma_load_4d(sa, &xb, bar, c - c1, w0 + tp.dx[t], h0 + tp.dy[t], n0);
         tc::tma_load_3d(sb, &wm, bar, c, tp.wt[t], nt * BN);
     }
+    // ---- row-halo path (3x3, W % 128 == 0): one 3 x 130-pixel slab per 64-channel chunk
+    __device__ int halo_chunks() const { return (c1 + c2) / BK; }
+    __device__ void load_halo(int chunk, uint8_t *dst, uint64_t *bar, int mt) const {
+        int n0, h0, w0;
+        pt.origin(mt, n0, h0, w0);
+        const int c = chunk * BK;
+        if (c < c1) tc::tma_load_4d(dst, &xa, bar, c, w0 - 1, h0 - 1, n0);
+        else tc::tma_load_4d(dst, &xb, bar, c - c1, w0 - 1, h0 - 1, n0);
+    }
+    template <int BN>
+    __device__ void load_tap_b(int tap, int chunk, uint8_t *dst, uint64_t *bar, int nt) const {
+        tc::tma_load_3d(dst, &wm, bar, chunk * BK, tap, nt * BN);
+    }
+    __device__ int view_row(int tap) const { return (taps[0].dy[tap] + 1) * 130 + taps[0].dx[tap] + 1; }
+
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z) const {
         int n0, h0, w0, n, h, w;
@@ -164,6 +179,20 @@ struct DgradProb {
 #pragma unroll
         for (int j = 0; j < BN / 64; ++j) tc::tma_load_3d(sb + j * 8192, &wm, bar, nt * BN + j * 64, taps.wt[t], c);
     }
+    // ---- row-halo path: slab of dY around the tile; tap t reads dY[p - shift_t]
+    __device__ int halo_chunks() const { return cout / BK; }
+    __device__ void load_halo(int chunk, uint8_t *dst, uint64_t *bar, int mt) const {
+        int n0, h0, w0;
+        pt.origin(mt, n0, h0, w0);
+        tc::tma_load_4d(dst, &dym, bar, chunk * BK, w0 - 1, h0 - 1, n0);
+    }
+    template <int BN>
+    __device__ void load_tap_b(int tap, int chunk, uint8_t *dst, uint64_t *bar, int nt) const {
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j) tc::tma_load_3d(dst + j * 8192, &wm, bar, nt * BN + j * 64, tap, chunk * BK);
+    }
+    __device__ int view_row(int tap) const { return (1 - taps.dy[tap]) * 130 + 1 - taps.dx[tap]; }
+
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int) const {
         int n0, h0, w0, n, h, w;
@@ -240,6 +269,7 @@ struct WgradProb {
     int N, H, W, c1, c2, cout;
     int total_kb, kb_per_split;
     int halve;  // 2x2 halving conv: dY = 4 sub-pixel planes (5-D map), K runs over (class, pixel block)
+    int trans;  // narrow cout (< 128): D = [(tap, cin)][cout], A = shifted x, B = dY (no wasted M rows)
     float *dw;  // [cout][taps][c1+c2]
 
     __device__ void kb_range(int z, int &kb0, int &nkb) const {
@@ -251,6 +281,25 @@ struct WgradProb {
         tc::tma_prefetch_desc(&xa);
         if (c2) tc::tma_prefetch_desc(&xb);
     }
+    // one 64-channel x 64-pixel box of x for the 64-wide (tap, cin) block starting at col
+    __device__ __forceinline__ void load_x(uint8_t *dst, uint64_t *bar, int col, int cls, int n0, int h0,
+                                           int w0) const {
+        const int ct = c1 + c2;
+        int t = col / ct, c = col - t * ct;
+        if (t >= taps.n) t = 0, c = 0;  // padding rows of the last M tile: any valid box, never stored
+        int sy = taps.dy[t], sx = taps.dx[t];
+        if (halve) {  // output (2p + cy, 2q + cx) reads up[2p + cy + a][2q + cx + b] = x[p + (cy + a) / 2][...]
+            sy = ((cls >> 1) + (t >> 1)) >> 1;
+            sx = ((cls & 1) + (t & 1)) >> 1;
+        }
+        if (c < c1) tc::tma_load_4d(dst, &xa, bar, c, w0 + sx, h0 + sy, n0);
+        else tc::tma_load_4d(dst, &xb, bar, c - c1, w0 + sx, h0 + sy, n0);
+    }
+    __device__ __forceinline__ void load_dy(uint8_t *dst, uint64_t *bar, int c0, int cls, int n0, int h0,
+                                            int w0) const {
+        if (halve) tc::tma_load_5d(dst, &dym, bar, c0, w0, h0, n0, cls);
+        else tc::tma_load_4d(dst, &dym, bar, c0, w0, h0, n0);
+    }
     template <int BN>
     __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
         int n0, h0, w0, cls = 0;
@@ -260,25 +309,16 @@ struct WgradProb {
             kb -= cls * nblk;
         }
         pk.origin(kb, n0, h0, w0);
-        if (halve) {
-            tc::tma_load_5d(sa, &dym, bar, mt * BM, w0, h0, n0, cls);
-            tc::tma_load_5d(sa + 8192, &dym, bar, mt * BM + 64, w0, h0, n0, cls);
-        } else {
-            tc::tma_load_4d(sa, &dym, bar, mt * BM, w0, h0, n0);
-            tc::tma_load_4d(sa + 8192, &dym, bar, mt * BM + 64, w0, h0, n0);
-        }
-        const int ct = c1 + c2;
+        if (!trans) {
+            load_dy(sa, bar, mt * BM, cls, n0, h0, w0);
+            load_dy(sa + 8192, bar, mt * BM + 64, cls, n0, h0, w0);
 #pragma unroll
-        for (int j = 0; j < BN / 64; ++j) {
-            const int col = nt * BN + j * 64;
-            const int t = col / ct, c = col - t * ct;
-            int sy = taps.dy[t], sx = taps.dx[t];
-            if (halve) {  // output (2p + cy, 2q + cx) reads up[2p + cy + a][2q + cx + b] = x[p + (cy + a) / 2][...]
-                sy = ((cls >> 1) + (t >> 1)) >> 1;
-                sx = ((cls & 1) + (t & 1)) >> 1;
-            }
-            if (c < c1) tc::tma_load_4d(sb + j * 8192, &xa, bar, c, w0 + sx, h0 + sy, n0);
-            else tc::tma_load_4d(sb + j * 8192, &xb, bar, c - c1, w0 + sx, h0 + sy, n0);
+            for (int j = 0; j < BN / 64; ++j) load_x(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
+        } else {
+            load_x(sa, bar, mt * BM, cls, n0, h0, w0);
+            load_x(sa + 8192, bar, mt * BM + 64, cls, n0, h0, w0);
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) load_dy(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
         }
     }
     template <int BN>
@@ -289,10 +329,18 @@ struct WgradProb {
         for (int cc = 0; cc < BN / 32; ++cc) {
             float v[32];
             tc::tmem_ld32(tmem + cc * 32, v);
-            if (m >= cout) continue;
-            float *dst = dw + (size_t)m * ld + nt * BN + cc * 32;
+            if (!trans) {
+                if (m >= cout) continue;
+                float *dst = dw + (size_t)m * ld + nt * BN + cc * 32;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) tc::red_add_v4(dst + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                for (int q = 0; q < 8; ++q) tc::red_add_v4(dst + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            } else {
+                if (m >= ld) continue;
+                const int o0 = nt * BN + cc * 32;  // output channels; lanes hold consecutive (tap, cin)
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (o0 + j < cout) atomicAdd(dw + (size_t)(o0 + j) * ld + m, v[j]);
+            }
         }
     }
 };
@@ -300,11 +348,27 @@ struct WgradProb {
 // ------------------------------------------------------------------------------------
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
-    return 1024 + STAGES * (A_BYTES + BN * BK * 2) + (2 * STAGES + 1) * 8 + 16;
+    return 1024 + STAGES * (A_BYTES + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16;
 }
 
+struct TileGrid {  // persistent schedule: tile t -> (m fastest, then n, then split z)
+    int tm, tn, tz;
+    __device__ __forceinline__ int count() const { return tm * tn * tz; }
+    __device__ __forceinline__ void coords(int t, int &mt, int &nt, int &z) const {
+        mt = t % tm;
+        t /= tm;
+        nt = t % tn;
+        z = t / tn;
+    }
+};
+
+// Persistent, warp-specialised tcgen05 GEMM.  One CTA per SM walks the tile list; the
+// TMA producer streams K-blocks through a STAGES-deep smem ring across tile boundaries,
+// the MMA thread accumulates each tile into one of two TMEM accumulators (2 x BN fp32
+// columns), and the 4 epilogue warps drain the other accumulator concurrently, so TMA,
+// tensor cores and the epilogue all overlap.
 template <int BN, int STAGES, class P>
-__global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__ P p) {
+__global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__ P p, const TileGrid g) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int B_BYTES = BN * BK * 2;
@@ -312,46 +376,63 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
     uint8_t *sb = base + STAGES * A_BYTES;
     uint64_t *full = reinterpret_cast<uint64_t *>(sb + STAGES * B_BYTES);
     uint64_t *empty = full + STAGES;
-    uint64_t *tfull = empty + STAGES;
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(tfull + 1);
+    uint64_t *tfull = empty + STAGES;  // [2]
+    uint64_t *tempty = tfull + 2;      // [2]
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int mt = blockIdx.x, nt = blockIdx.y;
-    int kb0, nkb;
-    p.kb_range(blockIdx.z, kb0, nkb);
+    const int ntiles = g.count();
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 1);
         }
-        tc::mbar_init(tfull, 1);
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(&tfull[a], 1);
+            tc::mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+        }
         tc::fence_barrier_init();
     }
     if (warp == 0 && lane == 0) p.prefetch();
-    if (warp == 1) tc::tmem_alloc<BN>(tslot);
+    if (warp == 1) tc::tmem_alloc<2 * BN>(tslot);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tslot;
 
-    if (nkb > 0) {
-        if (warp == 0) {
-            if (lane == 0) {
-                for (int i = 0; i < nkb; ++i) {
-                    const int s = i % STAGES;
-                    const uint32_t ph = (i / STAGES) & 1;
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int mt, nt, z, kb0, nkb;
+                g.coords(t, mt, nt, z);
+                p.kb_range(z, kb0, nkb);
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
                     tc::mbar_wait(&empty[s], ph ^ 1);
                     tc::mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-                    p.template load<BN>(kb0 + i, sa + s * A_BYTES, sb + s * B_BYTES, &full[s], mt, nt, blockIdx.z);
+                    p.template load<BN>(kb0 + i, sa + s * A_BYTES, sb + s * B_BYTES, &full[s], mt, nt, z);
                 }
             }
-        } else if (warp == 1) {
-            if (lane == 0) {
-                constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, P::A_MN, P::B_MN);
-                for (int i = 0; i < nkb; ++i) {
-                    const int s = i % STAGES;
-                    const uint32_t ph = (i / STAGES) & 1;
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, P::A_MN, P::B_MN);
+            int it = 0, local = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+                int mt, nt, z, kb0, nkb;
+                g.coords(t, mt, nt, z);
+                p.kb_range(z, kb0, nkb);
+                const int acc = local & 1;
+                const uint32_t aph = (local >> 1) & 1;
+                tc::mbar_wait(&tempty[acc], aph ^ 1);  // epilogue has drained this accumulator
+                tc::tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
                     tc::mbar_wait(&full[s], ph);
                     tc::tc_fence_after();
                     const uint32_t a0 = tc::smem_u32(sa + s * A_BYTES);
@@ -362,23 +443,207 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
                                                     : tc::sw128_desc(a0 + k * 32, 16, 1024);
                         const uint64_t bd = P::B_MN ? tc::sw128_desc(b0 + k * 2048, 8192, 1024)
                                                     : tc::sw128_desc(b0 + k * 32, 16, 1024);
-                        tc::umma_f16(tmem, ad, bd, idesc, (i | k) != 0 ? 1u : 0u);
+                        tc::umma_f16(d, ad, bd, idesc, (i | k) != 0 ? 1u : 0u);
                     }
                     tc::umma_commit(&empty[s]);
                 }
-                tc::umma_commit(tfull);
+                tc::umma_commit(&tfull[acc]);
             }
-            __syncwarp();
-        } else {
-            tc::mbar_wait(tfull, 0);
+        }
+        __syncwarp();
+    } else {
+        const int sub = warp & 3;
+        int local = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+            int mt, nt, z;
+            g.coords(t, mt, nt, z);
+            const int acc = local & 1;
+            tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
             tc::tc_fence_after();
-            const int sub = warp & 3;
-            p.template epilogue<BN>(tmem + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, blockIdx.z);
+            p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z);
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_dealloc<BN>(tmem);
+    if (warp == 1) tc::tmem_dealloc<2 * BN>(tmem);
+}
+
+// Row-halo variant for 3x3 convs on wide images (W % 128 == 0; U-Net levels 0-1, where
+// the channel count is 64-128 and a per-tap TMA box per K-block would make the tile
+// latency/L2-bound).  An M tile is 128 consecutive pixels of one image row; per 64-channel
+// chunk the producer loads ONE 3 x 130-pixel halo slab (49,920 B, zero-filled outside the
+// image) and the 9 taps read their A operands as 128-row windows of that slab starting at
+// row (dy+1)*130 + (dx+1) -- the SW128 swizzle is address-based, so an unaligned window
+// start needs no descriptor base offset (probed on B200).  Weights stream through their own
+// BSTAGES-deep ring, one (tap, chunk) slab per stage.
+constexpr int HALO_ROWS = 3 * 130;
+constexpr int HALO_TX = HALO_ROWS * 128;        // bytes a halo load delivers
+constexpr int HALO_BYTES = (HALO_TX + 1023) / 1024 * 1024;
+
+constexpr int TAPS_PER_SLOT = 3;  // one kernel row per weight stage: 12 MMAs per barrier wait
+
+template <int BN, int BSTAGES, bool RES>
+constexpr int halo_smem_bytes() {
+    return 1024 + 2 * HALO_BYTES + (RES ? 9 : BSTAGES * TAPS_PER_SLOT) * BN * BK * 2 + (2 * 2 + 2 * BSTAGES + 6) * 8 +
+           16;
+}
+
+// RES (resident weights): single-chunk problems (64 input channels) keep all 9 weight taps
+// of the current column tile in smem; they are reloaded only when the persistent CTA moves
+// to another column tile, so the MMA thread waits once per tile (36 MMAs per wait).
+template <int BN, int BSTAGES, bool RES, class P>
+__global__ void __launch_bounds__(NTHREADS, 1) halo_gemm(const __grid_constant__ P p, const TileGrid g) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int B_TAP = BN * BK * 2;
+    constexpr int B_BYTES = RES ? 9 * B_TAP : TAPS_PER_SLOT * B_TAP;
+    constexpr int NBS = RES ? 1 : BSTAGES;
+    uint8_t *sa = base;                    // [2][HALO_BYTES]
+    uint8_t *sb = base + 2 * HALO_BYTES;   // [NBS][B_BYTES]
+    uint64_t *afull = reinterpret_cast<uint64_t *>(sb + NBS * B_BYTES);
+    uint64_t *aempty = afull + 2;
+    uint64_t *bfull = aempty + 2;
+    uint64_t *bempty = bfull + BSTAGES;
+    uint64_t *tfull = bempty + BSTAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = g.count();
+    const int nch = p.halo_chunks();
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&afull[s], 1);
+            tc::mbar_init(&aempty[s], 1);
+            tc::mbar_init(&tfull[s], 1);
+            tc::mbar_init(&tempty[s], 4);
+        }
+        for (int s = 0; s < BSTAGES; ++s) {
+            tc::mbar_init(&bfull[s], 1);
+            tc::mbar_init(&bempty[s], 1);
+        }
+        tc::fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) p.prefetch();
+    if (warp == 1) tc::tmem_alloc<2 * BN>(tslot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int ait = 0, bit = 0, cur_nt = -1, run = -1;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int mt, nt, z;
+                g.coords(t, mt, nt, z);
+                if (RES && nt != cur_nt) {  // (re)load the column tile's 9 weight taps
+                    if (run >= 0) tc::mbar_wait(&bempty[0], run & 1);
+                    ++run;
+                    cur_nt = nt;
+                    tc::mbar_expect_tx(&bfull[0], B_BYTES);
+                    for (int tap = 0; tap < 9; ++tap) p.template load_tap_b<BN>(tap, 0, sb + tap * B_TAP, &bfull[0], nt);
+                }
+                for (int ch = 0; ch < nch; ++ch, ++ait) {
+                    const int as = ait & 1;
+                    tc::mbar_wait(&aempty[as], ((ait >> 1) & 1) ^ 1);
+                    tc::mbar_expect_tx(&afull[as], HALO_TX);
+                    p.load_halo(ch, sa + as * HALO_BYTES, &afull[as], mt);
+                    if (RES) continue;
+                    for (int r = 0; r < 9 / TAPS_PER_SLOT; ++r, ++bit) {
+                        const int bs = bit % BSTAGES;
+                        tc::mbar_wait(&bempty[bs], ((bit / BSTAGES) & 1) ^ 1);
+                        tc::mbar_expect_tx(&bfull[bs], B_BYTES);
+                        for (int q = 0; q < TAPS_PER_SLOT; ++q)
+                            p.template load_tap_b<BN>(r * TAPS_PER_SLOT + q, ch, sb + bs * B_BYTES + q * B_TAP,
+                                                      &bfull[bs], nt);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, false, P::B_MN);
+            int ait = 0, bit = 0, local = 0, cur_nt = -1, run = -1;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+                int mt, nt, z;
+                g.coords(t, mt, nt, z);
+                if (RES && nt != cur_nt) {
+                    ++run;
+                    cur_nt = nt;
+                    tc::mbar_wait(&bfull[0], run & 1);
+                }
+                const int acc = local & 1;
+                tc::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+                tc::tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int ch = 0; ch < nch; ++ch, ++ait) {
+                    const int as = ait & 1;
+                    tc::mbar_wait(&afull[as], (ait >> 1) & 1);
+                    tc::tc_fence_after();
+                    const uint32_t abase = tc::smem_u32(sa + as * HALO_BYTES);
+                    for (int r = 0; r < 9 / TAPS_PER_SLOT; ++r) {
+                        int bs = 0;
+                        uint32_t bslot;
+                        if (RES) {
+                            bslot = tc::smem_u32(sb + r * TAPS_PER_SLOT * B_TAP);
+                        } else {
+                            bs = bit % BSTAGES;
+                            tc::mbar_wait(&bfull[bs], (bit / BSTAGES) & 1);
+                            tc::tc_fence_after();
+                            bslot = tc::smem_u32(sb + bs * B_BYTES);
+                        }
+#pragma unroll
+                        for (int q = 0; q < TAPS_PER_SLOT; ++q) {
+                            const int tap = r * TAPS_PER_SLOT + q;
+                            const uint32_t a0 = abase + p.view_row(tap) * 128;
+                            const uint32_t b0 = bslot + q * B_TAP;
+#pragma unroll
+                            for (int k = 0; k < BK / 16; ++k) {
+                                const uint64_t ad = tc::sw128_desc(a0 + k * 32, 16, 1024);
+                                const uint64_t bd = P::B_MN ? tc::sw128_desc(b0 + k * 2048, 8192, 1024)
+                                                            : tc::sw128_desc(b0 + k * 32, 16, 1024);
+                                tc::umma_f16(d, ad, bd, idesc, (ch | tap | k) != 0 ? 1u : 0u);
+                            }
+                        }
+                        if (!RES) {
+                            tc::umma_commit(&bempty[bs]);
+                            ++bit;
+                        }
+                    }
+                    tc::umma_commit(&aempty[as]);
+                }
+                tc::umma_commit(&tfull[acc]);
+                if (RES) {  // last tile of this column run: release the resident weights
+                    int nmt, nnt = -1, nz;
+                    if (t + (int)gridDim.x < ntiles) g.coords(t + gridDim.x, nmt, nnt, nz);
+                    if (nnt != nt) tc::umma_commit(&bempty[0]);
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        const int sub = warp & 3;
+        int local = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+            int mt, nt, z;
+            g.coords(t, mt, nt, z);
+            const int acc = local & 1;
+            tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
+            tc::tc_fence_after();
+            p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z);
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc<2 * BN>(tmem);
 }
 
 // ------------------------------------------------------------------------------------
@@ -404,6 +669,17 @@ bool map_act(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, const 
     cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
     cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
     cuuint32_t box[4] = {64, (cuuint32_t)pt.Wt, (cuuint32_t)pt.Ht, (cuuint32_t)pt.Nt};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(ptr), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// NHWC activation with the row-halo box (64 channels x 130 pixels x 3 rows x 1 image)
+bool map_halo(CUtensorMap *m, const void *ptr, int N, int H, int W, int C) {
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {64, 130, 3, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(ptr), dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -445,6 +721,16 @@ PixTile pix_tile(int N, int H, int W, int npx) {
     return t;
 }
 
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
 bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 
 Taps make_taps(int ksize) {
@@ -473,8 +759,43 @@ const int8_t HALVE_CLS[9] = {0, 1, 1, 2, 2, 3, 3, 3, 3};
 const int8_t HALVE_DY[9] = {0, 0, 0, 0, 1, 0, 0, 1, 1};
 const int8_t HALVE_DX[9] = {0, 0, 1, 0, 0, 0, 1, 0, 1};
 
+template <int BN, int BSTAGES, bool RES, class P>
+int launch_halo(const P &p, dim3 tiles, cudaStream_t st) {
+    constexpr int smem = halo_smem_bytes<BN, BSTAGES, RES>();
+    static_assert(smem <= 232448, "halo kernel smem");
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e =
+            cudaFuncSetAttribute(halo_gemm<BN, BSTAGES, RES, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return (int)e;
+        attr = true;
+    }
+    TileGrid g{(int)tiles.x, (int)tiles.y, (int)tiles.z};
+    const long long total = (long long)tiles.x * tiles.y * tiles.z;
+    const int grid = (int)(total < num_sms() ? total : num_sms());
+    halo_gemm<BN, BSTAGES, RES, P><<<grid, NTHREADS, smem, st>>>(p, g);
+    return (int)cudaGetLastError();
+}
+
+// halo-path dispatch: resident weights when one 64-channel chunk and BN = 64
+template <class P>
+int run_halo(const P &p, int nch, int ncols, dim3 tiles_m, cudaStream_t st) {
+    if (nch == 1) {
+        dim3 tiles(tiles_m.x, ncols / 64, 1);
+        return launch_halo<64, 1, true>(p, tiles, st);
+    }
+    if (ncols % 128 == 0) {
+        dim3 tiles(tiles_m.x, ncols / 128, 1);
+        return launch_halo<128, 2, false>(p, tiles, st);
+    }
+    dim3 tiles(tiles_m.x, ncols / 64, 1);
+    return launch_halo<64, 5, false>(p, tiles, st);
+}
+
+bool use_halo(int ksize, int w) { return ksize == 3 && w >= 128 && w % 128 == 0; }
+
 template <int BN, int STAGES, class P>
-int launch(const P &p, dim3 grid, cudaStream_t st) {
+int launch(const P &p, dim3 tiles, cudaStream_t st) {
     constexpr int smem = smem_bytes<BN, STAGES>();
     static bool attr = false;
     if (!attr) {
@@ -482,7 +803,10 @@ int launch(const P &p, dim3 grid, cudaStream_t st) {
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }
-    conv_gemm<BN, STAGES, P><<<grid, NTHREADS, smem, st>>>(p);
+    TileGrid g{(int)tiles.x, (int)tiles.y, (int)tiles.z};
+    const long long total = (long long)tiles.x * tiles.y * tiles.z;
+    const int grid = (int)(total < num_sms() ? total : num_sms());
+    conv_gemm<BN, STAGES, P><<<grid, NTHREADS, smem, st>>>(p, g);
     return (int)cudaGetLastError();
 }
 
@@ -498,6 +822,29 @@ int pick_bn(int ntot, long long m_tiles) {
 }
 
 bool shape_ok(int N, int H, int W) { return N > 0 && pow2(H) && pow2(W); }
+
+// Weight-gradient tiling.  cout >= 128: D = [cout][(tap, cin)] (M = cout); narrower layers
+// transpose the GEMM (M = (tap, cin), N = cout) so no TMEM lane holds a padding row.
+void wgrad_tiles(int ncols, int cout, int &trans, int &mtiles, int &ntiles, int &bn) {
+    trans = cout < BM;
+    if (!trans) {
+        mtiles = (cout + BM - 1) / BM;
+        bn = ncols % 256 == 0 ? 256 : (ncols % 128 == 0 ? 128 : 64);
+        ntiles = ncols / bn;
+    } else {
+        mtiles = (ncols + BM - 1) / BM;
+        bn = 64;  // cout is a multiple of 64 below 128
+        ntiles = cout / bn;
+    }
+}
+
+// K-blocks per split so that the persistent grid sees about two waves of tiles
+int split_k(int total_kb, long long tiles) {
+    int splits = (int)((2LL * num_sms() + tiles - 1) / tiles);
+    if (splits > total_kb) splits = total_kb;
+    if (splits < 1) splits = 1;
+    return (total_kb + splits - 1) / splits;
+}
 
 }  // namespace
 
@@ -515,13 +862,21 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
     p.omul = 1;
     p.N = n; p.H = h; p.W = w; p.c1 = c1; p.c2 = c2; p.cout = cout;
     p.bias = bias; p.drop = drop_scale; p.relu = relu; p.y = reinterpret_cast<bf16 *>(y);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (use_halo(ksize, w)) {
+        const int nch = (c1 + c2) / 64;
+        const int bn = (nch == 1 || cout % 128) ? 64 : 128;
+        if (!map_halo(&p.xa, x1, n, h, w, c1)) return ICE_EINVAL;
+        if (c2 && !map_halo(&p.xb, x2, n, h, w, c2)) return ICE_EINVAL;
+        if (!map_wgt(&p.wm, wgt, cout, 9, c1 + c2, bn)) return ICE_EINVAL;
+        return run_halo(p, nch, cout, dim3((unsigned)(p.pt.tw * p.pt.th * p.pt.tn)), st);
+    }
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     const int bn = pick_bn(cout, mtiles);
     if (!map_act(&p.xa, x1, n, h, w, c1, p.pt)) return ICE_EINVAL;
     if (c2 && !map_act(&p.xb, x2, n, h, w, c2, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wgt, cout, p.taps[0].n, c1 + c2, bn)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, cout / bn, 1);
-    cudaStream_t st = (cudaStream_t)stream;
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
     return launch<64, 8>(p, grid, st);
@@ -547,15 +902,20 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
     p.drop1 = drop_scale1; p.drop2 = drop_scale2;
     p.planes_out2 = dx2_planes;
     if (dx2_planes && ((h | w) & 1)) return ICE_EINVAL;
-    const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
+    cudaStream_t st = (cudaStream_t)stream;
     const int ct = c1 + c2;
+    if (use_halo(ksize, w)) {  // the epilogue picks dx1/dx2 (and the plane layout) per 32-column chunk
+        if (!map_halo(&p.dym, dy, n, h, w, cout)) return ICE_EINVAL;
+        if (!map_wgt(&p.wm, wgt, cout, 9, ct, 64)) return ICE_EINVAL;
+        return run_halo(p, cout / 64, ct, dim3((unsigned)(p.pt.tw * p.pt.th * p.pt.tn)), st);
+    }
+    const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     int bn = pick_bn(ct, mtiles);
     // a column tile must not straddle the dx1 / dx2 split
     while (bn > 64 && (c1 % bn)) bn >>= 1;
     if (!map_act(&p.dym, dy, n, h, w, cout, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wgt, cout, p.taps.n, ct, 64)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, ct / bn, 1);
-    cudaStream_t st = (cudaStream_t)stream;
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
     return launch<64, 8>(p, grid, st);
@@ -575,18 +935,11 @@ extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2
     p.N = n; p.H = h; p.W = w; p.c1 = c1; p.c2 = c2; p.cout = cout;
     p.dw = dw;
     const int ncols = p.taps.n * (c1 + c2);
-    const int mtiles = (cout + BM - 1) / BM;
-    int bn = 64;
-    if (ncols % 256 == 0) bn = 256;
-    else if (ncols % 128 == 0) bn = 128;
-    const int ntiles = ncols / bn;
+    int mtiles, ntiles, bn;
+    wgrad_tiles(ncols, cout, p.trans, mtiles, ntiles, bn);
     p.total_kb = p.pk.tw * p.pk.th * p.pk.tn;
-    const long long tiles = (long long)mtiles * ntiles;
-    int splits = (int)((2 * 148 + tiles - 1) / tiles);
-    if (splits > p.total_kb) splits = p.total_kb;
-    if (splits < 1) splits = 1;
-    p.kb_per_split = (p.total_kb + splits - 1) / splits;
-    splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
+    p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles);
+    const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
     if (!map_act(&p.dym, dy, n, h, w, cout, p.pk)) return ICE_EINVAL;
     if (!map_act(&p.xa, x1, n, h, w, c1, p.pk)) return ICE_EINVAL;
     if (c2 && !map_act(&p.xb, x2, n, h, w, c2, p.pk)) return ICE_EINVAL;
@@ -670,16 +1023,11 @@ extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_
     p.N = n; p.H = h; p.W = w; p.c1 = c; p.c2 = 0; p.cout = cout;
     p.dw = dw;
     const int ncols = 4 * c;
-    const int mtiles = (cout + BM - 1) / BM;
-    int bn = ncols % 256 == 0 ? 256 : (ncols % 128 == 0 ? 128 : 64);
-    const int ntiles = ncols / bn;
+    int mtiles, ntiles, bn;
+    wgrad_tiles(ncols, cout, p.trans, mtiles, ntiles, bn);
     p.total_kb = 4 * p.pk.tw * p.pk.th * p.pk.tn;
-    const long long tiles = (long long)mtiles * ntiles;
-    int splits = (int)((2 * 148 + tiles - 1) / tiles);
-    if (splits > p.total_kb) splits = p.total_kb;
-    if (splits < 1) splits = 1;
-    p.kb_per_split = (p.total_kb + splits - 1) / splits;
-    splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
+    p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles);
+    const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
     if (!map_planes(&p.dym, dy_planes, n, h, w, cout, p.pk)) return ICE_EINVAL;
     if (!map_act(&p.xa, x, n, h, w, c, p.pk)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);

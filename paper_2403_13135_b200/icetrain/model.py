@@ -309,19 +309,23 @@ class UNetEngine:
         return self.acts
 
     def _drop_masks(self, A: _Acts, seed: int, train: bool) -> None:
+        """Dropout2d scales for every DoubleConv output of this step, one launch."""
         A.drop = {}
         p = self.spec.dropout
         if not train or p == 0.0:
             return
-        st = _native.stream_handle()
         d = self.spec.depth
         blocks = [f"down.{i}" for i in range(d)] + ["bottleneck"] + [f"up.{j}" for j in range(d)]
-        for k, blk in enumerate(blocks):
-            c = self.by_name[blk + ".block.2"].cout_p
-            t = A.drop.get(blk)
-            t = torch.empty((A.B, c), dtype=torch.float32, device=self.device)
-            _native.call("ice_dropout_scale", A.B * c, float(p), (seed * 64 + k) & (2 ** 64 - 1), t.data_ptr(), st)
-            A.drop[blk] = t
+        widths = [self.by_name[blk + ".block.2"].cout_p for blk in blocks]
+        total = A.B * sum(widths)
+        if getattr(A, "drop_buf", None) is None or A.drop_buf.numel() != total:
+            A.drop_buf = torch.empty(total, dtype=torch.float32, device=self.device)
+        _native.call("ice_dropout_scale", total, float(p), seed & (2 ** 63 - 1), A.drop_buf.data_ptr(),
+                     _native.stream_handle())
+        off = 0
+        for blk, c in zip(blocks, widths):
+            A.drop[blk] = A.drop_buf[off: off + A.B * c].view(A.B, c)
+            off += A.B * c
 
     # ---- forward ------------------------------------------------------------------------
     def forward(self, images, train: bool, seed: int = 0, float_input: bool = False) -> _Acts:

@@ -41,6 +41,9 @@ SHAPES = [  # n, h, w, c1, c2, cout, ksize
     (4, 256, 256, 64, 0, 64, 3),
     (2, 16, 16, 64, 0, 64, 1),
     (33, 8, 8, 128, 128, 512, 3),
+    (2, 128, 128, 128, 0, 128, 3),   # row-halo path (W % 128 == 0)
+    (1, 4, 256, 64, 64, 64, 3),      # row-halo, concat input, 2 tiles per row
+    (3, 128, 128, 64, 0, 64, 3),
 ]
 
 
@@ -92,3 +95,48 @@ def test_wgrad(shape):
     wref = torch.zeros(cout, c1 + c2, k, k, device="cuda", requires_grad=True)
     F.conv2d(xin, wref, padding=k // 2).backward(nchw(dy))
     assert rel(dw.permute(0, 3, 1, 2), wref.grad) < 1e-3
+
+
+HALVE = [(2, 8, 8, 128, 64), (3, 4, 4, 256, 128), (2, 16, 16, 64, 64), (1, 2, 2, 512, 256)]
+
+
+def _halve_ref(x_nchw, w_oihw, b):
+    up = F.interpolate(x_nchw, scale_factor=2, mode="nearest")
+    return F.conv2d(F.pad(up, (0, 1, 0, 1)), w_oihw, b)
+
+
+def _planes(t):  # [n][2h][2w][c] -> [4][n][h][w][c], plane 2*(y&1)+(x&1)
+    return torch.stack([t[:, cy::2, cx::2, :] for cy in (0, 1) for cx in (0, 1)]).contiguous()
+
+
+@pytest.mark.parametrize("shape", HALVE, ids=str)
+def test_halve_fprop_dgrad_wgrad(shape):
+    """model.py:79-88,105,128: Upsample(x2, nearest) -> pad(0,1,0,1) -> Conv2d(k=2)."""
+    from paper_2403_13135_b200 import _native
+    n, h, w, c, cout = shape
+    torch.manual_seed(4)
+    x = rnd(n, h, w, c)
+    w32 = (torch.randn(cout, 2, 2, c, device="cuda") * 0.05)
+    wc = torch.empty(cout, 9, c, dtype=torch.bfloat16, device="cuda")
+    st = _native.stream_handle()
+    _native.call("ice_halve_prep", w32.data_ptr(), cout, c, wc.data_ptr(), st)
+    b = torch.randn(cout, device="cuda")
+    y = torch.empty(n, 2 * h, 2 * w, cout, dtype=torch.bfloat16, device="cuda")
+    _native.call("ice_halve_fprop", x.data_ptr(), c, n, h, w, wc.data_ptr(), b.data_ptr(), cout, y.data_ptr(), st)
+    w_oihw = w32.permute(0, 3, 1, 2).contiguous()
+    ref = _halve_ref(nchw(x), w_oihw, b)
+    assert rel(nchw(y), ref) < 1e-2
+    # backward
+    dy = rnd(n, 2 * h, 2 * w, cout)
+    ref_relu = torch.relu(rnd(n, h, w, c))
+    dx = torch.empty(n, h, w, c, dtype=torch.bfloat16, device="cuda")
+    dyp = _planes(dy)
+    _native.call("ice_halve_dgrad", dyp.data_ptr(), cout, n, h, w, wc.data_ptr(), c, dx.data_ptr(),
+                 ref_relu.data_ptr(), None, st)
+    dw = torch.zeros(cout, 2, 2, c, device="cuda")
+    _native.call("ice_halve_wgrad", x.data_ptr(), c, dyp.data_ptr(), cout, n, h, w, dw.data_ptr(), st)
+    xin = nchw(x).requires_grad_(True)
+    wref = w_oihw.clone().requires_grad_(True)
+    _halve_ref(xin, wref, b).backward(nchw(dy))
+    assert rel(nchw(dx), xin.grad * (nchw(ref_relu) > 0)) < 1e-2
+    assert rel(dw.permute(0, 3, 1, 2), wref.grad) < 1e-2
