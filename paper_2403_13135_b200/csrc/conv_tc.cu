@@ -838,12 +838,28 @@ void wgrad_tiles(int ncols, int cout, int &trans, int &mtiles, int &ntiles, int 
     }
 }
 
-// K-blocks per split so that the persistent grid sees about two waves of tiles
+// K-blocks per split.  The persistent grid runs ceil(units / SMs) rounds of equal-size
+// units (units = tiles * splits), so pick the split count whose last round is fullest
+// (>= 4 K-blocks per split); fewer splits (fewer fp32 atomics) win ties.
 int split_k(int total_kb, long long tiles) {
-    int splits = (int)((2LL * num_sms() + tiles - 1) / tiles);
-    if (splits > total_kb) splits = total_kb;
-    if (splits < 1) splits = 1;
-    return (total_kb + splits - 1) / splits;
+    const long long sms = num_sms();
+    int best = 1;
+    double best_eff = -1.0;
+    for (int s = 1; s <= total_kb; ++s) {
+        const int kps = (total_kb + s - 1) / s;
+        if ((total_kb + kps - 1) / kps != s) continue;  // not an exact split count
+        if (kps < 4 && s > 1) break;
+        const long long units = tiles * s;
+        const long long rounds = (units + sms - 1) / sms;
+        double eff = (double)units / (double)(rounds * sms);
+        eff *= (double)total_kb / ((double)kps * s);  // short last split
+        if (eff > best_eff + 1e-3) {
+            best_eff = eff;
+            best = s;
+        }
+        if (units > 8 * sms) break;
+    }
+    return (total_kb + best - 1) / best;
 }
 
 }  // namespace
