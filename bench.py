@@ -234,12 +234,16 @@ def main():
     from paper_2403_13135_b200.icetrain import Adam, UNet, UNetSpec, synchronized_step
     from paper_2403_13135_b200.icetrain.train import GradBucketer, device_step
 
+    # one GPU per rank; modulo the device count only matters for functional runs of
+    # several ranks on one GPU (ICE_DIST_BACKEND=gloo), NCCL needs distinct GPUs
+    local_rank %= max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("ICE_DIST_BACKEND", "nccl")
+        tdist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
         dist = tdist
     _native.require_cuda()
 
@@ -375,7 +379,7 @@ def main():
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-                "data": "synthetic (T-gray tiles generate_corpus(101, 4224, 0.3), labels by K1 on GPU)",
+                "data": f"synthetic (T-gray tiles generate_corpus(101, {args.corpus}, 0.3), labels by K1 on GPU)",
                 "config": {"workload": "paper U-Net (depth 5, base 64, dropout 0.1) train step on 4224 "
                                        "synthetic 256x256 tiles, batch 32/GPU, Adam",
                            "global_batch": union, "seq_len": None, "parallelism": f"dp{world}",

@@ -158,6 +158,20 @@ def readiness_order(spec: UNetSpec):
     return names
 
 
+def flat_layout(spec: UNetSpec):
+    """(layers, name -> Layer, numel): each layer's weight and bias slice of the flat
+    fp32/bf16 parameter buffers, in readiness order, 256-byte aligned (TMA needs 16 B)."""
+    layers, by_name = build_layers(spec)
+    off = 0
+    for name in readiness_order(spec):
+        L = by_name[name]
+        L.w_off = off
+        off += (L.w_numel + 63) // 64 * 64
+        L.b_off = off
+        off += (L.cout_p + 63) // 64 * 64
+    return layers, by_name, (off + 63) // 64 * 64
+
+
 def init_reference_params(spec: UNetSpec) -> "OrderedDict[str, torch.Tensor]":
     """nn.Conv2d default init drawn in the reference's construction order (model.py:91-109):
     under torch.manual_seed(s) this equals icetrain.model.UNet(spec).state_dict()."""
@@ -214,22 +228,13 @@ class UNetEngine:
         _native.require_cuda()
         self.spec = spec
         self.device = torch.device(device or "cuda")
-        self.layers, self.by_name = build_layers(spec)
-        off = 0
-        for name in readiness_order(spec):
-            L = self.by_name[name]
-            L.w_off = off  # 256-byte aligned slices (TMA needs 16 B; vector kernels like more)
-            off += (L.w_numel + 63) // 64 * 64
-            L.b_off = off
-            off += (L.cout_p + 63) // 64 * 64
-        off = (off + 63) // 64 * 64
-        self.numel = off
+        self.layers, self.by_name, self.numel = flat_layout(spec)
         f32 = dict(dtype=torch.float32, device=self.device)
-        self.params = torch.zeros(off, **f32)
-        self.grads = torch.zeros(off, **f32)
-        self.exp_avg = torch.zeros(off, **f32)
-        self.exp_avg_sq = torch.zeros(off, **f32)
-        self.wbf16 = torch.zeros(off, dtype=torch.bfloat16, device=self.device)
+        self.params = torch.zeros(self.numel, **f32)
+        self.grads = torch.zeros(self.numel, **f32)
+        self.exp_avg = torch.zeros(self.numel, **f32)
+        self.exp_avg_sq = torch.zeros(self.numel, **f32)
+        self.wbf16 = torch.zeros(self.numel, dtype=torch.bfloat16, device=self.device)
         self.halve_wc = {}
         for L in self.layers:
             if L.kind == "halve":

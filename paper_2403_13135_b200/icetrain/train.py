@@ -76,42 +76,56 @@ def _as_nhwc(x: torch.Tensor, device) -> tuple:
     return t.to(device, torch.float32, non_blocking=True).contiguous(), True
 
 
+def plan_buckets(spec, bucket_bytes: int = 64 << 20):
+    """Contiguous [start, stop) slices of the flat gradient buffer, in backward-readiness
+    order, each closed by the layer whose gradient completes it: [(start, stop, last)]."""
+    from .model import flat_layout, readiness_order
+    _, by_name, numel = flat_layout(spec)
+    names = readiness_order(spec)
+    buckets, start, limit = [], 0, bucket_bytes // 4
+    for k, name in enumerate(names):
+        L = by_name[name]
+        hi = L.b_off + L.cout_p
+        last = k == len(names) - 1
+        if hi - start >= limit or last:
+            buckets.append((start, numel if last else hi, name))
+            start = hi
+    return buckets
+
+
 class GradBucketer:
     """Bucketed SUM all-reduce of the flat gradient buffer, overlapped with backward.
 
     Buckets are contiguous slices of UNetEngine.grads (laid out in readiness order); when
-    backward reports a layer done, every bucket whose last layer is complete is launched on
-    a side stream after an event recorded on the compute stream.  `finish()` joins the side
-    stream back into the compute stream."""
+    backward reports a layer done, every bucket that layer completes is all-reduced -- on
+    CUDA from a side stream after an event recorded on the compute stream, so it overlaps
+    the rest of backward.  `finish()` joins the side stream back into the compute stream.
+    Works on CPU tensors too (gloo), synchronously."""
 
     def __init__(self, engine, bucket_bytes: int = 64 << 20, group=None):
-        from .model import readiness_order
         self.engine, self.group = engine, group
-        self.stream = torch.cuda.Stream(device=engine.device)
-        names = readiness_order(engine.spec)
-        self.buckets = []  # (start, stop, last layer name)
-        start = 0
-        limit = bucket_bytes // 4
-        for k, name in enumerate(names):
-            lo, hi = engine.layer_slice(name)
-            last = k == len(names) - 1
-            if hi - start >= limit or last:
-                self.buckets.append((start, engine.numel if last else hi, name))
-                start = hi
-        self.pending = []
+        self.cuda = engine.grads.is_cuda
+        self.stream = torch.cuda.Stream(device=engine.grads.device) if self.cuda else None
+        self.buckets = plan_buckets(engine.spec, bucket_bytes)
+        self.by_last = {}
+        for b in self.buckets:
+            self.by_last.setdefault(b[2], []).append(b)
 
     def on_layer_done(self, name: str) -> None:
         dist = _dist()
-        for start, stop, last in self.buckets:
-            if last == name:
-                ev = torch.cuda.Event()
-                ev.record(torch.cuda.current_stream())
-                with torch.cuda.stream(self.stream):
-                    self.stream.wait_event(ev)
-                    dist.all_reduce(self.engine.grads[start:stop], group=self.group)
+        for start, stop, _ in self.by_last.get(name, ()):
+            if not self.cuda:
+                dist.all_reduce(self.engine.grads[start:stop], group=self.group)
+                continue
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            with torch.cuda.stream(self.stream):
+                self.stream.wait_event(ev)
+                dist.all_reduce(self.engine.grads[start:stop], group=self.group)
 
     def finish(self) -> None:
-        torch.cuda.current_stream().wait_stream(self.stream)
+        if self.cuda:
+            torch.cuda.current_stream().wait_stream(self.stream)
 
 
 def device_step(model, optimizer, x, y, union_count: int, bucketer=None) -> None:
@@ -183,6 +197,13 @@ def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
     for opt in optimizers:
         opt.step()
     return mean_loss, total
+
+
+def rank_shards(union: torch.Tensor, n_replicas: int, rank: int, local: int) -> tuple:
+    """This process's replicas' slices of a union batch: torch.tensor_split of the union into
+    n_replicas pieces exactly as the reference (train.py:161-163), replicas numbered
+    rank-major (rank r owns pieces [r * local, (r + 1) * local))."""
+    return torch.tensor_split(union, n_replicas)[rank * local:(rank + 1) * local]
 
 
 def _validate_pairs(pairs: list, spec: UNetSpec) -> None:
@@ -259,9 +280,7 @@ def _fit(pairs: list, spec: UNetSpec, config: TrainConfig, replicas: int) -> tup
         span = config.batch_size * n_replicas
         loss_sum, seen = 0.0, 0
         for start in range(0, len(order), span):
-            union = order[start:start + span]
-            pieces = torch.tensor_split(union, n_replicas)
-            mine = pieces[rank * local:(rank + 1) * local]
+            mine = rank_shards(order[start:start + span], n_replicas, rank, local)
             shards = [(x_train[p.to(device)], y_train[p.to(device)]) for p in mine]
             loss, count = synchronized_step(models, optimizers, shards)
             loss_sum += loss * count
