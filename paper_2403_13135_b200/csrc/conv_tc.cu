@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "icelabel_b200.h"
@@ -270,6 +271,7 @@ struct WgradProb {
     int total_kb, kb_per_split;
     int halve;  // 2x2 halving conv: dY = 4 sub-pixel planes (5-D map), K runs over (class, pixel block)
     int trans;  // narrow cout (< 128): D = [(tap, cin)][cout], A = shifted x, B = dY (no wasted M rows)
+    int nbx, nby;  // non-halve: maps are 5-D (64, W, H, N, C/64) and one TMA box carries nb 64-ch blocks
     float *dw;  // [cout][taps][c1+c2]
 
     __device__ void kb_range(int z, int &kb0, int &nkb) const {
@@ -292,13 +294,19 @@ struct WgradProb {
             sy = ((cls >> 1) + (t >> 1)) >> 1;
             sx = ((cls & 1) + (t & 1)) >> 1;
         }
-        if (c < c1) tc::tma_load_4d(dst, &xa, bar, c, w0 + sx, h0 + sy, n0);
-        else tc::tma_load_4d(dst, &xb, bar, c - c1, w0 + sx, h0 + sy, n0);
+        if (nbx == 1) {
+            if (c < c1) tc::tma_load_4d(dst, &xa, bar, c, w0 + sx, h0 + sy, n0);
+            else tc::tma_load_4d(dst, &xb, bar, c - c1, w0 + sx, h0 + sy, n0);
+        } else {
+            if (c < c1) tc::tma_load_5d(dst, &xa, bar, 0, w0 + sx, h0 + sy, n0, c >> 6);
+            else tc::tma_load_5d(dst, &xb, bar, 0, w0 + sx, h0 + sy, n0, (c - c1) >> 6);
+        }
     }
     __device__ __forceinline__ void load_dy(uint8_t *dst, uint64_t *bar, int c0, int cls, int n0, int h0,
                                             int w0) const {
-        if (halve) tc::tma_load_5d(dst, &dym, bar, c0, w0, h0, n0, cls);
-        else tc::tma_load_4d(dst, &dym, bar, c0, w0, h0, n0);
+        const int img = halve ? cls * N + n0 : n0;  // sub-pixel planes [4][N] flatten to 4N images
+        if (nby == 1) tc::tma_load_4d(dst, &dym, bar, c0, w0, h0, img);
+        else tc::tma_load_5d(dst, &dym, bar, 0, w0, h0, img, c0 >> 6);
     }
     template <int BN>
     __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
@@ -309,16 +317,14 @@ struct WgradProb {
             kb -= cls * nblk;
         }
         pk.origin(kb, n0, h0, w0);
+        // one TMA box carries nb consecutive 64-channel blocks ([block][pixel][64 ch] in smem)
+        const int bx = nbx, by = nby;
         if (!trans) {
-            load_dy(sa, bar, mt * BM, cls, n0, h0, w0);
-            load_dy(sa + 8192, bar, mt * BM + 64, cls, n0, h0, w0);
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j) load_x(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
+            for (int j = 0; j < 2; j += by) load_dy(sa + j * 8192, bar, mt * BM + j * 64, cls, n0, h0, w0);
+            for (int j = 0; j < BN / 64; j += bx) load_x(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
         } else {
-            load_x(sa, bar, mt * BM, cls, n0, h0, w0);
-            load_x(sa + 8192, bar, mt * BM + 64, cls, n0, h0, w0);
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j) load_dy(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
+            for (int j = 0; j < 2; j += bx) load_x(sa + j * 8192, bar, mt * BM + j * 64, cls, n0, h0, w0);
+            for (int j = 0; j < BN / 64; j += by) load_dy(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
         }
     }
     template <int BN>
@@ -646,6 +652,163 @@ __global__ void __launch_bounds__(NTHREADS, 1) halo_gemm(const __grid_constant__
     if (warp == 1) tc::tmem_dealloc<2 * BN>(tmem);
 }
 
+// Row-halo weight gradient for 3x3 convs with narrow outputs (cout 64/128) on wide images
+// (W % 64 == 0, U-Net levels 0-1).  Transposed GEMM D[(tap, cin)][cout] = sum_p x[p+s_t] dY[p]:
+// a K-block is a 64-pixel row segment; per K-block the producer loads, for every 64-channel
+// chunk of x, ONE 3 x 66-pixel halo slab (zero-filled outside the image) plus the dY segment.
+// An M tile is a pair of (tap, chunk) windows of those slabs (MN-major, K = pixel rows): the
+// two 64-row blocks sit at arbitrary row offsets, expressed through the descriptor's LBO
+// (unaligned windows / LBO are legal, the swizzle is address-based -- probed on B200).  A CTA
+// owns a group of G M tiles (G x cout <= 512 TMEM columns) for a split of the pixels, so each
+// K-block feeds G x 4 MMAs from one barrier wait.
+struct HWgrad {
+    CUtensorMap xm[4];  // per 64-channel chunk: halo box (64, 66, 3, 1) on its source
+    CUtensorMap dym;    // dY: (64 ch x 64 px x cout/64 blocks)
+    int N, H, W, ct, cout, nchx;
+    int total_kb, kb_per_split, groups, G, total_mt;
+    float *dw;  // [cout][9][ct]
+};
+
+constexpr int HW_HALO_ROWS = 3 * 66;
+constexpr int HW_HALO_TX = HW_HALO_ROWS * 128;                  // 25,344 B
+constexpr int HW_HALO_BYTES = (HW_HALO_TX + 1023) / 1024 * 1024;  // 25,600 B
+
+template <int COUT, int NCH, int STAGES>
+constexpr int hw_stage_bytes() {
+    return NCH * HW_HALO_BYTES + (COUT / 64) * 8192;
+}
+template <int COUT, int NCH, int STAGES>
+constexpr int hw_smem_bytes() {
+    return 1024 + STAGES * hw_stage_bytes<COUT, NCH, STAGES>() + (2 * STAGES + 2) * 8 + 16;
+}
+
+__device__ __forceinline__ int hw_view_row(int tap) { return (tap / 3) * 66 + tap % 3; }
+
+template <int COUT, int NCH, int STAGES>
+__global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_constant__ HWgrad p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int STAGE = hw_stage_bytes<COUT, NCH, STAGES>();
+    constexpr int TX = NCH * HW_HALO_TX + (COUT / 64) * 8192;
+    constexpr int TCOLS = 512;
+    uint64_t *full = reinterpret_cast<uint64_t *>(base + STAGES * STAGE);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 1;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int units = p.groups * ((p.total_kb + p.kb_per_split - 1) / p.kb_per_split);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(tfull, 1);
+        tc::mbar_init(tempty, 4);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        for (int c = 0; c < NCH; ++c) tc::tma_prefetch_desc(&p.xm[c]);
+        tc::tma_prefetch_desc(&p.dym);
+    }
+    if (warp == 1) tc::tmem_alloc<TCOLS>(tslot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int segs = p.W / 64;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                const int split = u / p.groups;
+                const int kb0 = split * p.kb_per_split, kb1 = min(p.total_kb, kb0 + p.kb_per_split);
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    tc::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    tc::mbar_expect_tx(&full[s], TX);
+                    const int seg = kb % segs, row = kb / segs;
+                    const int h = row % p.H, n = row / p.H, w0 = seg * 64;
+                    uint8_t *st = base + s * STAGE;
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+                        tc::tma_load_4d(st + c * HW_HALO_BYTES, &p.xm[c], &full[s], 0, w0 - 1, h - 1, n);
+                    if (COUT == 64) tc::tma_load_4d(st + NCH * HW_HALO_BYTES, &p.dym, &full[s], 0, w0, h, n);
+                    else tc::tma_load_5d(st + NCH * HW_HALO_BYTES, &p.dym, &full[s], 0, w0, h, n, 0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16(BM, COUT, true, true);
+            int it = 0, local = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
+                const int grp = u % p.groups, split = u / p.groups;
+                const int kb0 = split * p.kb_per_split, kb1 = min(p.total_kb, kb0 + p.kb_per_split);
+                const int mt0 = grp * p.G, mt1 = min(p.total_mt, mt0 + p.G);
+                tc::mbar_wait(tempty, (local & 1) ^ 1);
+                tc::tc_fence_after();
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    tc::mbar_wait(&full[s], (it / STAGES) & 1);
+                    tc::tc_fence_after();
+                    const uint32_t st = tc::smem_u32(base + s * STAGE);
+                    const uint32_t bbase = st + NCH * HW_HALO_BYTES;
+                    for (int mt = mt0; mt < mt1; ++mt) {
+                        // blocks 2 mt, 2 mt + 1 of the (tap, chunk) list; a missing second block repeats the first
+                        const int b0 = 2 * mt, b1 = min(2 * mt + 1, 9 * NCH - 1);
+                        const uint32_t a0 = st + (b0 % NCH) * HW_HALO_BYTES + hw_view_row(b0 / NCH) * 128;
+                        const uint32_t a1 = st + (b1 % NCH) * HW_HALO_BYTES + hw_view_row(b1 / NCH) * 128;
+                        const uint32_t d = tmem + (mt - mt0) * COUT;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint64_t ad = tc::sw128_desc(a0 + k * 2048, a1 - a0, 1024);
+                            const uint64_t bd = tc::sw128_desc(bbase + k * 2048, 8192, 1024);
+                            tc::umma_f16(d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                        }
+                    }
+                    tc::umma_commit(&empty[s]);
+                }
+                tc::umma_commit(tfull);
+            }
+        }
+        __syncwarp();
+    } else {
+        const int sub = warp & 3;
+        const int r = sub * 32 + lane;  // TMEM lane = row of the M tile
+        const int ld = 9 * p.ct;
+        int local = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
+            const int grp = u % p.groups;
+            const int mt0 = grp * p.G, mt1 = min(p.total_mt, mt0 + p.G);
+            tc::mbar_wait(tfull, local & 1);
+            tc::tc_fence_after();
+            for (int mt = mt0; mt < mt1; ++mt) {
+                const int b = 2 * mt + (r >> 6);
+                const bool valid = b < 9 * NCH;
+                const int tap = b / NCH, c = (b % NCH) * 64 + (r & 63);
+                float *dst = p.dw + (size_t)tap * p.ct + c;
+#pragma unroll
+                for (int cc = 0; cc < COUT / 32; ++cc) {
+                    float v[32];
+                    tc::tmem_ld32(tmem + (mt - mt0) * COUT + cc * 32 + ((uint32_t)(sub * 32) << 16), v);
+                    if (!valid) continue;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) atomicAdd(dst + (size_t)(cc * 32 + j) * ld, v[j]);
+                }
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tempty);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc<TCOLS>(tmem);
+}
+
 // ------------------------------------------------------------------------------------
 // host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -673,6 +836,22 @@ bool map_act(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, const 
     return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(ptr), dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// NHWC activation as 5-D (64, W, H, N, C/64): box = 64 ch x pixel box x nb channel blocks, so
+// one TMA instruction lands nb MN-major 64-channel blocks back to back ([block][px][64] in smem)
+bool map_act_blocked(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, const PixTile &pt, int nb) {
+    cuuint64_t dims[5] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N, (cuuint64_t)(C / 64)};
+    cuuint64_t strides[4] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2, 128};
+    cuuint32_t box[5] = {64, (cuuint32_t)pt.Wt, (cuuint32_t)pt.Ht, (cuuint32_t)pt.Nt, (cuuint32_t)nb};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(ptr), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool map_act_nb(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, const PixTile &pt, int nb) {
+    return nb == 1 ? map_act(m, ptr, N, H, W, C, pt) : map_act_blocked(m, ptr, N, H, W, C, pt, nb);
 }
 
 // NHWC activation with the row-halo box (64 channels x 130 pixels x 3 rows x 1 image)
@@ -862,6 +1041,63 @@ int split_k(int total_kb, long long tiles) {
     return (total_kb + best - 1) / best;
 }
 
+
+bool map_halo64(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, int c0) {
+    // halo box (64 ch, 66 px, 3 rows, 1 image) starting at channel c0 of a C-channel NHWC tensor
+    const char *base = reinterpret_cast<const char *>(ptr) + (size_t)c0 * 2;
+    cuuint64_t dims[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {64, 66, 3, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<char *>(base), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int COUT, int NCH, int STAGES>
+int launch_hwgrad(HWgrad &p, cudaStream_t st) {
+    constexpr int smem = hw_smem_bytes<COUT, NCH, STAGES>();
+    static_assert(smem <= 232448, "hwgrad smem");
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(hwgrad_kernel<COUT, NCH, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem);
+        if (e != cudaSuccess) return (int)e;
+        attr = true;
+    }
+    p.total_mt = (9 * NCH + 1) / 2;
+    const int gmax = 512 / COUT;
+    p.groups = (p.total_mt + gmax - 1) / gmax;
+    p.G = (p.total_mt + p.groups - 1) / p.groups;
+    p.kb_per_split = split_k(p.total_kb, p.groups);
+    const long long units = (long long)p.groups * ((p.total_kb + p.kb_per_split - 1) / p.kb_per_split);
+    const int grid = (int)(units < num_sms() ? units : num_sms());
+    hwgrad_kernel<COUT, NCH, STAGES><<<grid, NTHREADS, smem, st>>>(p);
+    return (int)cudaGetLastError();
+}
+
+// halo weight-gradient path: 3x3, W % 64 == 0, cout in {64, 128}, cin / 64 in {1, 2}
+int try_hwgrad(const uint16_t *x1, int c1, const uint16_t *x2, int c2, const uint16_t *dy, int cout, int n, int h,
+               int w, float *dw, cudaStream_t st) {
+    const int nch = (c1 + c2) / 64;
+    if (w % 64 || w < 64 || (cout != 64 && cout != 128) || (nch != 1 && nch != 2)) return 1;
+    HWgrad p;
+    memset(&p, 0, sizeof p);
+    p.N = n; p.H = h; p.W = w; p.ct = c1 + c2; p.cout = cout; p.nchx = nch; p.dw = dw;
+    p.total_kb = n * h * (w / 64);
+    for (int c = 0; c < nch; ++c) {
+        const int cc = c * 64;
+        const bool ok = cc < c1 ? map_halo64(&p.xm[c], x1, n, h, w, c1, cc) : map_halo64(&p.xm[c], x2, n, h, w, c2, cc - c1);
+        if (!ok) return ICE_EINVAL;
+    }
+    PixTile seg{64, 1, 1, w / 64, h, n};
+    if (!map_act_nb(&p.dym, dy, n, h, w, cout, seg, cout / 64)) return ICE_EINVAL;
+    if (cout == 64 && nch == 1) return launch_hwgrad<64, 1, 6>(p, st);
+    if (cout == 64) return launch_hwgrad<64, 2, 3>(p, st);
+    if (nch == 1) return launch_hwgrad<128, 1, 5>(p, st);
+    return launch_hwgrad<128, 2, 3>(p, st);
+}
+
 }  // namespace
 
 extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2, int32_t n, int32_t h,
@@ -944,6 +1180,10 @@ extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2
     if (!x1 || !dy || !dw || c1 <= 0 || c1 % 64 || c2 < 0 || c2 % 64 || (c2 && !x2) || cout <= 0 || cout % 64 ||
         (ksize != 1 && ksize != 3) || !shape_ok(n, h, w))
         return ICE_EINVAL;
+    if (ksize == 3 && !getenv("ICE_NO_HALO_WGRAD")) {
+        const int rc = try_hwgrad(x1, c1, x2, c2, dy, cout, n, h, w, dw, (cudaStream_t)stream);
+        if (rc <= 0) return rc;  // 1 = not applicable
+    }
     WgradProb p;
     memset(&p, 0, sizeof p);
     p.pk = pix_tile(n, h, w, BK);
@@ -956,9 +1196,20 @@ extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2
     p.total_kb = p.pk.tw * p.pk.th * p.pk.tn;
     p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles);
     const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
-    if (!map_act(&p.dym, dy, n, h, w, cout, p.pk)) return ICE_EINVAL;
-    if (!map_act(&p.xa, x1, n, h, w, c1, p.pk)) return ICE_EINVAL;
-    if (c2 && !map_act(&p.xb, x2, n, h, w, c2, p.pk)) return ICE_EINVAL;
+    // channel blocks per TMA box: as many consecutive 64-blocks as the tile reads from one
+    // (tap, source) run; dY supplies 2 blocks (A, M = 128) or BN/64 (B, transposed)
+    {
+        const int want_x = p.trans ? 2 : bn / 64, want_y = p.trans ? bn / 64 : 2;
+        int nbx = want_x;
+        while (nbx > 1 && ((c1 % (64 * nbx)) || (c2 % (64 * nbx)))) nbx >>= 1;
+        int nby = want_y;
+        while (nby > 1 && (cout % (64 * nby))) nby >>= 1;
+        p.nbx = nbx;
+        p.nby = nby;
+    }
+    if (!map_act_nb(&p.dym, dy, n, h, w, cout, p.pk, p.nby)) return ICE_EINVAL;
+    if (!map_act_nb(&p.xa, x1, n, h, w, c1, p.pk, p.nbx)) return ICE_EINVAL;
+    if (c2 && !map_act_nb(&p.xb, x2, n, h, w, c2, p.pk, p.nbx)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
     cudaStream_t st = (cudaStream_t)stream;
     if (bn == 256) return launch<256, 4>(p, grid, st);
@@ -1044,8 +1295,17 @@ extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_
     p.total_kb = 4 * p.pk.tw * p.pk.th * p.pk.tn;
     p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles);
     const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
-    if (!map_planes(&p.dym, dy_planes, n, h, w, cout, p.pk)) return ICE_EINVAL;
-    if (!map_act(&p.xa, x, n, h, w, c, p.pk)) return ICE_EINVAL;
+    {
+        const int want_x = p.trans ? 2 : bn / 64, want_y = p.trans ? bn / 64 : 2;
+        int nbx = want_x;
+        while (nbx > 1 && (c % (64 * nbx))) nbx >>= 1;
+        int nby = want_y;
+        while (nby > 1 && (cout % (64 * nby))) nby >>= 1;
+        p.nbx = nbx;
+        p.nby = nby;
+    }
+    if (!map_act_nb(&p.dym, dy_planes, 4 * n, h, w, cout, p.pk, p.nby)) return ICE_EINVAL;
+    if (!map_act_nb(&p.xa, x, n, h, w, c, p.pk, p.nbx)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
     cudaStream_t st = (cudaStream_t)stream;
     if (bn == 256) return launch<256, 4>(p, grid, st);
