@@ -261,7 +261,9 @@ def main():
         dist.broadcast(model.engine.params, 0)
         model.engine.refresh_working_weights()
     opt = Adam(model.parameters(), lr=1e-3)
-    bucketer = GradBucketer(model.engine) if dist else None
+    # optimizer-in-backward: each gradient bucket is (all-reduced and) Adam-stepped on a side
+    # stream as soon as backward completes it
+    bucketer = GradBucketer(model.engine, bucket_bytes=(64 << 20) if dist else (16 << 20), optimizer=opt)
     union = BATCH * world
     gen = torch.Generator().manual_seed(1234)
 

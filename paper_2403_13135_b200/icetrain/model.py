@@ -294,8 +294,8 @@ class UNetEngine:
         _native.call("ice_cast_bf16", self.params.data_ptr(), self.numel, self.wbf16.data_ptr(), st)
         self.prep_halves()
 
-    def prep_halves(self) -> None:
-        st = _native.stream_handle()
+    def prep_halves(self, stream=None) -> None:
+        st = _native.stream_handle(stream)
         for name, wc in self.halve_wc.items():
             L = self.by_name[name]
             _native.call("ice_halve_prep", self.w(name).data_ptr(), L.cout_p, L.cin_p, wc.data_ptr(), st)
@@ -466,11 +466,17 @@ class UNetEngine:
 
     # ---- optimizer ------------------------------------------------------------------------
     def adam(self, step: int, lr: float, betas=(0.9, 0.999), eps: float = 1e-8) -> None:
-        st = _native.stream_handle()
-        _native.call("ice_adam", self.params.data_ptr(), self.grads.data_ptr(), self.exp_avg.data_ptr(),
-                     self.exp_avg_sq.data_ptr(), self.numel, int(step), float(lr), float(betas[0]), float(betas[1]),
-                     float(eps), self.wbf16.data_ptr(), st)
+        self.adam_slice(0, self.numel, step, lr, betas, eps)
         self.prep_halves()
+
+    def adam_slice(self, start: int, stop: int, step: int, lr: float, betas=(0.9, 0.999), eps: float = 1e-8,
+                   stream=None) -> None:
+        """Fused Adam on flat elements [start, stop) (a gradient bucket); 4-element aligned."""
+        st = _native.stream_handle(stream)
+        off4, off2 = start * 4, start * 2
+        _native.call("ice_adam", self.params.data_ptr() + off4, self.grads.data_ptr() + off4,
+                     self.exp_avg.data_ptr() + off4, self.exp_avg_sq.data_ptr() + off4, stop - start, int(step),
+                     float(lr), float(betas[0]), float(betas[1]), float(eps), self.wbf16.data_ptr() + off2, st)
 
     def zero_grad(self) -> None:
         _native.call("ice_fill_f32", self.grads.data_ptr(), self.numel, 0.0, _native.stream_handle())

@@ -21,6 +21,15 @@ class Adam:
         for e in self.engines:
             e.adam(self.step_count, self.lr, self.betas, self.eps)
 
+    # ---- optimizer-in-backward (used by train.StepOverlap): the step count advances once,
+    # then each gradient bucket is updated as soon as it is final, on a side stream
+    def begin_overlapped_step(self) -> int:
+        self.step_count += 1
+        return self.step_count
+
+    def step_slice(self, engine, start: int, stop: int, stream=None) -> None:
+        engine.adam_slice(start, stop, self.step_count, self.lr, self.betas, self.eps, stream)
+
     def zero_grad(self, set_to_none: bool = True) -> None:
         for e in self.engines:
             e.zero_grad()

@@ -94,22 +94,29 @@ def plan_buckets(spec, bucket_bytes: int = 64 << 20):
 
 
 class GradBucketer:
-    """Bucketed SUM all-reduce of the flat gradient buffer, overlapped with backward.
+    """Bucketed SUM all-reduce of the flat gradient buffer, overlapped with backward,
+    optionally fused with the optimizer (optimizer-in-backward).
 
     Buckets are contiguous slices of UNetEngine.grads (laid out in readiness order); when
-    backward reports a layer done, every bucket that layer completes is all-reduced -- on
-    CUDA from a side stream after an event recorded on the compute stream, so it overlaps
-    the rest of backward.  `finish()` joins the side stream back into the compute stream.
-    Works on CPU tensors too (gloo), synchronously."""
+    backward reports the layer that completes a bucket, the bucket is -- on a side stream,
+    after an event recorded on the compute stream -- all-reduced (under torch.distributed)
+    and, if an optimizer is attached, immediately stepped with the fused Adam kernel.  The
+    HBM-bound Adam pass and the NCCL transfers thereby overlap the tensor-bound remainder of
+    backward.  `finish()` re-derives the halving-conv weight slabs and joins the side stream
+    back into the compute stream.  Works on CPU tensors too (gloo, synchronously, no Adam)."""
 
-    def __init__(self, engine, bucket_bytes: int = 64 << 20, group=None):
-        self.engine, self.group = engine, group
+    def __init__(self, engine, bucket_bytes: int = 64 << 20, group=None, optimizer=None):
+        self.engine, self.group, self.optimizer = engine, group, optimizer
         self.cuda = engine.grads.is_cuda
         self.stream = torch.cuda.Stream(device=engine.grads.device) if self.cuda else None
         self.buckets = plan_buckets(engine.spec, bucket_bytes)
         self.by_last = {}
         for b in self.buckets:
             self.by_last.setdefault(b[2], []).append(b)
+
+    def begin(self) -> None:
+        if self.optimizer is not None:
+            self.optimizer.begin_overlapped_step()
 
     def on_layer_done(self, name: str) -> None:
         dist = _dist()
@@ -121,11 +128,17 @@ class GradBucketer:
             ev.record(torch.cuda.current_stream())
             with torch.cuda.stream(self.stream):
                 self.stream.wait_event(ev)
-                dist.all_reduce(self.engine.grads[start:stop], group=self.group)
+                if dist is not None and dist.get_world_size() > 1:
+                    dist.all_reduce(self.engine.grads[start:stop], group=self.group)
+                if self.optimizer is not None:
+                    self.optimizer.step_slice(self.engine, start, stop, self.stream)
 
     def finish(self) -> None:
-        if self.cuda:
-            torch.cuda.current_stream().wait_stream(self.stream)
+        if not self.cuda:
+            return
+        if self.optimizer is not None:
+            self.engine.prep_halves(self.stream)
+        torch.cuda.current_stream().wait_stream(self.stream)
 
 
 def device_step(model, optimizer, x, y, union_count: int, bucketer=None) -> None:
@@ -138,10 +151,14 @@ def device_step(model, optimizer, x, y, union_count: int, bucketer=None) -> None
     S = x.shape[1]
     A = engine.forward(x, train=model.training, seed=step)
     dz = engine.head(A, y, train=True, grad_scale=1.0 / (union_count * S * S))
+    fused = bucketer is not None and bucketer.optimizer is optimizer
+    if fused:
+        bucketer.begin()
     engine.backward(A, dz, on_layer_done=bucketer.on_layer_done if bucketer else None)
     if bucketer:
         bucketer.finish()
-    optimizer.step()
+    if not fused:
+        optimizer.step()
 
 
 def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
@@ -165,9 +182,17 @@ def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
     A = None
     seed = getattr(optimizers[0], "step_count", 0) + 1
     bucketer = None
-    if dist is not None and dist.get_world_size() > 1:
-        bucketer = getattr(engine, "_bucketer", None) or GradBucketer(engine)
-        engine._bucketer = bucketer
+    fused = len(models) == 1 and isinstance(optimizers[0], Adam)
+    if fused or (dist is not None and dist.get_world_size() > 1):
+        key = (id(optimizers[0]) if fused else None)
+        bucketer = getattr(engine, "_bucketer", None)
+        if bucketer is None or getattr(bucketer, "_key", None) != key:
+            bucketer = GradBucketer(engine, bucket_bytes=(64 << 20) if dist else (16 << 20),
+                                    optimizer=optimizers[0] if fused else None)
+            bucketer._key = key
+            engine._bucketer = bucketer
+        if fused:
+            bucketer.begin()
     live = [(k, s) for k, s in enumerate(shards) if counts[k] > 0]
     for idx, (k, (x, y)) in enumerate(live):
         xin, is_float = _as_nhwc(x, device)
@@ -192,10 +217,11 @@ def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
         dist.all_reduce(stats)
     S = models[0].spec.input_size if A.S is None else A.S
     mean_loss = float(stats[0].item()) / (total * S * S)
-    for m in models[1:]:
-        m.engine.grads.copy_(engine.grads)
-    for opt in optimizers:
-        opt.step()
+    if not fused:
+        for m in models[1:]:
+            m.engine.grads.copy_(engine.grads)
+        for opt in optimizers:
+            opt.step()
     return mean_loss, total
 
 
