@@ -199,42 +199,63 @@ __global__ void maxpool_bwd_kernel(const uint16_t *__restrict__ x, const uint16_
 }
 
 // ---- head: out 1x1 conv 64 -> 3 (model.py:109,130) + CrossEntropyLoss (train.py:89,96) --
-// Per pixel: logits, log-softmax loss, argmax hit; backward dlogits = (p - onehot) * scale,
-// dh = dlogits W, dz = dh * drop * [h > 0] (the ReLU/Dropout2d of up.4's output), and
-// block-reduced dW (3 x 64), db (3), loss sum, correct count.
+// One thread per pixel (64 bf16 channels = 8 x 16 B loads).  Forward: 3 logits, log-softmax
+// loss, argmax hit.  Backward: dlogits = (p - onehot) * scale; dz = (dlogits W) * drop *
+// [h > 0] (the ReLU/Dropout2d of up.{d-1}'s output); dW[k][c] = sum_p dlogits_k h_c via a
+// per-warp smem stage (lane l owns channels 2l, 2l+1 of all 32 staged pixels), db and
+// loss/hit counts via warp reductions; one atomic per lane per block at the end.  h is read
+// and dz written with coalesced 16 B accesses through the same per-warp stage.
 constexpr int HEAD_NT = 256;
 constexpr int HC = 64;
 
-__global__ void __launch_bounds__(HEAD_NT) head_ce_kernel(
+__global__ void __launch_bounds__(HEAD_NT, 2) head_ce_kernel(
     const uint16_t *__restrict__ hact, long long npx, int hw, const uint8_t *__restrict__ labels,
     const float *__restrict__ w_out, const float *__restrict__ b_out, const float *__restrict__ drop, float grad_scale,
     uint16_t *__restrict__ dz, float *__restrict__ dw, float *__restrict__ db, float *__restrict__ stats,
     float *__restrict__ logits_out) {
     __shared__ float sw[3 * HC];
-    __shared__ uint16_t sh[HEAD_NT][HC + 2];
-    __shared__ float sd[HEAD_NT][3];
+    __shared__ float sdrop[HC];
+    // per-warp staging of 32 pixels x 128 B (row pitch 144 B: conflict-free 16 B row reads)
+    __shared__ __align__(16) uint8_t stage[HEAD_NT / 32][32 * 144];
+    __shared__ float sdl[HEAD_NT / 32][32][4];  // per warp: dlogits of its 32 pixels
     for (int i = threadIdx.x; i < 3 * HC; i += HEAD_NT) sw[i] = w_out[i];
     __syncthreads();
+    const int lane = threadIdx.x & 31;
+    uint8_t *wst = stage[threadIdx.x >> 5];
+    long long cur_img = -1;
     const bool train = dw != nullptr;
-    float acc_w = 0.f;  // thread t < 192 owns dW[t / 64][t % 64]
-    float acc_b = 0.f, loss_sum = 0.f, correct = 0.f;
+    float accw[6] = {0, 0, 0, 0, 0, 0};
+    float accb0 = 0.f, accb1 = 0.f, accb2 = 0.f, loss_sum = 0.f, correct = 0.f;
     const float b0 = b_out[0], b1 = b_out[1], b2 = b_out[2];
-    for (long long base = (long long)blockIdx.x * HEAD_NT; base < npx; base += (long long)gridDim.x * HEAD_NT) {
+    const long long stride = (long long)gridDim.x * HEAD_NT;
+    for (long long base = (long long)blockIdx.x * HEAD_NT; base < npx; base += stride) {
         const long long p = base + threadIdx.x;
         const bool valid = p < npx;
-        float h[HC];
-        if (valid) {
-            const uint4 *src = reinterpret_cast<const uint4 *>(hact + p * HC);
+        if (train && drop && hw % HEAD_NT == 0 && base / hw != cur_img) {  // block-uniform
+            cur_img = base / hw;
+            __syncthreads();
+            if (threadIdx.x < HC) sdrop[threadIdx.x] = drop[cur_img * HC + threadIdx.x];
+            __syncthreads();
+        }
+        // coalesced load of the warp's 32 pixels (4 KB) into smem, then each lane reads its row
+        const long long p0 = base + (threadIdx.x & ~31);
+        {
+            const uint4 *src = reinterpret_cast<const uint4 *>(hact + p0 * HC);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                uint4 u = src[q];
-                const uint16_t *e = reinterpret_cast<const uint16_t *>(&u);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) h[q * 8 + j] = bf(e[j]);
+                const int idx = q * 32 + lane, px = idx >> 3, ch = idx & 7;
+                uint4 u = p0 + px < npx ? src[idx] : make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4 *>(wst + px * 144 + ch * 16) = u;
             }
-        } else {
+            __syncwarp();
+        }
+        float h[HC];
 #pragma unroll
-            for (int j = 0; j < HC; ++j) h[j] = 0.f;
+        for (int q = 0; q < 8; ++q) {
+            uint4 u = *reinterpret_cast<const uint4 *>(wst + lane * 144 + q * 16);
+            const uint16_t *e = reinterpret_cast<const uint16_t *>(&u);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) h[q * 8 + j] = bf(e[j]);
         }
         float l0 = b0, l1 = b1, l2 = b2;
 #pragma unroll
@@ -265,10 +286,34 @@ __global__ void __launch_bounds__(HEAD_NT) head_ce_kernel(
                 d2 = (e2 * inv - (y == 2)) * grad_scale;
             }
         }
-        if (!train) continue;
-        if (valid && dz) {
+        if (!train) {
+            __syncwarp();
+            continue;
+        }
+        // dW[k][c] over this warp's 32 pixels: lane l owns channels 2l, 2l+1 (6 entries); the
+        // pixels' h stay staged in smem, their dlogits go through a small per-warp table
+        {
+            float *dl = sdl[threadIdx.x >> 5][lane];
+            dl[0] = d0;
+            dl[1] = d1;
+            dl[2] = d2;
+            __syncwarp();
+#pragma unroll 4
+            for (int q = 0; q < 32; ++q) {
+                const uint32_t hv = *reinterpret_cast<const uint32_t *>(wst + q * 144 + lane * 4);
+                const float h0 = bf((uint16_t)(hv & 0xffffu)), h1 = bf((uint16_t)(hv >> 16));
+                const float4 dq = *reinterpret_cast<const float4 *>(sdl[threadIdx.x >> 5][q]);
+                accw[0] = fmaf(dq.x, h0, accw[0]);
+                accw[1] = fmaf(dq.x, h1, accw[1]);
+                accw[2] = fmaf(dq.y, h0, accw[2]);
+                accw[3] = fmaf(dq.y, h1, accw[3]);
+                accw[4] = fmaf(dq.z, h0, accw[4]);
+                accw[5] = fmaf(dq.z, h1, accw[5]);
+            }
+            __syncwarp();
+        }
+        if (dz) {
             const long long img = p / hw;
-            uint4 *dst = reinterpret_cast<uint4 *>(dz + p * HC);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 uint32_t pk[4];
@@ -279,42 +324,46 @@ __global__ void __launch_bounds__(HEAD_NT) head_ce_kernel(
                     for (int u = 0; u < 2; ++u) {
                         const int j = q * 8 + e * 2 + u;
                         float v = d0 * sw[j] + d1 * sw[HC + j] + d2 * sw[2 * HC + j];
-                        if (drop) v *= drop[img * HC + j];
+                        if (drop) v *= hw % HEAD_NT == 0 ? sdrop[j] : __ldg(drop + img * HC + j);
                         g[u] = h[j] > 0.f ? v : 0.f;
                     }
                     pk[e] = (uint32_t)to_bf(g[0]) | ((uint32_t)to_bf(g[1]) << 16);
                 }
-                dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                *reinterpret_cast<uint4 *>(wst + lane * 144 + q * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
-        }
-        __syncthreads();
+            __syncwarp();
+            uint4 *dst = reinterpret_cast<uint4 *>(dz + p0 * HC);
 #pragma unroll
-        for (int j = 0; j < HC; ++j) sh[threadIdx.x][j] = to_bf(h[j]);
-        sd[threadIdx.x][0] = d0;
-        sd[threadIdx.x][1] = d1;
-        sd[threadIdx.x][2] = d2;
-        __syncthreads();
-        if (threadIdx.x < 3 * HC) {
-            const int k = threadIdx.x / HC, j = threadIdx.x % HC;
-            float s = 0.f;
-            for (int r = 0; r < HEAD_NT; ++r) s = fmaf(sd[r][k], bf(sh[r][j]), s);
-            acc_w += s;
-        } else if (threadIdx.x < 3 * HC + 3) {
-            const int k = threadIdx.x - 3 * HC;
-            float s = 0.f;
-            for (int r = 0; r < HEAD_NT; ++r) s += sd[r][k];
-            acc_b += s;
+            for (int q = 0; q < 8; ++q) {
+                const int idx = q * 32 + lane, px = idx >> 3, ch = idx & 7;
+                if (p0 + px < npx) dst[idx] = *reinterpret_cast<const uint4 *>(wst + px * 144 + ch * 16);
+            }
+            __syncwarp();
         }
-    }
-    if (train) {
-        if (threadIdx.x < 3 * HC) atomicAdd(&dw[threadIdx.x], acc_w);
-        else if (threadIdx.x < 3 * HC + 3) atomicAdd(&db[threadIdx.x - 3 * HC], acc_b);
+        accb0 += d0;
+        accb1 += d1;
+        accb2 += d2;
     }
     for (int o = 16; o; o >>= 1) {
         loss_sum += __shfl_xor_sync(0xffffffffu, loss_sum, o);
         correct += __shfl_xor_sync(0xffffffffu, correct, o);
+        accb0 += __shfl_xor_sync(0xffffffffu, accb0, o);
+        accb1 += __shfl_xor_sync(0xffffffffu, accb1, o);
+        accb2 += __shfl_xor_sync(0xffffffffu, accb2, o);
     }
-    if ((threadIdx.x & 31) == 0 && stats) {
+    if (train) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            atomicAdd(&dw[k * HC + 2 * lane], accw[2 * k]);
+            atomicAdd(&dw[k * HC + 2 * lane + 1], accw[2 * k + 1]);
+        }
+        if (lane == 0) {
+            atomicAdd(&db[0], accb0);
+            atomicAdd(&db[1], accb1);
+            atomicAdd(&db[2], accb2);
+        }
+    }
+    if (lane == 0 && stats) {
         atomicAdd(&stats[0], loss_sum);
         atomicAdd(&stats[1], correct);
     }
