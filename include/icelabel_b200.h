@@ -100,13 +100,15 @@ int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c
  * i.e. the fused backward of "ReLU -> Dropout2d" for the tensor that fed the conv, plus an
  * optional second gradient contribution (the skip path).  Optional pointers may be NULL.
  * dx2_planes != 0 writes dx2 as four sub-pixel planes [4][n][h/2][w/2][c2] (plane
- * 2*(y&1)+(x&1)), the layout ice_halve_dgrad / ice_halve_wgrad consume. */
+ * 2*(y&1)+(x&1)), the layout ice_halve_dgrad / ice_halve_wgrad consume.
+ * dbias{1,2} (fp32 [c1] / [c2], may be NULL): += column sums of dx{1,2} -- the bias gradient
+ * of the layer whose pre-activation gradient dx_i is, fused into the epilogue. */
 int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32_t h, int32_t w,
                    int32_t ksize, const uint16_t *wgt, int32_t c1, int32_t c2,
                    uint16_t *dx1, const uint16_t *relu_ref1, const float *drop_scale1,
                    const uint16_t *add1, uint16_t *dx2, const uint16_t *relu_ref2,
                    const float *drop_scale2, const uint16_t *add2, int32_t dx2_planes,
-                   void *stream);
+                   float *dbias1, float *dbias2, void *stream);
 
 /* Weight gradient: dw[cout][ksize][ksize][c1 + c2] (fp32) += sum over pixels of
  * dy[p][cout] * x[p + tap][c].  dw must be zeroed by the caller before the first call. */
@@ -123,10 +125,11 @@ int ice_halve_fprop(const uint16_t *x, int32_t c, int32_t n, int32_t h, int32_t 
                     void *stream);
 
 /* Halving conv data gradient: dx[n][h][w][c] = (sum over sub-pixel classes and taps of
- * dy_planes[cls][n][h - dy][w - dx][cout] * wc^T) * drop_scale[n][c] * [relu_ref > 0]. */
+ * dy_planes[cls][n][h - dy][w - dx][cout] * wc^T) * drop_scale[n][c] * [relu_ref > 0];
+ * dbias (may be NULL) += column sums of dx (fused bias gradient). */
 int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t n, int32_t h, int32_t w,
                     const uint16_t *wc, int32_t c, uint16_t *dx, const uint16_t *relu_ref,
-                    const float *drop_scale, void *stream);
+                    const float *drop_scale, float *dbias, void *stream);
 
 /* Halving conv weight gradient: dw[cout][2][2][c] (fp32, caller-zeroed) +=
  * sum over classes/pixels of dy_planes[cls][p] (x) x[p + ((cy + a) / 2, (cx + b) / 2)]. */
@@ -158,20 +161,23 @@ int ice_maxpool_fwd(const uint16_t *x, int32_t n, int32_t h, int32_t w, int32_t 
 
 /* Fused backward of ReLU -> Dropout2d -> {skip, MaxPool2d} for a down block output x:
  * dz = (add + maxpool_backward(dpool)) * drop[n][c] * [x > 0]; add/drop may be NULL.
- * Ties route to the first maximum in window order, like torch's CPU max_pool2d. */
+ * Ties route to the first maximum in window order, like torch's CPU max_pool2d.
+ * dbias (fp32 [c], may be NULL) += sum of dz over pixels (fused bias gradient). */
 int ice_maxpool_bwd(const uint16_t *x, const uint16_t *dpool, const uint16_t *add,
                     const float *drop, int32_t n, int32_t h, int32_t w, int32_t c,
-                    uint16_t *dz, void *stream);
+                    uint16_t *dz, float *dbias, void *stream);
 
 /* Head (model.py:109,130 out = Conv2d(64, 3, 1)) + nn.CrossEntropyLoss (train.py:89,96).
  * h bf16 [npx][64] (hw pixels per image), labels u8 [npx], w_out fp32 [3][64], b_out [3].
  * Accumulates stats[0] += sum of per-pixel losses, stats[1] += argmax hits (if stats).
  * Training (dw, db non-NULL): dlogits = (softmax - onehot) * grad_scale; dw += dlogits^T h,
  * db += sum dlogits, and dz (if non-NULL) = (dlogits W) * drop[n][c] * [h > 0].
- * logits (optional) fp32 [npx][3]. */
+ * logits (optional) fp32 [npx][3]; dzbias (optional) fp32 [64] += sum of dz (the bias
+ * gradient of the conv that produced h). */
 int ice_head_ce(const uint16_t *h, int64_t npx, int32_t hw, const uint8_t *labels,
                 const float *w_out, const float *b_out, const float *drop, float grad_scale,
-                uint16_t *dz, float *dw, float *db, float *stats, float *logits, void *stream);
+                uint16_t *dz, float *dw, float *db, float *stats, float *logits, float *dzbias,
+                void *stream);
 
 /* Bias gradient: db[c] += sum_rows dz[row][c] (dz bf16 [rows][c], c % 8 == 0, c <= 2048). */
 int ice_bias_grad(const uint16_t *dz, int64_t rows, int32_t c, float *db, void *stream);

@@ -50,17 +50,17 @@ SIGNATURES = {
     "ice_rgb_to_hsv": [_V, _I64, _V, _V],
     "ice_conv_fprop": [_V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, _V, _I32, _I32, _V, _V, _V],
     "ice_conv_dgrad": [_V, _I32, _I32, _I32, _I32, _I32, _V, _I32, _I32, _V, _V, _V, _V, _V, _V, _V, _V, _I32,
-                       _V],
+                       _V, _V, _V],
     "ice_halve_fprop": [_V, _I32, _I32, _I32, _I32, _V, _V, _I32, _V, _V],
-    "ice_halve_dgrad": [_V, _I32, _I32, _I32, _I32, _V, _I32, _V, _V, _V, _V],
+    "ice_halve_dgrad": [_V, _I32, _I32, _I32, _I32, _V, _I32, _V, _V, _V, _V, _V],
     "ice_halve_wgrad": [_V, _I32, _V, _I32, _I32, _I32, _I32, _V, _V],
     "ice_stem_im2col": [_V, _I32, _I32, _I32, _V, _V],
     "ice_stem_im2col_f32": [_V, _I32, _I32, _I32, _V, _V],
     "ice_pad_weights": [_V, _I32, _I32, _V, _I32, _V],
     "ice_halve_prep": [_V, _I32, _I32, _V, _V],
     "ice_maxpool_fwd": [_V, _I32, _I32, _I32, _I32, _V, _V],
-    "ice_maxpool_bwd": [_V, _V, _V, _V, _I32, _I32, _I32, _I32, _V, _V],
-    "ice_head_ce": [_V, _I64, _I32, _V, _V, _V, _V, _F32, _V, _V, _V, _V, _V, _V],
+    "ice_maxpool_bwd": [_V, _V, _V, _V, _I32, _I32, _I32, _I32, _V, _V, _V],
+    "ice_head_ce": [_V, _I64, _I32, _V, _V, _V, _V, _F32, _V, _V, _V, _V, _V, _V, _V],
     "ice_bias_grad": [_V, _I64, _I32, _V, _V],
     "ice_dropout_scale": [_I32, _F32, ctypes.c_uint64, _V, _V],
     "ice_adam": [_V, _V, _V, _V, _I64, _I64, _F32, _F32, _F32, _F32, _V, _V],

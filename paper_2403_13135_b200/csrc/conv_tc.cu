@@ -32,7 +32,8 @@ using bf16 = __nv_bfloat16;
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = one 128-byte swizzle row
 constexpr int A_BYTES = BM * BK * 2;
-constexpr int NTHREADS = 192;
+constexpr int EPI_WARPS = 8;  // two warps per TMEM lane quarter, each draining half the columns
+constexpr int NTHREADS = 64 + 32 * EPI_WARPS;
 
 struct PixTile {  // a box of Wt x Ht x Nt pixels, and how many boxes tile (W, H, N)
     int Wt, Ht, Nt, tw, th, tn;
@@ -57,6 +58,22 @@ struct Taps {
     int n;
     int8_t dy[9], dx[9], plane[9], wt[9];  // pixel shift, source plane (5-D maps), weight tap
 };
+
+// Column sums of a warp's 32 rows x 32 columns (one row per lane): after 31 shuffles lane j
+// holds the sum of column j over the 32 rows.
+__device__ __forceinline__ float warp_col_sum32(float (&v)[32], int lane) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const bool hi = lane & o;
+            const float send = hi ? v[i] : v[i + o];
+            const float keep = hi ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0];
+}
 
 // ------------------------------------------------------------------------------------
 struct FpropProb {
@@ -107,7 +124,9 @@ struct FpropProb {
     __device__ int view_row(int tap) const { return (taps[0].dy[tap] + 1) * 130 + taps[0].dx[tap] + 1; }
 
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z) const {
+    __device__ void flush_bias(int, int, int, float *) const {}
+    template <int BN>
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *) const {
         int n0, h0, w0, n, h, w;
         pt.origin(mt, n0, h0, w0);
         pt.pixel(row, n0, h0, w0, n, h, w);
@@ -118,7 +137,7 @@ struct FpropProb {
             w = 2 * w + (z & 1);
         }
 #pragma unroll 1
-        for (int cc = 0; cc < BN / 32; ++cc) {
+        for (int cc = cc0; cc < cc1; ++cc) {
             float v[32];
             tc::tmem_ld32(tmem + cc * 32, v);
             if (!valid) continue;
@@ -160,6 +179,7 @@ struct DgradProb {
     bf16 *out1, *out2;
     const bf16 *ref1, *ref2, *add1, *add2;
     const float *drop1, *drop2;
+    float *db1, *db2;  // fused bias gradients of the layers whose pre-activation grads these are
 
     __device__ void kb_range(int, int &kb0, int &nkb) const {
         kb0 = 0;
@@ -194,8 +214,29 @@ struct DgradProb {
     }
     __device__ int view_row(int tap) const { return (1 - taps.dy[tap]) * 130 + 1 - taps.dx[tap]; }
 
+    // lane j of each epilogue warp keeps, per owned 32-column chunk, the running sum of
+    // column j over all rows it has stored for the current column tile
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int) const {
+    __device__ void flush_bias(int nt, int cc0, int cc1, float *bacc) const {
+        const int lane = threadIdx.x & 31;
+        constexpr int NCH = BN / 32, PER = (NCH + 1) / 2;
+#pragma unroll
+        for (int ci = 0; ci < PER; ++ci) {
+            const int cc = cc0 + ci;
+            if (cc < cc1) {
+                int col = nt * BN + cc * 32 + lane;
+                float *db = db1;
+                if (col >= c1) {
+                    col -= c1;
+                    db = db2;
+                }
+                if (db && bacc[ci] != 0.f) atomicAdd(db + col, bacc[ci]);
+            }
+            bacc[ci] = 0.f;
+        }
+    }
+    template <int BN>
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *bacc) const {
         int n0, h0, w0, n, h, w;
         pt.origin(mt, n0, h0, w0);
         pt.pixel(row, n0, h0, w0, n, h, w);
@@ -203,59 +244,74 @@ struct DgradProb {
         const size_t pix = ((size_t)n * H + h) * W + w;
         const size_t pix_planes =
             ((((size_t)((h & 1) * 2 + (w & 1)) * N + n) * (H >> 1) + (h >> 1)) * (W >> 1)) + (w >> 1);
-#pragma unroll 1
-        for (int cc = 0; cc < BN / 32; ++cc) {
+        const int lane = threadIdx.x & 31;
+        constexpr int NCH = BN / 32, PER = (NCH + 1) / 2;
+#pragma unroll
+        for (int ci = 0; ci < PER; ++ci) {  // compile-time index into bacc (no local memory)
+            const int cc = cc0 + ci;
+            if (cc >= cc1) break;
             float v[32];
             tc::tmem_ld32(tmem + cc * 32, v);
-            if (!valid) continue;
             int col = nt * BN + cc * 32;
             bf16 *out;
             const bf16 *ref, *add;
             const float *drop;
+            float *db;
             int cs;
             if (col < c1) {
-                out = out1; ref = ref1; add = add1; drop = drop1; cs = c1;
+                out = out1; ref = ref1; add = add1; drop = drop1; cs = c1; db = db1;
             } else {
                 col -= c1;
-                out = out2; ref = ref2; add = add2; drop = drop2; cs = c2;
+                out = out2; ref = ref2; add = add2; drop = drop2; cs = c2; db = db2;
             }
-            if (!out) continue;
+            if (!out) continue;  // warp-uniform
             const size_t off = ((out == out2 && planes_out2) ? pix_planes : pix) * cs + col;
-            float extra[32];
+            if (valid) {
+                if (add) {
+                    const uint4 *ap = reinterpret_cast<const uint4 *>(add + off);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) extra[j] = 0.f;
-            if (add) {
-                const uint4 *ap = reinterpret_cast<const uint4 *>(add + off);
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 u = ap[q];
+                        const bf16 *b = reinterpret_cast<const bf16 *>(&u);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) v[q * 8 + e] += __bfloat162float(b[e]);
+                    }
+                }
+                if (ref) {
+                    const uint4 *rp = reinterpret_cast<const uint4 *>(ref + off);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 u = rp[q];
+                        const bf16 *b = reinterpret_cast<const bf16 *>(&u);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            if (!(__bfloat162float(b[e]) > 0.f)) v[q * 8 + e] = 0.f;
+                    }
+                }
+                if (drop) {
+                    const float4 *dp = reinterpret_cast<const float4 *>(drop + (size_t)n * cs + col);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 d = __ldg(dp + q);
+                        v[4 * q] *= d.x;
+                        v[4 * q + 1] *= d.y;
+                        v[4 * q + 2] *= d.z;
+                        v[4 * q + 3] *= d.w;
+                    }
+                }
+                uint4 *dst = reinterpret_cast<uint4 *>(out + off);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    uint4 u = ap[q];
-                    const bf16 *b = reinterpret_cast<const bf16 *>(&u);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) extra[q * 8 + e] = __bfloat162float(b[e]);
+                    dst[q] = make_uint4(tc::pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), tc::pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
+                                        tc::pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), tc::pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
                 }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = 0.f;
             }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += extra[j];
-            if (ref) {
-                const uint4 *rp = reinterpret_cast<const uint4 *>(ref + off);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint4 u = rp[q];
-                    const bf16 *b = reinterpret_cast<const bf16 *>(&u);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        if (!(__bfloat162float(b[e]) > 0.f)) v[q * 8 + e] = 0.f;
-                }
-            }
-            if (drop) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] *= __ldg(drop + (size_t)n * cs + col + j);
-            }
-            uint4 *dst = reinterpret_cast<uint4 *>(out + off);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                dst[q] = make_uint4(tc::pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), tc::pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
-                                    tc::pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), tc::pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+            if (db) {  // warp-uniform: bias gradient = column sums of the (fp32) gradient
+
+                bacc[cc - cc0] += warp_col_sum32(v, lane);
             }
         }
     }
@@ -328,11 +384,13 @@ struct WgradProb {
         }
     }
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int) const {
+    __device__ void flush_bias(int, int, int, float *) const {}
+    template <int BN>
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *) const {
         const int m = mt * BM + row;
         const int ld = taps.n * (c1 + c2);
 #pragma unroll 1
-        for (int cc = 0; cc < BN / 32; ++cc) {
+        for (int cc = cc0; cc < cc1; ++cc) {
             float v[32];
             tc::tmem_ld32(tmem + cc * 32, v);
             if (!trans) {
@@ -396,7 +454,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(&tfull[a], 1);
-            tc::mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+            tc::mbar_init(&tempty[a], EPI_WARPS);  // one arrive per epilogue warp
         }
         tc::fence_barrier_init();
     }
@@ -458,19 +516,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
         }
         __syncwarp();
     } else {
-        const int sub = warp & 3;
+        const int sub = warp & 3, half = (warp - 2) >> 2;
+        constexpr int NCH = BN / 32, PER = (NCH + 1) / 2;
+        const int cc0 = half * PER, cc1 = min(NCH, (half + 1) * PER);
+        float bacc[4] = {0.f, 0.f, 0.f, 0.f};  // fused bias-gradient partial sums (DgradProb)
+        int cur_nt = -1;
         int local = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
             int mt, nt, z;
             g.coords(t, mt, nt, z);
+            if (nt != cur_nt) {
+                if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
+                cur_nt = nt;
+            }
             const int acc = local & 1;
             tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
             tc::tc_fence_after();
-            p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z);
+            p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z, cc0,
+                                    cc1, bacc);
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
+        if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -526,7 +594,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) halo_gemm(const __grid_constant__
             tc::mbar_init(&afull[s], 1);
             tc::mbar_init(&aempty[s], 1);
             tc::mbar_init(&tfull[s], 1);
-            tc::mbar_init(&tempty[s], 4);
+            tc::mbar_init(&tempty[s], EPI_WARPS);
         }
         for (int s = 0; s < BSTAGES; ++s) {
             tc::mbar_init(&bfull[s], 1);
@@ -633,19 +701,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) halo_gemm(const __grid_constant__
         }
         __syncwarp();
     } else {
-        const int sub = warp & 3;
+        const int sub = warp & 3, half = (warp - 2) >> 2;
+        constexpr int NCH = BN / 32, PER = (NCH + 1) / 2;
+        const int cc0 = half * PER, cc1 = min(NCH, (half + 1) * PER);
+        float bacc[4] = {0.f, 0.f, 0.f, 0.f};  // fused bias-gradient partial sums (DgradProb)
+        int cur_nt = -1;
         int local = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
             int mt, nt, z;
             g.coords(t, mt, nt, z);
+            if (nt != cur_nt) {
+                if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
+                cur_nt = nt;
+            }
             const int acc = local & 1;
             tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
             tc::tc_fence_after();
-            p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z);
+            p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z, cc0,
+                                    cc1, bacc);
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
+        if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -705,7 +783,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
             tc::mbar_init(&empty[s], 1);
         }
         tc::mbar_init(tfull, 1);
-        tc::mbar_init(tempty, 4);
+        tc::mbar_init(tempty, EPI_WARPS);
         tc::fence_barrier_init();
     }
     if (warp == 0 && lane == 0) {
@@ -776,8 +854,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
         }
         __syncwarp();
     } else {
-        const int sub = warp & 3;
+        const int sub = warp & 3, half = (warp - 2) >> 2;
         const int r = sub * 32 + lane;  // TMEM lane = row of the M tile
+        constexpr int NCC = COUT / 32, PER = (NCC + 1) / 2;
         const int ld = 9 * p.ct;
         int local = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
@@ -791,7 +870,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                 const int tap = b / NCH, c = (b % NCH) * 64 + (r & 63);
                 float *dst = p.dw + (size_t)tap * p.ct + c;
 #pragma unroll
-                for (int cc = 0; cc < COUT / 32; ++cc) {
+                for (int cc = half * PER; cc < min(NCC, (half + 1) * PER); ++cc) {
                     float v[32];
                     tc::tmem_ld32(tmem + (mt - mt0) * COUT + cc * 32 + ((uint32_t)(sub * 32) << 16), v);
                     if (!valid) continue;
@@ -1138,7 +1217,7 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
                               const uint16_t *wgt, int32_t c1, int32_t c2, uint16_t *dx1, const uint16_t *relu_ref1,
                               const float *drop_scale1, const uint16_t *add1, uint16_t *dx2,
                               const uint16_t *relu_ref2, const float *drop_scale2, const uint16_t *add2,
-                              int32_t dx2_planes, void *stream) {
+                              int32_t dx2_planes, float *dbias1, float *dbias2, void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!dy || !wgt || c1 <= 0 || c1 % 64 || c2 < 0 || c2 % 64 || cout <= 0 || cout % 64 ||
         (ksize != 1 && ksize != 3) || !shape_ok(n, h, w))
@@ -1152,6 +1231,7 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
     p.ref1 = reinterpret_cast<const bf16 *>(relu_ref1); p.ref2 = reinterpret_cast<const bf16 *>(relu_ref2);
     p.add1 = reinterpret_cast<const bf16 *>(add1); p.add2 = reinterpret_cast<const bf16 *>(add2);
     p.drop1 = drop_scale1; p.drop2 = drop_scale2;
+    p.db1 = dbias1; p.db2 = dbias2;
     p.planes_out2 = dx2_planes;
     if (dx2_planes && ((h | w) & 1)) return ICE_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1247,7 +1327,7 @@ extern "C" int ice_halve_fprop(const uint16_t *x, int32_t c, int32_t n, int32_t 
 
 extern "C" int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t n, int32_t h, int32_t w,
                                const uint16_t *wc, int32_t c, uint16_t *dx, const uint16_t *relu_ref,
-                               const float *drop_scale, void *stream) {
+                               const float *drop_scale, float *dbias, void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!dy_planes || !wc || !dx || c <= 0 || c % 64 || cout <= 0 || cout % 64 || !shape_ok(n, h, w))
         return ICE_EINVAL;
@@ -1266,6 +1346,7 @@ extern "C" int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t 
     p.out1 = reinterpret_cast<bf16 *>(dx);
     p.ref1 = reinterpret_cast<const bf16 *>(relu_ref);
     p.drop1 = drop_scale;
+    p.db1 = dbias;
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     const int bn = pick_bn(c, mtiles);
     if (!map_planes(&p.dym, dy_planes, n, h, w, cout, p.pt)) return ICE_EINVAL;

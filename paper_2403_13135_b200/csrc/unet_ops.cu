@@ -153,12 +153,16 @@ __global__ void maxpool_fwd_kernel(const uint16_t *__restrict__ x, int n, int h,
 
 // dz = (add + maxpool_backward(dpool)) * drop[n][c] * [x > 0]: the fused backward of
 // "ReLU -> Dropout2d -> {skip, MaxPool2d}" for a down block's output x (model.py:115-118).
+// The grid-stride is a multiple of c/8, so each thread always owns the same 8 channels and
+// keeps their bias-gradient partial sums (sum of dz) in registers.
 __global__ void maxpool_bwd_kernel(const uint16_t *__restrict__ x, const uint16_t *__restrict__ dpool,
                                    const uint16_t *__restrict__ add, const float *__restrict__ drop, int n, int h, int w,
-                                   int c, uint16_t *__restrict__ dz) {
+                                   int c, uint16_t *__restrict__ dz, float *__restrict__ dbias) {
     const int ho = h / 2, wo = w / 2, cv = c / 8;
     const long long total = (long long)n * ho * wo * cv;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    float bsum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long stride = (long long)gridDim.x * blockDim.x;  // multiple of cv (host)
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += stride) {
         const int cg = (int)(i % cv);
         long long p = i / cv;
         const int xo = (int)(p % wo);
@@ -190,11 +194,24 @@ __global__ void maxpool_bwd_kernel(const uint16_t *__restrict__ x, const uint16_
             for (int k = 0; k < 4; ++k) {
                 float d = bf(reinterpret_cast<const uint16_t *>(&av[k])[e]) + (k == arg ? bf(pg[e]) : 0.f);
                 d = v[k] > 0.f ? d * s : 0.f;
+                bsum[e] += d;
                 reinterpret_cast<uint16_t *>(&out[k])[e] = to_bf(d);
             }
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) reinterpret_cast<uint4 *>(dz)[idx[k]] = out[k];
+    }
+    if (dbias) {  // block reduction per channel (thread t owns channel group t % cv), then atomics
+        __shared__ float red[256 * 8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) red[threadIdx.x * 8 + e] = bsum[e];
+        __syncthreads();
+        for (int ch = threadIdx.x; ch < c; ch += blockDim.x) {
+            const int cg = ch >> 3, e = ch & 7;
+            float acc = 0.f;
+            for (int t = cg; t < (int)blockDim.x; t += cv) acc += red[t * 8 + e];
+            if (acc != 0.f) atomicAdd(&dbias[ch], acc);
+        }
     }
 }
 
@@ -212,7 +229,7 @@ __global__ void __launch_bounds__(HEAD_NT, 2) head_ce_kernel(
     const uint16_t *__restrict__ hact, long long npx, int hw, const uint8_t *__restrict__ labels,
     const float *__restrict__ w_out, const float *__restrict__ b_out, const float *__restrict__ drop, float grad_scale,
     uint16_t *__restrict__ dz, float *__restrict__ dw, float *__restrict__ db, float *__restrict__ stats,
-    float *__restrict__ logits_out) {
+    float *__restrict__ logits_out, float *__restrict__ dzbias) {
     __shared__ float sw[3 * HC];
     __shared__ float sdrop[HC];
     // per-warp staging of 32 pixels x 128 B (row pitch 144 B: conflict-free 16 B row reads)
@@ -225,6 +242,7 @@ __global__ void __launch_bounds__(HEAD_NT, 2) head_ce_kernel(
     long long cur_img = -1;
     const bool train = dw != nullptr;
     float accw[6] = {0, 0, 0, 0, 0, 0};
+    float accz0 = 0.f, accz1 = 0.f;  // bias gradient of the conv that produced h: sum of dz
     float accb0 = 0.f, accb1 = 0.f, accb2 = 0.f, loss_sum = 0.f, correct = 0.f;
     const float b0 = b_out[0], b1 = b_out[1], b2 = b_out[2];
     const long long stride = (long long)gridDim.x * HEAD_NT;
@@ -332,6 +350,14 @@ __global__ void __launch_bounds__(HEAD_NT, 2) head_ce_kernel(
                 *reinterpret_cast<uint4 *>(wst + lane * 144 + q * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
             __syncwarp();
+            if (dzbias) {  // lane l sums channels 2l, 2l+1 of the 32 staged dz rows
+#pragma unroll 4
+                for (int q = 0; q < 32; ++q) {
+                    const uint32_t zv = *reinterpret_cast<const uint32_t *>(wst + q * 144 + lane * 4);
+                    accz0 += bf((uint16_t)(zv & 0xffffu));
+                    accz1 += bf((uint16_t)(zv >> 16));
+                }
+            }
             uint4 *dst = reinterpret_cast<uint4 *>(dz + p0 * HC);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -361,6 +387,10 @@ __global__ void __launch_bounds__(HEAD_NT, 2) head_ce_kernel(
             atomicAdd(&db[0], accb0);
             atomicAdd(&db[1], accb1);
             atomicAdd(&db[2], accb2);
+        }
+        if (dzbias && dz) {
+            atomicAdd(&dzbias[2 * lane], accz0);
+            atomicAdd(&dzbias[2 * lane + 1], accz1);
         }
     }
     if (lane == 0 && stats) {
@@ -501,22 +531,28 @@ extern "C" int ice_maxpool_fwd(const uint16_t *x, int32_t n, int32_t h, int32_t 
 }
 
 extern "C" int ice_maxpool_bwd(const uint16_t *x, const uint16_t *dpool, const uint16_t *add, const float *drop,
-                               int32_t n, int32_t h, int32_t w, int32_t c, uint16_t *dz, void *stream) {
+                               int32_t n, int32_t h, int32_t w, int32_t c, uint16_t *dz, float *dbias, void *stream) {
     if (!x || !dpool || !dz || n < 1 || h < 2 || w < 2 || (h | w) & 1 || c % 8) return ICE_EINVAL;
-    maxpool_bwd_kernel<<<grid_for((long long)n * (h / 2) * (w / 2) * (c / 8), 256), 256, 0, (cudaStream_t)stream>>>(
-        x, dpool, add, drop, n, h, w, c, dz);
+    const long long total = (long long)n * (h / 2) * (w / 2) * (c / 8);
+    const int cv = c / 8, threads = 256;
+    // grid * threads must be a multiple of cv (fixed channels per thread for the bias sums)
+    if (cv > threads || threads % cv) return ICE_EINVAL;  // c <= 2048, power-of-two channel groups
+    long long blocks = (total + threads - 1) / threads;
+    if (blocks > 148LL * 4) blocks = 148LL * 4;
+    maxpool_bwd_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(x, dpool, add, drop, n, h, w, c, dz,
+                                                                                dbias);
     LAUNCH_CHECK();
 }
 
 extern "C" int ice_head_ce(const uint16_t *h, int64_t npx, int32_t hw, const uint8_t *labels, const float *w_out,
                            const float *b_out, const float *drop, float grad_scale, uint16_t *dz, float *dw, float *db,
-                           float *stats, float *logits, void *stream) {
+                           float *stats, float *logits, float *dzbias, void *stream) {
     if (!h || !labels || !w_out || !b_out || npx < 0 || hw < 1 || ((dw == nullptr) != (db == nullptr))) return ICE_EINVAL;
     if (npx == 0) return ICE_OK;
     unsigned blocks = grid_for(npx, HEAD_NT);
     if (blocks > 148 * 4) blocks = 148 * 4;
     head_ce_kernel<<<blocks, HEAD_NT, 0, (cudaStream_t)stream>>>(h, npx, hw, labels, w_out, b_out, drop, grad_scale,
-                                                                 dz, dw, db, stats, logits);
+                                                                 dz, dw, db, stats, logits, dzbias);
     LAUNCH_CHECK();
 }
 

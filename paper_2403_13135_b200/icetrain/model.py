@@ -384,7 +384,8 @@ class UNetEngine:
                      _native.ptr(A.drop.get(f"up.{d - 1}")) if train else None, float(grad_scale),
                      _native.ptr(dz), _native.ptr(self.w("out", self.grads)) if train else None,
                      _native.ptr(self.b("out", self.grads)) if train else None, A.stats.data_ptr(),
-                     _native.ptr(logits), st)
+                     _native.ptr(logits), _native.ptr(self.b(f"up.{d - 1}.block.2", self.grads)) if train else None,
+                     st)
         return dz
 
     # ---- backward -----------------------------------------------------------------------
@@ -408,17 +409,15 @@ class UNetEngine:
             n0, n2, hn = f"up.{j}.block.0", f"up.{j}.block.2", f"halve.{j}.conv"
             # up.j.block.2 : u1 -> u2
             ops.conv_wgrad(A.u1[j], dz, self.w(n2, G))
-            self._bias_grad(n2, dz)
             dz1 = A.dz_b[L]
-            ops.conv_dgrad(dz, self.wb16(n2), A.u1[j].shape[3], out1=dz1, ref1=A.u1[j])
+            ops.conv_dgrad(dz, self.wb16(n2), A.u1[j].shape[3], out1=dz1, ref1=A.u1[j], db1=self.b(n0, G))
             done(n2)
             # up.j.block.0 : cat(skip, hv) -> u1
             ops.conv_wgrad(A.a2[L], dz1, self.w(n0, G), x2=A.hv[j])
-            self._bias_grad(n0, dz1)
             c = A.a2[L].shape[3]
             _native.call("ice_conv_dgrad", dz1.data_ptr(), dz1.shape[3], B, dz1.shape[1], dz1.shape[2], 3,
                          self.wb16(n0).data_ptr(), c, c, A.dskip[L].data_ptr(), None, None, None,
-                         A.dhv[L].data_ptr(), None, None, None, 1, st)
+                         A.dhv[L].data_ptr(), None, None, None, 1, None, self.b(hn, G).data_ptr(), st)
             done(n0)
             # halve.j : x_prev -> hv
             xprev = A.b2 if j == 0 else A.u2[j - 1]
@@ -426,20 +425,20 @@ class UNetEngine:
             s = xprev.shape[1]
             _native.call("ice_halve_wgrad", xprev.data_ptr(), hl.cin_p, A.dhv[L].data_ptr(), hl.cout_p, B, s, s,
                          self.w(hn, G).data_ptr(), st)
-            self._bias_grad(hn, A.dhv[L])
             dz = A.dz_a[L + 1]
             drop_prev = A.drop.get("bottleneck" if j == 0 else f"up.{j - 1}")
+            prev_name = "bottleneck.block.2" if j == 0 else f"up.{j - 1}.block.2"
             _native.call("ice_halve_dgrad", A.dhv[L].data_ptr(), hl.cout_p, B, s, s, self.halve_wc[hn].data_ptr(),
-                         hl.cin_p, dz.data_ptr(), xprev.data_ptr(), _native.ptr(drop_prev), st)
+                         hl.cin_p, dz.data_ptr(), xprev.data_ptr(), _native.ptr(drop_prev),
+                         self.b(prev_name, G).data_ptr(), st)
             done(hn)
         # bottleneck
         ops.conv_wgrad(A.b1, dz, self.w("bottleneck.block.2", G))
-        self._bias_grad("bottleneck.block.2", dz)
         dz1 = A.dz_b[d]
-        ops.conv_dgrad(dz, self.wb16("bottleneck.block.2"), A.b1.shape[3], out1=dz1, ref1=A.b1)
+        ops.conv_dgrad(dz, self.wb16("bottleneck.block.2"), A.b1.shape[3], out1=dz1, ref1=A.b1,
+                       db1=self.b("bottleneck.block.0", G))
         done("bottleneck.block.2")
         ops.conv_wgrad(A.pool[d - 1], dz1, self.w("bottleneck.block.0", G))
-        self._bias_grad("bottleneck.block.0", dz1)
         ops.conv_dgrad(dz1, self.wb16("bottleneck.block.0"), A.pool[d - 1].shape[3], out1=A.dpool[d - 1])
         done("bottleneck.block.0")
         # down path
@@ -449,17 +448,15 @@ class UNetEngine:
             dz2 = A.dz_a[i]
             _native.call("ice_maxpool_bwd", a2.data_ptr(), A.dpool[i].data_ptr(), A.dskip[i].data_ptr(),
                          _native.ptr(A.drop.get(f"down.{i}")), B, a2.shape[1], a2.shape[2], a2.shape[3],
-                         dz2.data_ptr(), st)
+                         dz2.data_ptr(), self.b(n2, G).data_ptr(), st)
             ops.conv_wgrad(A.a1[i], dz2, self.w(n2, G))
-            self._bias_grad(n2, dz2)
             dz1 = A.dz_b[i]
-            ops.conv_dgrad(dz2, self.wb16(n2), A.a1[i].shape[3], out1=dz1, ref1=A.a1[i])
+            ops.conv_dgrad(dz2, self.wb16(n2), A.a1[i].shape[3], out1=dz1, ref1=A.a1[i], db1=self.b(n0, G))
             done(n2)
             if i == 0:
                 ops.conv_wgrad(A.stem, dz1, self.w(n0, G), ksize=1)
             else:
                 ops.conv_wgrad(A.pool[i - 1], dz1, self.w(n0, G))
-            self._bias_grad(n0, dz1)
             if i > 0:
                 ops.conv_dgrad(dz1, self.wb16(n0), A.pool[i - 1].shape[3], out1=A.dpool[i - 1])
             done(n0)

@@ -41,7 +41,8 @@ def conv_fprop(x1, wgt, bias=None, x2=None, relu=True, drop=None, ksize=3, out=N
 
 
 def conv_dgrad(dy, wgt, c1, c2=0, ksize=3, out1=None, out2=None, ref1=None, ref2=None, drop1=None,
-               drop2=None, add1=None, add2=None, want2=True, planes2=False, stream=None):
+               drop2=None, add1=None, add2=None, want2=True, planes2=False, db1=None, db2=None,
+               stream=None):
     n, h, w, cout = dy.shape
     if tuple(wgt.shape) != (cout, ksize, ksize, c1 + c2):
         raise ValueError(f"weight shape {tuple(wgt.shape)} != {(cout, ksize, ksize, c1 + c2)}")
@@ -52,7 +53,7 @@ def conv_dgrad(dy, wgt, c1, c2=0, ksize=3, out1=None, out2=None, ref1=None, ref2
     _native.call("ice_conv_dgrad", _c(dy, BF16, "dy"), cout, n, h, w, ksize, _c(wgt, BF16, "wgt"), c1, c2,
                  _c(out1, BF16), _c(ref1, BF16), _c(drop1, torch.float32), _c(add1, BF16),
                  _c(out2, BF16), _c(ref2, BF16), _c(drop2, torch.float32), _c(add2, BF16), int(planes2),
-                 _native.stream_handle(stream))
+                 _c(db1, torch.float32), _c(db2, torch.float32), _native.stream_handle(stream))
     return out1, out2
 
 

@@ -71,13 +71,15 @@ def test_dgrad(shape):
     ref1 = torch.relu(rnd(n, h, w, c1))
     add1 = rnd(n, h, w, c1)
     drop1 = (torch.rand(n, c1, device="cuda") > 0.2).float() / 0.8
-    d1, d2 = ops.conv_dgrad(dy, wt, c1, c2, ksize=k, ref1=ref1, add1=add1, drop1=drop1)
+    db1 = torch.zeros(c1, device="cuda")
+    d1, d2 = ops.conv_dgrad(dy, wt, c1, c2, ksize=k, ref1=ref1, add1=add1, drop1=drop1, db1=db1)
     xin = torch.zeros(n, c1 + c2, h, w, device="cuda", requires_grad=True)
     out = F.conv2d(xin, krsc_to_oihw(wt), padding=k // 2)
     out.backward(nchw(dy))
     g = xin.grad
     want1 = (g[:, :c1] + nchw(add1)) * drop1[:, :, None, None] * (nchw(ref1) > 0)
     assert rel(nchw(d1), want1) < 1e-2
+    assert rel(db1, want1.sum((0, 2, 3))) < 1e-2  # fused bias gradient
     if c2:
         assert rel(nchw(d2), g[:, c1:]) < 1e-2
 
@@ -131,12 +133,14 @@ def test_halve_fprop_dgrad_wgrad(shape):
     ref_relu = torch.relu(rnd(n, h, w, c))
     dx = torch.empty(n, h, w, c, dtype=torch.bfloat16, device="cuda")
     dyp = _planes(dy)
+    dbx = torch.zeros(c, device="cuda")
     _native.call("ice_halve_dgrad", dyp.data_ptr(), cout, n, h, w, wc.data_ptr(), c, dx.data_ptr(),
-                 ref_relu.data_ptr(), None, st)
+                 ref_relu.data_ptr(), None, dbx.data_ptr(), st)
     dw = torch.zeros(cout, 2, 2, c, device="cuda")
     _native.call("ice_halve_wgrad", x.data_ptr(), c, dyp.data_ptr(), cout, n, h, w, dw.data_ptr(), st)
     xin = nchw(x).requires_grad_(True)
     wref = w_oihw.clone().requires_grad_(True)
     _halve_ref(xin, wref, b).backward(nchw(dy))
     assert rel(nchw(dx), xin.grad * (nchw(ref_relu) > 0)) < 1e-2
+    assert rel(dbx, (xin.grad * (nchw(ref_relu) > 0)).sum((0, 2, 3))) < 1e-2
     assert rel(dw.permute(0, 3, 1, 2), wref.grad) < 1e-2
