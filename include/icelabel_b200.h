@@ -183,13 +183,20 @@ int ice_head_ce(const uint16_t *h, int64_t npx, int32_t hw, const uint8_t *label
 int ice_bias_grad(const uint16_t *dz, int64_t rows, int32_t c, float *db, void *stream);
 
 /* Dropout2d multipliers (model.py:74-75): out[i] = (u_i >= p) / (1 - p), u from a
- * counter-based hash of (seed, i). */
-int ice_dropout_scale(int32_t count, float p, uint64_t seed, float *out, void *stream);
+ * counter-based hash of (seed + f(*step_dev), i); step_dev (may be NULL) is the device step
+ * counter, so CUDA-graph replays draw fresh masks. */
+int ice_dropout_scale(int32_t count, float p, uint64_t seed, const int64_t *step_dev, float *out,
+                      void *stream);
 
 /* torch.optim.Adam step (defaults of train.py:149: no weight decay, no amsgrad) over flat
- * fp32 buffers, fused with the bf16 working-copy write and zeroing of g. */
-int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64_t step, float lr,
-             float beta1, float beta2, float eps, uint16_t *out_bf16, void *stream);
+ * fp32 buffers, fused with the bf16 working-copy write and zeroing of g.  The step t is
+ * `step`, or *step_dev when step_dev is non-NULL (bias corrections computed on the device). */
+int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64_t step,
+             const int64_t *step_dev, float lr, float beta1, float beta2, float eps,
+             uint16_t *out_bf16, void *stream);
+
+/* *counter += delta on the device (the step counter advanced inside CUDA graphs). */
+int ice_counter_add(int64_t *counter, int64_t delta, void *stream);
 
 /* fp32 -> bf16 cast; fill. */
 int ice_cast_bf16(const float *src, int64_t n, uint16_t *dst, void *stream);

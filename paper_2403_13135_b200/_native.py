@@ -62,8 +62,9 @@ SIGNATURES = {
     "ice_maxpool_bwd": [_V, _V, _V, _V, _I32, _I32, _I32, _I32, _V, _V, _V],
     "ice_head_ce": [_V, _I64, _I32, _V, _V, _V, _V, _F32, _V, _V, _V, _V, _V, _V, _V],
     "ice_bias_grad": [_V, _I64, _I32, _V, _V],
-    "ice_dropout_scale": [_I32, _F32, ctypes.c_uint64, _V, _V],
-    "ice_adam": [_V, _V, _V, _V, _I64, _I64, _F32, _F32, _F32, _F32, _V, _V],
+    "ice_dropout_scale": [_I32, _F32, ctypes.c_uint64, _V, _V, _V],
+    "ice_adam": [_V, _V, _V, _V, _I64, _I64, _V, _F32, _F32, _F32, _F32, _V, _V],
+    "ice_counter_add": [_V, _I64, _V],
     "ice_cast_bf16": [_V, _I64, _V, _V],
     "ice_fill_f32": [_V, _I64, _F32, _V],
     "ice_conv_wgrad": [_V, _I32, _V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, _V],

@@ -433,7 +433,9 @@ __device__ __forceinline__ uint32_t mix32(uint64_t x) {
     x ^= x >> 33;
     return (uint32_t)x;
 }
-__global__ void dropout_scale_kernel(int count, float p, unsigned long long seed, float *__restrict__ out) {
+__global__ void dropout_scale_kernel(int count, float p, unsigned long long seed, const long long *__restrict__ step,
+                                     float *__restrict__ out) {
+    if (step) seed += 0x632BE59BD9B4E019ULL * (unsigned long long)(*step);  // device step counter (graph replays)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
         const float u = (mix32(seed * 0x9E3779B97F4A7C15ULL + (unsigned long long)i) >> 8) * (1.0f / 16777216.0f);
         out[i] = u >= p ? 1.0f / (1.0f - p) : 0.0f;
@@ -444,7 +446,12 @@ __global__ void dropout_scale_kernel(int count, float p, unsigned long long seed
 // writes the bf16 working copy and zeroes the gradient for the next step ---------------
 __global__ void adam_kernel(float *__restrict__ p, float *__restrict__ g, float *__restrict__ m, float *__restrict__ v,
                             long long n, float lr_corr, float b1, float b2, float eps, float bc2_sqrt,
-                            uint16_t *__restrict__ out_bf16) {
+                            uint16_t *__restrict__ out_bf16, const long long *__restrict__ step_dev, float lr) {
+    if (step_dev) {  // bias corrections from the device step counter (CUDA-graph replays)
+        const double t = (double)*step_dev;
+        lr_corr = (float)((double)lr / (1.0 - pow((double)b1, t)));
+        bc2_sqrt = (float)sqrt(1.0 - pow((double)b2, t));
+    }
     const long long n4 = n / 4;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
         float4 pp = reinterpret_cast<float4 *>(p)[i];
@@ -567,22 +574,34 @@ extern "C" int ice_bias_grad(const uint16_t *dz, int64_t rows, int32_t c, float 
     LAUNCH_CHECK();
 }
 
-extern "C" int ice_dropout_scale(int32_t count, float p, uint64_t seed, float *out, void *stream) {
+extern "C" int ice_dropout_scale(int32_t count, float p, uint64_t seed, const int64_t *step_dev, float *out,
+                                 void *stream) {
     if (!out || count < 0 || p < 0.f || p >= 1.f) return ICE_EINVAL;
     if (count == 0) return ICE_OK;
-    dropout_scale_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(count, p, seed, out);
+    dropout_scale_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(
+        count, p, seed, reinterpret_cast<const long long *>(step_dev), out);
     LAUNCH_CHECK();
 }
 
-extern "C" int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64_t step, float lr, float beta1,
-                        float beta2, float eps, uint16_t *out_bf16, void *stream) {
-    if (!p || !g || !m || !v || n < 0 || step < 1) return ICE_EINVAL;
+extern "C" int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64_t step, const int64_t *step_dev,
+                        float lr, float beta1, float beta2, float eps, uint16_t *out_bf16, void *stream) {
+    if (!p || !g || !m || !v || n < 0 || (step < 1 && !step_dev)) return ICE_EINVAL;
     if (n == 0) return ICE_OK;
     // torch.optim.Adam (_single_tensor_adam): step_size = lr / (1 - b1^t), denom = sqrt(v)/sqrt(1 - b2^t) + eps
-    const double bc1 = 1.0 - pow((double)beta1, (double)step);
-    const double bc2 = 1.0 - pow((double)beta2, (double)step);
+    const double t = step < 1 ? 1.0 : (double)step;
+    const double bc1 = 1.0 - pow((double)beta1, t);
+    const double bc2 = 1.0 - pow((double)beta2, t);
     adam_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, (cudaStream_t)stream>>>(
-        p, g, m, v, n, (float)(lr / bc1), beta1, beta2, eps, (float)sqrt(bc2), out_bf16);
+        p, g, m, v, n, (float)(lr / bc1), beta1, beta2, eps, (float)sqrt(bc2), out_bf16,
+        reinterpret_cast<const long long *>(step_dev), lr);
+    LAUNCH_CHECK();
+}
+
+__global__ void counter_add_kernel(long long *c, long long d) { *c += d; }
+
+extern "C" int ice_counter_add(int64_t *counter, int64_t delta, void *stream) {
+    if (!counter) return ICE_EINVAL;
+    counter_add_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<long long *>(counter), delta);
     LAUNCH_CHECK();
 }
 

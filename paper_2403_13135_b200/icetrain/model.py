@@ -243,6 +243,9 @@ class UNetEngine:
         self._acts_cache = {}
         # loss sum / correct count of the current step, shared by all shard shapes
         self.stats = torch.zeros(2, dtype=torch.float32, device=self.device)
+        # optimizer step counter on the device: Adam bias corrections and dropout seeds read it,
+        # so a captured CUDA graph of a whole train step replays correctly
+        self.step_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.training = True
         self.n_real_params = sum(L.cout * L.cin * L.k * L.k + L.cout for L in self.layers)
 
@@ -325,8 +328,8 @@ class UNetEngine:
         total = A.B * sum(widths)
         if getattr(A, "drop_buf", None) is None or A.drop_buf.numel() != total:
             A.drop_buf = torch.empty(total, dtype=torch.float32, device=self.device)
-        _native.call("ice_dropout_scale", total, float(p), seed & (2 ** 63 - 1), A.drop_buf.data_ptr(),
-                     _native.stream_handle())
+        _native.call("ice_dropout_scale", total, float(p), seed & (2 ** 63 - 1), self.step_dev.data_ptr(),
+                     A.drop_buf.data_ptr(), _native.stream_handle())
         off = 0
         for blk, c in zip(blocks, widths):
             A.drop[blk] = A.drop_buf[off: off + A.B * c].view(A.B, c)
@@ -462,7 +465,11 @@ class UNetEngine:
             done(n0)
 
     # ---- optimizer ------------------------------------------------------------------------
+    def advance_step(self, stream=None) -> None:
+        _native.call("ice_counter_add", self.step_dev.data_ptr(), 1, _native.stream_handle(stream))
+
     def adam(self, step: int, lr: float, betas=(0.9, 0.999), eps: float = 1e-8) -> None:
+        self.advance_step()
         self.adam_slice(0, self.numel, step, lr, betas, eps)
         self.prep_halves()
 
@@ -473,7 +480,8 @@ class UNetEngine:
         off4, off2 = start * 4, start * 2
         _native.call("ice_adam", self.params.data_ptr() + off4, self.grads.data_ptr() + off4,
                      self.exp_avg.data_ptr() + off4, self.exp_avg_sq.data_ptr() + off4, stop - start, int(step),
-                     float(lr), float(betas[0]), float(betas[1]), float(eps), self.wbf16.data_ptr() + off2, st)
+                     self.step_dev.data_ptr(), float(lr), float(betas[0]), float(betas[1]), float(eps),
+                     self.wbf16.data_ptr() + off2, st)
 
     def zero_grad(self) -> None:
         _native.call("ice_fill_f32", self.grads.data_ptr(), self.numel, 0.0, _native.stream_handle())

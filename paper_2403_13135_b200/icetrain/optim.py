@@ -25,6 +25,8 @@ class Adam:
     # then each gradient bucket is updated as soon as it is final, on a side stream
     def begin_overlapped_step(self) -> int:
         self.step_count += 1
+        for e in self.engines:
+            e.advance_step()
         return self.step_count
 
     def step_slice(self, engine, start: int, stop: int, stream=None) -> None:

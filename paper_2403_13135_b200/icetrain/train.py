@@ -147,9 +147,10 @@ def device_step(model, optimizer, x, y, union_count: int, bucketer=None) -> None
     bucketer is given), fused Adam.  x: u8 NHWC [n, S, S, 3], y: u8 [n, S, S].
     The step's loss sum / hit count accumulate in model.engine.stats."""
     engine = model.engine
-    step = optimizer.step_count + 1
     S = x.shape[1]
-    A = engine.forward(x, train=model.training, seed=step)
+    # dropout masks: per-rank seed + the engine's device step counter (graph-replay safe)
+    dist = _dist()
+    A = engine.forward(x, train=model.training, seed=1 + (dist.get_rank() if dist else 0))
     dz = engine.head(A, y, train=True, grad_scale=1.0 / (union_count * S * S))
     fused = bucketer is not None and bucketer.optimizer is optimizer
     if fused:
@@ -159,6 +160,40 @@ def device_step(model, optimizer, x, y, union_count: int, bucketer=None) -> None
         bucketer.finish()
     if not fused:
         optimizer.step()
+
+
+class GraphedStep:
+    """A whole device_step captured once as a CUDA graph and replayed (single process):
+    ~140 kernel launches (+ the optimizer-in-backward side stream) become one graph launch.
+    Inputs are copied into static device buffers before each replay; the Adam step count and
+    dropout seeds advance through the engine's device step counter, so replays are real
+    consecutive training steps."""
+
+    def __init__(self, model, optimizer, x, y, union_count: int, bucketer=None, warmup: int = 2):
+        self.model, self.optimizer = model, optimizer
+        self.x = x.clone()
+        self.y = y.clone()
+        self.union, self.bucketer = union_count, bucketer
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                device_step(model, optimizer, self.x, self.y, union_count, bucketer)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            device_step(model, optimizer, self.x, self.y, union_count, bucketer)
+        # the capture itself did not run the step: undo its host-side step bookkeeping
+        optimizer.step_count -= 1
+
+    def __call__(self, x=None, y=None) -> None:
+        if x is not None:
+            self.x.copy_(x, non_blocking=True)
+        if y is not None:
+            self.y.copy_(y, non_blocking=True)
+        self.graph.replay()
+        self.optimizer.step_count += 1
 
 
 def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
@@ -180,7 +215,7 @@ def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
     if total == 0:
         raise ValueError("synchronized step got only empty shards")
     A = None
-    seed = getattr(optimizers[0], "step_count", 0) + 1
+    rank_seed = 1 + 1009 * (dist.get_rank() if dist is not None else 0)
     bucketer = None
     fused = len(models) == 1 and isinstance(optimizers[0], Adam)
     if fused or (dist is not None and dist.get_world_size() > 1):
@@ -197,7 +232,7 @@ def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
     for idx, (k, (x, y)) in enumerate(live):
         xin, is_float = _as_nhwc(x, device)
         S = xin.shape[1]
-        A = engine.forward(xin, train=models[0].training, seed=seed * 1009 + k, float_input=is_float)
+        A = engine.forward(xin, train=models[0].training, seed=rank_seed + k, float_input=is_float)
         if idx == 0:
             A.stats.zero_()
         A.labels.copy_(y.to(device, non_blocking=True), non_blocking=True)
