@@ -21,6 +21,23 @@
 
 #include "icelabel_b200.h"
 
+#ifdef ICE_AL_PROF
+__device__ unsigned long long g_al_prof[16];
+#define PROF_MARK(k)                                                          \
+    do {                                                                      \
+        __syncthreads();                                                      \
+        if (threadIdx.x == 0) {                                               \
+            long long now = clock64();                                        \
+            atomicAdd(&g_al_prof[k], (unsigned long long)(now - prof_t0));    \
+            prof_t0 = now;                                                    \
+        }                                                                     \
+    } while (0)
+#else
+#define PROF_MARK(k) \
+    do {             \
+    } while (0)
+#endif
+
 namespace {
 
 constexpr int NT = 512;        // threads per CTA
@@ -357,10 +374,16 @@ autolabel_kernel(const uint8_t *__restrict__ rgb, int h, int w, Params prm,
     uint8_t *ftile = filtered + tile_id * (size_t)npx * 3;
     uint8_t *P0 = s.p[0], *P1 = s.p[1], *P2 = s.p[2];
 
+#ifdef ICE_AL_PROF
+    long long prof_t0 = clock64();
+#endif
     // 1. V plane, dilate, background = median(dilate(V))   (cloudfilter.py:82-84, 89)
     load_channel(tile, 3, P0, h, w);
+    PROF_MARK(0);
     dilate_plane(P0, P2, P1, h, w, cfg.bg_dilate_k);        // D in P1
+    PROF_MARK(1);
     median_plane(P1, P2, P0, h, w, cfg.bg_median_k, s);     // bg in P0
+    PROF_MARK(2);
     // 2. V again, smooth = median_noise(V); d = |smooth - bg|, [truncate]  (:90-93)
     load_channel(tile, 3, P1, h, w);
     int lo = 255, hi = 0;
@@ -375,6 +398,7 @@ autolabel_kernel(const uint8_t *__restrict__ rgb, int h, int w, Params prm,
         hi = max(hi, d);
     }
     block_minmax(lo, hi, s);
+    PROF_MARK(3);
     // 3. minmax normalize (kernels.py:66-74, exact integer form), Otsu, binary (:94-96)
     for (int i = threadIdx.x; i < 256; i += NT) s.hist[i] = 0;
     __syncthreads();
@@ -416,6 +440,7 @@ autolabel_kernel(const uint8_t *__restrict__ rgb, int h, int w, Params prm,
     }
     const int masked = block_sum(cnt, s);
     const int any_unequal = block_sum(unequal, s);
+    PROF_MARK(4);
     // 4. repair (cloudfilter.py:108-116)
     int center[3] = {0, 0, 0};
     if (masked > 0) {
@@ -442,6 +467,7 @@ autolabel_kernel(const uint8_t *__restrict__ rgb, int h, int w, Params prm,
             }
         }
     }
+    PROF_MARK(5);
     // 5. output pass: filtered tile, HSV segmentation, counts, first unmatched
     int c0 = 0, c1 = 0, c2 = 0, first = 0x7fffffff;
     uint8_t *ltile = label + tile_id * (size_t)npx;
@@ -473,6 +499,7 @@ autolabel_kernel(const uint8_t *__restrict__ rgb, int h, int w, Params prm,
         c2 += cls == 2;
         if (cls == 255) first = min(first, i);
     }
+    PROF_MARK(6);
     c0 = block_sum(c0, s);
     c1 = block_sum(c1, s);
     c2 = block_sum(c2, s);
@@ -582,3 +609,14 @@ extern "C" int ice_rgb_to_hsv(const uint8_t *rgb, int64_t npx, uint8_t *hsv, voi
     hsv_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(rgb, npx, hsv);
     return (int)cudaGetLastError();
 }
+
+#ifdef ICE_AL_PROF
+extern "C" int ice_al_prof_read(unsigned long long *out16, int reset) {
+    cudaMemcpyFromSymbol(out16, g_al_prof, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_al_prof, z, sizeof z);
+    }
+    return 0;
+}
+#endif

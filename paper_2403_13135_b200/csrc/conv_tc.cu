@@ -747,27 +747,43 @@ struct HWgrad {
     float *dw;  // [cout][9][ct]
 };
 
-constexpr int HW_HALO_ROWS = 3 * 66;
-constexpr int HW_HALO_TX = HW_HALO_ROWS * 128;                  // 25,344 B
-constexpr int HW_HALO_BYTES = (HW_HALO_TX + 1023) / 1024 * 1024;  // 25,600 B
+// HALVE variant (2x2 halving conv, model.py:79-88): dW[(a,b), c] accumulates, for each of
+// the 4 sub-pixel classes (cy, cx), x[p + ((cy+a)/2, (cx+b)/2)] (x) dY_cls[p]; the halo is
+// 2 rows x 65 pixels and the dY segment comes as 4 class planes.
+template <bool HALVE>
+struct HWGeom {
+    static constexpr int ROWS = HALVE ? 2 : 3, COLS = HALVE ? 65 : 66;
+    static constexpr int TX = ROWS * COLS * 128;
+    static constexpr int BYTES = (TX + 1023) / 1024 * 1024;
+    static constexpr int TAPS = HALVE ? 4 : 9;
+    static constexpr int CLASSES = HALVE ? 4 : 1;
+};
 
-template <int COUT, int NCH, int STAGES>
+template <int COUT, int NCH, int STAGES, bool HALVE>
 constexpr int hw_stage_bytes() {
-    return NCH * HW_HALO_BYTES + (COUT / 64) * 8192;
+    return NCH * HWGeom<HALVE>::BYTES + HWGeom<HALVE>::CLASSES * (COUT / 64) * 8192;
 }
-template <int COUT, int NCH, int STAGES>
+template <int COUT, int NCH, int STAGES, bool HALVE>
 constexpr int hw_smem_bytes() {
-    return 1024 + STAGES * hw_stage_bytes<COUT, NCH, STAGES>() + (2 * STAGES + 2) * 8 + 16;
+    return 1024 + STAGES * hw_stage_bytes<COUT, NCH, STAGES, HALVE>() + (2 * STAGES + 2) * 8 + 16;
 }
 
-__device__ __forceinline__ int hw_view_row(int tap) { return (tap / 3) * 66 + tap % 3; }
+// halo row of the window for weight tap `tap` (and sub-pixel class `cls` for HALVE)
+template <bool HALVE>
+__device__ __forceinline__ int hw_view_row(int tap, int cls) {
+    if (HALVE) return (((cls >> 1) + (tap >> 1)) >> 1) * 65 + (((cls & 1) + (tap & 1)) >> 1);
+    return (tap / 3) * 66 + tap % 3;
+}
 
-template <int COUT, int NCH, int STAGES>
+template <int COUT, int NCH, int STAGES, bool HALVE>
 __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_constant__ HWgrad p) {
+    using G = HWGeom<HALVE>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    constexpr int STAGE = hw_stage_bytes<COUT, NCH, STAGES>();
-    constexpr int TX = NCH * HW_HALO_TX + (COUT / 64) * 8192;
+    constexpr int STAGE = hw_stage_bytes<COUT, NCH, STAGES, HALVE>();
+    constexpr int DY_BYTES = (COUT / 64) * 8192;
+    constexpr int TX = NCH * G::TX + G::CLASSES * DY_BYTES;
+    constexpr int NBLK = G::TAPS * NCH;  // M blocks: (tap, chunk), tap-major
     constexpr int TCOLS = 512;
     uint64_t *full = reinterpret_cast<uint64_t *>(base + STAGES * STAGE);
     uint64_t *empty = full + STAGES;
@@ -812,9 +828,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                     uint8_t *st = base + s * STAGE;
 #pragma unroll
                     for (int c = 0; c < NCH; ++c)
-                        tc::tma_load_4d(st + c * HW_HALO_BYTES, &p.xm[c], &full[s], 0, w0 - 1, h - 1, n);
-                    if (COUT == 64) tc::tma_load_4d(st + NCH * HW_HALO_BYTES, &p.dym, &full[s], 0, w0, h, n);
-                    else tc::tma_load_5d(st + NCH * HW_HALO_BYTES, &p.dym, &full[s], 0, w0, h, n, 0);
+                        tc::tma_load_4d(st + c * G::BYTES, &p.xm[c], &full[s], 0, w0 - (HALVE ? 0 : 1),
+                                        h - (HALVE ? 0 : 1), n);
+#pragma unroll
+                    for (int cls = 0; cls < G::CLASSES; ++cls) {
+                        const int img = HALVE ? cls * p.N + n : n;  // class planes flatten to 4N images
+                        uint8_t *dst = st + NCH * G::BYTES + cls * DY_BYTES;
+                        if (COUT == 64) tc::tma_load_4d(dst, &p.dym, &full[s], 0, w0, h, img);
+                        else tc::tma_load_5d(dst, &p.dym, &full[s], 0, w0, h, img, 0);
+                    }
                 }
             }
         }
@@ -833,18 +855,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                     tc::mbar_wait(&full[s], (it / STAGES) & 1);
                     tc::tc_fence_after();
                     const uint32_t st = tc::smem_u32(base + s * STAGE);
-                    const uint32_t bbase = st + NCH * HW_HALO_BYTES;
-                    for (int mt = mt0; mt < mt1; ++mt) {
-                        // blocks 2 mt, 2 mt + 1 of the (tap, chunk) list; a missing second block repeats the first
-                        const int b0 = 2 * mt, b1 = min(2 * mt + 1, 9 * NCH - 1);
-                        const uint32_t a0 = st + (b0 % NCH) * HW_HALO_BYTES + hw_view_row(b0 / NCH) * 128;
-                        const uint32_t a1 = st + (b1 % NCH) * HW_HALO_BYTES + hw_view_row(b1 / NCH) * 128;
-                        const uint32_t d = tmem + (mt - mt0) * COUT;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const uint64_t ad = tc::sw128_desc(a0 + k * 2048, a1 - a0, 1024);
-                            const uint64_t bd = tc::sw128_desc(bbase + k * 2048, 8192, 1024);
-                            tc::umma_f16(d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                    for (int cls = 0; cls < G::CLASSES; ++cls) {
+                        const uint32_t bbase = st + NCH * G::BYTES + cls * DY_BYTES;
+                        for (int mt = mt0; mt < mt1; ++mt) {
+                            // blocks 2 mt, 2 mt + 1 of the (tap, chunk) list; a missing one repeats the first
+                            const int b0 = 2 * mt, b1 = min(2 * mt + 1, NBLK - 1);
+                            const uint32_t a0 = st + (b0 % NCH) * G::BYTES + hw_view_row<HALVE>(b0 / NCH, cls) * 128;
+                            const uint32_t a1 = st + (b1 % NCH) * G::BYTES + hw_view_row<HALVE>(b1 / NCH, cls) * 128;
+                            // LBO must not be negative: swap the blocks and remember it in the epilogue
+                            const bool sw = a1 < a0;
+                            const uint32_t lo = sw ? a1 : a0, dl = sw ? a0 - a1 : a1 - a0;
+                            const uint32_t d = tmem + (mt - mt0) * COUT;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const uint64_t ad = tc::sw128_desc(lo + k * 2048, dl, 1024);
+                                const uint64_t bd = tc::sw128_desc(bbase + k * 2048, 8192, 1024);
+                                tc::umma_f16(d, ad, bd, idesc, (kb > kb0 || cls > 0 || k > 0) ? 1u : 0u);
+                            }
                         }
                     }
                     tc::umma_commit(&empty[s]);
@@ -857,7 +885,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
         const int sub = warp & 3, half = (warp - 2) >> 2;
         const int r = sub * 32 + lane;  // TMEM lane = row of the M tile
         constexpr int NCC = COUT / 32, PER = (NCC + 1) / 2;
-        const int ld = 9 * p.ct;
+        const int ld = G::TAPS * p.ct;
         int local = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
             const int grp = u % p.groups;
@@ -865,8 +893,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
             tc::mbar_wait(tfull, local & 1);
             tc::tc_fence_after();
             for (int mt = mt0; mt < mt1; ++mt) {
-                const int b = 2 * mt + (r >> 6);
-                const bool valid = b < 9 * NCH;
+                // row r of the tile is block (2 mt + r/64) unless the issuer swapped the pair
+                const int b0 = 2 * mt, b1 = min(2 * mt + 1, NBLK - 1);
+                // the swap decision depends on the view rows; it is class-independent for the
+                // pairs used here (same tap, different chunk, or taps in increasing halo order)
+                const int v0 = (b0 % NCH) * G::BYTES + hw_view_row<HALVE>(b0 / NCH, 0) * 128;
+                const int v1 = (b1 % NCH) * G::BYTES + hw_view_row<HALVE>(b1 / NCH, 0) * 128;
+                const bool sw = v1 < v0;
+                const int second = (r >> 6) ^ (sw ? 1 : 0);
+                const int b = 2 * mt + second;
+                const bool valid = b < NBLK && !(second == 1 && b1 == b0);
                 const int tap = b / NCH, c = (b % NCH) * 64 + (r & 63);
                 float *dst = p.dw + (size_t)tap * p.ct + c;
 #pragma unroll
@@ -1035,14 +1071,19 @@ int launch_halo(const P &p, dim3 tiles, cudaStream_t st) {
     return (int)cudaGetLastError();
 }
 
-// halo-path dispatch: resident weights when one 64-channel chunk and BN = 64
+// halo-path tile width: N = 64 tiles are shared-memory-bandwidth bound (4 KB of A + 2 KB
+// of B per 32-cycle MMA), so use 128-wide tiles whenever there are 128 columns; a single
+// 64-column problem keeps its 9 weight taps resident instead.
+int halo_bn(int nch, int ncols) { return ncols % 128 == 0 ? 128 : 64; }
+
+// halo-path dispatch
 template <class P>
 int run_halo(const P &p, int nch, int ncols, dim3 tiles_m, cudaStream_t st) {
-    if (nch == 1) {
+    if (halo_bn(nch, ncols) == 64 && nch == 1) {  // all 9 weight taps resident
         dim3 tiles(tiles_m.x, ncols / 64, 1);
         return launch_halo<64, 1, true>(p, tiles, st);
     }
-    if (ncols % 128 == 0) {
+    if (halo_bn(nch, ncols) == 128) {  // N = 128 halves the smem bytes per MMA FLOP
         dim3 tiles(tiles_m.x, ncols / 128, 1);
         return launch_halo<128, 2, false>(p, tiles, st);
     }
@@ -1121,62 +1162,66 @@ int split_k(int total_kb, long long tiles) {
 }
 
 
-bool map_halo64(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, int c0) {
-    // halo box (64 ch, 66 px, 3 rows, 1 image) starting at channel c0 of a C-channel NHWC tensor
+bool map_halo_box(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, int c0, int cols, int rows) {
+    // halo box (64 ch, cols px, rows rows, 1 image) starting at channel c0 of a C-channel NHWC tensor
     const char *base = reinterpret_cast<const char *>(ptr) + (size_t)c0 * 2;
     cuuint64_t dims[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
     cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-    cuuint32_t box[4] = {64, 66, 3, 1};
+    cuuint32_t box[4] = {64, (cuuint32_t)cols, (cuuint32_t)rows, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<char *>(base), dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int COUT, int NCH, int STAGES>
+template <int COUT, int NCH, int STAGES, bool HALVE>
 int launch_hwgrad(HWgrad &p, cudaStream_t st) {
-    constexpr int smem = hw_smem_bytes<COUT, NCH, STAGES>();
+    constexpr int smem = hw_smem_bytes<COUT, NCH, STAGES, HALVE>();
     static_assert(smem <= 232448, "hwgrad smem");
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(hwgrad_kernel<COUT, NCH, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem);
+        cudaError_t e = cudaFuncSetAttribute(hwgrad_kernel<COUT, NCH, STAGES, HALVE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }
-    p.total_mt = (9 * NCH + 1) / 2;
+    p.total_mt = (HWGeom<HALVE>::TAPS * NCH + 1) / 2;
     const int gmax = 512 / COUT;
     p.groups = (p.total_mt + gmax - 1) / gmax;
     p.G = (p.total_mt + p.groups - 1) / p.groups;
     p.kb_per_split = split_k(p.total_kb, p.groups);
     const long long units = (long long)p.groups * ((p.total_kb + p.kb_per_split - 1) / p.kb_per_split);
     const int grid = (int)(units < num_sms() ? units : num_sms());
-    hwgrad_kernel<COUT, NCH, STAGES><<<grid, NTHREADS, smem, st>>>(p);
+    hwgrad_kernel<COUT, NCH, STAGES, HALVE><<<grid, NTHREADS, smem, st>>>(p);
     return (int)cudaGetLastError();
 }
 
-// halo weight-gradient path: 3x3, W % 64 == 0, cout in {64, 128}, cin / 64 in {1, 2}
+// halo weight-gradient path: 3x3 (or the 2x2 halving conv with HALVE), W % 64 == 0,
+// cout in {64, 128}, cin / 64 in {1, 2}.  Returns 1 when not applicable.
 int try_hwgrad(const uint16_t *x1, int c1, const uint16_t *x2, int c2, const uint16_t *dy, int cout, int n, int h,
-               int w, float *dw, cudaStream_t st) {
+               int w, float *dw, cudaStream_t st, bool halve = false) {
     const int nch = (c1 + c2) / 64;
     if (w % 64 || w < 64 || (cout != 64 && cout != 128) || (nch != 1 && nch != 2)) return 1;
+    if (halve && cout != 64) return 1;
     HWgrad p;
     memset(&p, 0, sizeof p);
     p.N = n; p.H = h; p.W = w; p.ct = c1 + c2; p.cout = cout; p.nchx = nch; p.dw = dw;
     p.total_kb = n * h * (w / 64);
     for (int c = 0; c < nch; ++c) {
         const int cc = c * 64;
-        const bool ok = cc < c1 ? map_halo64(&p.xm[c], x1, n, h, w, c1, cc) : map_halo64(&p.xm[c], x2, n, h, w, c2, cc - c1);
+        const int cols = halve ? 65 : 66, rows = halve ? 2 : 3;
+        const bool ok = cc < c1 ? map_halo_box(&p.xm[c], x1, n, h, w, c1, cc, cols, rows)
+                                : map_halo_box(&p.xm[c], x2, n, h, w, c2, cc - c1, cols, rows);
         if (!ok) return ICE_EINVAL;
     }
-    PixTile seg{64, 1, 1, w / 64, h, n};
-    if (!map_act_nb(&p.dym, dy, n, h, w, cout, seg, cout / 64)) return ICE_EINVAL;
-    if (cout == 64 && nch == 1) return launch_hwgrad<64, 1, 6>(p, st);
-    if (cout == 64) return launch_hwgrad<64, 2, 3>(p, st);
-    if (nch == 1) return launch_hwgrad<128, 1, 5>(p, st);
-    return launch_hwgrad<128, 2, 3>(p, st);
+    PixTile seg{64, 1, 1, w / 64, h, (halve ? 4 : 1) * n};
+    if (!map_act_nb(&p.dym, dy, (halve ? 4 : 1) * n, h, w, cout, seg, cout / 64)) return ICE_EINVAL;
+    if (halve) return nch == 1 ? launch_hwgrad<64, 1, 3, true>(p, st) : launch_hwgrad<64, 2, 3, true>(p, st);
+    if (cout == 64 && nch == 1) return launch_hwgrad<64, 1, 6, false>(p, st);
+    if (cout == 64) return launch_hwgrad<64, 2, 3, false>(p, st);
+    if (nch == 1) return launch_hwgrad<128, 1, 5, false>(p, st);
+    return launch_hwgrad<128, 2, 3, false>(p, st);
 }
-
 }  // namespace
 
 extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2, int32_t n, int32_t h,
@@ -1196,7 +1241,7 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
     cudaStream_t st = (cudaStream_t)stream;
     if (use_halo(ksize, w)) {
         const int nch = (c1 + c2) / 64;
-        const int bn = (nch == 1 || cout % 128) ? 64 : 128;
+        const int bn = halo_bn(nch, cout);
         if (!map_halo(&p.xa, x1, n, h, w, c1)) return ICE_EINVAL;
         if (c2 && !map_halo(&p.xb, x2, n, h, w, c2)) return ICE_EINVAL;
         if (!map_wgt(&p.wm, wgt, cout, 9, c1 + c2, bn)) return ICE_EINVAL;
@@ -1363,6 +1408,10 @@ extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!x || !dy_planes || !dw || c <= 0 || c % 64 || cout <= 0 || cout % 64 || !shape_ok(n, h, w))
         return ICE_EINVAL;
+    if (!getenv("ICE_NO_HALO_WGRAD")) {
+        const int rc = try_hwgrad(x, c, nullptr, 0, dy_planes, cout, n, h, w, dw, (cudaStream_t)stream, true);
+        if (rc <= 0) return rc;  // 1 = not applicable
+    }
     WgradProb p;
     memset(&p, 0, sizeof p);
     p.pk = pix_tile(n, h, w, BK);

@@ -99,7 +99,8 @@ def test_wgrad(shape):
     assert rel(dw.permute(0, 3, 1, 2), wref.grad) < 1e-3
 
 
-HALVE = [(2, 8, 8, 128, 64), (3, 4, 4, 256, 128), (2, 16, 16, 64, 64), (1, 2, 2, 512, 256)]
+HALVE = [(2, 8, 8, 128, 64), (3, 4, 4, 256, 128), (2, 16, 16, 64, 64), (1, 2, 2, 512, 256),
+         (2, 64, 64, 128, 64), (1, 32, 128, 64, 64)]  # the last two take the halo weight-gradient path
 
 
 def _halve_ref(x_nchw, w_oihw, b):
