@@ -88,3 +88,20 @@ def test_paper_spec_parameter_count():
     sd = init_reference_params(spec)
     assert sum(v.numel() for v in sd.values()) == 124_362_307
     assert len(sd) == 56
+
+
+def test_oracle_trajectory_matches_reference():
+    """The oracle port reproduces the reference's 200-step loss trajectory (first 20 steps
+    checked here to keep the CPU suite fast)."""
+    from tests.golden.trajectory_data import SEED, batch_order, corpus
+    gold = torch.load(os.path.join(os.path.dirname(__file__), "golden", "unet_trajectory.pt"))
+    spec = UNetSpec(**gold["spec"])
+    x_u8, y = corpus()
+    x = unet_ref.images_to_input(x_u8)
+    yt = torch.from_numpy(y)
+    torch.manual_seed(SEED)
+    model = unet_ref.RefUNet(spec)
+    opt = torch.optim.Adam(model.parameters(), lr=1e-3)
+    for step, idx in enumerate(batch_order()[:20]):
+        loss, _ = unet_ref.synchronized_step([model], [opt], [(x[idx], yt[idx])])
+        assert loss == pytest.approx(gold["losses"][step], rel=1e-4), step
