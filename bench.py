@@ -211,6 +211,23 @@ def autolabel_bench(corpus_dev, n_tiles: int, reps: int):
     return ms, out
 
 
+def segment_bench(corpus_dev, n_tiles: int, reps: int):
+    """K1s (segment only, `icelabel label`) over n_tiles resident tiles: HBM-bound, 4 B/px."""
+    from paper_2403_13135_b200 import icelabel as il
+    idx = torch.arange(n_tiles, device=corpus_dev.device) % corpus_dev.shape[0]
+    tiles = corpus_dev[idx]
+    out = il.segment_batch(tiles)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        il.segment_batch(tiles, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    del tiles
+    return e0.elapsed_time(e1) / reps
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -376,13 +393,25 @@ def main():
             al_ms = float(t.item())
         px = n_tiles * world * SIZE * SIZE
         gbs = px * 7 / (al_ms / 1000.0) / 1e9
+        seg_ms = segment_bench(corpus_dev, n_tiles, reps=5)
+        if dist:
+            t = torch.tensor([seg_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            seg_ms = float(t.item())
+        seg_gbs = px * 4 / (seg_ms / 1000.0) / 1e9
         autolabel = {"metric": "auto-label Mpixel/s (fused filter + HSV labeler, 100k 256^2 tiles)",
                      "value": round(px / (al_ms / 1000.0) / 1e6, 1), "unit": "Mpixel/s",
                      "ms": round(al_ms, 2), "tiles": n_tiles * world,
                      "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
                                   "frac": round(gbs / hbm, 4), "traffic": None,
                                   "note": "7 B/px algorithmic (RGB in, filtered + label out); "
-                                          "the 21x21 medians make K1 on-chip-bound"}}
+                                          "the 21x21 medians make K1 on-chip-bound"},
+                     "segment_only": {"metric": "label-only (K1s, icelabel label) Mpixel/s",
+                                      "value": round(px / (seg_ms / 1000.0) / 1e6, 1), "unit": "Mpixel/s",
+                                      "ms": round(seg_ms, 3),
+                                      "roofline": {"bound": "hbm", "achieved": round(seg_gbs, 1), "peak": hbm,
+                                                   "unit": "GB/s", "frac": round(seg_gbs / hbm, 4),
+                                                   "traffic": None, "note": "4 B/px (RGB in, label out)"}}}
 
     # ---- CPU baseline (rank 0, N = 1 only): bounded sample of the reference step -------
     cpu = None

@@ -48,6 +48,7 @@ constexpr int PLANE = MAXD * PITCH;
 struct Params {
     IceFilterCfg cfg;
     IceScheme scheme;
+    int v_only;  // every range passes all hues and saturations: classify on V alone
 };
 
 struct Smem {
@@ -241,16 +242,44 @@ __device__ __forceinline__ void hsv_of(int R, int G, int B, int &H, int &S, int 
     }
 }
 
-__device__ __forceinline__ int classify(int R, int G, int B, const IceScheme &sc) {
-    int H, S, V;
-    hsv_of(R, G, B, H, S, V);
+// NEED_H / NEED_S = false when every range of the scheme passes all hues / saturations
+// (the shipped ross-sea-summer preset): then only V = max(r, g, b) decides the class, and
+// the two integer divisions of the HSV conversion are skipped -- exact, since H <= 179 and
+// S <= 255 always lie inside full-range boxes.
+// Scheme ranges unpacked into registers (indexing the by-value IceScheme parameter through a
+// reference spills it to local memory and reloads it per pixel).
+struct SchemeR {
+    int lo[3][3], hi[3][3], cls[3];
+    __device__ __forceinline__ explicit SchemeR(const IceScheme &sc) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        if (H >= sc.lo[k][0] && H <= sc.hi[k][0] && S >= sc.lo[k][1] && S <= sc.hi[k][1] &&
-            V >= sc.lo[k][2] && V <= sc.hi[k][2])
-            return sc.cls[k];
+        for (int k = 0; k < 3; ++k) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                lo[k][c] = sc.lo[k][c];
+                hi[k][c] = sc.hi[k][c];
+            }
+            cls[k] = sc.cls[k];
+        }
     }
-    return 255;
+};
+
+template <bool NEED_H = true, bool NEED_S = true>
+__device__ __forceinline__ int classify(int R, int G, int B, const SchemeR &sc) {
+    int H = 0, S = 0, V;
+    if (NEED_H || NEED_S) {
+        hsv_of(R, G, B, H, S, V);
+    } else {
+        V = max(R, max(G, B));
+    }
+    int out = 255;
+#pragma unroll
+    for (int k = 2; k >= 0; --k) {  // first matching range wins
+        bool in = V >= sc.lo[k][2] && V <= sc.hi[k][2];
+        if (NEED_H) in = in && H >= sc.lo[k][0] && H <= sc.hi[k][0];
+        if (NEED_S) in = in && S >= sc.lo[k][1] && S <= sc.hi[k][1];
+        out = in ? sc.cls[k] : out;
+    }
+    return out;
 }
 
 __global__ void hsv_kernel(const uint8_t *__restrict__ rgb, int64_t npx, uint8_t *__restrict__ hsv) {
@@ -472,6 +501,7 @@ autolabel_kernel(const uint8_t *__restrict__ rgb, int h, int w, Params prm,
     int c0 = 0, c1 = 0, c2 = 0, first = 0x7fffffff;
     uint8_t *ltile = label + tile_id * (size_t)npx;
     uint8_t *mtile = maskout ? maskout + tile_id * (size_t)npx : nullptr;
+    const SchemeR scr(prm.scheme);
     for (int i = threadIdx.x; i < npx; i += NT) {
         int R = tile[3 * i], G = tile[3 * i + 1], B = tile[3 * i + 2];
         const bool mk = masked > 0 && (s.maskbits[i >> 5] >> (i & 31) & 1);
@@ -492,7 +522,7 @@ autolabel_kernel(const uint8_t *__restrict__ rgb, int h, int w, Params prm,
         ftile[3 * i] = (uint8_t)R;
         ftile[3 * i + 1] = (uint8_t)G;
         ftile[3 * i + 2] = (uint8_t)B;
-        int cls = classify(R, G, B, prm.scheme);
+        const int cls = prm.v_only ? classify<false, false>(R, G, B, scr) : classify(R, G, B, scr);
         ltile[i] = (uint8_t)cls;
         c0 += cls == 0;
         c1 += cls == 1;
@@ -520,8 +550,9 @@ autolabel_kernel(const uint8_t *__restrict__ rgb, int h, int w, Params prm,
 // K1s: segment only.  One CTA per tile, any size.
 constexpr int SEG_NT = 256;
 __global__ void __launch_bounds__(SEG_NT)
-segment_kernel(const uint8_t *__restrict__ rgb, int npx, IceScheme sc, uint8_t *__restrict__ label,
+segment_kernel(const uint8_t *__restrict__ rgb, int npx, IceScheme sc_in, uint8_t *__restrict__ label,
                uint32_t *__restrict__ counts, int32_t *__restrict__ unmatched) {
+    const SchemeR sc(sc_in);
     __shared__ int red[4][SEG_NT / 32];
     const size_t tile_id = blockIdx.x;
     const uint8_t *tile = rgb + tile_id * (size_t)npx * 3;
@@ -557,6 +588,95 @@ segment_kernel(const uint8_t *__restrict__ rgb, int npx, IceScheme sc, uint8_t *
     }
 }
 
+// K1s vectorised: 16 pixels per thread per step (3 x 16 B RGB loads, one 16 B label store);
+// requires npx % 16 == 0 (tile bases are then 16 B aligned).  HBM-bound: 4 B/px.
+constexpr int SEG_VNT = 128, SEG_U = 4;
+template <bool NH, bool NS>
+__global__ void __launch_bounds__(SEG_VNT)
+segment_vec_kernel(const uint8_t *__restrict__ rgb, int npx, IceScheme sc_in, uint8_t *__restrict__ label,
+                   uint32_t *__restrict__ counts, int32_t *__restrict__ unmatched) {
+    const SchemeR sc(sc_in);
+    __shared__ int red[4][SEG_VNT / 32];
+    const size_t tile_id = blockIdx.x;
+    const uint4 *tile = reinterpret_cast<const uint4 *>(rgb + tile_id * (size_t)npx * 3);
+    uint4 *ltile = reinterpret_cast<uint4 *>(label + tile_id * (size_t)npx);
+    int c0 = 0, c1 = 0, c2 = 0, first = 0x7fffffff;
+    // Each warp moves SEG_U x 32 groups (SEG_U x 1,536 B) per step with fully coalesced 512 B
+    // loads (all issued before any is consumed), bounced through shared memory so that lane l
+    // then owns group l of each 32-group slice (pixels 16 l .. 16 l + 15).
+    __shared__ uint4 stage[SEG_VNT / 32][SEG_U * 96];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int ngroups = npx / 16;
+    uint4 *st = stage[wid];
+    for (int gb = wid * 32 * SEG_U; gb < ngroups; gb += SEG_VNT * SEG_U) {
+        const int valid = min(32 * SEG_U, ngroups - gb);
+        uint4 r[3 * SEG_U];
+#pragma unroll
+        for (int j = 0; j < 3 * SEG_U; ++j) {
+            const int idx = j * 32 + lane;
+            if (idx < 3 * valid) r[j] = __ldg(tile + 3 * (size_t)gb + idx);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 3 * SEG_U; ++j) st[j * 32 + lane] = r[j];
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < SEG_U; ++u) {
+            const int gl = u * 32 + lane;
+            if (gl < valid) {
+                const uint4 a = st[3 * gl], b = st[3 * gl + 1], c = st[3 * gl + 2];
+                const uint32_t wv[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+                uint32_t lw[4] = {0, 0, 0, 0};
+                const int g = gb + gl;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int R = (wv[(3 * k) >> 2] >> (8 * ((3 * k) & 3))) & 255;
+                    const int G = (wv[(3 * k + 1) >> 2] >> (8 * ((3 * k + 1) & 3))) & 255;
+                    const int B = (wv[(3 * k + 2) >> 2] >> (8 * ((3 * k + 2) & 3))) & 255;
+                    const int cls = classify<NH, NS>(R, G, B, sc);
+                    lw[k >> 2] |= (uint32_t)cls << (8 * (k & 3));
+                    c0 += cls == 0;
+                    c1 += cls == 1;
+                    c2 += cls == 2;
+                    if (cls == 255) first = min(first, 16 * g + k);
+                }
+                ltile[g] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+        first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        int wi = threadIdx.x >> 5;
+        red[0][wi] = c0; red[1][wi] = c1; red[2][wi] = c2; red[3][wi] = first;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < SEG_VNT / 32; ++i) {
+            c0 += red[0][i]; c1 += red[1][i]; c2 += red[2][i]; first = min(first, red[3][i]);
+        }
+        counts[3 * tile_id] = c0;
+        counts[3 * tile_id + 1] = c1;
+        counts[3 * tile_id + 2] = c2;
+        unmatched[tile_id] = first == 0x7fffffff ? -1 : first;
+    }
+}
+
+bool full_hue(const IceScheme &sc) {
+    for (int k = 0; k < 3; ++k)
+        if (sc.lo[k][0] != 0 || sc.hi[k][0] < 179) return false;
+    return true;
+}
+bool full_sat(const IceScheme &sc) {
+    for (int k = 0; k < 3; ++k)
+        if (sc.lo[k][1] != 0 || sc.hi[k][1] != 255) return false;
+    return true;
+}
+
 bool window_ok(int k, int h, int w) { return k >= 3 && (k & 1) && k <= (h < w ? h : w); }
 
 }  // namespace
@@ -577,6 +697,7 @@ extern "C" int ice_autolabel(const uint8_t *rgb, int64_t n, int32_t h, int32_t w
     Params prm;
     prm.cfg = *cfg;
     prm.scheme = *scheme;
+    prm.v_only = full_hue(*scheme) && full_sat(*scheme);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(autolabel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -596,8 +717,17 @@ extern "C" int ice_segment(const uint8_t *rgb, int64_t n, int32_t h, int32_t w,
     if (n == 0) return ICE_OK;
     if (!rgb || !label || !counts || !unmatched || n > 0x7fffffff) return ICE_EINVAL;
     if ((int64_t)h * w > 0x7fffffff / 3) return ICE_ETOOBIG;
-    segment_kernel<<<(unsigned)n, SEG_NT, 0, (cudaStream_t)stream>>>(rgb, h * w, *scheme, label, counts,
-                                                                      unmatched);
+    const int npx = h * w;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (npx % 16 == 0 && (reinterpret_cast<uintptr_t>(rgb) & 15) == 0 && (reinterpret_cast<uintptr_t>(label) & 15) == 0) {
+        const bool nh = !full_hue(*scheme), ns = !full_sat(*scheme);
+        if (!nh && !ns) segment_vec_kernel<false, false><<<(unsigned)n, SEG_VNT, 0, st>>>(rgb, npx, *scheme, label, counts, unmatched);
+        else if (nh && ns) segment_vec_kernel<true, true><<<(unsigned)n, SEG_VNT, 0, st>>>(rgb, npx, *scheme, label, counts, unmatched);
+        else if (nh) segment_vec_kernel<true, false><<<(unsigned)n, SEG_VNT, 0, st>>>(rgb, npx, *scheme, label, counts, unmatched);
+        else segment_vec_kernel<false, true><<<(unsigned)n, SEG_VNT, 0, st>>>(rgb, npx, *scheme, label, counts, unmatched);
+    } else {
+        segment_kernel<<<(unsigned)n, SEG_NT, 0, st>>>(rgb, npx, *scheme, label, counts, unmatched);
+    }
     return (int)cudaGetLastError();
 }
 
