@@ -596,6 +596,18 @@ __global__ void __launch_bounds__(SEG_VNT)
 segment_vec_kernel(const uint8_t *__restrict__ rgb, int npx, IceScheme sc_in, uint8_t *__restrict__ label,
                    uint32_t *__restrict__ counts, int32_t *__restrict__ unmatched) {
     const SchemeR sc(sc_in);
+    __shared__ uint32_t vlut[256];  // V -> class | count increment (V-only schemes)
+    if (!NH && !NS) {
+        for (int v = threadIdx.x; v < 256; v += SEG_VNT) {
+            int cls = 255;
+#pragma unroll
+            for (int k = 2; k >= 0; --k)
+                if (v >= sc.lo[k][2] && v <= sc.hi[k][2]) cls = sc.cls[k];
+            const int slot = cls == 255 ? 3 : cls;
+            vlut[v] = (uint32_t)cls | (slot <= 3 ? 1u << (12 + 5 * slot) : 0u);
+        }
+        __syncthreads();
+    }
     __shared__ int red[4][SEG_VNT / 32];
     const size_t tile_id = blockIdx.x;
     const uint4 *tile = reinterpret_cast<const uint4 *>(rgb + tile_id * (size_t)npx * 3);
@@ -628,6 +640,33 @@ segment_vec_kernel(const uint8_t *__restrict__ rgb, int npx, IceScheme sc_in, ui
                 const uint32_t wv[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
                 uint32_t lw[4] = {0, 0, 0, 0};
                 const int g = gb + gl;
+                if (!NH && !NS) {
+                    // V-only scheme: one shared-memory lookup per pixel yields the class byte and a
+                    // packed count increment; the 16 increments of a group sum without overflow.
+                    uint32_t sum = 0;
+                    uint32_t e[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        // one PRMT per channel byte (zero-extended), one 3-way max
+                        const uint32_t R = __byte_perm(wv[(3 * k) >> 2], 0, 0x4440 | ((3 * k) & 3));
+                        const uint32_t G = __byte_perm(wv[(3 * k + 1) >> 2], 0, 0x4440 | ((3 * k + 1) & 3));
+                        const uint32_t B = __byte_perm(wv[(3 * k + 2) >> 2], 0, 0x4440 | ((3 * k + 2) & 3));
+                        e[k] = vlut[max(R, max(G, B))];
+                        sum += e[k];
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        lw[q] = __byte_perm(__byte_perm(e[4 * q], e[4 * q + 1], 0x0040),
+                                            __byte_perm(e[4 * q + 2], e[4 * q + 3], 0x0040), 0x5410);
+                    c0 += (sum >> 12) & 31;
+                    c1 += (sum >> 17) & 31;
+                    c2 += (sum >> 22) & 31;
+                    if (sum >> 27) {
+#pragma unroll
+                        for (int k = 15; k >= 0; --k)
+                            if ((e[k] & 255) == 255) first = min(first, 16 * g + k);
+                    }
+                } else {
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
                     const int R = (wv[(3 * k) >> 2] >> (8 * ((3 * k) & 3))) & 255;
@@ -639,6 +678,7 @@ segment_vec_kernel(const uint8_t *__restrict__ rgb, int npx, IceScheme sc_in, ui
                     c1 += cls == 1;
                     c2 += cls == 2;
                     if (cls == 255) first = min(first, 16 * g + k);
+                }
                 }
                 ltile[g] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
             }

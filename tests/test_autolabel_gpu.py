@@ -137,6 +137,67 @@ def test_segment_batch_counts_and_unmatched():
         assert res["counts"][i].tolist() == np.bincount(want.ravel(), minlength=256)[:3].tolist()
 
 
+HUE_ONLY = il.SegmentationScheme("hue-only", (
+    il.ColorRange(il.ClassId.THICK_ICE, (20, 0, 205), (150, 255, 255)),
+    il.ColorRange(il.ClassId.THIN_ICE, (0, 0, 31), (179, 255, 204)),
+    il.ColorRange(il.ClassId.OPEN_WATER, (40, 0, 0), (179, 255, 30))))
+HUE_SAT = il.SegmentationScheme("hue-sat", (
+    il.ColorRange(il.ClassId.THICK_ICE, (20, 10, 205), (150, 255, 255)),
+    il.ColorRange(il.ClassId.THIN_ICE, (0, 0, 31), (170, 240, 204)),
+    il.ColorRange(il.ClassId.OPEN_WATER, (0, 30, 0), (179, 255, 30))))
+
+
+def _ranges(scheme):
+    return tuple((int(r.class_id), tuple(r.lower), tuple(r.upper)) for r in scheme.ranges)
+
+
+@pytest.mark.parametrize("scheme", [il.ROSS_SEA_SUMMER, SAT_ONLY, HUE_ONLY, HUE_SAT], ids=lambda s: s.name)
+@pytest.mark.parametrize("shape", [(5, 64, 64), (3, 16, 48), (2, 256, 256)])
+def test_segment_vec_variants_vs_oracle(scheme, shape):
+    """K1s vectorised kernel (npx % 16 == 0): one template variant per scheme kind."""
+    rng = np.random.default_rng(shape[1] * 7 + len(scheme.name))
+    tiles = rng.integers(0, 256, shape + (3,), dtype=np.uint8)
+    tiles[0] = 0
+    tiles[-1, ::2] = 255
+    res = il.segment_batch(torch.from_numpy(tiles).cuda(), scheme)
+    lab = res["label"].cpu().numpy()
+    for i in range(shape[0]):
+        want, first = orc.segment(tiles[i], _ranges(scheme))
+        assert np.array_equal(lab[i], want), i
+        assert int(res["unmatched"][i]) == first, i
+        assert res["counts"][i].tolist() == np.bincount(want.ravel(), minlength=256)[:3].tolist(), i
+
+
+def test_segment_vec_raw_scheme_gaps_and_overlaps():
+    """C ABI with a raw IceScheme the Python types would reject: V gaps (unmatched pixels),
+    overlapping ranges (first wins) and a class id outside 0..2 (labelled, never counted)."""
+    from paper_2403_13135_b200 import _native
+    ranges = ((0, (0, 0, 200), (179, 255, 250)), (2, (0, 0, 10), (179, 255, 60)),
+              (7, (0, 0, 40), (179, 255, 220)))  # class-id order, as the oracle applies them
+    sc = _native.IceScheme()
+    for k, (c, lo, hi) in enumerate(ranges):
+        for ch in range(3):
+            sc.lo[k][ch], sc.hi[k][ch] = lo[ch], hi[ch]
+        sc.cls[k] = c
+    rng = np.random.default_rng(9)
+    tiles = rng.integers(0, 256, (6, 32, 64, 3), dtype=np.uint8)
+    tiles[1] = 255  # all unmatched from pixel 0
+    tiles[2] = 5
+    dev = torch.from_numpy(tiles).cuda()
+    n, h, w, _ = tiles.shape
+    label = torch.empty((n, h, w), dtype=torch.uint8, device="cuda")
+    counts = torch.empty((n, 3), dtype=torch.int32, device="cuda")
+    unmatched = torch.empty(n, dtype=torch.int32, device="cuda")
+    _native.call("ice_segment", dev.data_ptr(), n, h, w, sc, label.data_ptr(), counts.data_ptr(),
+                 unmatched.data_ptr(), _native.stream_handle())
+    lab = label.cpu().numpy()
+    for i in range(n):
+        want, first = orc.segment(tiles[i], ranges)
+        assert np.array_equal(lab[i], want), i
+        assert int(unmatched[i]) == first, i
+        assert counts[i].tolist() == np.bincount(want.ravel(), minlength=256)[:3].tolist(), i
+
+
 def test_empty_batch_and_window_errors():
     out = il.autolabel(torch.empty((0, 32, 32, 3), dtype=torch.uint8, device="cuda"))
     assert out["label"].shape == (0, 32, 32)
