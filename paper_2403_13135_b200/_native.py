@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_C", "libicelabel_b200.so")
+LIB_PATH = os.environ.get("ICE_LIB_PATH") or os.path.join(_HERE, "_C", "libicelabel_b200.so")
 
 ICE_OK, ICE_EINVAL, ICE_EWINDOW, ICE_ETOOBIG, ICE_ENODRIVER = 0, -1, -2, -3, -4
 _ERRNAMES = {ICE_EINVAL: "ICE_EINVAL", ICE_EWINDOW: "ICE_EWINDOW", ICE_ETOOBIG: "ICE_ETOOBIG",

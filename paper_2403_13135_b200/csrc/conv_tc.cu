@@ -59,6 +59,20 @@ struct Taps {
     int8_t dy[9], dx[9], plane[9], wt[9];  // pixel shift, source plane (5-D maps), weight tap
 };
 
+// 8 consecutive floats (or `fill` when p is null); 16 B vector loads when p is aligned
+__device__ __forceinline__ void ld8(const float *p, float fill, float (&o)[8]) {
+    if (!p) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = fill;
+    } else if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(p)), b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+        o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = __ldg(p + i);
+    }
+}
+
 // Column sums of a warp's 32 rows x 32 columns (one row per lane): after 31 shuffles lane j
 // holds the sum of column j over the 32 rows.
 __device__ __forceinline__ float warp_col_sum32(float (&v)[32], int lane) {
@@ -143,23 +157,21 @@ struct FpropProb {
             if (!valid) continue;
             const int col0 = nt * BN + cc * 32;
             uint4 *dst = reinterpret_cast<uint4 *>(y + ((size_t)((size_t)n * OH + h) * OW + w) * cout + col0);
+            const float *dr = drop ? drop + (size_t)n * cout + col0 : nullptr;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
+                float bq[8], dq[8];
+                ld8(bias ? bias + col0 + q * 8 : nullptr, 0.f, bq);
+                ld8(dr ? dr + q * 8 : nullptr, 1.f, dq);
                 uint32_t pk[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    int j = q * 8 + e * 2;
-                    float a = v[j] + (bias ? __ldg(bias + col0 + j) : 0.f);
-                    float b = v[j + 1] + (bias ? __ldg(bias + col0 + j + 1) : 0.f);
+                    float a = v[q * 8 + 2 * e] + bq[2 * e], b = v[q * 8 + 2 * e + 1] + bq[2 * e + 1];
                     if (relu) {
                         a = fmaxf(a, 0.f);
                         b = fmaxf(b, 0.f);
                     }
-                    if (drop) {
-                        a *= __ldg(drop + (size_t)n * cout + col0 + j);
-                        b *= __ldg(drop + (size_t)n * cout + col0 + j + 1);
-                    }
-                    pk[e] = tc::pack_bf16(a, b);
+                    pk[e] = tc::pack_bf16(a * dq[2 * e], b * dq[2 * e + 1]);
                 }
                 dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
@@ -499,16 +511,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
                     const uint32_t ph = (it / STAGES) & 1;
                     tc::mbar_wait(&full[s], ph);
                     tc::tc_fence_after();
-                    const uint32_t a0 = tc::smem_u32(sa + s * A_BYTES);
-                    const uint32_t b0 = tc::smem_u32(sb + s * B_BYTES);
+                    // descriptors built once per stage; per-k steps are plain adds of the
+                    // encoded (addr >> 4) start field (smem offsets stay below 2^18, no carry)
+                    const uint64_t ad0 = tc::sw128_desc(tc::smem_u32(sa + s * A_BYTES), P::A_MN ? 8192 : 16, 1024);
+                    const uint64_t bd0 = tc::sw128_desc(tc::smem_u32(sb + s * B_BYTES), P::B_MN ? 8192 : 16, 1024);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        const uint64_t ad = P::A_MN ? tc::sw128_desc(a0 + k * 2048, 8192, 1024)
-                                                    : tc::sw128_desc(a0 + k * 32, 16, 1024);
-                        const uint64_t bd = P::B_MN ? tc::sw128_desc(b0 + k * 2048, 8192, 1024)
-                                                    : tc::sw128_desc(b0 + k * 32, 16, 1024);
-                        tc::umma_f16(d, ad, bd, idesc, (i | k) != 0 ? 1u : 0u);
-                    }
+                    for (int k = 0; k < BK / 16; ++k)
+                        tc::umma_f16(d, ad0 + (P::A_MN ? 128 : 2) * k, bd0 + (P::B_MN ? 128 : 2) * k, idesc,
+                                     (i | k) != 0 ? 1u : 0u);
                     tc::umma_commit(&empty[s]);
                 }
                 tc::umma_commit(&tfull[acc]);
@@ -568,8 +578,8 @@ constexpr int halo_smem_bytes() {
 // RES (resident weights): single-chunk problems (64 input channels) keep all 9 weight taps
 // of the current column tile in smem; they are reloaded only when the persistent CTA moves
 // to another column tile, so the MMA thread waits once per tile (36 MMAs per wait).
-template <int BN, int BSTAGES, bool RES, class P>
-__global__ void __launch_bounds__(NTHREADS, 1) halo_gemm(const __grid_constant__ P p, const TileGrid g) {
+template <int BN, int BSTAGES, bool RES, class P, bool DUAL>
+__global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const __grid_constant__ P p, const TileGrid g) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int B_TAP = BN * BK * 2;
@@ -625,8 +635,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) halo_gemm(const __grid_constant__
                 for (int ch = 0; ch < nch; ++ch, ++ait) {
                     const int as = ait & 1;
                     tc::mbar_wait(&aempty[as], ((ait >> 1) & 1) ^ 1);
+#ifdef ICE_EXP_NOTMA
+                    tc::mbar_arrive(&afull[as]);
+#else
                     tc::mbar_expect_tx(&afull[as], HALO_TX);
                     p.load_halo(ch, sa + as * HALO_BYTES, &afull[as], mt);
+#endif
                     if (RES) continue;
                     for (int r = 0; r < 9 / TAPS_PER_SLOT; ++r, ++bit) {
                         const int bs = bit % BSTAGES;
@@ -639,9 +653,48 @@ __global__ void __launch_bounds__(NTHREADS, 1) halo_gemm(const __grid_constant__
                 }
             }
         }
+    } else if (DUAL && (warp == 1 || warp == 2 + EPI_WARPS)) {
+        // Two MMA issuers (single column tile, resident weights): the tensor pipe accepts an
+        // MMA only when the previous one is nearly done, so an issuer's per-tile barrier waits
+        // and bookkeeping would idle it; issuer i owns the CTA's tiles j = i mod 2 together
+        // with A slot i and accumulator i, and the other issuer's MMAs fill its gaps.
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, false, P::B_MN);
+            const int iss = warp == 1 ? 0 : 1;
+            uint32_t voff[9];
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) voff[tap] = p.view_row(tap) * 8;
+            const uint64_t adesc = tc::sw128_desc(tc::smem_u32(sa + iss * HALO_BYTES), 16, 1024);
+            const uint64_t bdesc = tc::sw128_desc(tc::smem_u32(sb), P::B_MN ? 8192 : 16, 1024);
+            const uint32_t d = tmem + iss * BN;
+            tc::mbar_wait(&bfull[0], 0);
+            int j = iss;
+            for (int t = blockIdx.x + iss * gridDim.x; t < ntiles; t += 2 * gridDim.x, j += 2) {
+                const uint32_t ph = (j >> 1) & 1;
+                tc::mbar_wait(&tempty[iss], ph ^ 1);
+                tc::mbar_wait(&afull[iss], ph);
+                tc::tc_fence_after();
+#pragma unroll
+                for (int tap = 0; tap < 9; ++tap) {
+                    const uint64_t ad = adesc + voff[tap];
+                    const uint64_t bd = bdesc + tap * (B_TAP >> 4);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        tc::umma_f16(d, ad + 2 * k, bd + (P::B_MN ? 128 : 2) * k, idesc, (tap | k) != 0 ? 1u : 0u);
+                }
+                tc::umma_commit(&aempty[iss]);
+                tc::umma_commit(&tfull[iss]);
+            }
+        }
+        __syncwarp();
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, false, P::B_MN);
+            // per-tap window offsets in descriptor units (128 B halo rows), hoisted out of the
+            // tile loop: a constant-bank load chain per tap would stall every tap's first MMA
+            uint32_t voff[9];
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) voff[tap] = p.view_row(tap) * 8;
             int ait = 0, bit = 0, local = 0, cur_nt = -1, run = -1;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
                 int mt, nt, z;
@@ -659,7 +712,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) halo_gemm(const __grid_constant__
                     const int as = ait & 1;
                     tc::mbar_wait(&afull[as], (ait >> 1) & 1);
                     tc::tc_fence_after();
-                    const uint32_t abase = tc::smem_u32(sa + as * HALO_BYTES);
+                    const uint64_t adesc = tc::sw128_desc(tc::smem_u32(sa + as * HALO_BYTES), 16, 1024);
+#pragma unroll
                     for (int r = 0; r < 9 / TAPS_PER_SLOT; ++r) {
                         int bs = 0;
                         uint32_t bslot;
@@ -671,18 +725,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) halo_gemm(const __grid_constant__
                             tc::tc_fence_after();
                             bslot = tc::smem_u32(sb + bs * B_BYTES);
                         }
+                        const uint64_t bdesc = tc::sw128_desc(bslot, P::B_MN ? 8192 : 16, 1024);
 #pragma unroll
                         for (int q = 0; q < TAPS_PER_SLOT; ++q) {
                             const int tap = r * TAPS_PER_SLOT + q;
-                            const uint32_t a0 = abase + p.view_row(tap) * 128;
-                            const uint32_t b0 = bslot + q * B_TAP;
+                            const uint64_t ad = adesc + voff[tap];
+                            const uint64_t bd = bdesc + q * (B_TAP >> 4);
 #pragma unroll
-                            for (int k = 0; k < BK / 16; ++k) {
-                                const uint64_t ad = tc::sw128_desc(a0 + k * 32, 16, 1024);
-                                const uint64_t bd = P::B_MN ? tc::sw128_desc(b0 + k * 2048, 8192, 1024)
-                                                            : tc::sw128_desc(b0 + k * 32, 16, 1024);
-                                tc::umma_f16(d, ad, bd, idesc, (ch | tap | k) != 0 ? 1u : 0u);
-                            }
+                            for (int k = 0; k < BK / 16; ++k)
+                                tc::umma_f16(d, ad + 2 * k, bd + (P::B_MN ? 128 : 2) * k, idesc,
+                                             (ch | tap | k) != 0 ? 1u : 0u);
                         }
                         if (!RES) {
                             tc::umma_commit(&bempty[bs]);
@@ -700,7 +752,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) halo_gemm(const __grid_constant__
             }
         }
         __syncwarp();
-    } else {
+    } else if (warp < 2 + EPI_WARPS) {
         const int sub = warp & 3, half = (warp - 2) >> 2;
         constexpr int NCH = BN / 32, PER = (NCH + 1) / 2;
         const int cc0 = half * PER, cc1 = min(NCH, (half + 1) * PER);
@@ -717,8 +769,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) halo_gemm(const __grid_constant__
             const int acc = local & 1;
             tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
             tc::tc_fence_after();
+#ifndef ICE_EXP_NOEPI
             p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z, cc0,
                                     cc1, bacc);
+#endif
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
@@ -867,12 +921,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                             const bool sw = a1 < a0;
                             const uint32_t lo = sw ? a1 : a0, dl = sw ? a0 - a1 : a1 - a0;
                             const uint32_t d = tmem + (mt - mt0) * COUT;
+                            const uint64_t ad = tc::sw128_desc(lo, dl, 1024);
+                            const uint64_t bd = tc::sw128_desc(bbase, 8192, 1024);
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const uint64_t ad = tc::sw128_desc(lo + k * 2048, dl, 1024);
-                                const uint64_t bd = tc::sw128_desc(bbase + k * 2048, 8192, 1024);
-                                tc::umma_f16(d, ad, bd, idesc, (kb > kb0 || cls > 0 || k > 0) ? 1u : 0u);
-                            }
+                            for (int k = 0; k < 4; ++k)
+                                tc::umma_f16(d, ad + 128 * k, bd + 128 * k, idesc,
+                                             (kb > kb0 || cls > 0 || k > 0) ? 1u : 0u);
                         }
                     }
                     tc::umma_commit(&empty[s]);
@@ -1053,21 +1107,21 @@ const int8_t HALVE_CLS[9] = {0, 1, 1, 2, 2, 3, 3, 3, 3};
 const int8_t HALVE_DY[9] = {0, 0, 0, 0, 1, 0, 0, 1, 1};
 const int8_t HALVE_DX[9] = {0, 0, 1, 0, 0, 0, 1, 0, 1};
 
-template <int BN, int BSTAGES, bool RES, class P>
+template <int BN, int BSTAGES, bool RES, class P, bool DUAL = false>
 int launch_halo(const P &p, dim3 tiles, cudaStream_t st) {
     constexpr int smem = halo_smem_bytes<BN, BSTAGES, RES>();
     static_assert(smem <= 232448, "halo kernel smem");
     static bool attr = false;
     if (!attr) {
-        cudaError_t e =
-            cudaFuncSetAttribute(halo_gemm<BN, BSTAGES, RES, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(halo_gemm<BN, BSTAGES, RES, P, DUAL>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }
     TileGrid g{(int)tiles.x, (int)tiles.y, (int)tiles.z};
     const long long total = (long long)tiles.x * tiles.y * tiles.z;
     const int grid = (int)(total < num_sms() ? total : num_sms());
-    halo_gemm<BN, BSTAGES, RES, P><<<grid, NTHREADS, smem, st>>>(p, g);
+    halo_gemm<BN, BSTAGES, RES, P, DUAL><<<grid, NTHREADS + (DUAL ? 32 : 0), smem, st>>>(p, g);
     return (int)cudaGetLastError();
 }
 
@@ -1081,6 +1135,7 @@ template <class P>
 int run_halo(const P &p, int nch, int ncols, dim3 tiles_m, cudaStream_t st) {
     if (halo_bn(nch, ncols) == 64 && nch == 1) {  // all 9 weight taps resident
         dim3 tiles(tiles_m.x, ncols / 64, 1);
+        if (ncols == 64 && !getenv("ICE_NO_DUAL")) return launch_halo<64, 1, true, P, true>(p, tiles, st);
         return launch_halo<64, 1, true>(p, tiles, st);
     }
     if (halo_bn(nch, ncols) == 128) {  // N = 128 halves the smem bytes per MMA FLOP
