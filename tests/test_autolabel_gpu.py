@@ -206,3 +206,76 @@ def test_empty_batch_and_window_errors():
     res = il.process_tile(il.Tile(il.SceneRaster(np.zeros((5, 5, 3), np.uint8)), "s", 0, 0),
                           il.FilterConfig(), il.ROSS_SEA_SUMMER)
     assert res.error == "ValueError: window 7 exceeds image extent (5, 5)"
+
+
+def _edge_tiles():
+    """Hand-made 256 x 256 tiles for the SWAR kernel's corner cases."""
+    rng = np.random.default_rng(2024)
+    const = np.full((256, 256, 3), 97, np.uint8)
+    white = np.full((256, 256, 3), 255, np.uint8)
+    black = np.zeros((256, 256, 3), np.uint8)
+    two = np.where(rng.random((256, 256, 1)) < 0.5, 20, 230).astype(np.uint8).repeat(3, 2)
+    stripes = np.zeros((256, 256, 3), np.uint8)
+    stripes[:, ::7] = 255
+    stripes[::5] = 128
+    corner = np.full((256, 256, 3), 200, np.uint8)
+    corner[:11, :11] = 3        # exercises the replicated border weights of the 21 x 21 window
+    corner[-11:, -11:] = 250
+    ramp = np.broadcast_to(np.arange(256, dtype=np.uint8)[None, :, None], (256, 256, 3)).copy()
+    return [const, white, black, two, stripes, corner, ramp, ramp.transpose(1, 0, 2).copy()]
+
+
+def _run_path(tiles, mode, cfg=None, scheme=il.ROSS_SEA_SUMMER):
+    from paper_2403_13135_b200 import _native
+    _native.call("ice_autolabel_set_path", mode)
+    try:
+        dev = torch.from_numpy(np.stack(tiles)).cuda()
+        res = il.autolabel(dev, cfg or il.FilterConfig(), scheme, want_mask=True)
+        torch.cuda.synchronize()
+        return {k: v.cpu().numpy() for k, v in res.items() if v is not None}
+    finally:
+        _native.call("ice_autolabel_set_path", 0)
+
+
+@pytest.mark.parametrize("cfg", [il.FilterConfig(), il.FilterConfig(mask_mode="fixed", fixed_t=40),
+                                 il.FilterConfig(diff_truncate=True, truncate_t=9)],
+                         ids=["default", "fixed40", "trunc9"])
+def test_swar_kernel_matches_generic_kernel(cfg):
+    """The SWAR 256 x 256 kernel and the generic kernel agree on every output."""
+    tiles = [rgb for rgb, _ in synth.corpus(13, 12, 0.5)]
+    tiles += [synth.tint(t, 13, i) for i, t in enumerate(tiles[:4])]
+    tiles += [synth.random_tile(300 + i) for i in range(3)] + _edge_tiles()
+    fast = _run_path(tiles, 2, cfg)
+    gen = _run_path(tiles, 1, cfg)
+    for k in gen:
+        for i in range(len(tiles)):
+            assert np.array_equal(fast[k][i], gen[k][i]), (k, i)
+
+
+def test_swar_kernel_vs_oracle_hsv_scheme():
+    """SWAR kernel with a hue/saturation scheme (per-pixel HSV classify) against the oracle."""
+    tiles = [synth.tint(rgb, 17, i) for i, (rgb, _) in enumerate(synth.corpus(17, 4, 1.0))]
+    tiles += [synth.random_tile(900), _edge_tiles()[3]]
+    out = _run_path(tiles, 2, None, SAT_ONLY)
+    for i, t in enumerate(tiles):
+        f, m, a = orc.apply_filter(t)
+        assert np.array_equal(out["filtered"][i], f), i
+        assert np.array_equal(out["mask"][i], m), i
+        assert out["affected"][i] == a, i
+        lbl, first = orc.segment(f, _ranges(SAT_ONLY))
+        assert np.array_equal(out["label"][i], lbl), i
+        assert out["unmatched"][i] == first, i
+
+
+def test_swar_kernel_edge_tiles_vs_oracle():
+    tiles = _edge_tiles()
+    out = _run_path(tiles, 2)
+    for i, t in enumerate(tiles):
+        f, m, a = orc.apply_filter(t)
+        lbl, first = orc.segment(f)
+        assert np.array_equal(out["filtered"][i], f), i
+        assert np.array_equal(out["mask"][i], m), i
+        assert out["affected"][i] == a, i
+        assert np.array_equal(out["label"][i], lbl), i
+        assert out["unmatched"][i] == first, i
+        assert out["counts"][i].tolist() == np.bincount(lbl.ravel(), minlength=256)[:3].tolist(), i

@@ -1,0 +1,44 @@
+"""Time K1 paths over resident T-gray / T-rand tiles (CUDA events).  Dev tool, not the bench.
+
+    python tools/time_autolabel.py [--tiles 14800] [--kind tgray|trand|tint] [--path 0|1|2]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2403_13135_b200 import _native  # noqa: E402
+from paper_2403_13135_b200 import icelabel as il  # noqa: E402
+from paper_2403_13135_b200.icelabel import synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--tiles", type=int, default=14800)
+ap.add_argument("--uniq", type=int, default=296)
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--kind", default="tgray")
+ap.add_argument("--path", type=int, default=0)
+a = ap.parse_args()
+if a.kind == "trand":
+    u = np.stack([synth.random_tile(i) for i in range(a.uniq)])
+elif a.kind == "tint":
+    u = np.stack([synth.tint(t, 101, i) for i, (t, _) in enumerate(synth.corpus(101, a.uniq, 0.3))])
+else:
+    u = np.stack([t for t, _ in synth.corpus(101, a.uniq, 0.3)])
+x = torch.from_numpy(u).cuda()[torch.arange(a.tiles) % a.uniq]
+_native.call("ice_autolabel_set_path", a.path)
+out = il.autolabel(x)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(a.reps):
+    il.autolabel(x, out=out)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / a.reps
+px = a.tiles * 65536
+print(f"{a.kind} path={a.path} tiles={a.tiles}: {ms:.2f} ms  {px / ms / 1e6:.1f} Gpx/s  "
+      f"{px * 7 / ms / 1e6:.1f} GB/s  us/tile/SM={ms * 1000 * 148 / a.tiles:.1f}")
