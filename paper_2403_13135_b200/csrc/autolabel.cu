@@ -740,6 +740,8 @@ struct SmemF {
     uint8_t vals[256];
     int red[NTF / 32][4];
     int bc[8];
+    int act[16];            // median21 block activity, [band][half]
+    uint32_t hist_v[256];   // histogram of V (channel median of the gray repair)
 };
 
 __device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, int n) { return __funnelshift_r(lo, hi, n); }
@@ -759,15 +761,6 @@ __device__ __forceinline__ uint32_t gt4(uint32_t x, uint32_t c4, uint32_t c7f) {
 __device__ __forceinline__ uint32_t ldw(const uint32_t *row, int k) {
     return k < 0 ? rep0(row[0]) : (k > 63 ? rep3(row[63]) : row[k]);
 }
-__device__ __forceinline__ void ce(uint32_t &a, uint32_t &b) {
-    const uint32_t lo = vmin(a, b), hi = vmax(a, b);
-    a = lo;
-    b = hi;
-}
-__device__ __forceinline__ uint32_t med3(uint32_t a, uint32_t b, uint32_t c) {
-    return vmax(vmin(a, b), vmin(vmax(a, b), c));
-}
-
 // ---- 7 x 7 dilation (kernels.py:49-54): src -> tmp (row max) -> dst (column max) ----------
 // Also records the presence of every value of dst in s.flags.
 __device__ void dilate7(const uint32_t *src, uint32_t *tmp, uint32_t *dst, SmemF &s) {
@@ -841,48 +834,74 @@ __device__ int collect_values(SmemF &s) {
 }
 
 // ---- row pass of one threshold: dst(y, x) = #{j in [x-10, x+10] : src(y, clamp j) > t} ----
+// 16 output words per call.  local j <-> word k = m0 - 3 + j.  s2: 2-px sums, s4: 4-px sums
+// (<= 4 per byte), t_k = s4_k + .. + s4_{k+4} + i_{k+5}: the 21 px from 4k + byte.
+// EDGE: 0 interior, 1 left tile edge (m0 == 0), 2 right tile edge (m0 == 48).
+template <int EDGE>
+__device__ __forceinline__ void row_chunk(const uint32_t *sr, uint32_t *dr, int m0, uint32_t c4, uint32_t c7f) {
+    uint32_t I[23], S2[22], S4[21], T[17];
+#pragma unroll
+    for (int j = 0; j < 23; ++j) {
+        uint32_t w;
+        if (EDGE == 1 && j < 3) w = rep0(sr[0]);
+        else if (EDGE == 2 && j >= 19) w = rep3(sr[63]);
+        else w = sr[m0 - 3 + j];
+        I[j] = gt4(w, c4, c7f);
+    }
+#pragma unroll
+    for (int j = 0; j < 22; ++j) S2[j] = I[j] + fsr(I[j], I[j + 1], 8);
+#pragma unroll
+    for (int j = 0; j < 21; ++j) S4[j] = S2[j] + fsr(S2[j], S2[j + 1], 16);
+#pragma unroll
+    for (int j = 0; j < 17; ++j) T[j] = (S4[j] + S4[j + 1]) + (S4[j + 2] + S4[j + 3]) + S4[j + 4] + I[j + 5];
+    // pixel 4m + i has its window start at 4(m - 3) + i + 2
+#pragma unroll
+    for (int j = 0; j < 16; ++j) dr[m0 + j] = fsr(T[j], T[j + 1], 16);
+}
+
 __device__ __forceinline__ void row_counts(const uint32_t *src, uint32_t *dst, uint32_t c4, uint32_t c7f) {
     const int row = threadIdx.x & 255, half = threadIdx.x >> 8;
     const uint32_t *sr = src + row * WP;
     uint32_t *dr = dst + row * WP;
-    // Two chunks of 16 output words.  local j <-> word k = m0 - 3 + j.  s2: 2-px sums, s4:
-    // 4-px sums (<= 4 per byte), t_k = s4_k + .. + s4_{k+4} + i_{k+5}: the 21 px from 4k + byte
-#pragma unroll 1
-    for (int m0 = half * 32; m0 < half * 32 + 32; m0 += 16) {
-        uint32_t I[23], S2[22], S4[21], T[17];
-#pragma unroll
-        for (int j = 0; j < 23; ++j) I[j] = gt4(ldw(sr, m0 - 3 + j), c4, c7f);
-#pragma unroll
-        for (int j = 0; j < 22; ++j) S2[j] = I[j] + fsr(I[j], I[j + 1], 8);
-#pragma unroll
-        for (int j = 0; j < 21; ++j) S4[j] = S2[j] + fsr(S2[j], S2[j + 1], 16);
-#pragma unroll
-        for (int j = 0; j < 17; ++j) T[j] = (S4[j] + S4[j + 1]) + (S4[j + 2] + S4[j + 3]) + S4[j + 4] + I[j + 5];
-        // pixel 4m + i has its window start at 4(m - 3) + i + 2
-#pragma unroll
-        for (int j = 0; j < 16; ++j) dr[m0 + j] = fsr(T[j], T[j + 1], 16);
+    if (half == 0) {
+        row_chunk<1>(sr, dr, 0, c4, c7f);
+        row_chunk<0>(sr, dr, 16, c4, c7f);
+    } else {
+        row_chunk<0>(sr, dr, 32, c4, c7f);
+        row_chunk<2>(sr, dr, 48, c4, c7f);
     }
 }
 
 // ---- column pass: window count >= MGE (median > t) adds gap to the pixel's median --------
-__device__ __forceinline__ uint32_t col_pass(const uint32_t *cnt, uint32_t *acc, uint32_t gap) {
-    const int c = threadIdx.x & 63, y0 = (threadIdx.x >> 6) * 32;
+// Sliding 16-bit lane sums (even / odd pixels of the word), biased by K so that bit 15 of a
+// lane is the comparison.  EDGE: 0 interior band, 1 top band, 2 bottom band (clamped rows).
+template <int EDGE>
+__device__ __forceinline__ uint32_t col_band(const uint32_t *cnt, uint32_t *acc, uint32_t gap, int c, int y0) {
     constexpr uint32_t M = 0x00ff00ffu;
     constexpr uint32_t K = (0x8000u - MGE) * 0x00010001u;
-    uint32_t ae = 0, ao = 0, any = 0;
+    uint32_t ae = K, ao = K, any = 0;
 #pragma unroll
     for (int j = -MR; j <= MR; ++j) {
-        const uint32_t w = cnt[clampi(y0 + j, 0, 255) * WP + c];
+        const uint32_t w = cnt[(EDGE ? clampi(y0 + j, 0, 255) : y0 + j) * WP + c];
         ae += w & M;
         ao += (w >> 8) & M;
     }
+    const uint32_t *pn = cnt + (y0 + MR + 1) * WP + c;
+    const uint32_t *po = cnt + (y0 - MR) * WP + c;
+    uint32_t *pa = acc + y0 * WP + c;
 #pragma unroll 8
-    for (int y = y0; y < y0 + 32; ++y) {
-        const uint32_t bits = (((ae + K) >> 15) & 0x00010001u) | (((ao + K) >> 7) & 0x01000100u);
-        acc[y * WP + c] += bits * gap;
+    for (int y = 0; y < 32; ++y) {
+        const uint32_t bits = ((ae >> 15) & 0x00010001u) | ((ao >> 7) & 0x01000100u);
+        pa[y * WP] += bits * gap;
         any |= bits;
-        const uint32_t n = cnt[min(y + MR + 1, 255) * WP + c];
-        const uint32_t o = cnt[max(y - MR, 0) * WP + c];
+        uint32_t n, o;
+        if (EDGE == 0) {
+            n = pn[y * WP];
+            o = po[y * WP];
+        } else {
+            n = cnt[min(y0 + y + MR + 1, 255) * WP + c];
+            o = cnt[max(y0 + y - MR, 0) * WP + c];
+        }
         ae += (n & M) - (o & M);
         ao += ((n >> 8) & M) - ((o >> 8) & M);
     }
@@ -891,54 +910,129 @@ __device__ __forceinline__ uint32_t col_pass(const uint32_t *cnt, uint32_t *acc,
 
 // 21 x 21 median of src (kernels.py:42-46) into the plane acc ("col" map).  The value set
 // must already be flagged in s.flags (dilate7 does that).  tmp is scratch.
+// Block skipping: a (band, half) block whose pixels all had median <= t after a pass stays
+// final for every larger threshold (the counts are monotone in t), so its column pass is
+// skipped, and a row-pass warp runs only while a block it feeds (+-10 rows) is active.
 __device__ void median21(const uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s) {
     const int nd = collect_values(s);
+#ifdef ICE_AL_PROF
+    if (threadIdx.x == 0) atomicAdd(&g_al_prof[8], (unsigned long long)nd);
+#endif
     const uint32_t v0 = s.vals[0] * 0x01010101u;
-    {
-        const int c = threadIdx.x & 63, y0 = (threadIdx.x >> 6) * 32;
-        for (int y = y0; y < y0 + 32; ++y) acc[y * WP + c] = v0;
-    }
+    const int c = threadIdx.x & 63, band = threadIdx.x >> 6, lane = threadIdx.x & 31;
+    const int rwarp = (threadIdx.x & 255) >> 5, rhalf = threadIdx.x >> 8;  // row map: rows 32 rwarp..
+    for (int y = band * 32; y < band * 32 + 32; ++y) acc[y * WP + c] = v0;
+    if (threadIdx.x < 16) s.act[threadIdx.x] = 1;
     uint32_t any = 1;
     for (int i = 0; i + 1 < nd; ++i) {
         const uint32_t t = s.vals[i], gap = (uint32_t)s.vals[i + 1] - t;
         const uint32_t c4 = (255u - t) * 0x01010101u;
-        if (!__syncthreads_or(any)) break;  // previous pass moved no pixel: medians all final
-        row_counts(src, tmp, c4, c4 & 0x7f7f7f7fu);
+        if (!__syncthreads_or(any)) break;  // no pixel moved in the previous pass: all final
+        const int* act = s.act;
+        if (act[2 * rwarp + rhalf] | (rwarp > 0 ? act[2 * (rwarp - 1) + rhalf] : 0) |
+            (rwarp < 7 ? act[2 * (rwarp + 1) + rhalf] : 0))
+            row_counts(src, tmp, c4, c4 & 0x7f7f7f7fu);
         __syncthreads();
-        any = col_pass(tmp, acc, gap);
+        const int blk = 2 * band + (c >> 5);
+#ifdef ICE_AL_PROF
+        if (threadIdx.x == 0) {
+            int na = 0;
+            for (int k = 0; k < 16; ++k) na += act[k];
+            atomicAdd(&g_al_prof[9], 1ull);
+            atomicAdd(&g_al_prof[10], (unsigned long long)na);
+        }
+#endif
+        any = 0;
+        if (act[blk]) {
+            any = band == 0 ? col_band<1>(tmp, acc, gap, c, 0)
+                            : (band == 7 ? col_band<2>(tmp, acc, gap, c, 224) : col_band<0>(tmp, acc, gap, c, band * 32));
+            const bool wa = __any_sync(0xffffffffu, any != 0);
+            if (lane == 0) s.act[blk] = wa;
+        }
     }
     __syncthreads();
     if (threadIdx.x < 256) s.flags[threadIdx.x] = 0;  // ready for the next median
 }
 
 // ---- 3 x 3 median (noise_median_k = 3) of src into dst, "col" map ----------------------
+// In 16-bit lanes (native VIMNMX.U16x2): E = even pixels (bytes 0, 2), O = odd (bytes 1, 3).
+// Even pixel 4c+2i has neighbours O_{c-1}/O_c (funnel) and O_c; odd pixel 4c+2i+1 has E_c
+// and E_c/E_{c+1}.  Column-sorted triples give median9 = med3(max of mins, med of mids,
+// min of maxes).
+__device__ __forceinline__ uint32_t mn2(uint32_t a, uint32_t b) { return __vminu2(a, b); }
+__device__ __forceinline__ uint32_t mx2(uint32_t a, uint32_t b) { return __vmaxu2(a, b); }
+__device__ __forceinline__ void sort3_2(uint32_t a, uint32_t b, uint32_t c, uint32_t &lo, uint32_t &md,
+                                        uint32_t &hi) {
+    const uint32_t l1 = mn2(a, b), h1 = mx2(a, b);
+    lo = mn2(l1, c);
+    const uint32_t m2 = mx2(l1, c);
+    md = mn2(h1, m2);
+    hi = mx2(h1, m2);
+}
+__device__ __forceinline__ uint32_t med3_2(uint32_t a, uint32_t b, uint32_t c) {
+    return mx2(mn2(a, b), mn2(mx2(a, b), c));
+}
+__device__ __forceinline__ uint32_t even16(uint32_t w) { return __byte_perm(w, 0, 0x4240); }
+__device__ __forceinline__ uint32_t odd16(uint32_t w) { return __byte_perm(w, 0, 0x4341); }
+
 __device__ void median3_plane(const uint32_t *src, uint32_t *dst) {
     const int c = threadIdx.x & 63, y0 = (threadIdx.x >> 6) * 32;
-    auto ld3 = [&](int y, uint32_t &l, uint32_t &m, uint32_t &r) {
+    // per row: Ol = odd half of the left word, E/O of the own word, Er = even half of the right
+    auto ld = [&](int y, uint32_t &ol, uint32_t &e, uint32_t &o, uint32_t &er) {
         const uint32_t *row = src + clampi(y, 0, 255) * WP;
-        m = row[c];
-        l = c > 0 ? row[c - 1] : rep0(m);
-        r = c < 63 ? row[c + 1] : rep3(m);
+        const uint32_t m = row[c];
+        const uint32_t l = c > 0 ? row[c - 1] : rep0(m);
+        const uint32_t r = c < 63 ? row[c + 1] : rep3(m);
+        ol = odd16(l);
+        e = even16(m);
+        o = odd16(m);
+        er = even16(r);
     };
-    uint32_t al, am, ar, bl, bm, br;
-    ld3(y0 - 1, al, am, ar);
-    ld3(y0, bl, bm, br);
-#pragma unroll 4
+    uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+    ld(y0 - 1, a0, a1, a2, a3);
+    ld(y0, b0, b1, b2, b3);
+#pragma unroll 2
     for (int y = y0; y < y0 + 32; ++y) {
-        uint32_t cl, cm, cr;
-        ld3(y + 1, cl, cm, cr);
-        uint32_t l0 = al, l1 = bl, l2 = cl, m0 = am, m1 = bm, m2 = cm, r0 = ar, r1 = br, r2 = cr;
-        ce(l0, l1); ce(l1, l2); ce(l0, l1);
-        ce(m0, m1); ce(m1, m2); ce(m0, m1);
-        ce(r0, r1); ce(r1, r2); ce(r0, r1);
-        // column-sorted triples: median9 = med3(max of mins, med of mids, min of maxes)
-        const uint32_t lo = vmax(vmax(fsl(l0, m0, 8), m0), fsr(m0, r0, 8));
-        const uint32_t md = med3(fsl(l1, m1, 8), m1, fsr(m1, r1, 8));
-        const uint32_t hi = vmin(vmin(fsl(l2, m2, 8), m2), fsr(m2, r2, 8));
-        dst[y * WP + c] = med3(lo, md, hi);
-        al = bl; am = bm; ar = br;
-        bl = cl; bm = cm; br = cr;
+        uint32_t c0, c1, c2, c3;
+        ld(y + 1, c0, c1, c2, c3);
+        uint32_t olL, olM, olH, eL, eM, eH, oL, oM, oH, erL, erM, erH;
+        sort3_2(a0, b0, c0, olL, olM, olH);
+        sort3_2(a1, b1, c1, eL, eM, eH);
+        sort3_2(a2, b2, c2, oL, oM, oH);
+        sort3_2(a3, b3, c3, erL, erM, erH);
+        // even pixels: left = fsl(Ol, O, 16), centre = E, right = O
+        const uint32_t ev = med3_2(mx2(mx2(fsl(olL, oL, 16), eL), oL), med3_2(fsl(olM, oM, 16), eM, oM),
+                                   mn2(mn2(fsl(olH, oH, 16), eH), oH));
+        // odd pixels: left = E, centre = O, right = fsr(E, Er, 16)
+        const uint32_t od = med3_2(mx2(mx2(eL, oL), fsr(eL, erL, 16)), med3_2(eM, oM, fsr(eM, erM, 16)),
+                                   mn2(mn2(eH, oH), fsr(eH, erH, 16)));
+        dst[y * WP + c] = ev | (od << 8);
+        a0 = b0; a1 = b1; a2 = b2; a3 = b3;
+        b0 = c0; b1 = c1; b2 = c2; b3 = c3;
     }
+}
+
+// ---- sub-histograms: 64 copies (one per 8 lanes), stride 257 words (bank-spread) ------------
+constexpr int SH = 64, SHS = 257;  // 64 x 257 words = 65,792 B <= one plane
+__device__ __forceinline__ void subhist_zero(uint32_t *sh) {
+    for (int i = threadIdx.x; i < SH * SHS; i += NTF) sh[i] = 0;
+}
+__device__ __forceinline__ void subhist_add4(uint32_t *sh, uint32_t w) {
+    uint32_t *h = sh + (threadIdx.x >> 3) * SHS;
+    atomicAdd(h + (w & 255), 1u);
+    atomicAdd(h + ((w >> 8) & 255), 1u);
+    atomicAdd(h + ((w >> 16) & 255), 1u);
+    atomicAdd(h + (w >> 24), 1u);
+}
+__device__ __forceinline__ void subhist_reduce(const uint32_t *sh, uint32_t *hist) {
+    // 512 threads: bin = tid & 255, half the copies each
+    const int v = threadIdx.x & 255, h0 = (threadIdx.x >> 8) * (SH / 2);
+    uint32_t t = 0;
+#pragma unroll 8
+    for (int k = 0; k < SH / 2; ++k) t += sh[(h0 + k) * SHS + v];
+    if (threadIdx.x >= 256) hist[v] = t;
+    __syncthreads();
+    if (threadIdx.x < 256) hist[v] += t;
 }
 
 // RGB (16 px in 3 uint4) -> 4 words of R, G, B (pixels 4q .. 4q+3)
@@ -972,7 +1066,7 @@ __device__ __forceinline__ void pack16(const uint32_t (&R)[4], const uint32_t (&
 
 // V = max(r, g, b) (cloudfilter.py:89) or one channel of the tile into a plane ("group" map);
 // returns whether any pixel has unequal channels
-__device__ int load_plane(const uint8_t *tile, int ch, uint32_t *dst) {
+__device__ int load_plane(const uint8_t *tile, int ch, uint32_t *dst, uint32_t *sh = nullptr) {
     int uneq = 0;
     const uint4 *t4 = reinterpret_cast<const uint4 *>(tile);
     for (int g = threadIdx.x; g < 4096; g += NTF) {
@@ -983,6 +1077,7 @@ __device__ int load_plane(const uint8_t *tile, int ch, uint32_t *dst) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             d[q] = ch == 3 ? vmax(R[q], vmax(G[q], B[q])) : (ch == 0 ? R[q] : (ch == 1 ? G[q] : B[q]));
+            if (sh) subhist_add4(sh, d[q]);
             uneq |= (R[q] ^ G[q]) | (G[q] ^ B[q]);
         }
     }
@@ -1044,19 +1139,24 @@ autolabel256_kernel(const uint8_t *__restrict__ rgb, Params prm, uint8_t *__rest
             s.vlut[v] = (uint32_t)cls | (1u << (12 + 5 * slot));
         }
     }
-    // 1. V plane (cloudfilter.py:89), D = dilate7(V) (cloudfilter.py:84)
-    const int any_unequal = __syncthreads_or(load_plane(tile, 3, P0));
+    subhist_zero(P2);
+    __syncthreads();
+    // 1. V plane (cloudfilter.py:89) + its histogram, D = dilate7(V) (cloudfilter.py:84)
+    const int any_unequal = __syncthreads_or(load_plane(tile, 3, P0, P2));
+    subhist_reduce(P2, s.hist_v);
     PROF_MARK(0);
-    dilate7(P0, P1, P2, s);  // D in P2
+    dilate7(P0, P1, P2, s);  // D in P2 (its column pass starts after a barrier: P2 reads done)
     PROF_MARK(1);
     // 2. bg = median21(D) (estimate_background, cloudfilter.py:82-84) into P1
     median21(P2, P0, P1, s);
     PROF_MARK(2);
-    // 3. smooth = median3(V) (:90), d = |smooth - bg| [truncated] (:91-93) into P2
+    // 3. smooth = median3(V) (:90), d = |smooth - bg| [truncated] (:91-93) into P2, histogram
     load_plane(tile, 3, P0);  // V again (L2-resident re-read)
     __syncthreads();
     median3_plane(P0, P2);
-    uint32_t wlo = 0xffffffffu, whi = 0;
+    __syncthreads();
+    subhist_zero(P0);
+    __syncthreads();
     const uint32_t tt4 = (uint32_t)cfg.truncate_t * 0x01010101u;
 #pragma unroll 4
     for (int y = 0; y < 32; ++y) {
@@ -1064,28 +1164,25 @@ autolabel256_kernel(const uint8_t *__restrict__ rgb, Params prm, uint8_t *__rest
         uint32_t d = __vabsdiffu4(P2[o], P1[o]);
         if (cfg.diff_truncate) d = vmin(d, tt4);
         P2[o] = d;
-        wlo = vmin(wlo, d);
-        whi = vmax(whi, d);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) hist_add(s.hist, (d >> (8 * k)) & 255, true);
-    }
-    int lo = min(min(wlo & 255, (wlo >> 8) & 255), min((wlo >> 16) & 255, wlo >> 24));
-    int hi = max(max(whi & 255, (whi >> 8) & 255), max((whi >> 16) & 255, whi >> 24));
-    for (int o = 16; o; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-        s.red[threadIdx.x >> 5][1] = lo;
-        s.red[threadIdx.x >> 5][2] = hi;
+        subhist_add4(P0, d);
     }
     __syncthreads();
-    lo = 255;
-    hi = 0;
-    for (int i = 0; i < NTF / 32; ++i) {
-        lo = min(lo, s.red[i][1]);
-        hi = max(hi, s.red[i][2]);
+    subhist_reduce(P0, s.hist);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // lo / hi of d from the histogram
+        const int lane = threadIdx.x;
+        uint32_t nz = 0;
+        for (int j = 0; j < 8; ++j) nz |= (s.hist[8 * lane + j] != 0) << j;
+        const unsigned have = __ballot_sync(0xffffffffu, nz != 0);
+        const int wlo = __ffs(have) - 1, whi = 31 - __clz(have);
+        const uint32_t nlo = __shfl_sync(0xffffffffu, nz, wlo), nhi = __shfl_sync(0xffffffffu, nz, whi);
+        if (lane == 0) {
+            s.bc[2] = 8 * wlo + __ffs(nlo) - 1;
+            s.bc[3] = 8 * whi + 31 - __clz(nhi);
+        }
     }
+    __syncthreads();
+    const int lo = s.bc[2], hi = s.bc[3];
     const int range = hi - lo;
     PROF_MARK(3);
     // 4. minmax normalize (kernels.py:66-74, exact integer form) applied to the histogram
@@ -1122,11 +1219,7 @@ autolabel256_kernel(const uint8_t *__restrict__ rgb, Params prm, uint8_t *__rest
     if (masked > 0) {
         if (!any_unequal) {
             // R == G == B everywhere: every channel equals V, bg_c == bg(V) (kept in P1)
-            if (threadIdx.x < 256) s.hist[threadIdx.x] = 0;
-            __syncthreads();
-            channel_hist(tile, 3, s.hist);
-            __syncthreads();
-            center = center_from_hist(s.hist, NPX);
+            center = center_from_hist(s.hist_v, NPX);
         } else {
             // mask bits, then per channel: bg_c = median21(dilate7(c)), masked pixels repaired
             for (int w = threadIdx.x; w < 2048; w += NTF) {

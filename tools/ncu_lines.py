@@ -1,0 +1,61 @@
+"""Attribute ncu warp-stall samples / executed instructions of one kernel to source lines.
+
+    python tools/ncu_lines.py <report.ncu-rep> <kernel regex> <cubin> [--top 40]
+
+ncu's SASS page (--page source --print-source sass) lists runtime addresses; offsets from
+the function start match the cubin, whose line table nvdisasm -g prints.
+"""
+import argparse
+import collections
+import csv
+import io
+import re
+import subprocess
+
+ap = argparse.ArgumentParser()
+ap.add_argument("rep")
+ap.add_argument("kernel")
+ap.add_argument("cubin")
+ap.add_argument("--top", type=int, default=40)
+a = ap.parse_args()
+
+out = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
+                      "regex:" + a.kernel], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+name = rows[0][1]
+hdr = rows[1]
+rows = [r for r in rows[2:] if len(r) == len(hdr)]
+i_s, i_e = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
+num = lambda v: int(v) if v.strip().isdigit() else 0
+base = int(rows[0][0], 16)
+
+# mangled name from the cubin whose SASS length matches
+dis = subprocess.run(["nvdisasm", "-g", a.cubin], capture_output=True, text=True).stdout
+funcs = re.split(r"\n\s*\.text\.", dis)
+line_of = {}
+for f in funcs:
+    fname = f.split(":", 1)[0].strip()
+    if not re.search(a.kernel, fname):
+        continue
+    cur = None
+    for ln in f.splitlines():
+        m = re.search(r'line (\d+)', ln)
+        if m and "//##" in ln:
+            cur = int(m.group(1))
+            continue
+        m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
+        if m and cur is not None:
+            line_of[int(m.group(1), 16)] = cur
+    break
+agg = collections.Counter()
+inst = collections.Counter()
+for r in rows:
+    off = int(r[0], 16) - base
+    ln = line_of.get(off, -1)
+    agg[ln] += num(r[i_s])
+    inst[ln] += num(r[i_e])
+tot = sum(agg.values()) or 1
+itot = sum(inst.values()) or 1
+print(f"{name[:90]}\n total samples {tot}, warp-instructions {itot}, mapped lines {len(line_of)}")
+for ln, v in agg.most_common(a.top):
+    print(f"  line {ln:5d}: {100 * v / tot:5.1f}% stalls  {100 * inst[ln] / itot:5.1f}% inst")

@@ -21,6 +21,7 @@ ap.add_argument("--uniq", type=int, default=296)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--kind", default="tgray")
 ap.add_argument("--path", type=int, default=0)
+ap.add_argument("--prof", action="store_true", help="needs ICE_LIB_PATH=.../_C/prof/libicelabel_b200.so")
 a = ap.parse_args()
 if a.kind == "trand":
     u = np.stack([synth.random_tile(i) for i in range(a.uniq)])
@@ -39,6 +40,19 @@ for _ in range(a.reps):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.reps
+if a.prof:
+    import ctypes
+    lib = _native.load()
+    buf = (ctypes.c_ulonglong * 16)()
+    lib.ice_al_prof_read(buf, 1)
+    il.autolabel(x, out=out)
+    torch.cuda.synchronize()
+    lib.ice_al_prof_read(buf, 1)
+    tot = sum(buf[:8]) or 1
+    print("phase cycles per tile:", [round(buf[i] / a.tiles) for i in range(8)],
+          "share:", [round(buf[i] / tot, 3) for i in range(8)])
+    print("per tile: distinct values %.1f, passes %.1f, active col blocks/pass %.1f" %
+          (buf[8] / a.tiles, buf[9] / a.tiles, buf[10] / max(1, buf[9])))
 px = a.tiles * 65536
 print(f"{a.kind} path={a.path} tiles={a.tiles}: {ms:.2f} ms  {px / ms / 1e6:.1f} Gpx/s  "
       f"{px * 7 / ms / 1e6:.1f} GB/s  us/tile/SM={ms * 1000 * 148 / a.tiles:.1f}")
