@@ -738,6 +738,7 @@ struct SmemF {
     uint32_t vlut[256];
     uint8_t flags[256];
     uint8_t vals[256];
+    uint8_t rank[256];      // value -> 0x80 | index in vals (median21 rank mode)
     int red[NTF / 32][4];
     int bc[8];
     int act[16];            // median21 block activity, [band][half]
@@ -746,6 +747,8 @@ struct SmemF {
 
 __device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, int n) { return __funnelshift_r(lo, hi, n); }
 __device__ __forceinline__ uint32_t fsl(uint32_t lo, uint32_t hi, int n) { return __funnelshift_l(lo, hi, n); }
+__device__ __forceinline__ uint32_t even16(uint32_t w) { return __byte_perm(w, 0, 0x4240); }  // bytes 0, 2
+__device__ __forceinline__ uint32_t odd16(uint32_t w) { return __byte_perm(w, 0, 0x4341); }   // bytes 1, 3
 __device__ __forceinline__ uint32_t rep0(uint32_t w) { return __byte_perm(w, 0, 0x0000); }
 __device__ __forceinline__ uint32_t rep3(uint32_t w) { return __byte_perm(w, 0, 0x3333); }
 __device__ __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) { return __vmaxu4(a, b); }
@@ -825,7 +828,11 @@ __device__ int collect_values(SmemF &s) {
         for (int i = 0; i < wid; ++i) base += s.red[i][0];
         const int v = 32 * wid + lane;
         const unsigned b = __ballot_sync(0xffffffffu, s.flags[v] != 0);
-        if (s.flags[v]) s.vals[base + __popc(b & ((1u << lane) - 1))] = (uint8_t)v;
+        const int r = base + __popc(b & ((1u << lane) - 1));
+        if (s.flags[v]) {
+            s.vals[r] = (uint8_t)v;
+            s.rank[v] = (uint8_t)(0x80 | r);
+        }
     }
     __syncthreads();
     int nd = 0;
@@ -837,38 +844,44 @@ __device__ int collect_values(SmemF &s) {
 // 16 output words per call.  local j <-> word k = m0 - 3 + j.  s2: 2-px sums, s4: 4-px sums
 // (<= 4 per byte), t_k = s4_k + .. + s4_{k+4} + i_{k+5}: the 21 px from 4k + byte.
 // EDGE: 0 interior, 1 left tile edge (m0 == 0), 2 right tile edge (m0 == 48).
-template <int EDGE>
-__device__ __forceinline__ void row_chunk(const uint32_t *sr, uint32_t *dr, int m0, uint32_t c4, uint32_t c7f) {
-    uint32_t I[23], S2[22], S4[21], T[17];
+// RANK: the plane holds 0x80 | rank(value) (nd <= 128) and "x > t_i" is one subtraction:
+// bit 7 of (0x80 + r - (i + 1)) per byte (no borrow since r, i + 1 <= 128); k = (i+1)*0x01010101.
+// Otherwise the plane holds values and gt4 (c = (255 - t) * 0x01010101) is used.
+template <int EDGE, bool RANK>
+__device__ __forceinline__ void row_chunk(const uint32_t *sr, uint32_t *dr, int m0, uint32_t k) {
+    uint32_t I[23], S2[22], S4[21], S8[19], T[17];
 #pragma unroll
     for (int j = 0; j < 23; ++j) {
         uint32_t w;
         if (EDGE == 1 && j < 3) w = rep0(sr[0]);
         else if (EDGE == 2 && j >= 19) w = rep3(sr[63]);
         else w = sr[m0 - 3 + j];
-        I[j] = gt4(w, c4, c7f);
+        I[j] = RANK ? ((w - k) >> 7) & 0x01010101u : gt4(w, k, k & 0x7f7f7f7fu);
     }
 #pragma unroll
     for (int j = 0; j < 22; ++j) S2[j] = I[j] + fsr(I[j], I[j + 1], 8);
 #pragma unroll
     for (int j = 0; j < 21; ++j) S4[j] = S2[j] + fsr(S2[j], S2[j + 1], 16);
 #pragma unroll
-    for (int j = 0; j < 17; ++j) T[j] = (S4[j] + S4[j + 1]) + (S4[j + 2] + S4[j + 3]) + S4[j + 4] + I[j + 5];
+    for (int j = 0; j < 19; ++j) S8[j] = S4[j] + S4[j + 1];
+#pragma unroll
+    for (int j = 0; j < 17; ++j) T[j] = S8[j] + S8[j + 2] + S4[j + 4] + I[j + 5];
     // pixel 4m + i has its window start at 4(m - 3) + i + 2
 #pragma unroll
     for (int j = 0; j < 16; ++j) dr[m0 + j] = fsr(T[j], T[j + 1], 16);
 }
 
-__device__ __forceinline__ void row_counts(const uint32_t *src, uint32_t *dst, uint32_t c4, uint32_t c7f) {
+template <bool RANK>
+__device__ __forceinline__ void row_counts(const uint32_t *src, uint32_t *dst, uint32_t k) {
     const int row = threadIdx.x & 255, half = threadIdx.x >> 8;
     const uint32_t *sr = src + row * WP;
     uint32_t *dr = dst + row * WP;
     if (half == 0) {
-        row_chunk<1>(sr, dr, 0, c4, c7f);
-        row_chunk<0>(sr, dr, 16, c4, c7f);
+        row_chunk<1, RANK>(sr, dr, 0, k);
+        row_chunk<0, RANK>(sr, dr, 16, k);
     } else {
-        row_chunk<0>(sr, dr, 32, c4, c7f);
-        row_chunk<2>(sr, dr, 48, c4, c7f);
+        row_chunk<0, RANK>(sr, dr, 32, k);
+        row_chunk<2, RANK>(sr, dr, 48, k);
     }
 }
 
@@ -902,8 +915,10 @@ __device__ __forceinline__ uint32_t col_band(const uint32_t *cnt, uint32_t *acc,
             n = cnt[min(y0 + y + MR + 1, 255) * WP + c];
             o = cnt[max(y0 + y - MR, 0) * WP + c];
         }
-        ae += (n & M) - (o & M);
-        ao += ((n >> 8) & M) - ((o >> 8) & M);
+        // per byte 128 + n - o in [107, 149]: no borrow; the 128 bias is removed per lane
+        const uint32_t df = (n | 0x80808080u) - o;
+        ae += even16(df) - 0x00800080u;
+        ao += odd16(df) - 0x00800080u;
     }
     return any;
 }
@@ -913,7 +928,7 @@ __device__ __forceinline__ uint32_t col_band(const uint32_t *cnt, uint32_t *acc,
 // Block skipping: a (band, half) block whose pixels all had median <= t after a pass stays
 // final for every larger threshold (the counts are monotone in t), so its column pass is
 // skipped, and a row-pass warp runs only while a block it feeds (+-10 rows) is active.
-__device__ void median21(const uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s) {
+__device__ void median21(uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s) {
     const int nd = collect_values(s);
 #ifdef ICE_AL_PROF
     if (threadIdx.x == 0) atomicAdd(&g_al_prof[8], (unsigned long long)nd);
@@ -923,15 +938,25 @@ __device__ void median21(const uint32_t *src, uint32_t *tmp, uint32_t *acc, Smem
     const int rwarp = (threadIdx.x & 255) >> 5, rhalf = threadIdx.x >> 8;  // row map: rows 32 rwarp..
     for (int y = band * 32; y < band * 32 + 32; ++y) acc[y * WP + c] = v0;
     if (threadIdx.x < 16) s.act[threadIdx.x] = 1;
+    const bool rank_mode = nd <= 128;
+    if (rank_mode) {  // src plane -> 0x80 | rank (in place; values come back through s.vals)
+        for (int i = threadIdx.x; i < 256 * 64; i += NTF) {
+            uint32_t *w = src + (i >> 6) * WP + (i & 63);
+            const uint32_t v = *w;
+            *w = s.rank[v & 255] | (uint32_t)s.rank[(v >> 8) & 255] << 8 | (uint32_t)s.rank[(v >> 16) & 255] << 16 |
+                 (uint32_t)s.rank[v >> 24] << 24;
+        }
+    }
     uint32_t any = 1;
     for (int i = 0; i + 1 < nd; ++i) {
         const uint32_t t = s.vals[i], gap = (uint32_t)s.vals[i + 1] - t;
-        const uint32_t c4 = (255u - t) * 0x01010101u;
         if (!__syncthreads_or(any)) break;  // no pixel moved in the previous pass: all final
         const int* act = s.act;
         if (act[2 * rwarp + rhalf] | (rwarp > 0 ? act[2 * (rwarp - 1) + rhalf] : 0) |
-            (rwarp < 7 ? act[2 * (rwarp + 1) + rhalf] : 0))
-            row_counts(src, tmp, c4, c4 & 0x7f7f7f7fu);
+            (rwarp < 7 ? act[2 * (rwarp + 1) + rhalf] : 0)) {
+            if (rank_mode) row_counts<true>(src, tmp, (uint32_t)(i + 1) * 0x01010101u);
+            else row_counts<false>(src, tmp, (255u - t) * 0x01010101u);
+        }
         __syncthreads();
         const int blk = 2 * band + (c >> 5);
 #ifdef ICE_AL_PROF
@@ -972,8 +997,6 @@ __device__ __forceinline__ void sort3_2(uint32_t a, uint32_t b, uint32_t c, uint
 __device__ __forceinline__ uint32_t med3_2(uint32_t a, uint32_t b, uint32_t c) {
     return mx2(mn2(a, b), mn2(mx2(a, b), c));
 }
-__device__ __forceinline__ uint32_t even16(uint32_t w) { return __byte_perm(w, 0, 0x4240); }
-__device__ __forceinline__ uint32_t odd16(uint32_t w) { return __byte_perm(w, 0, 0x4341); }
 
 __device__ void median3_plane(const uint32_t *src, uint32_t *dst) {
     const int c = threadIdx.x & 63, y0 = (threadIdx.x >> 6) * 32;
