@@ -1133,15 +1133,20 @@ __device__ __forceinline__ int block_sum_f(int v, SmemF &s) {
     return t;
 }
 
-__global__ void __launch_bounds__(NTF, 1)
-autolabel256_kernel(const uint8_t *__restrict__ rgb, Params prm, uint8_t *__restrict__ filtered,
-                    uint8_t *__restrict__ label, uint8_t *__restrict__ maskout, uint32_t *__restrict__ affected,
-                    uint32_t *__restrict__ counts, int32_t *__restrict__ unmatched) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    SmemF &s = *reinterpret_cast<SmemF *>(smem_raw);
+__device__ __forceinline__ void prefetch_tile_l2(const uint8_t *tile) {
+    // 196,608 B = 12 x 16 KB bulk L2 prefetches
+    if (threadIdx.x < 12)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tile + threadIdx.x * 16384), "r"(16384)
+                     : "memory");
+}
+
+__device__ __forceinline__ void process_tile256(const uint8_t *__restrict__ rgb, const Params &prm,
+                                                uint8_t *__restrict__ filtered, uint8_t *__restrict__ label,
+                                                uint8_t *__restrict__ maskout, uint32_t *__restrict__ affected,
+                                                uint32_t *__restrict__ counts, int32_t *__restrict__ unmatched,
+                                                SmemF &s, const size_t tile_id) {
     const IceFilterCfg &cfg = prm.cfg;
     constexpr int NPX = 65536;
-    const size_t tile_id = blockIdx.x;
     const uint8_t *tile = rgb + tile_id * (size_t)NPX * 3;
     uint8_t *ftile = filtered + tile_id * (size_t)NPX * 3;
     uint32_t *P0 = s.p[0], *P1 = s.p[1], *P2 = s.p[2];
@@ -1153,14 +1158,6 @@ autolabel256_kernel(const uint8_t *__restrict__ rgb, Params prm, uint8_t *__rest
         s.flags[threadIdx.x] = 0;
         s.hist[threadIdx.x] = 0;
         s.hist2[threadIdx.x] = 0;
-        if (prm.v_only) {
-            int cls = 255;
-            const int v = threadIdx.x;
-            for (int k = 2; k >= 0; --k)
-                if (v >= prm.scheme.lo[k][2] && v <= prm.scheme.hi[k][2]) cls = prm.scheme.cls[k];
-            const int slot = cls == 255 ? 3 : cls;
-            s.vlut[v] = (uint32_t)cls | (1u << (12 + 5 * slot));
-        }
     }
     subhist_zero(P2);
     __syncthreads();
@@ -1266,16 +1263,19 @@ autolabel256_kernel(const uint8_t *__restrict__ rgb, Params prm, uint8_t *__rest
                 const int c_ch = center_from_hist(s.hist, NPX);
                 dilate7(P0, P1, P2, s);
                 median21(P2, P0, P1, s);  // bg_c in P1
+                load_plane(tile, ch, P0);  // the channel again (L2-resident re-read)
+                __syncthreads();
 #pragma unroll 2
                 for (int y = 0; y < 32; ++y) {
                     const int yy = y0 + y;
                     const uint32_t mb = (s.maskbits[yy * 8 + (cc >> 3)] >> (4 * (cc & 7))) & 15;
                     if (mb) {
+                        const uint32_t chw = P0[yy * WP + cc], bgw = P1[yy * WP + cc];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             if (mb >> k & 1) {
                                 const int i = yy * 256 + 4 * cc + k;
-                                const int f = (int)tile[3 * i + ch] - (int)((P1[yy * WP + cc] >> (8 * k)) & 255) + c_ch;
+                                const int f = (int)((chw >> (8 * k)) & 255) - (int)((bgw >> (8 * k)) & 255) + c_ch;
                                 ftile[3 * i + ch] = (uint8_t)clampi(f, 0, 255);
                             }
                         }
@@ -1412,6 +1412,30 @@ autolabel256_kernel(const uint8_t *__restrict__ rgb, Params prm, uint8_t *__rest
         counts[3 * tile_id + 2] = c2;
         unmatched[tile_id] = first == 0x7fffffff ? -1 : first;
     }
+    __syncthreads();  // shared state is reused by the next tile
+}
+
+// One CTA per tile (the hardware scheduler balances hazy / clean tiles); each CTA prefetches
+// into L2 the RGB of the tile one "wave" ahead (blockIdx.x + ahead), which runs about one
+// tile-time later on some SM, so its loads hit L2.
+__global__ void __launch_bounds__(NTF, 1)
+autolabel256_kernel(const uint8_t *__restrict__ rgb, int n, int ahead, Params prm, uint8_t *__restrict__ filtered,
+                    uint8_t *__restrict__ label, uint8_t *__restrict__ maskout, uint32_t *__restrict__ affected,
+                    uint32_t *__restrict__ counts, int32_t *__restrict__ unmatched) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    SmemF &s = *reinterpret_cast<SmemF *>(smem_raw);
+    if (threadIdx.x < 256 && prm.v_only) {
+        int cls = 255;
+        const int v = threadIdx.x;
+        for (int k = 2; k >= 0; --k)
+            if (v >= prm.scheme.lo[k][2] && v <= prm.scheme.hi[k][2]) cls = prm.scheme.cls[k];
+        const int slot = cls == 255 ? 3 : cls;
+        s.vlut[v] = (uint32_t)cls | (1u << (12 + 5 * slot));
+    }
+    const int t = blockIdx.x;
+    if (t < ahead) prefetch_tile_l2(rgb + (size_t)t * 65536 * 3);
+    if (t + ahead < n) prefetch_tile_l2(rgb + (size_t)(t + ahead) * 65536 * 3);
+    process_tile256(rgb, prm, filtered, label, maskout, affected, counts, unmatched, s, (size_t)t);
 }
 
 }  // namespace fastk
@@ -1463,8 +1487,15 @@ extern "C" int ice_autolabel(const uint8_t *rgb, int64_t n, int32_t h, int32_t w
             if (e != cudaSuccess) return (int)e;
             attr_fast = true;
         }
+        static int n_sm = 0;
+        if (!n_sm) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+            if (n_sm <= 0) n_sm = 148;
+        }
         fastk::autolabel256_kernel<<<(unsigned)n, fastk::NTF, sizeof(fastk::SmemF), (cudaStream_t)stream>>>(
-            rgb, prm, filtered, label, mask, affected, counts, unmatched);
+            rgb, (int)n, n_sm, prm, filtered, label, mask, affected, counts, unmatched);
         return (int)cudaGetLastError();
     }
     static bool attr_set = false;

@@ -49,13 +49,22 @@ for f in funcs:
     break
 agg = collections.Counter()
 inst = collections.Counter()
+stall_cols = [(h, i) for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+reasons = collections.defaultdict(collections.Counter)
+total_reasons = collections.Counter()
 for r in rows:
     off = int(r[0], 16) - base
     ln = line_of.get(off, -1)
     agg[ln] += num(r[i_s])
     inst[ln] += num(r[i_e])
+    for h, i in stall_cols:
+        reasons[ln][h[6:]] += num(r[i])
+        total_reasons[h[6:]] += num(r[i])
 tot = sum(agg.values()) or 1
 itot = sum(inst.values()) or 1
 print(f"{name[:90]}\n total samples {tot}, warp-instructions {itot}, mapped lines {len(line_of)}")
+rt = sum(total_reasons.values()) or 1
+print(" stall reasons:", ", ".join(f"{k} {100 * v / rt:.1f}%" for k, v in total_reasons.most_common(8)))
 for ln, v in agg.most_common(a.top):
-    print(f"  line {ln:5d}: {100 * v / tot:5.1f}% stalls  {100 * inst[ln] / itot:5.1f}% inst")
+    top = ", ".join(f"{k} {100 * c / max(1, sum(reasons[ln].values())):.0f}%" for k, c in reasons[ln].most_common(3))
+    print(f"  line {ln:5d}: {100 * v / tot:5.1f}% stalls  {100 * inst[ln] / itot:5.1f}% inst  [{top}]")
