@@ -193,6 +193,31 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _cv_chunk(tiles):
+    import cv2
+    cv2.setNumThreads(1)  # as the reference (kernels.py:18)
+    from oracle import autolabel_cv
+    for t in tiles:
+        autolabel_cv.process_tile(t)
+    return len(tiles)
+
+
+def cpu_autolabel_rate(corpus: np.ndarray, per_core: int = 24):
+    """Reference-algorithm CPU labeler (oracle/autolabel_cv.py: OpenCV + NumPy, the calls the
+    reference's process_tile makes) on all host cores, one process per core as the
+    reference's run_local (engine.py:236-325).  Returns (Mpixel/s, cores, tiles, seconds)."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    n = min(len(corpus), cores * per_core)
+    chunks = [corpus[i::cores][: per_core] for i in range(cores)]
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_cv_chunk, [c[:1] for c in chunks])  # warm the workers (imports)
+        t0 = time.perf_counter()
+        done = sum(pool.map(_cv_chunk, chunks))
+        dt = time.perf_counter() - t0
+    return done * corpus.shape[1] * corpus.shape[2] / dt / 1e6, cores, done, dt
+
+
 def autolabel_bench(corpus_dev, n_tiles: int, reps: int):
     """K1 over n_tiles tiles (tile i = corpus[i mod len]) resident in HBM."""
     from paper_2403_13135_b200 import icelabel as il
@@ -400,19 +425,36 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             seg_ms = float(t.item())
         seg_gbs = px * 4 / (seg_ms / 1000.0) / 1e9
+        al_traffic = None
+        try:
+            tj = json.load(open(prof_path))
+            if tj.get("ice_autolabel_bytes_per_tile"):
+                al_traffic = tj["ice_autolabel_bytes_per_tile"] * n_tiles
+        except Exception:
+            pass
         autolabel = {"metric": "auto-label Mpixel/s (fused filter + HSV labeler, 100k 256^2 tiles)",
                      "value": round(px / (al_ms / 1000.0) / 1e6, 1), "unit": "Mpixel/s",
                      "ms": round(al_ms, 2), "tiles": n_tiles * world,
                      "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
-                                  "frac": round(gbs / hbm, 4), "traffic": None,
+                                  "frac": round(gbs / hbm, 4), "traffic": al_traffic,
                                   "note": "7 B/px algorithmic (RGB in, filtered + label out); "
-                                          "the 21x21 medians make K1 on-chip-bound"},
+                                          "the 21x21 medians make K1 integer-ALU-bound (SWAR kernel)"},
                      "segment_only": {"metric": "label-only (K1s, icelabel label) Mpixel/s",
                                       "value": round(px / (seg_ms / 1000.0) / 1e6, 1), "unit": "Mpixel/s",
                                       "ms": round(seg_ms, 3),
                                       "roofline": {"bound": "hbm", "achieved": round(seg_gbs, 1), "peak": hbm,
                                                    "unit": "GB/s", "frac": round(seg_gbs / hbm, 4),
                                                    "traffic": None, "note": "4 B/px (RGB in, label out)"}}}
+
+    if autolabel is not None and rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            rate, cores, done, dt = cpu_autolabel_rate(corpus)
+            autolabel["cpu_baseline"] = {
+                "value": round(rate, 3), "unit": "Mpixel/s", "cores": cores, "kind": "port",
+                "sample": f"{done} T-gray tiles through oracle/autolabel_cv.py process_tile (OpenCV + NumPy, "
+                          f"the reference's own calls), {cores} processes, {dt:.1f} s"}
+        except Exception as exc:  # the GPU number stands without it
+            autolabel["cpu_baseline"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
 
     # ---- CPU baseline (rank 0, N = 1 only): bounded sample of the reference step -------
     cpu = None

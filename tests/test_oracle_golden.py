@@ -83,3 +83,21 @@ def test_minmax_and_otsu_known_answers():
     bimodal = np.array([[20] * 8 + [200] * 8] * 4, np.uint8)
     t = orc.otsu_threshold(bimodal)
     assert 20 <= t < 200
+
+
+@pytest.mark.parametrize("rec", [r for r in GOLDEN["cases"] if r["op"] == "process_tile" and not r["error"]
+                                 and not r.get("cfg") and r.get("scheme", "ross-sea-summer") == "ross-sea-summer"],
+                         ids=lambda r: r["name"])
+def test_cv_baseline_port_matches_reference(rec):
+    """oracle/autolabel_cv.py (the auto-label CPU baseline bench.py times) reproduces the
+    reference's process_tile digests with the default config."""
+    cv = pytest.importorskip("oracle.autolabel_cv")
+    if cv.cv2 is None:
+        pytest.skip("cv2 unavailable")
+    rgb = CASES[rec["name"]]["make"]()
+    if min(rgb.shape[:2]) < 21:
+        pytest.skip("window larger than the tile")
+    f, lbl, a, first = cv.process_tile(rgb)
+    assert sha(f) == rec["filtered_sha"]
+    assert sha(lbl) == rec["label_sha"]
+    assert a / (rgb.shape[0] * rgb.shape[1]) == rec["affected_fraction"]
