@@ -422,6 +422,154 @@ struct WgradProb {
 };
 
 // ------------------------------------------------------------------------------------
+// ------------------------------------------------------------------------------------
+// Split-K wrapper for fprop / dgrad problems whose (M, N) tile grid is smaller than one wave
+// of SMs (the 8 x 8 and 16 x 16 U-Net levels at batch 32: 16-64 M tiles).  Split z covers
+// K-blocks [z kps, (z+1) kps); the epilogue red.adds the fp32 partial tile into a row-major
+// [pixel][column] workspace, and a finishing kernel (split_finish_*) applies the problem's
+// own epilogue (bias / ReLU / Dropout2d, or gradient-sum / ReLU-backward / split / planes /
+// bias gradient) and re-zeroes the workspace.
+template <class P>
+struct SplitK {
+    static constexpr bool A_MN = P::A_MN, B_MN = P::B_MN;
+    P p;
+    float *ws;
+    int ld, kps, total_kb;
+    __device__ void kb_range(int z, int &kb0, int &nkb) const {
+        kb0 = z * kps;
+        nkb = min(kps, total_kb - kb0);
+    }
+    __device__ void prefetch() const { p.prefetch(); }
+    template <int BN>
+    __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
+        p.template load<BN>(kb, sa, sb, bar, mt, nt, 0);
+    }
+    template <int BN>
+    __device__ void flush_bias(int, int, int, float *) const {}
+    template <int BN>
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *) const {
+        int n0, h0, w0, n, h, w;
+        p.pt.origin(mt, n0, h0, w0);
+        p.pt.pixel(row, n0, h0, w0, n, h, w);
+        const bool valid = n < p.N;
+        float *dst = ws + (((size_t)n * p.H + h) * p.W + w) * ld + nt * BN;
+#pragma unroll 1
+        for (int cc = cc0; cc < cc1; ++cc) {
+            float v[32];
+            tc::tmem_ld32(tmem + cc * 32, v);
+            if (!valid) continue;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                tc::red_add_v4(dst + cc * 32 + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+    }
+};
+
+// y = act(ws + bias) * drop, bf16; ws re-zeroed.  One thread per 8 columns of one pixel.
+__global__ void split_finish_fprop(float *__restrict__ ws, long long npx, int hw, int cout, const float *__restrict__ bias,
+                                   const float *__restrict__ drop, int relu, bf16 *__restrict__ y) {
+    const int groups = cout / 8;
+    const long long total = npx * groups;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const long long px = i / groups;
+        const int col = (int)(i - px * groups) * 8;
+        float4 *src = reinterpret_cast<float4 *>(ws + px * cout + col);
+        const float4 a = src[0], b = src[1];
+        src[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        src[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}, bq[8], dq[8];
+        ld8(bias ? bias + col : nullptr, 0.f, bq);
+        ld8(drop ? drop + (px / hw) * cout + col : nullptr, 1.f, dq);
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float x0 = v[2 * e] + bq[2 * e], x1 = v[2 * e + 1] + bq[2 * e + 1];
+            if (relu) {
+                x0 = fmaxf(x0, 0.f);
+                x1 = fmaxf(x1, 0.f);
+            }
+            pk[e] = tc::pack_bf16(x0 * dq[2 * e], x1 * dq[2 * e + 1]);
+        }
+        *reinterpret_cast<uint4 *>(y + px * cout + col) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+}
+
+// dgrad finish: the DgradProb epilogue on the reduced sums.  Block = 256 columns (32
+// column groups of 8, one per lane) x FIN_STRIP pixels (8 warps, interleaved rows); the bias
+// gradient column sums reduce through shared memory, one atomic per column per block.
+constexpr int FIN_STRIP = 64;
+__global__ void __launch_bounds__(256) split_finish_dgrad(float *__restrict__ ws, int npx, int N, int H, int W,
+                                                          DgradProb p) {
+    __shared__ float red[8][32][9];
+    const int ct = p.c1 + p.c2, cblocks = ct / 256;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int cb = blockIdx.x % cblocks, strip = blockIdx.x / cblocks;
+    const int cg = cb * 32 + lane;
+    int col = cg * 8;
+    bf16 *out;
+    const bf16 *ref, *add;
+    const float *drop;
+    float *db;
+    int cs;
+    bool second = false;
+    if (col < p.c1) {
+        out = p.out1; ref = p.ref1; add = p.add1; drop = p.drop1; cs = p.c1; db = p.db1;
+    } else {
+        col -= p.c1;
+        out = p.out2; ref = p.ref2; add = p.add2; drop = p.drop2; cs = p.c2; db = p.db2;
+        second = true;
+    }
+    float dsum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int px0 = strip * FIN_STRIP, px1 = min(npx, px0 + FIN_STRIP);
+    for (int px = px0 + wid; px < px1; px += 8) {
+        float4 *src = reinterpret_cast<float4 *>(ws + (size_t)px * ct + cg * 8);
+        const float4 a = src[0], b = src[1];
+        src[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        src[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!out) continue;
+        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        const int n = px / (H * W), hw = px - n * H * W, h = hw / W, w = hw - h * W;
+        size_t pix = (size_t)px;
+        if (second && p.planes_out2)
+            pix = ((((size_t)((h & 1) * 2 + (w & 1)) * N + n) * (H >> 1) + (h >> 1)) * (W >> 1)) + (w >> 1);
+        const size_t off = pix * cs + col;
+        if (add) {
+            const uint4 u = *reinterpret_cast<const uint4 *>(add + off);
+            const bf16 *b8 = reinterpret_cast<const bf16 *>(&u);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] += __bfloat162float(b8[e]);
+        }
+        if (ref) {
+            const uint4 u = *reinterpret_cast<const uint4 *>(ref + off);
+            const bf16 *b8 = reinterpret_cast<const bf16 *>(&u);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (!(__bfloat162float(b8[e]) > 0.f)) v[e] = 0.f;
+        }
+        if (drop) {
+            float dq[8];
+            ld8(drop + (size_t)n * cs + col, 1.f, dq);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] *= dq[e];
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dsum[e] += v[e];
+        *reinterpret_cast<uint4 *>(out + off) =
+            make_uint4(tc::pack_bf16(v[0], v[1]), tc::pack_bf16(v[2], v[3]), tc::pack_bf16(v[4], v[5]), tc::pack_bf16(v[6], v[7]));
+    }
+    if (!db || !out) return;  // block-uniform (one column region per block)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[wid][lane][e] = dsum[e];
+    __syncthreads();
+    // 256 threads: thread -> (column group, element) = (tid >> 3, tid & 7)
+    const int g = threadIdx.x >> 3, e = threadIdx.x & 7;
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][g][e];
+    const int gcol = (cb * 32 + g) * 8 + e - (second ? p.c1 : 0);
+    atomicAdd(db + gcol, t);
+}
+
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
     return 1024 + STAGES * (A_BYTES + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16;
@@ -1177,6 +1325,65 @@ int pick_bn(int ntot, long long m_tiles) {
 
 bool shape_ok(int N, int H, int W) { return N > 0 && pow2(H) && pow2(W); }
 
+// fprop / dgrad tiling for the non-halo path.  N = 256 tiles run at ~95% of the MMA peak,
+// N = 128 tiles at ~60% (their A + B operand stream per FLOP is 1.5x larger and becomes
+// L2-bound), so 256-wide tiles are kept even when they give fewer tiles than SMs; below
+// 80% of a wave the K range is split (fp32 workspace + split_finish_*).
+void pick_tiling(int ntot, long long m_tiles, int &bn, int &splits, int total_kb) {
+    splits = 1;
+    if (ntot % 256) {
+        bn = pick_bn(ntot, m_tiles);
+        return;
+    }
+    bn = 256;
+    const long long tiles = m_tiles * (ntot / 256);
+    const long long sms = num_sms();
+    if (tiles * 5 >= sms * 4) return;
+    for (int sp = 2; sp <= 4; ++sp) {
+        if (total_kb / sp < 8) break;
+        splits = sp;
+        const long long units = tiles * sp;
+        const double eff = (double)units / (double)(((units + sms - 1) / sms) * sms);
+        if (eff >= 0.85) break;
+    }
+}
+
+// Split-K workspace: one fp32 [pixels][columns] buffer per process, grown on an eager call
+// (never inside stream capture), kept zeroed by the finishing kernels.  Calls that split
+// must not run concurrently on different streams (the U-Net issues convs on one stream).
+float *split_workspace(size_t bytes, cudaStream_t st) {
+    static float *ws = nullptr;
+    static size_t cap = 0;
+    if (bytes <= cap) return ws;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    if (ws) {
+        cudaStreamSynchronize(st);
+        cudaFree(ws);
+        ws = nullptr;
+        cap = 0;
+    }
+    if (cudaMalloc(&ws, bytes) != cudaSuccess) {
+        ws = nullptr;
+        return nullptr;
+    }
+    if (cudaMemsetAsync(ws, 0, bytes, st) != cudaSuccess) return nullptr;
+    cap = bytes;
+    return ws;
+}
+
+template <class P>
+int launch_split(const P &p, long long mtiles, int ncols, int total_kb, int splits, cudaStream_t st, float *ws) {
+    SplitK<P> q;
+    q.p = p;
+    q.ws = ws;
+    q.ld = ncols;
+    q.kps = (total_kb + splits - 1) / splits;
+    q.total_kb = total_kb;
+    const int z = (total_kb + q.kps - 1) / q.kps;
+    return launch<256, 4>(q, dim3((unsigned)mtiles, ncols / 256, (unsigned)z), st);
+}
+
 // Weight-gradient tiling.  cout >= 128: D = [cout][(tap, cin)] (M = cout); narrower layers
 // transpose the GEMM (M = (tap, cin), N = cout) so no TMEM lane holds a padding row.
 void wgrad_tiles(int ncols, int cout, int &trans, int &mtiles, int &ntiles, int &bn) {
@@ -1303,10 +1510,26 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
         return run_halo(p, nch, cout, dim3((unsigned)(p.pt.tw * p.pt.th * p.pt.tn)), st);
     }
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
-    const int bn = pick_bn(cout, mtiles);
+    int bn, splits;
+    const int total_kb = p.taps[0].n * ((c1 + c2) / BK);
+    pick_tiling(cout, mtiles, bn, splits, total_kb);
+    if (getenv("ICE_NO_SPLITK")) splits = 1;
     if (!map_act(&p.xa, x1, n, h, w, c1, p.pt)) return ICE_EINVAL;
     if (c2 && !map_act(&p.xb, x2, n, h, w, c2, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wgt, cout, p.taps[0].n, c1 + c2, bn)) return ICE_EINVAL;
+    if (splits > 1) {
+        const long long npx = (long long)n * h * w;
+        float *ws = split_workspace((size_t)npx * cout * 4, st);
+        if (ws) {
+            int rc = launch_split(p, mtiles, cout, total_kb, splits, st, ws);
+            if (rc) return rc;
+            const long long work = npx * (cout / 8), nblk = (work + 255) / 256;
+            const unsigned fgrid = (unsigned)(nblk < 148 * 16 ? nblk : 148 * 16);
+            split_finish_fprop<<<fgrid, 256, 0, st>>>(
+                ws, npx, h * w, cout, bias, drop_scale, relu, p.y);
+            return (int)cudaGetLastError();
+        }
+    }
     dim3 grid((unsigned)mtiles, cout / bn, 1);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
@@ -1342,11 +1565,28 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
         return run_halo(p, cout / 64, ct, dim3((unsigned)(p.pt.tw * p.pt.th * p.pt.tn)), st);
     }
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
-    int bn = pick_bn(ct, mtiles);
+    int bn, splits;
+    const int total_kb = p.taps.n * (cout / BK);
+    pick_tiling(ct, mtiles, bn, splits, total_kb);
+    if (getenv("ICE_NO_SPLITK")) splits = 1;
     // a column tile must not straddle the dx1 / dx2 split
-    while (bn > 64 && (c1 % bn)) bn >>= 1;
+    while (bn > 64 && (c1 % bn)) {
+        bn >>= 1;
+        splits = 1;
+    }
     if (!map_act(&p.dym, dy, n, h, w, cout, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wgt, cout, p.taps.n, ct, 64)) return ICE_EINVAL;
+    if (splits > 1) {
+        const long long npx = (long long)n * h * w;
+        float *ws = split_workspace((size_t)npx * ct * 4, st);
+        if (ws) {
+            int rc = launch_split(p, mtiles, ct, total_kb, splits, st, ws);
+            if (rc) return rc;
+            const int blocks = (ct / 256) * (int)((npx + FIN_STRIP - 1) / FIN_STRIP);
+            split_finish_dgrad<<<blocks, 256, 0, st>>>(ws, (int)npx, n, h, w, p);
+            return (int)cudaGetLastError();
+        }
+    }
     dim3 grid((unsigned)mtiles, ct / bn, 1);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);

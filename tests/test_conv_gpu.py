@@ -44,6 +44,8 @@ SHAPES = [  # n, h, w, c1, c2, cout, ksize
     (2, 128, 128, 128, 0, 128, 3),   # row-halo path (W % 128 == 0)
     (1, 4, 256, 64, 64, 64, 3),      # row-halo, concat input, 2 tiles per row
     (3, 128, 128, 64, 0, 64, 3),
+    (32, 8, 8, 1024, 0, 2048, 3),    # bottleneck: 256-wide tiles; dgrad splits K (64 tiles)
+    (8, 8, 8, 256, 256, 512, 3),     # 8 tiles: fprop and dgrad both split K, concat input
 ]
 
 
@@ -145,3 +147,38 @@ def test_halve_fprop_dgrad_wgrad(shape):
     assert rel(nchw(dx), xin.grad * (nchw(ref_relu) > 0)) < 1e-2
     assert rel(dbx, (xin.grad * (nchw(ref_relu) > 0)).sum((0, 2, 3))) < 1e-2
     assert rel(dw.permute(0, 3, 1, 2), wref.grad) < 1e-2
+
+
+def test_dgrad_split_k_planes_and_both_outputs():
+    """Split-K dgrad finisher: dx1 / dx2 split at c1, sub-pixel planes for dx2, gradient sums,
+    ReLU-backward masks, Dropout2d scales and both bias gradients."""
+    n, h, w, c1, c2, cout = 4, 8, 8, 256, 256, 512
+    torch.manual_seed(7)
+    dy = rnd(n, h, w, cout)
+    wt = rnd(cout, 3, 3, c1 + c2, scale=0.05)
+    ref1, ref2 = torch.relu(rnd(n, h, w, c1)), torch.relu(rnd(n, h, w, c2))
+    add1 = rnd(n, h, w, c1)
+    add2p = rnd(4, n, h // 2, w // 2, c2)
+    drop1 = (torch.rand(n, c1, device="cuda") > 0.2).float() / 0.8
+    drop2 = (torch.rand(n, c2, device="cuda") > 0.5).float() / 0.5
+    db1 = torch.zeros(c1, device="cuda")
+    db2 = torch.zeros(c2, device="cuda")
+    out2 = torch.empty(4, n, h // 2, w // 2, c2, dtype=torch.bfloat16, device="cuda")
+    ref2p = _planes(ref2)
+    d1, d2 = ops.conv_dgrad(dy, wt, c1, c2, ref1=ref1, add1=add1, drop1=drop1, db1=db1, out2=out2,
+                            ref2=ref2p, add2=add2p, drop2=drop2, db2=db2, planes2=True)
+    xin = torch.zeros(n, c1 + c2, h, w, device="cuda", requires_grad=True)
+    F.conv2d(xin, krsc_to_oihw(wt), padding=1).backward(nchw(dy))
+    g = xin.grad
+    want1 = (g[:, :c1] + nchw(add1)) * drop1[:, :, None, None] * (nchw(ref1) > 0)
+    add2 = torch.empty(n, h, w, c2, dtype=torch.bfloat16, device="cuda")
+    for p_, (cy, cx) in enumerate([(0, 0), (0, 1), (1, 0), (1, 1)]):
+        add2[:, cy::2, cx::2] = add2p[p_]
+    want2 = (g[:, c1:] + nchw(add2)) * drop2[:, :, None, None] * (nchw(ref2) > 0)
+    got2 = torch.empty(n, h, w, c2, dtype=torch.bfloat16, device="cuda")
+    for p_, (cy, cx) in enumerate([(0, 0), (0, 1), (1, 0), (1, 1)]):
+        got2[:, cy::2, cx::2] = d2[p_]
+    assert rel(nchw(d1), want1) < 1e-2
+    assert rel(nchw(got2), want2) < 1e-2
+    assert rel(db1, want1.sum((0, 2, 3))) < 1e-2
+    assert rel(db2, want2.sum((0, 2, 3))) < 1e-2
