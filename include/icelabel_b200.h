@@ -208,6 +208,41 @@ int ice_counter_add(int64_t *counter, int64_t delta, void *stream);
 int ice_cast_bf16(const float *src, int64_t n, uint16_t *dst, void *stream);
 int ice_fill_f32(float *dst, int64_t n, float value, void *stream);
 
+/* ---------------------------------------------------------------------------------
+ * Data path around the hot paths: u8 byte work, HBM-bound.
+ * --------------------------------------------------------------------------------- */
+
+/* cut_tiles (icetrain/data.py:55-66): img u8 [h][w][c] -> tiles u8 [rows*cols][size][size][c],
+ * rows = ceil(h/size), cols = ceil(w/size), tile t = (t / cols, t % cols), zero padded. */
+int ice_cut_tiles(const uint8_t *img, int32_t h, int32_t w, int32_t c, int32_t size, uint8_t *tiles,
+                  void *stream);
+
+/* stitch_tiles (data.py:69-80): inverse of ice_cut_tiles for a grid `cols` tiles wide
+ * (cols <= 0: ceil(w/size)), padding cropped to h x w. */
+int ice_stitch_tiles(const uint8_t *tiles, int32_t cols, int32_t size, int32_t c, int32_t h, int32_t w,
+                     uint8_t *out, void *stream);
+
+/* encode_labels (data.py:47-52): class index u8 [npx] -> RGB u8 [npx][3] from colors u8
+ * [ncls][3].  *first_bad (caller-initialised to UINT64_MAX) = min index of a class >= ncls. */
+int ice_encode_labels(const uint8_t *mask, int64_t npx, const uint8_t *colors, int32_t ncls, uint8_t *rgb,
+                      uint64_t *first_bad, void *stream);
+
+/* decode_labels (data.py:35-44): RGB u8 [npx][3] -> class index u8 [npx] (last matching
+ * colour wins, 255 for unknown); *first_bad = min index of an unknown colour. */
+int ice_decode_labels(const uint8_t *rgb, int64_t npx, const uint8_t *colors, int32_t ncls, uint8_t *mask,
+                      uint64_t *first_bad, void *stream);
+
+/* Inference head (infer.py:47 model.probabilities(x).argmax(1); softmax is monotone, so the
+ * argmax of the out 1x1 conv logits): h bf16 [npx][64], w_out fp32 [3][64], b_out [3] ->
+ * mask u8 [npx], first maximum on ties (torch.argmax). */
+int ice_head_argmax(const uint16_t *h, int64_t npx, const float *w_out, const float *b_out, uint8_t *mask,
+                    void *stream);
+
+/* confusion (icelabel/metrics.py:108-113): counts u64 [k][k] += #(pred == a, ref == b),
+ * k <= 4; pixels with a label >= k are added to *bad instead. */
+int ice_confusion(const uint8_t *pred, const uint8_t *ref, int64_t npx, int32_t k, uint64_t *counts, uint64_t *bad,
+                  void *stream);
+
 #ifdef __cplusplus
 }
 #endif

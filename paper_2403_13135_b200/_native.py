@@ -47,6 +47,12 @@ SIGNATURES = {
     "ice_autolabel": [_V, _I64, _I32, _I32, ctypes.POINTER(IceFilterCfg), ctypes.POINTER(IceScheme),
                       _V, _V, _V, _V, _V, _V, _V],
     "ice_autolabel_set_path": [_I32],
+    "ice_cut_tiles": [_V, _I32, _I32, _I32, _I32, _V, _V],
+    "ice_stitch_tiles": [_V, _I32, _I32, _I32, _I32, _I32, _V, _V],
+    "ice_encode_labels": [_V, _I64, _V, _I32, _V, _V, _V],
+    "ice_decode_labels": [_V, _I64, _V, _I32, _V, _V, _V],
+    "ice_head_argmax": [_V, _I64, _V, _V, _V, _V],
+    "ice_confusion": [_V, _V, _I64, _I32, _V, _V, _V],
     "ice_segment": [_V, _I64, _I32, _I32, ctypes.POINTER(IceScheme), _V, _V, _V, _V],
     "ice_rgb_to_hsv": [_V, _I64, _V, _V],
     "ice_conv_fprop": [_V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, _V, _I32, _I32, _V, _V, _V],

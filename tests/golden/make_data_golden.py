@@ -1,0 +1,61 @@
+"""Generate tests/golden/data_golden.json from the REFERENCE (run where /root/reference exists).
+
+    python tests/golden/make_data_golden.py
+
+Records sha256 digests of the reference's cut_tiles / stitch_tiles / encode_labels /
+decode_labels (pkg/trainer/src/icetrain/data.py:35-80) outputs, and its confusion counts and
+report (pkg/src/icelabel/metrics.py:108-142), on the seeded inputs of tests/golden/data_cases.py.
+"""
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, "/root/reference/pkg/trainer/src")
+
+from icetrain.data import cut_tiles, decode_labels, encode_labels, stitch_tiles  # noqa: E402  (reference)
+from icelabel.metrics import confusion, report  # noqa: E402
+from icelabel.raster import LabelMask  # noqa: E402
+
+from tests.golden import data_cases as dc  # noqa: E402
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+out = {"cut": [], "codec": []}
+for h, w in dc.SIZES:
+    img = dc.scene(h, w)
+    tiles = cut_tiles(img, dc.TILE)
+    rec = {"h": h, "w": w, "n_tiles": len(tiles), "tiles": [[sha(t), r, c] for t, r, c in tiles]}
+    m = dc.mask(h, w)
+    mt = cut_tiles(m.astype(np.int64), dc.TILE)
+    rec["mask_tiles"] = [[sha(t), str(t.dtype)] for t, _, _ in mt]
+    rec["stitch"] = sha(stitch_tiles(tiles, h, w))
+    out["cut"].append(rec)
+    enc = encode_labels(m.astype(np.int64))
+    dec = decode_labels(enc)
+    out["codec"].append({"h": h, "w": w, "encode": sha(enc), "decode": sha(dec), "decode_dtype": str(dec.dtype)})
+bad = encode_labels(dc.mask(17, 40).astype(np.int64))
+bad[3, 5] = (1, 2, 3)
+try:
+    decode_labels(bad, "x.png")
+except ValueError as exc:
+    out["decode_error"] = str(exc)
+try:
+    encode_labels(np.array([[0, 3]]))
+except ValueError as exc:
+    out["encode_error"] = str(exc)
+pred, ref = dc.pred_ref()
+cm = confusion(LabelMask(pred), LabelMask(ref))
+out["confusion"] = cm.counts.tolist()
+out["report"] = report(cm, 0.5).to_dict()
+out["report_csv"] = report(cm).to_csv()
+json.dump(out, open(os.path.join(os.path.dirname(__file__), "data_golden.json"), "w"), indent=1)
+print("ok")

@@ -1,0 +1,38 @@
+"""Pin oracle/data_ref.py to the reference's data-path outputs (tests/golden/data_golden.json)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+
+from oracle import data_ref as orc
+from tests.golden import data_cases as dc
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "data_golden.json")))
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_cut_stitch_oracle_matches_reference():
+    for rec in GOLDEN["cut"]:
+        img = dc.scene(rec["h"], rec["w"])
+        tiles = orc.cut_tiles(img, dc.TILE)
+        assert [[sha(t), r, c] for t, r, c in tiles] == rec["tiles"]
+        assert sha(orc.stitch_tiles(tiles, rec["h"], rec["w"])) == rec["stitch"]
+        mt = orc.cut_tiles(dc.mask(rec["h"], rec["w"]).astype(np.int64), dc.TILE)
+        assert [[sha(t), str(t.dtype)] for t, _, _ in mt] == rec["mask_tiles"]
+
+
+def test_codec_oracle_matches_reference():
+    for rec in GOLDEN["codec"]:
+        m = dc.mask(rec["h"], rec["w"]).astype(np.int64)
+        enc = orc.encode_labels(m)
+        assert sha(enc) == rec["encode"]
+        assert sha(orc.decode_labels(enc)) == rec["decode"]
+
+
+def test_confusion_oracle_matches_reference():
+    pred, ref = dc.pred_ref()
+    assert orc.confusion(pred, ref).tolist() == GOLDEN["confusion"]
