@@ -137,10 +137,34 @@ struct FpropProb {
     }
     __device__ int view_row(int tap) const { return (taps[0].dy[tap] + 1) * 130 + taps[0].dx[tap] + 1; }
 
+    // Epilogue operands of the NEXT tile, loaded before the accumulator wait: lane j holds
+    // bias[col0 + j] and (when all 32 rows of the warp are one image) drop[n][col0 + j] of
+    // the first two 32-column chunks; the epilogue broadcasts them with shuffles.
+    struct Pre {
+        float b[2], d[2];
+        int uni;
+    };
+    template <int BN>
+    __device__ void pre_load(Pre &pr, int row, int mt, int nt, int, int cc0, int cc1) const {
+        int n0, h0, w0, n, h, w;
+        pt.origin(mt, n0, h0, w0);
+        pt.pixel(row, n0, h0, w0, n, h, w);
+        const int lane = threadIdx.x & 31;
+        const int n_first = __shfl_sync(0xffffffffu, n, 0);
+        pr.uni = __all_sync(0xffffffffu, n == n_first) && n_first < N;
+#pragma unroll
+        for (int ci = 0; ci < 2; ++ci) {
+            const int col = nt * BN + (cc0 + ci) * 32 + lane;
+            const bool have = cc0 + ci < cc1;
+            pr.b[ci] = (have && bias) ? __ldg(bias + col) : 0.f;
+            pr.d[ci] = (have && drop && pr.uni) ? __ldg(drop + (size_t)n_first * cout + col) : 1.f;
+        }
+    }
     template <int BN>
     __device__ void flush_bias(int, int, int, float *) const {}
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *) const {
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *,
+                             const Pre &pr) const {
         int n0, h0, w0, n, h, w;
         pt.origin(mt, n0, h0, w0);
         pt.pixel(row, n0, h0, w0, n, h, w);
@@ -154,8 +178,39 @@ struct FpropProb {
         for (int cc = cc0; cc < cc1; ++cc) {
             float v[32];
             tc::tmem_ld32(tmem + cc * 32, v);
-            if (!valid) continue;
             const int col0 = nt * BN + cc * 32;
+            const int ci = cc - cc0;
+            if (ci < 2) {  // warp-uniform: prefetched operands, broadcast by shuffles
+                const float bsrc = ci == 0 ? pr.b[0] : pr.b[1];
+                const float dsrc = ci == 0 ? pr.d[0] : pr.d[1];
+                float dl[32];
+                if (drop && !pr.uni && valid) {  // rows of several images (tiny levels)
+                    const float *dr = drop + (size_t)n * cout + col0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        float t8[8];
+                        ld8(dr + q * 8, 1.f, t8);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) dl[q * 8 + e] = t8[e];
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float bj = __shfl_sync(0xffffffffu, bsrc, j);
+                    const float dj = __shfl_sync(0xffffffffu, dsrc, j);
+                    float a = v[j] + bj;
+                    if (relu) a = fmaxf(a, 0.f);
+                    v[j] = a * ((drop && !pr.uni) ? dl[j] : dj);
+                }
+                if (!valid) continue;
+                uint4 *dst = reinterpret_cast<uint4 *>(y + ((size_t)((size_t)n * OH + h) * OW + w) * cout + col0);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    dst[q] = make_uint4(tc::pack_bf16(v[q * 8], v[q * 8 + 1]), tc::pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
+                                        tc::pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), tc::pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+                continue;
+            }
+            if (!valid) continue;
             uint4 *dst = reinterpret_cast<uint4 *>(y + ((size_t)((size_t)n * OH + h) * OW + w) * cout + col0);
             const float *dr = drop ? drop + (size_t)n * cout + col0 : nullptr;
 #pragma unroll
@@ -247,8 +302,14 @@ struct DgradProb {
             bacc[ci] = 0.f;
         }
     }
+    // (register prefetch of the next tile's ReLU-reference rows measured slower: the
+    // extra in-flight loads contend with the epilogue's stores)
+    struct Pre {};
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *bacc) const {
+    __device__ void pre_load(Pre &, int, int, int, int, int, int) const {}
+    template <int BN>
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *bacc,
+                             const Pre &pr) const {
         int n0, h0, w0, n, h, w;
         pt.origin(mt, n0, h0, w0);
         pt.pixel(row, n0, h0, w0, n, h, w);
@@ -395,10 +456,13 @@ struct WgradProb {
             for (int j = 0; j < BN / 64; j += by) load_dy(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
         }
     }
+    struct Pre {};
+    template <int BN>
+    __device__ void pre_load(Pre &, int, int, int, int, int, int) const {}
     template <int BN>
     __device__ void flush_bias(int, int, int, float *) const {}
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *) const {
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *, const Pre &) const {
         const int m = mt * BM + row;
         const int ld = taps.n * (c1 + c2);
 #pragma unroll 1
@@ -444,10 +508,13 @@ struct SplitK {
     __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
         p.template load<BN>(kb, sa, sb, bar, mt, nt, 0);
     }
+    struct Pre {};
+    template <int BN>
+    __device__ void pre_load(Pre &, int, int, int, int, int, int) const {}
     template <int BN>
     __device__ void flush_bias(int, int, int, float *) const {}
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *) const {
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *, const Pre &) const {
         int n0, h0, w0, n, h, w;
         p.pt.origin(mt, n0, h0, w0);
         p.pt.pixel(row, n0, h0, w0, n, h, w);
@@ -680,6 +747,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
         float bacc[4] = {0.f, 0.f, 0.f, 0.f};  // fused bias-gradient partial sums (DgradProb)
         int cur_nt = -1;
         int local = 0;
+        typename P::Pre pre;
+        if (blockIdx.x < (unsigned)ntiles) {
+            int mt, nt, z;
+            g.coords(blockIdx.x, mt, nt, z);
+            p.template pre_load<BN>(pre, sub * 32 + lane, mt, nt, z, cc0, cc1);
+        }
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
             int mt, nt, z;
             g.coords(t, mt, nt, z);
@@ -687,11 +760,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
                 if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
                 cur_nt = nt;
             }
+            const typename P::Pre cur = pre;
+            if (t + (int)gridDim.x < ntiles) {  // next tile's epilogue operands, ahead of the wait
+                int mt2, nt2, z2;
+                g.coords(t + gridDim.x, mt2, nt2, z2);
+                p.template pre_load<BN>(pre, sub * 32 + lane, mt2, nt2, z2, cc0, cc1);
+            }
             const int acc = local & 1;
             tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
             tc::tc_fence_after();
             p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z, cc0,
-                                    cc1, bacc);
+                                    cc1, bacc, cur);
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
@@ -907,6 +986,12 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
         float bacc[4] = {0.f, 0.f, 0.f, 0.f};  // fused bias-gradient partial sums (DgradProb)
         int cur_nt = -1;
         int local = 0;
+        typename P::Pre pre;
+        if (blockIdx.x < (unsigned)ntiles) {
+            int mt, nt, z;
+            g.coords(blockIdx.x, mt, nt, z);
+            p.template pre_load<BN>(pre, sub * 32 + lane, mt, nt, z, cc0, cc1);
+        }
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
             int mt, nt, z;
             g.coords(t, mt, nt, z);
@@ -914,12 +999,18 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
                 if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
                 cur_nt = nt;
             }
+            const typename P::Pre cur = pre;
+            if (t + (int)gridDim.x < ntiles) {  // next tile's epilogue operands, ahead of the wait
+                int mt2, nt2, z2;
+                g.coords(t + gridDim.x, mt2, nt2, z2);
+                p.template pre_load<BN>(pre, sub * 32 + lane, mt2, nt2, z2, cc0, cc1);
+            }
             const int acc = local & 1;
             tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
             tc::tc_fence_after();
 #ifndef ICE_EXP_NOEPI
             p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z, cc0,
-                                    cc1, bacc);
+                                    cc1, bacc, cur);
 #endif
             tc::tc_fence_before();
             __syncwarp();

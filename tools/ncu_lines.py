@@ -10,6 +10,7 @@ import collections
 import csv
 import io
 import re
+import os
 import subprocess
 
 ap = argparse.ArgumentParser()
@@ -32,21 +33,27 @@ base = int(rows[0][0], 16)
 # mangled name from the cubin whose SASS length matches
 dis = subprocess.run(["nvdisasm", "-g", a.cubin], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s*\.text\.", dis)
-line_of = {}
+best = None
 for f in funcs:
     fname = f.split(":", 1)[0].strip()
     if not re.search(a.kernel, fname):
         continue
     cur = None
+    lo = {}
     for ln in f.splitlines():
-        m = re.search(r'line (\d+)', ln)
+        m = re.search(r'File "([^"]+)", line (\d+)', ln)
         if m and "//##" in ln:
-            cur = int(m.group(1))
+            cur = f"{os.path.basename(m.group(1))}:{m.group(2)}"
             continue
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if m and cur is not None:
-            line_of[int(m.group(1), 16)] = cur
-    break
+            lo[int(m.group(1), 16)] = cur
+    n_inst = (max(lo) // 16 + 1) if lo else 0
+    # the instantiation whose SASS length matches the profiled kernel's
+    score = abs(n_inst - len(rows))
+    if best is None or score < best[0]:
+        best = (score, lo, fname)
+line_of = best[1] if best else {}
 agg = collections.Counter()
 inst = collections.Counter()
 stall_cols = [(h, i) for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
@@ -54,7 +61,7 @@ reasons = collections.defaultdict(collections.Counter)
 total_reasons = collections.Counter()
 for r in rows:
     off = int(r[0], 16) - base
-    ln = line_of.get(off, -1)
+    ln = line_of.get(off, "?")
     agg[ln] += num(r[i_s])
     inst[ln] += num(r[i_e])
     for h, i in stall_cols:
@@ -67,4 +74,4 @@ rt = sum(total_reasons.values()) or 1
 print(" stall reasons:", ", ".join(f"{k} {100 * v / rt:.1f}%" for k, v in total_reasons.most_common(8)))
 for ln, v in agg.most_common(a.top):
     top = ", ".join(f"{k} {100 * c / max(1, sum(reasons[ln].values())):.0f}%" for k, c in reasons[ln].most_common(3))
-    print(f"  line {ln:5d}: {100 * v / tot:5.1f}% stalls  {100 * inst[ln] / itot:5.1f}% inst  [{top}]")
+    print(f"  {ln:28s}: {100 * v / tot:5.1f}% stalls  {100 * inst[ln] / itot:5.1f}% inst  [{top}]")
