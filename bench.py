@@ -101,6 +101,68 @@ def _scene_chunk(args):
     return np.stack([synth.scene(seed, i, SIZE, bool(flags[i]))[0] for i in range(lo, hi)])
 
 
+def _scene512_chunk(args):
+    from paper_2403_13135_b200.icelabel import synth
+    seed, count, haze, lo, hi = args
+    flags = synth.haze_flags(seed, count, haze)
+    out = [synth.scene(seed, i, 512, bool(flags[i])) for i in range(lo, hi)]
+    return np.stack([o[0] for o in out]), np.stack([o[1] for o in out])
+
+
+def config5_bench(dev, dist, world, rank, steps: int = 10, warmup: int = 3, count: int = 64):
+    """BASELINE config 5 geometry on this job's GPUs: the paper U-Net on 512 x 512 tiles
+    (generate_corpus(101, 64, 0.3, size=512) with the generator's truth labels), batch 16 per
+    GPU, device-timed like the headline.  Returns a dict for the JSON line."""
+    import multiprocessing as mp
+    from paper_2403_13135_b200.icetrain import Adam, UNet, UNetSpec
+    from paper_2403_13135_b200.icetrain.train import GradBucketer, GraphedStep, device_step
+    bounds = np.linspace(0, count, 9).astype(int)
+    with mp.get_context("fork").Pool(8) as pool:
+        parts = pool.map(_scene512_chunk, [(101, count, 0.3, int(bounds[i]), int(bounds[i + 1])) for i in range(8)])
+    x_all = torch.from_numpy(np.concatenate([p[0] for p in parts])).to(dev)
+    y_all = torch.from_numpy(np.concatenate([p[1] for p in parts])).to(dev)
+    batch = 16
+    torch.manual_seed(0)
+    model = UNet(UNetSpec(input_size=512), dev)
+    if dist:
+        dist.broadcast(model.engine.params, 0)
+        model.engine.refresh_working_weights()
+    opt = Adam(model.parameters(), lr=1e-3)
+    bucketer = GradBucketer(model.engine, bucket_bytes=(64 << 20) if dist else (16 << 20), optimizer=opt)
+    gen = torch.Generator().manual_seed(55)
+    union = batch * world
+    idx = [torch.randperm(count, generator=gen)[:union][rank * batch:(rank + 1) * batch].to(dev)
+           for _ in range(warmup + steps)]
+    xs = [x_all[i].contiguous() for i in idx]
+    ys = [y_all[i].contiguous() for i in idx]
+    graphed = GraphedStep(model, opt, xs[0], ys[0], union, bucketer) if world == 1 else None
+    run = (lambda i: graphed(xs[i], ys[i])) if graphed else (lambda i: device_step(model, opt, xs[i], ys[i], union, bucketer))
+    for i in range(warmup):
+        run(i)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(warmup, warmup + steps):
+        run(i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = union * steps / (ms / 1000.0)
+    del model, opt, bucketer, graphed
+    torch.cuda.empty_cache()
+    return {"metric": "U-Net train images/sec @512^2 (config 5 geometry: paper U-Net, batch 16/GPU)",
+            "value": round(value, 2), "unit": UNIT, "ms_per_step": round(ms / steps, 3), "steps": steps,
+            "warmup": warmup, "n_gpus": world, "global_batch": union,
+            "tflops": round(1622.4e9 * union / (ms / steps / 1000.0) / 1e12, 1),
+            "data": "synthetic generate_corpus(101, 64, 0.3, size=512) tiles, generator truth labels"}
+
+
 def make_corpus(count: int, workers: int = 8) -> np.ndarray:
     """T-gray tiles generate_corpus(101, count, 0.3), in parallel."""
     import multiprocessing as mp
@@ -263,6 +325,7 @@ def main():
     ap.add_argument("--corpus", type=int, default=CORPUS)
     ap.add_argument("--no-autolabel", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-config5", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
 
@@ -456,6 +519,17 @@ def main():
         except Exception as exc:  # the GPU number stands without it
             autolabel["cpu_baseline"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
 
+    launch_mode = "CUDA graph per step" if graphed is not None else "eager"
+    config5 = None
+    if not args.no_config5:
+        del graphed
+        torch.cuda.empty_cache()
+        graphed = None
+        try:
+            config5 = config5_bench(dev, dist, world, rank)
+        except Exception as exc:  # the headline stands without it
+            config5 = {"unavailable": f"{type(exc).__name__}: {exc}"}
+
     # ---- CPU baseline (rank 0, N = 1 only): bounded sample of the reference step -------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -473,12 +547,12 @@ def main():
                                        "synthetic 256x256 tiles, batch 32/GPU, Adam",
                            "global_batch": union, "seq_len": None, "parallelism": f"dp{world}",
                            "l2": "per-step working set (activations, 124M params) >> 126 MB L2; no flush",
-                           "launch": "CUDA graph per step" if graphed is not None else "eager"},
+                           "launch": launch_mode},
                 "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": 8, "steps": e2e_steps,
                         "api": "icetrain.synchronized_step([model], [opt], [(pinned u8 NHWC, pinned u8)])"},
                 "gpu_launches": int(launches), "clocks": clocks.summary(), "roofline": roofline,
-                "cpu_baseline": cpu, "autolabel": autolabel, "kernels": kernels,
+                "cpu_baseline": cpu, "autolabel": autolabel, "config5": config5, "kernels": kernels,
                 "tflops_step": round(405.6e9 * BATCH / (ms / args.steps / 1000.0) / 1e12, 1),
                 "loss_last": round(loss, 4)}
         print(json.dumps(line), flush=True)

@@ -7,6 +7,7 @@ reference itself (tests/golden/unet_golden.pt) or from the pinned oracle
 """
 import os
 
+import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
@@ -220,3 +221,48 @@ def test_loss_trajectory_200_steps():
     best = min(evals)
     assert best[0] <= 2.0 * gold["eval_loss"], (evals, gold["eval_loss"])
     assert best[1] >= 0.98, evals
+
+
+def test_config5_512_tiles_forward_and_grads_match_oracle():
+    """BASELINE config 5 geometry (512 x 512 tiles): the engine at 512^2 (desk width, base 16)
+    against the fp32 CPU oracle -- logits, loss and whole-model gradient."""
+    spec = UNetSpec(input_size=512, base_channels=16, dropout=0.0)
+    rng = np.random.default_rng(512)
+    images = torch.from_numpy(rng.integers(0, 256, (2, 512, 512, 3), dtype=np.uint8))
+    labels = torch.from_numpy(rng.integers(0, 3, (2, 512, 512)))
+    torch.manual_seed(0)
+    model = UNet(spec)
+    ref = unet_ref.RefUNet(spec)
+    ref.load_state_dict({k: v.cpu() for k, v in model.state_dict().items()})
+    x = unet_ref.images_to_input(images.numpy())
+    assert rel(model(x), ref(x).detach()) < 2e-2
+    loss, grads = engine_grads(model, images, labels)
+    out = ref(x)
+    want = torch.nn.functional.cross_entropy(out, labels)
+    want.backward()
+    assert abs(loss - float(want.detach())) / float(want.detach()) < 2e-2
+    g_ours = torch.cat([grads[k].flatten().double().cpu() for k in sorted(grads)])
+    g_ref = torch.cat([dict(ref.named_parameters())[k].grad.flatten().double() for k in sorted(grads)])
+    assert rel(g_ours, g_ref) < 2e-2
+
+
+def test_config5_paper_width_512_step_runs():
+    """Paper width (base 64) at 512^2, batch 4: full train steps (fused Adam) stay finite and
+    fit a learnable target (class = #channels above 128, capped at 2) on a repeated batch."""
+    from paper_2403_13135_b200.icetrain import Adam
+    from paper_2403_13135_b200.icetrain.train import device_step
+    spec = UNetSpec(input_size=512, dropout=0.0)
+    rng = np.random.default_rng(5)
+    xh = rng.integers(0, 256, (4, 512, 512, 3), dtype=np.uint8)
+    yh = np.minimum((xh > 128).sum(-1), 2).astype(np.uint8)
+    x, y = torch.from_numpy(xh).cuda(), torch.from_numpy(yh).cuda()
+    torch.manual_seed(0)
+    model = UNet(spec)
+    opt = Adam(model.parameters(), lr=1e-3)
+    losses = []
+    for _ in range(6):
+        model.engine.stats.zero_()
+        device_step(model, opt, x, y, 4)
+        torch.cuda.synchronize()
+        losses.append(float(model.engine.stats[0]) / y.numel())
+    assert all(np.isfinite(losses)) and losses[-1] < losses[0]
