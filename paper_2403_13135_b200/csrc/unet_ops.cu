@@ -225,7 +225,7 @@ __global__ void maxpool_bwd_kernel(const uint16_t *__restrict__ x, const uint16_
 constexpr int HEAD_NT = 256;
 constexpr int HC = 64;
 
-__global__ void __launch_bounds__(HEAD_NT, 2) head_ce_kernel(
+__global__ void __launch_bounds__(HEAD_NT, 4) head_ce_kernel(
     const uint16_t *__restrict__ hact, long long npx, int hw, const uint8_t *__restrict__ labels,
     const float *__restrict__ w_out, const float *__restrict__ b_out, const float *__restrict__ drop, float grad_scale,
     uint16_t *__restrict__ dz, float *__restrict__ dw, float *__restrict__ db, float *__restrict__ stats,
@@ -267,20 +267,21 @@ __global__ void __launch_bounds__(HEAD_NT, 2) head_ce_kernel(
             }
             __syncwarp();
         }
-        float h[HC];
+        // the lane's activation row is read from the stage twice (logits here, the ReLU mask
+        // of dz below) instead of being held in 64 registers: 4 blocks per SM instead of 2
+        float l0 = b0, l1 = b1, l2 = b2;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             uint4 u = *reinterpret_cast<const uint4 *>(wst + lane * 144 + q * 16);
             const uint16_t *e = reinterpret_cast<const uint16_t *>(&u);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) h[q * 8 + j] = bf(e[j]);
-        }
-        float l0 = b0, l1 = b1, l2 = b2;
-#pragma unroll
-        for (int j = 0; j < HC; ++j) {
-            l0 = fmaf(sw[j], h[j], l0);
-            l1 = fmaf(sw[HC + j], h[j], l1);
-            l2 = fmaf(sw[2 * HC + j], h[j], l2);
+            for (int jj = 0; jj < 8; ++jj) {
+                const int j = q * 8 + jj;
+                const float hj = bf(e[jj]);
+                l0 = fmaf(sw[j], hj, l0);
+                l1 = fmaf(sw[HC + j], hj, l1);
+                l2 = fmaf(sw[2 * HC + j], hj, l2);
+            }
         }
         float d0 = 0.f, d1 = 0.f, d2 = 0.f;
         if (valid) {
@@ -334,6 +335,8 @@ __global__ void __launch_bounds__(HEAD_NT, 2) head_ce_kernel(
             const long long img = p / hw;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
+                const uint4 hu = *reinterpret_cast<const uint4 *>(wst + lane * 144 + q * 16);
+                const uint16_t *he = reinterpret_cast<const uint16_t *>(&hu);
                 uint32_t pk[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(HEAD_NT, 2) head_ce_kernel(
                         const int j = q * 8 + e * 2 + u;
                         float v = d0 * sw[j] + d1 * sw[HC + j] + d2 * sw[2 * HC + j];
                         if (drop) v *= hw % HEAD_NT == 0 ? sdrop[j] : __ldg(drop + img * HC + j);
-                        g[u] = h[j] > 0.f ? v : 0.f;
+                        g[u] = bf(he[e * 2 + u]) > 0.f ? v : 0.f;
                     }
                     pk[e] = (uint32_t)to_bf(g[0]) | ((uint32_t)to_bf(g[1]) << 16);
                 }
