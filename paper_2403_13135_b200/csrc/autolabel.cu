@@ -742,6 +742,8 @@ struct SmemF {
     int red[NTF / 32][4];
     int bc[8];
     int act[16];            // median21 block activity, [band][half]
+    int kmin[16], kmax[16]; // median21 coarse buckets per block
+    unsigned int done_bits; // median21: blocks whose current bucket is final
     uint32_t hist_v[256];   // histogram of V (channel median of the gray repair)
 };
 
@@ -888,7 +890,10 @@ __device__ __forceinline__ void row_counts(const uint32_t *src, uint32_t *dst, u
 // ---- column pass: window count >= MGE (median > t) adds gap to the pixel's median --------
 // Sliding 16-bit lane sums (even / odd pixels of the word), biased by K so that bit 15 of a
 // lane is the comparison.  EDGE: 0 interior band, 1 top band, 2 bottom band (clamped rows).
-template <int EDGE>
+// MODE 0: acc += bits * arg (value-mode median, arg = value gap); MODE 1: acc += bits (rank
+// units); MODE 2: acc += bits where acc <= i (arg = (i | 0x80) per byte: the fine pass of
+// rank i counts only for pixels whose coarse bucket holds i).
+template <int EDGE, int MODE>
 __device__ __forceinline__ uint32_t col_band(const uint32_t *cnt, uint32_t *acc, uint32_t gap, int c, int y0) {
     constexpr uint32_t M = 0x00ff00ffu;
     constexpr uint32_t K = (0x8000u - MGE) * 0x00010001u;
@@ -904,8 +909,16 @@ __device__ __forceinline__ uint32_t col_band(const uint32_t *cnt, uint32_t *acc,
     uint32_t *pa = acc + y0 * WP + c;
 #pragma unroll 8
     for (int y = 0; y < 32; ++y) {
-        const uint32_t bits = ((ae >> 15) & 0x00010001u) | ((ao >> 7) & 0x01000100u);
-        pa[y * WP] += bits * gap;
+        uint32_t bits = ((ae >> 15) & 0x00010001u) | ((ao >> 7) & 0x01000100u);
+        if (MODE == 0) {
+            pa[y * WP] += bits * gap;
+        } else if (MODE == 1) {
+            pa[y * WP] += bits;
+        } else {
+            const uint32_t a = pa[y * WP];
+            bits &= ((gap - a) >> 7) & 0x01010101u;  // 0x80 + i - acc: bit 7 <=> acc <= i (both < 128)
+            pa[y * WP] = a + bits;
+        }
         any |= bits;
         uint32_t n, o;
         if (EDGE == 0) {
@@ -923,22 +936,56 @@ __device__ __forceinline__ uint32_t col_band(const uint32_t *cnt, uint32_t *acc,
     return any;
 }
 
+template <int MODE>
+__device__ __forceinline__ uint32_t col_pass(const uint32_t *tmp, uint32_t *acc, uint32_t arg, int c, int band) {
+    return band == 0 ? col_band<1, MODE>(tmp, acc, arg, c, 0)
+                     : (band == 7 ? col_band<2, MODE>(tmp, acc, arg, c, 224) : col_band<0, MODE>(tmp, acc, arg, c, band * 32));
+}
+
 // 21 x 21 median of src (kernels.py:42-46) into the plane acc ("col" map).  The value set
-// must already be flagged in s.flags (dilate7 does that).  tmp is scratch.
-// Block skipping: a (band, half) block whose pixels all had median <= t after a pass stays
-// final for every larger threshold (the counts are monotone in t), so its column pass is
-// skipped, and a row-pass warp runs only while a block it feeds (+-10 rows) is active.
-__device__ void median21(uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s) {
+// must already be flagged in s.flags (dilate7 does that).  tmp is scratch; src is clobbered.
+//
+// Rank mode (<= 128 distinct values; src rewritten as 0x80 | rank): the median's rank R(p) =
+// #{i : median > s_i} accumulates in acc, coarse-to-fine:
+//   1. coarse passes at ranks 8k+7 give the bucket K(p) = floor(R / 8) of every pixel; a
+//      (32-row x 128-px) block whose pixels all stopped is skipped from then on (counts are
+//      monotone in the threshold), and the loop ends when no block is active;
+//   2. acc becomes 8K; each block then runs only the fine ranks of the buckets its pixels
+//      occupy ([Kmin, Kmax] of the block), adding a pass's bit only where acc <= i (pixels of
+//      higher buckets have bit 1 there and are already counted by 8K);
+//   3. median = s_R through a byte LUT.
+// A row-pass warp runs only when one of the blocks it feeds (+-10 rows) runs the pass.
+// Value mode (> 128 distinct values): one pass per distinct value, acc += gap.
+constexpr int CG = 8;  // coarse group (ranks per bucket)
+#ifndef ICE_AL_COARSE_V
+#define ICE_AL_COARSE_V false
+#endif
+#ifndef ICE_AL_COARSE_C
+#define ICE_AL_COARSE_C true
+#endif
+
+__device__ void median21(uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s, bool coarse) {
     const int nd = collect_values(s);
 #ifdef ICE_AL_PROF
     if (threadIdx.x == 0) atomicAdd(&g_al_prof[8], (unsigned long long)nd);
 #endif
-    const uint32_t v0 = s.vals[0] * 0x01010101u;
     const int c = threadIdx.x & 63, band = threadIdx.x >> 6, lane = threadIdx.x & 31;
     const int rwarp = (threadIdx.x & 255) >> 5, rhalf = threadIdx.x >> 8;  // row map: rows 32 rwarp..
+    const int blk = 2 * band + (c >> 5);
+    const bool rank_mode = nd <= 128;
+    const bool two_level = rank_mode && coarse;
+    const uint32_t v0 = two_level ? 0u : s.vals[0] * 0x01010101u;
     for (int y = band * 32; y < band * 32 + 32; ++y) acc[y * WP + c] = v0;
     if (threadIdx.x < 16) s.act[threadIdx.x] = 1;
-    const bool rank_mode = nd <= 128;
+    // 16-bit block mask (bit 2*band + half) -> does this row-pass warp feed an active block?
+    const uint32_t feed = (1u << (2 * rwarp + rhalf)) | (rwarp > 0 ? 1u << (2 * (rwarp - 1) + rhalf) : 0u) |
+                          (rwarp < 7 ? 1u << (2 * (rwarp + 1) + rhalf) : 0u);
+    auto act_mask = [&]() {
+        uint32_t m = 0;
+#pragma unroll
+        for (int b2 = 0; b2 < 16; ++b2) m |= (s.act[b2] ? 1u : 0u) << b2;
+        return m;
+    };
     if (rank_mode) {  // src plane -> 0x80 | rank (in place; values come back through s.vals)
         for (int i = threadIdx.x; i < 256 * 64; i += NTF) {
             uint32_t *w = src + (i >> 6) * WP + (i & 63);
@@ -947,33 +994,112 @@ __device__ void median21(uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s) 
                  (uint32_t)s.rank[v >> 24] << 24;
         }
     }
-    uint32_t any = 1;
-    for (int i = 0; i + 1 < nd; ++i) {
-        const uint32_t t = s.vals[i], gap = (uint32_t)s.vals[i + 1] - t;
-        if (!__syncthreads_or(any)) break;  // no pixel moved in the previous pass: all final
-        const int* act = s.act;
-        if (act[2 * rwarp + rhalf] | (rwarp > 0 ? act[2 * (rwarp - 1) + rhalf] : 0) |
-            (rwarp < 7 ? act[2 * (rwarp + 1) + rhalf] : 0)) {
-            if (rank_mode) row_counts<true>(src, tmp, (uint32_t)(i + 1) * 0x01010101u);
-            else row_counts<false>(src, tmp, (255u - t) * 0x01010101u);
+    if (!two_level) {  // one pass per distinct value, acc += value gap, block skipping
+        uint32_t any = 1;
+        for (int i = 0; i + 1 < nd; ++i) {
+            const uint32_t t = s.vals[i], gap = (uint32_t)s.vals[i + 1] - t;
+            if (!__syncthreads_or(any)) break;  // no pixel moved in the previous pass: all final
+            if (s.act[2 * rwarp + rhalf] | (rwarp > 0 ? s.act[2 * (rwarp - 1) + rhalf] : 0) |
+                (rwarp < 7 ? s.act[2 * (rwarp + 1) + rhalf] : 0)) {
+                if (rank_mode) row_counts<true>(src, tmp, (uint32_t)(i + 1) * 0x01010101u);
+                else row_counts<false>(src, tmp, (255u - t) * 0x01010101u);
+            }
+            __syncthreads();
+            any = 0;
+            if (s.act[blk]) {
+                any = col_pass<0>(tmp, acc, gap, c, band);
+                const bool wa = __any_sync(0xffffffffu, any != 0);
+                if (lane == 0) s.act[blk] = wa;
+            }
         }
         __syncthreads();
-        const int blk = 2 * band + (c >> 5);
+        if (threadIdx.x < 256) s.flags[threadIdx.x] = 0;
+        return;
+    }
+    const int cg = CG;
+    // 1. coarse passes
+    uint32_t any = 1;
+    for (int i = cg - 1; i + 1 < nd; i += cg) {
+        if (!__syncthreads_or(any)) break;
+        if (act_mask() & feed) row_counts<true>(src, tmp, (uint32_t)(i + 1) * 0x01010101u);
+        __syncthreads();
 #ifdef ICE_AL_PROF
         if (threadIdx.x == 0) {
             int na = 0;
-            for (int k = 0; k < 16; ++k) na += act[k];
+            for (int k = 0; k < 16; ++k) na += s.act[k];
             atomicAdd(&g_al_prof[9], 1ull);
             atomicAdd(&g_al_prof[10], (unsigned long long)na);
         }
 #endif
         any = 0;
-        if (act[blk]) {
-            any = band == 0 ? col_band<1>(tmp, acc, gap, c, 0)
-                            : (band == 7 ? col_band<2>(tmp, acc, gap, c, 224) : col_band<0>(tmp, acc, gap, c, band * 32));
+        if (s.act[blk]) {
+            any = col_pass<1>(tmp, acc, 1u, c, band);
             const bool wa = __any_sync(0xffffffffu, any != 0);
             if (lane == 0) s.act[blk] = wa;
         }
+    }
+    __syncthreads();
+    // 2. buckets: per-block [Kmin, Kmax], acc = 8K
+    {
+        uint32_t mn = 0xffffffffu, mx = 0;
+        for (int y = band * 32; y < band * 32 + 32; ++y) {
+            const uint32_t a = acc[y * WP + c];
+            mn = vmin(mn, a);
+            mx = vmax(mx, a);
+            acc[y * WP + c] = a << 3;  // K <= 15: no byte overflow
+        }
+        int kmn = min(min(mn & 255, (mn >> 8) & 255), min((mn >> 16) & 255, mn >> 24));
+        int kmx = max(max(mx & 255, (mx >> 8) & 255), max((mx >> 16) & 255, mx >> 24));
+        for (int o = 16; o; o >>= 1) {
+            kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+            kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+        }
+        if (lane == 0) {
+            s.kmin[blk] = kmn;
+            s.kmax[blk] = kmx;
+        }
+    }
+    __syncthreads();
+    uint32_t span = 0, top = 0;  // blocks whose bucket range holds k / whose top bucket is k
+    for (int i = 0; i + 1 < nd; ++i) {
+        if (i % cg == cg - 1) continue;  // coarse rank: counted
+        const int k = i / cg;
+        if (i % cg == 0) {  // new bucket: static masks, clear the done set (rare: <= nd / 8 times)
+            span = 0;
+            top = 0;
+#pragma unroll
+            for (int b2 = 0; b2 < 16; ++b2) {
+                span |= (s.kmin[b2] <= k && k <= s.kmax[b2] ? 1u : 0u) << b2;
+                top |= (s.kmax[b2] == k ? 1u : 0u) << b2;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) s.done_bits = 0;
+            __syncthreads();
+        }
+        const uint32_t need = span & ~s.done_bits;
+        if (!need) continue;  // block-uniform
+        if (need & feed) row_counts<true>(src, tmp, (uint32_t)(i + 1) * 0x01010101u);
+        __syncthreads();
+#ifdef ICE_AL_PROF
+        if (threadIdx.x == 0) {
+            atomicAdd(&g_al_prof[9], 1ull);
+            atomicAdd(&g_al_prof[10], (unsigned long long)__popc(need));
+        }
+#endif
+        if ((need >> blk) & 1) {
+            // the block's top bucket holds no higher-bucket pixels: no mask needed
+            const uint32_t moved = ((top >> blk) & 1) ? col_pass<1>(tmp, acc, 1u, c, band)
+                                                      : col_pass<2>(tmp, acc, (uint32_t)(i | 0x80) * 0x01010101u, c, band);
+            // bucket k of this block is final once no pixel of it still moves
+            if (!__any_sync(0xffffffffu, moved != 0) && lane == 0) atomicOr(&s.done_bits, 1u << blk);
+        }
+        __syncthreads();
+    }
+    // 3. rank -> value
+    for (int y = band * 32; y < band * 32 + 32; ++y) {
+        const uint32_t r = acc[y * WP + c];
+        acc[y * WP + c] = s.vals[r & 255] | (uint32_t)s.vals[(r >> 8) & 255] << 8 |
+                          (uint32_t)s.vals[(r >> 16) & 255] << 16 | (uint32_t)s.vals[r >> 24] << 24;
     }
     __syncthreads();
     if (threadIdx.x < 256) s.flags[threadIdx.x] = 0;  // ready for the next median
@@ -1168,7 +1294,7 @@ __device__ __forceinline__ void process_tile256(const uint8_t *__restrict__ rgb,
     dilate7(P0, P1, P2, s);  // D in P2 (its column pass starts after a barrier: P2 reads done)
     PROF_MARK(1);
     // 2. bg = median21(D) (estimate_background, cloudfilter.py:82-84) into P1
-    median21(P2, P0, P1, s);
+    median21(P2, P0, P1, s, ICE_AL_COARSE_V);
     PROF_MARK(2);
     // 3. smooth = median3(V) (:90), d = |smooth - bg| [truncated] (:91-93) into P2, histogram
     load_plane(tile, 3, P0);  // V again (L2-resident re-read)
@@ -1262,7 +1388,7 @@ __device__ __forceinline__ void process_tile256(const uint8_t *__restrict__ rgb,
                 __syncthreads();
                 const int c_ch = center_from_hist(s.hist, NPX);
                 dilate7(P0, P1, P2, s);
-                median21(P2, P0, P1, s);  // bg_c in P1
+                median21(P2, P0, P1, s, ICE_AL_COARSE_C);  // bg_c in P1
                 load_plane(tile, ch, P0);  // the channel again (L2-resident re-read)
                 __syncthreads();
 #pragma unroll 2
