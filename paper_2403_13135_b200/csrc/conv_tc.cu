@@ -1440,7 +1440,8 @@ void pick_tiling(int ntot, long long m_tiles, int &bn, int &splits, int total_kb
 }
 
 // Split-K workspace: one fp32 [pixels][columns] buffer per process, grown on an eager call
-// (never inside stream capture), kept zeroed by the finishing kernels.  Calls that split
+// (never inside stream capture), kept zeroed by the finishing kernels.  A grown buffer never
+// frees its predecessor: CUDA graphs captured earlier keep pointing at it.  Calls that split
 // must not run concurrently on different streams (the U-Net issues convs on one stream).
 float *split_workspace(size_t bytes, cudaStream_t st) {
     static float *ws = nullptr;
@@ -1448,18 +1449,12 @@ float *split_workspace(size_t bytes, cudaStream_t st) {
     if (bytes <= cap) return ws;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-    if (ws) {
-        cudaStreamSynchronize(st);
-        cudaFree(ws);
-        ws = nullptr;
-        cap = 0;
-    }
-    if (cudaMalloc(&ws, bytes) != cudaSuccess) {
-        ws = nullptr;
-        return nullptr;
-    }
-    if (cudaMemsetAsync(ws, 0, bytes, st) != cudaSuccess) return nullptr;
-    cap = bytes;
+    size_t want = bytes < ((size_t)32 << 20) ? ((size_t)32 << 20) : 2 * bytes;
+    float *fresh = nullptr;
+    if (cudaMalloc(&fresh, want) != cudaSuccess) return nullptr;
+    if (cudaMemsetAsync(fresh, 0, want, st) != cudaSuccess) return nullptr;
+    ws = fresh;  // the previous buffer stays allocated (referenced by captured graphs)
+    cap = want;
     return ws;
 }
 

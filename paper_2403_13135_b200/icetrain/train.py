@@ -18,6 +18,7 @@ Every replica then applies the identical fused Adam step, so replicas never drif
 
 from __future__ import annotations
 
+import os
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -169,7 +170,8 @@ class GraphedStep:
     dropout seeds advance through the engine's device step counter, so replays are real
     consecutive training steps."""
 
-    def __init__(self, model, optimizer, x, y, union_count: int, bucketer=None, warmup: int = 2):
+    def __init__(self, model, optimizer, x, y, union_count: int, bucketer=None, warmup: int = 2,
+                 zero_stats: bool = False):
         self.model, self.optimizer = model, optimizer
         self.x = x.clone()
         self.y = y.clone()
@@ -183,6 +185,8 @@ class GraphedStep:
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
+            if zero_stats:  # the replay's loss sum / hit count start from zero
+                model.engine.stats.zero_()
             device_step(model, optimizer, self.x, self.y, union_count, bucketer)
         # the capture itself did not run the step: undo its host-side step bookkeeping
         optimizer.step_count -= 1

@@ -38,3 +38,4 @@ def test_graph_replay_equals_eager(dropout):
     # steps agree to rounding, not bit for bit
     rel = float((runs[0] - runs[1]).norm() / runs[0].norm())
     assert rel < 1e-5, rel
+
