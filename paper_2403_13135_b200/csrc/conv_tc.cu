@@ -101,6 +101,8 @@ struct FpropProb {
     const float *drop;  // [N][cout] or null
     int relu;
     bf16 *y;
+    CUtensorMap ym;     // y as (cout, W, H, N), box 32 ch x 32 px, SWIZZLE_64B (staged stores)
+    int y_tma;
 
     __device__ void kb_range(int z, int &kb0, int &nkb) const {
         kb0 = 0;
@@ -164,7 +166,7 @@ struct FpropProb {
     __device__ void flush_bias(int, int, int, float *) const {}
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *,
-                             const Pre &pr) const {
+                             const Pre &pr, uint8_t *stage = nullptr) const {
         int n0, h0, w0, n, h, w;
         pt.origin(mt, n0, h0, w0);
         pt.pixel(row, n0, h0, w0, n, h, w);
@@ -201,6 +203,22 @@ struct FpropProb {
                     float a = v[j] + bj;
                     if (relu) a = fmaxf(a, 0.f);
                     v[j] = a * ((drop && !pr.uni) ? dl[j] : dj);
+                }
+                if (stage && y_tma) {  // warp-uniform: rows of one image row, all valid (halo tiles)
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) pk[e] = tc::pack_bf16(v[2 * e], v[2 * e + 1]);
+                    const int lane = threadIdx.x & 31;
+                    if (lane == 0) tc::bulk_wait_read<1>();  // this buffer's previous store has read smem
+                    __syncwarp();
+                    tc::stage_row64(stage, lane, pk);
+                    tc::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tc::tma_store_4d(&ym, stage, col0, w, h, n);  // lane 0's pixel starts the box
+                        tc::bulk_commit();
+                    }
+                    continue;
                 }
                 if (!valid) continue;
                 uint4 *dst = reinterpret_cast<uint4 *>(y + ((size_t)((size_t)n * OH + h) * OW + w) * cout + col0);
@@ -247,6 +265,8 @@ struct DgradProb {
     const bf16 *ref1, *ref2, *add1, *add2;
     const float *drop1, *drop2;
     float *db1, *db2;  // fused bias gradients of the layers whose pre-activation grads these are
+    CUtensorMap o1m;   // dx1 as (c1, W, H, N), box 32 ch x 32 px, SWIZZLE_64B (staged stores)
+    int o1_tma;
 
     __device__ void kb_range(int, int &kb0, int &nkb) const {
         kb0 = 0;
@@ -309,7 +329,7 @@ struct DgradProb {
     __device__ void pre_load(Pre &, int, int, int, int, int, int) const {}
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *bacc,
-                             const Pre &pr) const {
+                             const Pre &pr, uint8_t *stage = nullptr) const {
         int n0, h0, w0, n, h, w;
         pt.origin(mt, n0, h0, w0);
         pt.pixel(row, n0, h0, w0, n, h, w);
@@ -372,11 +392,26 @@ struct DgradProb {
                         v[4 * q + 3] *= d.w;
                     }
                 }
-                uint4 *dst = reinterpret_cast<uint4 *>(out + off);
+                if (stage && o1_tma && out == out1) {  // warp-uniform (halo tiles: all rows valid)
+                    uint32_t pk[16];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    dst[q] = make_uint4(tc::pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), tc::pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
-                                        tc::pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), tc::pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+                    for (int e = 0; e < 16; ++e) pk[e] = tc::pack_bf16(v[2 * e], v[2 * e + 1]);
+                    if (lane == 0) tc::bulk_wait_read<1>();  // this buffer's previous store has read smem
+                    __syncwarp();
+                    tc::stage_row64(stage, lane, pk);
+                    tc::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tc::tma_store_4d(&o1m, stage, col, w, h, n);  // lane 0's pixel starts the box
+                        tc::bulk_commit();
+                    }
+                } else {
+                    uint4 *dst = reinterpret_cast<uint4 *>(out + off);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        dst[q] = make_uint4(tc::pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), tc::pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
+                                            tc::pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), tc::pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+                    }
                 }
             } else {
 #pragma unroll
@@ -462,7 +497,8 @@ struct WgradProb {
     template <int BN>
     __device__ void flush_bias(int, int, int, float *) const {}
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *, const Pre &) const {
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *, const Pre &,
+                             uint8_t * = nullptr) const {
         const int m = mt * BM + row;
         const int ld = taps.n * (c1 + c2);
 #pragma unroll 1
@@ -514,7 +550,8 @@ struct SplitK {
     template <int BN>
     __device__ void flush_bias(int, int, int, float *) const {}
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *, const Pre &) const {
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *, const Pre &,
+                             uint8_t * = nullptr) const {
         int n0, h0, w0, n, h, w;
         p.pt.origin(mt, n0, h0, w0);
         p.pt.pixel(row, n0, h0, w0, n, h, w);
@@ -794,12 +831,13 @@ constexpr int HALO_ROWS = 3 * 130;
 constexpr int HALO_TX = HALO_ROWS * 128;        // bytes a halo load delivers
 constexpr int HALO_BYTES = (HALO_TX + 1023) / 1024 * 1024;
 
-constexpr int TAPS_PER_SLOT = 3;  // one kernel row per weight stage: 12 MMAs per barrier wait
+constexpr int TAPS_PER_SLOT = 3;
+constexpr int STAGE_BYTES = 32 * 64;  // one warp's 32 px x 32 ch bf16 output box  // one kernel row per weight stage: 12 MMAs per barrier wait
 
 template <int BN, int BSTAGES, bool RES>
 constexpr int halo_smem_bytes() {
-    return 1024 + 2 * HALO_BYTES + (RES ? 9 : BSTAGES * TAPS_PER_SLOT) * BN * BK * 2 + (2 * 2 + 2 * BSTAGES + 6) * 8 +
-           16;
+    return 1024 + 2 * HALO_BYTES + (RES ? 9 : BSTAGES * TAPS_PER_SLOT) * BN * BK * 2 +
+           ((BN == 64 && RES) ? EPI_WARPS * 2 * STAGE_BYTES : 0) + (2 * 2 + 2 * BSTAGES + 6) * 8 + 16;
 }
 
 // RES (resident weights): single-chunk problems (64 input channels) keep all 9 weight taps
@@ -812,9 +850,13 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
     constexpr int B_TAP = BN * BK * 2;
     constexpr int B_BYTES = RES ? 9 * B_TAP : TAPS_PER_SLOT * B_TAP;
     constexpr int NBS = RES ? 1 : BSTAGES;
+    // BN = 64 resident-weight tiles stage each warp's 32 x 32 output box in shared memory and
+    // write it with a TMA store (per-lane 64-B row stores were the epilogue's bottleneck)
+    constexpr bool STAGE = BN == 64 && RES;
     uint8_t *sa = base;                    // [2][HALO_BYTES]
     uint8_t *sb = base + 2 * HALO_BYTES;   // [NBS][B_BYTES]
-    uint64_t *afull = reinterpret_cast<uint64_t *>(sb + NBS * B_BYTES);
+    uint8_t *sst = sb + NBS * B_BYTES;     // [EPI_WARPS][2][STAGE_BYTES] when STAGE
+    uint64_t *afull = reinterpret_cast<uint64_t *>(sst + (STAGE ? EPI_WARPS * 2 * STAGE_BYTES : 0));
     uint64_t *aempty = afull + 2;
     uint64_t *bfull = aempty + 2;
     uint64_t *bempty = bfull + BSTAGES;
@@ -1010,13 +1052,14 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
             tc::tc_fence_after();
 #ifndef ICE_EXP_NOEPI
             p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z, cc0,
-                                    cc1, bacc, cur);
+                                    cc1, bacc, cur, STAGE ? sst + ((warp - 2) * 2 + acc) * STAGE_BYTES : nullptr);
 #endif
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
         if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
+        if (STAGE && lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -1263,6 +1306,17 @@ bool map_act_nb(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, con
 }
 
 // NHWC activation with the row-halo box (64 channels x 130 pixels x 3 rows x 1 image)
+bool map_out32(CUtensorMap *m, const void *ptr, int N, int H, int W, int C) {
+    // NHWC bf16 output, box 32 channels x 32 pixels of one row, SWIZZLE_64B (staged TMA stores)
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {32, 32, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(ptr), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool map_halo(CUtensorMap *m, const void *ptr, int N, int H, int W, int C) {
     cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
     cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
@@ -1593,6 +1647,10 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
         if (!map_halo(&p.xa, x1, n, h, w, c1)) return ICE_EINVAL;
         if (c2 && !map_halo(&p.xb, x2, n, h, w, c2)) return ICE_EINVAL;
         if (!map_wgt(&p.wm, wgt, cout, 9, c1 + c2, bn)) return ICE_EINVAL;
+        if (nch == 1 && cout == 64 && !getenv("ICE_NO_STAGE")) {  // resident-weight path: staged TMA stores
+            if (!map_out32(&p.ym, y, n, h, w, cout)) return ICE_EINVAL;
+            p.y_tma = 1;
+        }
         return run_halo(p, nch, cout, dim3((unsigned)(p.pt.tw * p.pt.th * p.pt.tn)), st);
     }
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
@@ -1648,6 +1706,10 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
     if (use_halo(ksize, w)) {  // the epilogue picks dx1/dx2 (and the plane layout) per 32-column chunk
         if (!map_halo(&p.dym, dy, n, h, w, cout)) return ICE_EINVAL;
         if (!map_wgt(&p.wm, wgt, cout, 9, ct, 64)) return ICE_EINVAL;
+        if (cout == 64 && ct == 64 && c2 == 0 && dx1 && !getenv("ICE_NO_STAGE")) {  // resident weights
+            if (!map_out32(&p.o1m, dx1, n, h, w, c1)) return ICE_EINVAL;
+            p.o1_tma = 1;
+        }
         return run_halo(p, cout / 64, ct, dim3((unsigned)(p.pt.tw * p.pt.th * p.pt.tn)), st);
     }
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
