@@ -32,7 +32,11 @@ using bf16 = __nv_bfloat16;
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = one 128-byte swizzle row
 constexpr int A_BYTES = BM * BK * 2;
-constexpr int EPI_WARPS = 8;  // two warps per TMEM lane quarter, each draining half the columns
+constexpr int EPI_WARPS = 8;
+// single-buffered: with the staged ReLU reference (double-buffered, 32 KB) a second output
+// buffer would overflow the 227 KB of shared memory; a box's store reads smem in well under
+// the time the warp spends on the next tile's TMEM load and math
+constexpr int STAGE_BUFS = 1;  // two warps per TMEM lane quarter, each draining half the columns
 constexpr int NTHREADS = 64 + 32 * EPI_WARPS;
 
 struct PixTile {  // a box of Wt x Ht x Nt pixels, and how many boxes tile (W, H, N)
@@ -92,6 +96,9 @@ __device__ __forceinline__ float warp_col_sum32(float (&v)[32], int lane) {
 // ------------------------------------------------------------------------------------
 struct FpropProb {
     static constexpr bool A_MN = false, B_MN = false;
+    static constexpr bool STAGE_REF = false;
+    static constexpr int ref_tma = 0;
+    __device__ void load_ref(uint8_t *, uint64_t *, int, int) const {}
     CUtensorMap xa, xb, wm;
     PixTile pt;
     Taps taps[4];  // per blockIdx.z (the 4 sub-pixel classes of the halving conv; else 1)
@@ -166,7 +173,7 @@ struct FpropProb {
     __device__ void flush_bias(int, int, int, float *) const {}
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *,
-                             const Pre &pr, uint8_t *stage = nullptr) const {
+                             const Pre &pr, uint8_t *stage = nullptr, const uint8_t * = nullptr) const {
         int n0, h0, w0, n, h, w;
         pt.origin(mt, n0, h0, w0);
         pt.pixel(row, n0, h0, w0, n, h, w);
@@ -209,7 +216,7 @@ struct FpropProb {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) pk[e] = tc::pack_bf16(v[2 * e], v[2 * e + 1]);
                     const int lane = threadIdx.x & 31;
-                    if (lane == 0) tc::bulk_wait_read<1>();  // this buffer's previous store has read smem
+                    if (lane == 0) tc::bulk_wait_read<STAGE_BUFS - 1>();  // the buffer's last store has read smem
                     __syncwarp();
                     tc::stage_row64(stage, lane, pk);
                     tc::fence_proxy_async_smem();
@@ -255,7 +262,10 @@ struct FpropProb {
 // ------------------------------------------------------------------------------------
 struct DgradProb {
     static constexpr bool A_MN = false, B_MN = true;
+    static constexpr bool STAGE_REF = true;
     CUtensorMap dym, wm;  // dY (box 64 x pixel tile), weights (box 64 cin x 1 x 64 cout)
+    CUtensorMap refm;     // ReLU reference of dx1, box 64 ch x 128 px (halo BN = 64 tiles)
+    int ref_tma;          // the halo producer TMA-stages ref1 tiles into shared memory
     PixTile pt;
     Taps taps;
     int N, H, W, c1, c2, cout;
@@ -289,6 +299,12 @@ struct DgradProb {
     }
     // ---- row-halo path: slab of dY around the tile; tap t reads dY[p - shift_t]
     __device__ int halo_chunks() const { return cout / BK; }
+    // the tile's ReLU-reference rows (64 channels x 128 pixels, SWIZZLE_128B) for the epilogue
+    __device__ void load_ref(uint8_t *dst, uint64_t *bar, int mt, int nt) const {
+        int n0, h0, w0;
+        pt.origin(mt, n0, h0, w0);
+        tc::tma_load_4d(dst, &refm, bar, nt * 64, w0, h0, n0);
+    }
     __device__ void load_halo(int chunk, uint8_t *dst, uint64_t *bar, int mt) const {
         int n0, h0, w0;
         pt.origin(mt, n0, h0, w0);
@@ -329,7 +345,7 @@ struct DgradProb {
     __device__ void pre_load(Pre &, int, int, int, int, int, int) const {}
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *bacc,
-                             const Pre &pr, uint8_t *stage = nullptr) const {
+                             const Pre &pr, uint8_t *stage = nullptr, const uint8_t *ref_smem = nullptr) const {
         int n0, h0, w0, n, h, w;
         pt.origin(mt, n0, h0, w0);
         pt.pixel(row, n0, h0, w0, n, h, w);
@@ -374,7 +390,10 @@ struct DgradProb {
                     const uint4 *rp = reinterpret_cast<const uint4 *>(ref + off);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        uint4 u = rp[q];
+                        // staged tile (64 ch x 128 px, 128-B swizzle: 16-B chunk j of row r at j ^ (r & 7))
+                        uint4 u = (ref_smem && ref == ref1)
+                                      ? *reinterpret_cast<const uint4 *>(ref_smem + row * 128 + (((cc * 4 + q) ^ (row & 7)) << 4))
+                                      : rp[q];
                         const bf16 *b = reinterpret_cast<const bf16 *>(&u);
 #pragma unroll
                         for (int e = 0; e < 8; ++e)
@@ -396,7 +415,7 @@ struct DgradProb {
                     uint32_t pk[16];
 #pragma unroll
                     for (int e = 0; e < 16; ++e) pk[e] = tc::pack_bf16(v[2 * e], v[2 * e + 1]);
-                    if (lane == 0) tc::bulk_wait_read<1>();  // this buffer's previous store has read smem
+                    if (lane == 0) tc::bulk_wait_read<STAGE_BUFS - 1>();  // the buffer's last store has read smem
                     __syncwarp();
                     tc::stage_row64(stage, lane, pk);
                     tc::fence_proxy_async_smem();
@@ -498,7 +517,7 @@ struct WgradProb {
     __device__ void flush_bias(int, int, int, float *) const {}
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *, const Pre &,
-                             uint8_t * = nullptr) const {
+                             uint8_t * = nullptr, const uint8_t * = nullptr) const {
         const int m = mt * BM + row;
         const int ld = taps.n * (c1 + c2);
 #pragma unroll 1
@@ -551,7 +570,7 @@ struct SplitK {
     __device__ void flush_bias(int, int, int, float *) const {}
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *, const Pre &,
-                             uint8_t * = nullptr) const {
+                             uint8_t * = nullptr, const uint8_t * = nullptr) const {
         int n0, h0, w0, n, h, w;
         p.pt.origin(mt, n0, h0, w0);
         p.pt.pixel(row, n0, h0, w0, n, h, w);
@@ -832,12 +851,14 @@ constexpr int HALO_TX = HALO_ROWS * 128;        // bytes a halo load delivers
 constexpr int HALO_BYTES = (HALO_TX + 1023) / 1024 * 1024;
 
 constexpr int TAPS_PER_SLOT = 3;
-constexpr int STAGE_BYTES = 32 * 64;  // one warp's 32 px x 32 ch bf16 output box  // one kernel row per weight stage: 12 MMAs per barrier wait
+constexpr int STAGE_BYTES = 32 * 64;  // one warp's 32 px x 32 ch bf16 output box
+constexpr int REF_BYTES = 128 * 128;  // staged ReLU-reference tile: 128 px x 64 ch bf16  // one kernel row per weight stage: 12 MMAs per barrier wait
 
 template <int BN, int BSTAGES, bool RES>
-constexpr int halo_smem_bytes() {
+constexpr int halo_smem_bytes(bool refs = false) {
     return 1024 + 2 * HALO_BYTES + (RES ? 9 : BSTAGES * TAPS_PER_SLOT) * BN * BK * 2 +
-           ((BN == 64 && RES) ? EPI_WARPS * 2 * STAGE_BYTES : 0) + (2 * 2 + 2 * BSTAGES + 6) * 8 + 16;
+           ((BN == 64 && RES) ? EPI_WARPS * STAGE_BUFS * STAGE_BYTES : 0) + ((BN == 64 && RES && refs) ? 2 * REF_BYTES : 0) +
+           (2 * 2 + 2 * BSTAGES + 6 + 4) * 8 + 16;
 }
 
 // RES (resident weights): single-chunk problems (64 input channels) keep all 9 weight taps
@@ -855,14 +876,20 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
     constexpr bool STAGE = BN == 64 && RES;
     uint8_t *sa = base;                    // [2][HALO_BYTES]
     uint8_t *sb = base + 2 * HALO_BYTES;   // [NBS][B_BYTES]
-    uint8_t *sst = sb + NBS * B_BYTES;     // [EPI_WARPS][2][STAGE_BYTES] when STAGE
-    uint64_t *afull = reinterpret_cast<uint64_t *>(sst + (STAGE ? EPI_WARPS * 2 * STAGE_BYTES : 0));
+    uint8_t *sst = sb + NBS * B_BYTES;     // [EPI_WARPS][STAGE_BUFS][STAGE_BYTES] when STAGE
+    // ... and TMA-stage the tile's ReLU reference (dgrad) for the epilogue
+    constexpr bool REFS = STAGE && P::STAGE_REF;
+    uint8_t *sref = sst + (STAGE ? EPI_WARPS * STAGE_BUFS * STAGE_BYTES : 0);  // [2][REF_BYTES] when REFS
+    uint64_t *afull = reinterpret_cast<uint64_t *>(sref + (REFS ? 2 * REF_BYTES : 0));
     uint64_t *aempty = afull + 2;
     uint64_t *bfull = aempty + 2;
     uint64_t *bempty = bfull + BSTAGES;
     uint64_t *tfull = bempty + BSTAGES;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *rfull = tempty + 2;   // [2]
+    uint64_t *rempty = rfull + 2;   // [2]
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(rempty + 2);
+    const bool stage_ref = REFS && p.ref_tma;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = g.count();
@@ -874,6 +901,8 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
             tc::mbar_init(&aempty[s], 1);
             tc::mbar_init(&tfull[s], 1);
             tc::mbar_init(&tempty[s], EPI_WARPS);
+            tc::mbar_init(&rfull[s], 1);
+            tc::mbar_init(&rempty[s], EPI_WARPS);
         }
         for (int s = 0; s < BSTAGES; ++s) {
             tc::mbar_init(&bfull[s], 1);
@@ -890,10 +919,16 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
 
     if (warp == 0) {
         if (lane == 0) {
-            int ait = 0, bit = 0, cur_nt = -1, run = -1;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            int ait = 0, bit = 0, cur_nt = -1, run = -1, lt = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
                 int mt, nt, z;
                 g.coords(t, mt, nt, z);
+                if (REFS && stage_ref) {  // the epilogue's ReLU reference for this tile
+                    const int rs = lt & 1;
+                    tc::mbar_wait(&rempty[rs], ((lt >> 1) & 1) ^ 1);
+                    tc::mbar_expect_tx(&rfull[rs], REF_BYTES);
+                    p.load_ref(sref + rs * REF_BYTES, &rfull[rs], mt, nt);
+                }
                 if (RES && nt != cur_nt) {  // (re)load the column tile's 9 weight taps
                     if (run >= 0) tc::mbar_wait(&bempty[0], run & 1);
                     ++run;
@@ -1050,13 +1085,19 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
             const int acc = local & 1;
             tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
             tc::tc_fence_after();
+            if (REFS && stage_ref) tc::mbar_wait(&rfull[acc], (local >> 1) & 1);
 #ifndef ICE_EXP_NOEPI
             p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z, cc0,
-                                    cc1, bacc, cur, STAGE ? sst + ((warp - 2) * 2 + acc) * STAGE_BYTES : nullptr);
+                                    cc1, bacc, cur,
+                                    STAGE ? sst + ((warp - 2) * STAGE_BUFS + acc % STAGE_BUFS) * STAGE_BYTES : nullptr,
+                                    (REFS && stage_ref) ? sref + acc * REF_BYTES : nullptr);
 #endif
             tc::tc_fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                tc::mbar_arrive(&tempty[acc]);
+                if (REFS && stage_ref) tc::mbar_arrive(&rempty[acc]);
+            }
         }
         if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
         if (STAGE && lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
@@ -1402,7 +1443,7 @@ const int8_t HALVE_DX[9] = {0, 0, 1, 0, 0, 0, 1, 0, 1};
 
 template <int BN, int BSTAGES, bool RES, class P, bool DUAL = false>
 int launch_halo(const P &p, dim3 tiles, cudaStream_t st) {
-    constexpr int smem = halo_smem_bytes<BN, BSTAGES, RES>();
+    constexpr int smem = halo_smem_bytes<BN, BSTAGES, RES>(P::STAGE_REF);
     static_assert(smem <= 232448, "halo kernel smem");
     static bool attr = false;
     if (!attr) {
@@ -1709,6 +1750,17 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
         if (cout == 64 && ct == 64 && c2 == 0 && dx1 && !getenv("ICE_NO_STAGE")) {  // resident weights
             if (!map_out32(&p.o1m, dx1, n, h, w, c1)) return ICE_EINVAL;
             p.o1_tma = 1;
+            if (relu_ref1 && !getenv("ICE_NO_REF_TMA")) {  // ReLU reference staged by the producer
+                cuuint64_t dims[4] = {(cuuint64_t)c1, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+                cuuint64_t strides[3] = {(cuuint64_t)c1 * 2, (cuuint64_t)w * c1 * 2, (cuuint64_t)h * w * c1 * 2};
+                cuuint32_t box[4] = {64, 128, 1, 1};
+                cuuint32_t es[4] = {1, 1, 1, 1};
+                if (encode_fn()(&p.refm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t *>(relu_ref1), dims,
+                                strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                    return ICE_EINVAL;
+                p.ref_tma = 1;
+            }
         }
         return run_halo(p, cout / 64, ct, dim3((unsigned)(p.pt.tw * p.pt.th * p.pt.tn)), st);
     }
