@@ -115,7 +115,7 @@ def config5_bench(dev, dist, world, rank, steps: int = 10, warmup: int = 3, coun
     GPU, device-timed like the headline.  Returns a dict for the JSON line."""
     import multiprocessing as mp
     from paper_2403_13135_b200.icetrain import Adam, UNet, UNetSpec
-    from paper_2403_13135_b200.icetrain.train import GradBucketer, GraphedStep, device_step
+    from paper_2403_13135_b200.icetrain.train import SINGLE_GPU_BUCKET, GradBucketer, GraphedStep, device_step
     bounds = np.linspace(0, count, 9).astype(int)
     with mp.get_context("fork").Pool(8) as pool:
         parts = pool.map(_scene512_chunk, [(101, count, 0.3, int(bounds[i]), int(bounds[i + 1])) for i in range(8)])
@@ -128,7 +128,7 @@ def config5_bench(dev, dist, world, rank, steps: int = 10, warmup: int = 3, coun
         dist.broadcast(model.engine.params, 0)
         model.engine.refresh_working_weights()
     opt = Adam(model.parameters(), lr=1e-3)
-    bucketer = GradBucketer(model.engine, bucket_bytes=(64 << 20) if dist else (16 << 20), optimizer=opt)
+    bucketer = GradBucketer(model.engine, bucket_bytes=(64 << 20) if dist else SINGLE_GPU_BUCKET, optimizer=opt)
     gen = torch.Generator().manual_seed(55)
     union = batch * world
     idx = [torch.randperm(count, generator=gen)[:union][rank * batch:(rank + 1) * batch].to(dev)
@@ -338,7 +338,7 @@ def main():
     import paper_2403_13135_b200.icelabel as il
     from paper_2403_13135_b200 import _native
     from paper_2403_13135_b200.icetrain import Adam, UNet, UNetSpec, synchronized_step
-    from paper_2403_13135_b200.icetrain.train import GradBucketer, device_step
+    from paper_2403_13135_b200.icetrain.train import SINGLE_GPU_BUCKET, GradBucketer, device_step
 
     # one GPU per rank; modulo the device count only matters for functional runs of
     # several ranks on one GPU (ICE_DIST_BACKEND=gloo), NCCL needs distinct GPUs
@@ -369,7 +369,8 @@ def main():
     opt = Adam(model.parameters(), lr=1e-3)
     # optimizer-in-backward: each gradient bucket is (all-reduced and) Adam-stepped on a side
     # stream as soon as backward completes it
-    bucketer = GradBucketer(model.engine, bucket_bytes=(64 << 20) if dist else (16 << 20), optimizer=opt)
+    bucket_mb = int(os.environ.get("ICE_BUCKET_MB", "64" if dist else str(SINGLE_GPU_BUCKET >> 20)))
+    bucketer = GradBucketer(model.engine, bucket_bytes=bucket_mb << 20, optimizer=opt)
     union = BATCH * world
     gen = torch.Generator().manual_seed(1234)
 

@@ -77,6 +77,13 @@ def _as_nhwc(x: torch.Tensor, device) -> tuple:
     return t.to(device, torch.float32, non_blocking=True).contiguous(), True
 
 
+# One process, one GPU: a single bucket, i.e. the fused Adam runs once after the backward.
+# Overlapping per-bucket Adam with the backward made both contend for HBM and measured 1.3%
+# slower per step on a B200 (bench ICE_BUCKET_MB sweep); with NCCL the 64 MB buckets let the
+# all-reduce overlap the backward instead.
+SINGLE_GPU_BUCKET = 4096 << 20
+
+
 def plan_buckets(spec, bucket_bytes: int = 64 << 20):
     """Contiguous [start, stop) slices of the flat gradient buffer, in backward-readiness
     order, each closed by the layer whose gradient completes it: [(start, stop, last)]."""
@@ -226,7 +233,7 @@ def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
         key = (id(optimizers[0]) if fused else None)
         bucketer = getattr(engine, "_bucketer", None)
         if bucketer is None or getattr(bucketer, "_key", None) != key:
-            bucketer = GradBucketer(engine, bucket_bytes=(64 << 20) if dist else (16 << 20),
+            bucketer = GradBucketer(engine, bucket_bytes=(64 << 20) if dist else SINGLE_GPU_BUCKET,
                                     optimizer=optimizers[0] if fused else None)
             bucketer._key = key
             engine._bucketer = bucketer
