@@ -25,7 +25,8 @@ y = torch.randint(0, 3, (a.batch, 256, 256), dtype=torch.uint8, device=dev)
 torch.manual_seed(0)
 model = UNet(UNetSpec(), dev)
 opt = Adam(model.parameters())
-bucketer = GradBucketer(model.engine, bucket_bytes=16 << 20, optimizer=opt)
+from paper_2403_13135_b200.icetrain.train import SINGLE_GPU_BUCKET  # noqa: E402
+bucketer = GradBucketer(model.engine, bucket_bytes=SINGLE_GPU_BUCKET, optimizer=opt)
 for _ in range(3):
     device_step(model, opt, x, y, a.batch, bucketer)
 torch.cuda.synchronize()
