@@ -189,9 +189,16 @@ struct FpropProb {
             tc::tmem_ld32(tmem + cc * 32, v);
             const int col0 = nt * BN + cc * 32;
             const int ci = cc - cc0;
-            if (ci < 2) {  // warp-uniform: prefetched operands, broadcast by shuffles
+            if (ci < 2) {  // warp-uniform: prefetched operands, broadcast through shared memory
                 const float bsrc = ci == 0 ? pr.b[0] : pr.b[1];
                 const float dsrc = ci == 0 ? pr.d[0] : pr.d[1];
+                __shared__ __align__(16) float sbd[EPI_WARPS][64];  // per epilogue warp: bias | drop
+                float *mine = sbd[((threadIdx.x >> 5) - 2) & (EPI_WARPS - 1)];
+                const int ln = threadIdx.x & 31;
+                __syncwarp();
+                mine[ln] = bsrc;
+                mine[32 + ln] = dsrc;
+                __syncwarp();
                 float dl[32];
                 if (drop && !pr.uni && valid) {  // rows of several images (tiny levels)
                     const float *dr = drop + (size_t)n * cout + col0;
@@ -204,12 +211,17 @@ struct FpropProb {
                     }
                 }
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float bj = __shfl_sync(0xffffffffu, bsrc, j);
-                    const float dj = __shfl_sync(0xffffffffu, dsrc, j);
-                    float a = v[j] + bj;
-                    if (relu) a = fmaxf(a, 0.f);
-                    v[j] = a * ((drop && !pr.uni) ? dl[j] : dj);
+                for (int j4 = 0; j4 < 8; ++j4) {
+                    const float4 b4 = *reinterpret_cast<const float4 *>(mine + 4 * j4);
+                    const float4 d4 = *reinterpret_cast<const float4 *>(mine + 32 + 4 * j4);
+                    const float bb[4] = {b4.x, b4.y, b4.z, b4.w}, dd[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int j = 4 * j4 + e;
+                        float a = v[j] + bb[e];
+                        if (relu) a = fmaxf(a, 0.f);
+                        v[j] = a * ((drop && !pr.uni) ? dl[j] : dd[e]);
+                    }
                 }
                 if (stage && y_tma) {  // warp-uniform: rows of one image row, all valid (halo tiles)
                     uint32_t pk[16];
