@@ -936,6 +936,41 @@ __device__ __forceinline__ uint32_t col_band(const uint32_t *cnt, uint32_t *acc,
     return any;
 }
 
+// value-mode column pass with the band's 32 median words in registers (one-level loop)
+template <int EDGE>
+__device__ __forceinline__ uint32_t col_band_reg(const uint32_t *cnt, uint32_t (&ra)[32], uint32_t gap, int c, int y0) {
+    constexpr uint32_t M = 0x00ff00ffu;
+    constexpr uint32_t K = (0x8000u - MGE) * 0x00010001u;
+    uint32_t ae = K, ao = K, any = 0;
+#pragma unroll
+    for (int j = -MR; j <= MR; ++j) {
+        const uint32_t w = cnt[(EDGE ? clampi(y0 + j, 0, 255) : y0 + j) * WP + c];
+        ae += w & M;
+        ao += (w >> 8) & M;
+    }
+    const uint32_t *pn = cnt + (y0 + MR + 1) * WP + c;
+    const uint32_t *po = cnt + (y0 - MR) * WP + c;
+#pragma unroll
+    for (int y = 0; y < 32; ++y) {
+        const uint32_t bits = ((ae >> 15) & 0x00010001u) | ((ao >> 7) & 0x01000100u);
+        ra[y] += bits * gap;
+        any |= bits;
+        if (y == 31) break;
+        uint32_t n, o;
+        if (EDGE == 0) {
+            n = pn[y * WP];
+            o = po[y * WP];
+        } else {
+            n = cnt[min(y0 + y + MR + 1, 255) * WP + c];
+            o = cnt[max(y0 + y - MR, 0) * WP + c];
+        }
+        const uint32_t df = (n | 0x80808080u) - o;
+        ae += even16(df) - 0x00800080u;
+        ao += odd16(df) - 0x00800080u;
+    }
+    return any;
+}
+
 template <int MODE>
 __device__ __forceinline__ uint32_t col_pass(const uint32_t *tmp, uint32_t *acc, uint32_t arg, int c, int band) {
     return band == 0 ? col_band<1, MODE>(tmp, acc, arg, c, 0)
@@ -995,6 +1030,9 @@ __device__ void median21(uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s, 
         }
     }
     if (!two_level) {  // one pass per distinct value, acc += value gap, block skipping
+        uint32_t ra[32];  // this thread's 32 median words ("col" map), in registers
+#pragma unroll
+        for (int y = 0; y < 32; ++y) ra[y] = v0;
         uint32_t any = 1;
         for (int i = 0; i + 1 < nd; ++i) {
             const uint32_t t = s.vals[i], gap = (uint32_t)s.vals[i + 1] - t;
@@ -1007,11 +1045,15 @@ __device__ void median21(uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s, 
             __syncthreads();
             any = 0;
             if (s.act[blk]) {
-                any = col_pass<0>(tmp, acc, gap, c, band);
+                any = band == 0 ? col_band_reg<1>(tmp, ra, gap, c, 0)
+                                : (band == 7 ? col_band_reg<2>(tmp, ra, gap, c, 224)
+                                             : col_band_reg<0>(tmp, ra, gap, c, band * 32));
                 const bool wa = __any_sync(0xffffffffu, any != 0);
                 if (lane == 0) s.act[blk] = wa;
             }
         }
+#pragma unroll
+        for (int y = 0; y < 32; ++y) acc[(band * 32 + y) * WP + c] = ra[y];
         __syncthreads();
         if (threadIdx.x < 256) s.flags[threadIdx.x] = 0;
         return;
