@@ -38,6 +38,8 @@ BATCH = 32
 SIZE = 256
 CORPUS = 4224
 AUTOLABEL_TILES = 100_000
+WORKLOAD_CONFIG = {"workload": "paper U-Net (depth 5, base 64, dropout 0.1) train step on 4224 synthetic 256x256 "
+                               "tiles, batch 32/GPU, Adam", "seq_len": None}
 
 
 def peaks():
@@ -246,11 +248,12 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": round(rate, 4), "unit": UNIT, "impl": "reference", "n_gpus": 0,
             "steps": steps, "warmup": 1 if args.warmup else 0, "ms_per_step": round(1000 * dt / steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": "paper U-Net train step, 256^2, synthetic T-gray tiles",
-                                            "global_batch": batch, "seq_len": None, "parallelism": "cpu"},
+            "data": "synthetic (T-gray tiles, SURVEY.md 8(d))", "config": dict(WORKLOAD_CONFIG, global_batch=BATCH,
+                                                                          parallelism=f"cpu{threads}"),
             "cpu_baseline": {"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{steps} synchronized_step(s) at batch {batch} (of the batch-32 "
-                                       f"workload) on {threads} host threads, torch CPU fp32"},
+                             "sample": f"{steps} reference-equivalent synchronized_step(s) (oracle/unet_ref.py) at "
+                                       f"batch {batch} of the batch-{BATCH} workload, {threads} host threads, "
+                                       f"torch CPU fp32"},
             "e2e": {"value": round(rate, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -544,9 +547,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": f"synthetic (T-gray tiles generate_corpus(101, {args.corpus}, 0.3), labels by K1 on GPU)",
-                "config": {"workload": "paper U-Net (depth 5, base 64, dropout 0.1) train step on 4224 "
-                                       "synthetic 256x256 tiles, batch 32/GPU, Adam",
-                           "global_batch": union, "seq_len": None, "parallelism": f"dp{world}",
+                "config": {**WORKLOAD_CONFIG,
+                           "global_batch": union, "parallelism": f"dp{world}",
                            "l2": "per-step working set (activations, 124M params) >> 126 MB L2; no flush",
                            "launch": launch_mode},
                 "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
