@@ -869,7 +869,8 @@ constexpr int REF_BYTES = 128 * 128;  // staged ReLU-reference tile: 128 px x 64
 template <int BN, int BSTAGES, bool RES>
 constexpr int halo_smem_bytes(bool refs = false) {
     return 1024 + 2 * HALO_BYTES + (RES ? 9 : BSTAGES * TAPS_PER_SLOT) * BN * BK * 2 +
-           ((BN == 64 && RES) ? EPI_WARPS * STAGE_BUFS * STAGE_BYTES : 0) + ((BN == 64 && RES && refs) ? 2 * REF_BYTES : 0) +
+           (((BN == 64 && RES) || BN == 128) ? EPI_WARPS * STAGE_BUFS * STAGE_BYTES : 0) +
+           ((BN == 64 && RES && refs) ? 2 * REF_BYTES : 0) +
            (2 * 2 + 2 * BSTAGES + 6 + 4) * 8 + 16;
 }
 
@@ -885,12 +886,12 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
     constexpr int NBS = RES ? 1 : BSTAGES;
     // BN = 64 resident-weight tiles stage each warp's 32 x 32 output box in shared memory and
     // write it with a TMA store (per-lane 64-B row stores were the epilogue's bottleneck)
-    constexpr bool STAGE = BN == 64 && RES;
+    constexpr bool STAGE = (BN == 64 && RES) || BN == 128;
     uint8_t *sa = base;                    // [2][HALO_BYTES]
     uint8_t *sb = base + 2 * HALO_BYTES;   // [NBS][B_BYTES]
     uint8_t *sst = sb + NBS * B_BYTES;     // [EPI_WARPS][STAGE_BUFS][STAGE_BYTES] when STAGE
     // ... and TMA-stage the tile's ReLU reference (dgrad) for the epilogue
-    constexpr bool REFS = STAGE && P::STAGE_REF;
+    constexpr bool REFS = BN == 64 && RES && P::STAGE_REF;
     uint8_t *sref = sst + (STAGE ? EPI_WARPS * STAGE_BUFS * STAGE_BYTES : 0);  // [2][REF_BYTES] when REFS
     uint64_t *afull = reinterpret_cast<uint64_t *>(sref + (REFS ? 2 * REF_BYTES : 0));
     uint64_t *aempty = afull + 2;
@@ -1700,7 +1701,7 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
         if (!map_halo(&p.xa, x1, n, h, w, c1)) return ICE_EINVAL;
         if (c2 && !map_halo(&p.xb, x2, n, h, w, c2)) return ICE_EINVAL;
         if (!map_wgt(&p.wm, wgt, cout, 9, c1 + c2, bn)) return ICE_EINVAL;
-        if (nch == 1 && cout == 64 && !getenv("ICE_NO_STAGE")) {  // resident-weight path: staged TMA stores
+        if (((nch == 1 && cout == 64) || bn == 128) && !getenv("ICE_NO_STAGE")) {  // staged TMA stores
             if (!map_out32(&p.ym, y, n, h, w, cout)) return ICE_EINVAL;
             p.y_tma = 1;
         }
@@ -1759,9 +1760,12 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
     if (use_halo(ksize, w)) {  // the epilogue picks dx1/dx2 (and the plane layout) per 32-column chunk
         if (!map_halo(&p.dym, dy, n, h, w, cout)) return ICE_EINVAL;
         if (!map_wgt(&p.wm, wgt, cout, 9, ct, 64)) return ICE_EINVAL;
-        if (cout == 64 && ct == 64 && c2 == 0 && dx1 && !getenv("ICE_NO_STAGE")) {  // resident weights
+        const bool res64 = cout == 64 && ct == 64 && c2 == 0;  // resident-weight BN = 64 tiles
+        if ((res64 || halo_bn(cout / 64, ct) == 128) && dx1 && !getenv("ICE_NO_STAGE")) {  // staged TMA stores
             if (!map_out32(&p.o1m, dx1, n, h, w, c1)) return ICE_EINVAL;
             p.o1_tma = 1;
+        }
+        if (res64 && dx1 && !getenv("ICE_NO_STAGE")) {
             if (relu_ref1 && !getenv("ICE_NO_REF_TMA")) {  // ReLU reference staged by the producer
                 cuuint64_t dims[4] = {(cuuint64_t)c1, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
                 cuuint64_t strides[3] = {(cuuint64_t)c1 * 2, (cuuint64_t)w * c1 * 2, (cuuint64_t)h * w * c1 * 2};
