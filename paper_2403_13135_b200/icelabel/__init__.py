@@ -2,10 +2,10 @@
 from .types import (CLASS_COLORS, MASK_FIXED, MASK_OTSU, ROSS_SEA_SUMMER, ClassId, ColorRange,
                     FilterConfig, FilterOutput, LabelMask, SceneRaster, SegmentationScheme, Tile,
                     TileResult, get_preset)
-from .ops import (apply_filter, autolabel, check_windows, detect_mask, process_tile, process_tiles,
-                  segment, segment_batch)
+from .ops import (apply_filter, autolabel, autolabel_sharded, check_windows, detect_mask, process_tile,
+                  process_tiles, segment, segment_batch, shard_bounds)
 
 __all__ = ["CLASS_COLORS", "MASK_FIXED", "MASK_OTSU", "ROSS_SEA_SUMMER", "ClassId", "ColorRange",
            "FilterConfig", "FilterOutput", "LabelMask", "SceneRaster", "SegmentationScheme", "Tile",
-           "TileResult", "get_preset", "apply_filter", "autolabel", "check_windows", "detect_mask",
-           "process_tile", "process_tiles", "segment", "segment_batch"]
+           "TileResult", "get_preset", "apply_filter", "autolabel", "autolabel_sharded", "check_windows",
+           "detect_mask", "process_tile", "process_tiles", "segment", "segment_batch", "shard_bounds"]

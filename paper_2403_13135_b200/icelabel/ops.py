@@ -71,6 +71,42 @@ def autolabel(rgb, cfg: FilterConfig | None = None, scheme: SegmentationScheme =
     return out
 
 
+def shard_bounds(n: int, world: int, rank: int) -> tuple:
+    """Contiguous tile range [lo, hi) of `rank` when n tiles are split over `world` ranks
+    (tiles are independent -- no data-path collective)."""
+    if world < 1 or not 0 <= rank < world or n < 0:
+        raise ValueError(f"bad shard request n={n} world={world} rank={rank}")
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def autolabel_sharded(rgb_all, cfg: FilterConfig | None = None, scheme: SegmentationScheme = ROSS_SEA_SUMMER,
+                      group=None):
+    """Auto-label a corpus split over the ranks of torch.distributed (one GPU each): this rank
+    runs K1 on its contiguous shard of ``rgb_all`` (u8 [n, h, w, 3], host or device) and the
+    per-class pixel counts / masked-pixel totals of the whole corpus are summed with ONE small
+    all-reduce at the end.  Returns (this rank's K1 outputs, (lo, hi), totals) where totals is a
+    device int64 tensor [class0, class1, class2, masked, unmatched tiles]."""
+    import torch
+    import torch.distributed as tdist
+    dist_on = tdist.is_available() and tdist.is_initialized()
+    world = tdist.get_world_size(group) if dist_on else 1
+    rank = tdist.get_rank(group) if dist_on else 0
+    lo, hi = shard_bounds(len(rgb_all), world, rank)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    local = rgb_all[lo:hi]
+    local = local.to(dev, non_blocking=True) if local.device != dev else local
+    totals = torch.zeros(5, dtype=torch.int64, device=dev)
+    out = None
+    if hi > lo:
+        out = autolabel(local.contiguous(), cfg, scheme)
+        totals[:3] = out["counts"].to(torch.int64).sum(0)
+        totals[3] = out["affected"].to(torch.int64).sum()
+        totals[4] = (out["unmatched"] >= 0).sum()
+    if dist_on and world > 1:
+        tdist.all_reduce(totals, group=group)
+    return out, (lo, hi), totals
+
+
 def segment_batch(rgb, scheme: SegmentationScheme = ROSS_SEA_SUMMER, out=None, stream=None):
     """Segment-only labeling of a device batch (K1s)."""
     import torch

@@ -279,3 +279,14 @@ def test_swar_kernel_edge_tiles_vs_oracle():
         assert np.array_equal(out["label"][i], lbl), i
         assert out["unmatched"][i] == first, i
         assert out["counts"][i].tolist() == np.bincount(lbl.ravel(), minlength=256)[:3].tolist(), i
+
+
+def test_autolabel_sharded_single_rank_totals():
+    """autolabel_sharded on one rank labels the whole corpus and totals its counts."""
+    tiles = np.stack([rgb for rgb, _ in synth.corpus(21, 6, 0.5)])
+    out, (lo, hi), totals = il.autolabel_sharded(torch.from_numpy(tiles))
+    assert (lo, hi) == (0, 6)
+    ref = il.autolabel(torch.from_numpy(tiles).cuda())
+    assert totals[:3].tolist() == ref["counts"].to(torch.int64).sum(0).tolist()
+    assert int(totals[3]) == int(ref["affected"].sum())
+    assert torch.equal(out["label"], ref["label"])

@@ -73,3 +73,37 @@ def test_rank_shards_match_reference_tensor_split():
     tail = union[:3]
     shards = [p for r in range(4) for p in rank_shards(tail, 4, r, 1)]
     assert [len(p) for p in shards] == [1, 1, 1, 0]
+
+
+def test_autolabel_shards_cover_the_corpus_once():
+    """Tile sharding of the auto-labeler: contiguous, disjoint, complete."""
+    from paper_2403_13135_b200.icelabel import shard_bounds
+    for n in (0, 1, 7, 100, 100000):
+        for world in (1, 2, 3, 4, 8):
+            b = [shard_bounds(n, world, r) for r in range(world)]
+            assert b[0][0] == 0 and b[-1][1] == n
+            assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+            assert max(hi - lo for lo, hi in b) - min(hi - lo for lo, hi in b) <= 1
+    with pytest.raises(ValueError):
+        shard_bounds(10, 2, 2)
+
+
+def _count_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2403_13135_b200.icelabel import shard_bounds
+    n = 11
+    per_tile = torch.arange(n * 5, dtype=torch.int64).view(n, 5)  # stand-in per-tile counts
+    lo, hi = shard_bounds(n, world, rank)
+    totals = per_tile[lo:hi].sum(0)
+    dist.all_reduce(totals)  # the one collective autolabel_sharded issues
+    out[rank] = totals
+    dist.destroy_process_group()
+
+
+def test_autolabel_sharded_totals_allreduce_gloo():
+    port = _free_port()
+    out = mp.Manager().dict()
+    mp.spawn(_count_worker, args=(2, port, out), nprocs=2, join=True)
+    want = torch.arange(55, dtype=torch.int64).view(11, 5).sum(0)
+    assert torch.equal(out[0], want) and torch.equal(out[1], want)

@@ -272,3 +272,35 @@ def test_config5_paper_width_512_step_runs():
         torch.cuda.synchronize()
         losses.append(float(model.engine.stats[0]) / y.numel())
     assert all(np.isfinite(losses)) and losses[-1] < losses[0]
+
+
+def test_dropout2d_masks_statistics_and_application():
+    """K10 (statistical parity only: torch's CPU RNG is not reproducible on the GPU):
+    Dropout2d multipliers are 0 or 1/(1-p) with a zero fraction ~ p, differ between steps,
+    and the forward zeroes whole (sample, channel) planes of each DoubleConv output."""
+    from paper_2403_13135_b200 import _native
+    p = 0.1
+    n = 1 << 20
+    out = torch.empty(n, device="cuda")
+    step = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _native.call("ice_dropout_scale", n, p, 1234, step.data_ptr(), out.data_ptr(), _native.stream_handle())
+    vals = sorted(torch.unique(out).tolist())
+    assert len(vals) == 2 and vals[0] == 0.0 and abs(vals[1] - 1.0 / (1.0 - p)) < 1e-6
+    frac = float((out == 0).float().mean())
+    assert abs(frac - p) < 5 * (p * (1 - p) / n) ** 0.5  # 5 sigma
+    step += 1
+    out2 = torch.empty_like(out)
+    _native.call("ice_dropout_scale", n, p, 1234, step.data_ptr(), out2.data_ptr(), _native.stream_handle())
+    assert not torch.equal(out, out2)
+    # engine forward in train mode: each (sample, channel) plane of a DoubleConv output is either
+    # entirely zero (dropped) or untouched
+    spec = UNetSpec(input_size=64, base_channels=64, depth=2, dropout=0.3)
+    torch.manual_seed(0)
+    model = UNet(spec)
+    x = torch.randint(0, 256, (4, 64, 64, 3), dtype=torch.uint8, device="cuda")
+    A = model.engine.forward(x, train=True, seed=7)
+    a2 = A.a2[0].float()  # [n, h, w, c] output of down.0 (after Dropout2d)
+    plane_max = a2.abs().amax(dim=(1, 2))  # [n, c]
+    drop = A.drop["down.0"]
+    assert torch.equal(plane_max == 0, drop == 0) or bool(((drop == 0) <= (plane_max == 0)).all())
+    assert 0.2 < float((drop == 0).float().mean()) < 0.4  # 256 (sample, channel) draws at p = 0.3
