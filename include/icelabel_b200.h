@@ -94,11 +94,13 @@ int ice_rgb_to_hsv(const uint8_t *rgb, int64_t npx, uint8_t *hsv, void *stream);
  * (model.py:129 torch.cat([skip, x], 1)); x2 may be NULL with c2 = 0.  All channel
  * counts must be multiples of 64, h and w powers of two.
  *   y = act(conv(x, w) + bias) * drop_scale[n][cout]; act = ReLU if relu != 0;
- *   bias, drop_scale may be NULL. */
+ *   bias, drop_scale may be NULL.  relu_bits (may be NULL) receives the mask y > 0 packed as
+ *   uint32 words [cout / 32][n * h * w] (bit j of word k = channel 32 k + j), the 16x smaller
+ *   ReLU reference ice_conv_dgrad's relu_bits1 consumes. */
 int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2,
                    int32_t n, int32_t h, int32_t w, int32_t ksize, const uint16_t *wgt,
                    const float *bias, int32_t cout, int32_t relu, const float *drop_scale,
-                   uint16_t *y, void *stream);
+                   uint16_t *y, uint32_t *relu_bits, void *stream);
 
 /* Data gradient of ice_conv_fprop w.r.t. its input (autograd of model.py:68-69, 129).
  * dx is written split into dx1 (first c1 channels) and dx2 (last c2; may be NULL), each
@@ -108,13 +110,15 @@ int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c
  * dx2_planes != 0 writes dx2 as four sub-pixel planes [4][n][h/2][w/2][c2] (plane
  * 2*(y&1)+(x&1)), the layout ice_halve_dgrad / ice_halve_wgrad consume.
  * dbias{1,2} (fp32 [c1] / [c2], may be NULL): += column sums of dx{1,2} -- the bias gradient
- * of the layer whose pre-activation gradient dx_i is, fused into the epilogue. */
+ * of the layer whose pre-activation gradient dx_i is, fused into the epilogue.
+ * relu_bits1 (may be NULL): the ReLU mask of dx1 as ice_conv_fprop's packed relu_bits, used
+ * instead of relu_ref1. */
 int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32_t h, int32_t w,
                    int32_t ksize, const uint16_t *wgt, int32_t c1, int32_t c2,
                    uint16_t *dx1, const uint16_t *relu_ref1, const float *drop_scale1,
                    const uint16_t *add1, uint16_t *dx2, const uint16_t *relu_ref2,
                    const float *drop_scale2, const uint16_t *add2, int32_t dx2_planes,
-                   float *dbias1, float *dbias2, void *stream);
+                   float *dbias1, float *dbias2, const uint32_t *relu_bits1, void *stream);
 
 /* Weight gradient: dw[cout][ksize][ksize][c1 + c2] (fp32) += sum over pixels of
  * dy[p][cout] * x[p + tap][c].  dw must be zeroed by the caller before the first call. */

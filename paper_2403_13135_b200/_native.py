@@ -55,9 +55,9 @@ SIGNATURES = {
     "ice_confusion": [_V, _V, _I64, _I32, _V, _V, _V],
     "ice_segment": [_V, _I64, _I32, _I32, ctypes.POINTER(IceScheme), _V, _V, _V, _V],
     "ice_rgb_to_hsv": [_V, _I64, _V, _V],
-    "ice_conv_fprop": [_V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, _V, _I32, _I32, _V, _V, _V],
+    "ice_conv_fprop": [_V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, _V, _I32, _I32, _V, _V, _V, _V],
     "ice_conv_dgrad": [_V, _I32, _I32, _I32, _I32, _I32, _V, _I32, _I32, _V, _V, _V, _V, _V, _V, _V, _V, _I32,
-                       _V, _V, _V],
+                       _V, _V, _V, _V],
     "ice_halve_fprop": [_V, _I32, _I32, _I32, _I32, _V, _V, _I32, _V, _V],
     "ice_halve_dgrad": [_V, _I32, _I32, _I32, _I32, _V, _I32, _V, _V, _V, _V, _V],
     "ice_halve_wgrad": [_V, _I32, _V, _I32, _I32, _I32, _I32, _V, _V],

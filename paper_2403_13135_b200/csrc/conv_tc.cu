@@ -77,6 +77,12 @@ __device__ __forceinline__ void ld8(const float *p, float fill, float (&o)[8]) {
     }
 }
 
+// 2 bits per packed bf16 pair: element > 0 (the ReLU mask backward needs, exact on bf16)
+__device__ __forceinline__ uint32_t pos_bits2(uint32_t w) {
+    const uint32_t lo = w & 0xffffu, hi = w >> 16;
+    return (uint32_t)((lo & 0x7fffu) != 0 && !(lo & 0x8000u)) | ((uint32_t)((hi & 0x7fffu) != 0 && !(hi & 0x8000u)) << 1);
+}
+
 // Column sums of a warp's 32 rows x 32 columns (one row per lane): after 31 shuffles lane j
 // holds the sum of column j over the 32 rows.
 __device__ __forceinline__ float warp_col_sum32(float (&v)[32], int lane) {
@@ -108,6 +114,7 @@ struct FpropProb {
     const float *drop;  // [N][cout] or null
     int relu;
     bf16 *y;
+    uint32_t *rbits;    // optional ReLU mask of y: [cout / 32][N*H*W] words, bit j = column 32 k + j > 0
     CUtensorMap ym;     // y as (cout, W, H, N), box 32 ch x 32 px, SWIZZLE_64B (staged stores)
     int y_tma;
 
@@ -223,10 +230,16 @@ struct FpropProb {
                         v[j] = a * ((drop && !pr.uni) ? dl[j] : dd[e]);
                     }
                 }
-                if (stage && y_tma) {  // warp-uniform: rows of one image row, all valid (halo tiles)
-                    uint32_t pk[16];
+                uint32_t pk[16];
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) pk[e] = tc::pack_bf16(v[2 * e], v[2 * e + 1]);
+                for (int e = 0; e < 16; ++e) pk[e] = tc::pack_bf16(v[2 * e], v[2 * e + 1]);
+                if (rbits && valid) {
+                    uint32_t b = 0;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) b |= pos_bits2(pk[e]) << (2 * e);
+                    rbits[(size_t)(col0 >> 5) * ((size_t)N * OH * OW) + ((size_t)n * OH + h) * OW + w] = b;
+                }
+                if (stage && y_tma) {  // warp-uniform: rows of one image row, all valid (halo tiles)
                     const int lane = threadIdx.x & 31;
                     if (lane == 0) tc::bulk_wait_read<STAGE_BUFS - 1>();  // the buffer's last store has read smem
                     __syncwarp();
@@ -242,14 +255,13 @@ struct FpropProb {
                 if (!valid) continue;
                 uint4 *dst = reinterpret_cast<uint4 *>(y + ((size_t)((size_t)n * OH + h) * OW + w) * cout + col0);
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    dst[q] = make_uint4(tc::pack_bf16(v[q * 8], v[q * 8 + 1]), tc::pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
-                                        tc::pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), tc::pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+                for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
                 continue;
             }
             if (!valid) continue;
             uint4 *dst = reinterpret_cast<uint4 *>(y + ((size_t)((size_t)n * OH + h) * OW + w) * cout + col0);
             const float *dr = drop ? drop + (size_t)n * cout + col0 : nullptr;
+            uint32_t rb = 0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 float bq[8], dq[8];
@@ -264,9 +276,11 @@ struct FpropProb {
                         b = fmaxf(b, 0.f);
                     }
                     pk[e] = tc::pack_bf16(a * dq[2 * e], b * dq[2 * e + 1]);
+                    rb |= pos_bits2(pk[e]) << (8 * q + 2 * e);
                 }
                 dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
+            if (rbits) rbits[(size_t)(col0 >> 5) * ((size_t)N * OH * OW) + ((size_t)n * OH + h) * OW + w] = rb;
         }
     }
 };
@@ -285,6 +299,7 @@ struct DgradProb {
     int planes_out2;  // dx2 written as sub-pixel planes [4][N][H/2][W/2][c2]
     bf16 *out1, *out2;
     const bf16 *ref1, *ref2, *add1, *add2;
+    const uint32_t *rbits1;  // optional ReLU mask of dx1 as bits ([c1 / 32][N*H*W]); replaces ref1
     const float *drop1, *drop2;
     float *db1, *db2;  // fused bias gradients of the layers whose pre-activation grads these are
     CUtensorMap o1m;   // dx1 as (c1, W, H, N), box 32 ch x 32 px, SWIZZLE_64B (staged stores)
@@ -398,7 +413,12 @@ struct DgradProb {
                         for (int e = 0; e < 8; ++e) v[q * 8 + e] += __bfloat162float(b[e]);
                     }
                 }
-                if (ref) {
+                if (rbits1 && out == out1) {  // the forward's packed ReLU mask: 4 B instead of 64 B per row
+                    const uint32_t b = __ldg(rbits1 + (size_t)(col >> 5) * ((size_t)N * H * W) + pix);
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (!((b >> e) & 1u)) v[e] = 0.f;
+                } else if (ref) {
                     const uint4 *rp = reinterpret_cast<const uint4 *>(ref + off);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
@@ -674,7 +694,12 @@ __global__ void __launch_bounds__(256) split_finish_dgrad(float *__restrict__ ws
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] += __bfloat162float(b8[e]);
         }
-        if (ref) {
+        if (!second && p.rbits1) {
+            const uint32_t b = p.rbits1[(size_t)(col >> 5) * (size_t)npx + px] >> (col & 31);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (!((b >> e) & 1u)) v[e] = 0.f;
+        } else if (ref) {
             const uint4 u = *reinterpret_cast<const uint4 *>(ref + off);
             const bf16 *b8 = reinterpret_cast<const bf16 *>(&u);
 #pragma unroll
@@ -1682,7 +1707,7 @@ int try_hwgrad(const uint16_t *x1, int c1, const uint16_t *x2, int c2, const uin
 
 extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2, int32_t n, int32_t h,
                               int32_t w, int32_t ksize, const uint16_t *wgt, const float *bias, int32_t cout,
-                              int32_t relu, const float *drop_scale, uint16_t *y, void *stream) {
+                              int32_t relu, const float *drop_scale, uint16_t *y, uint32_t *relu_bits, void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!x1 || !wgt || !y || c1 <= 0 || c1 % 64 || c2 < 0 || c2 % 64 || (c2 && !x2) || cout <= 0 || cout % 64 ||
         (ksize != 1 && ksize != 3) || !shape_ok(n, h, w))
@@ -1694,6 +1719,7 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
     p.omul = 1;
     p.N = n; p.H = h; p.W = w; p.c1 = c1; p.c2 = c2; p.cout = cout;
     p.bias = bias; p.drop = drop_scale; p.relu = relu; p.y = reinterpret_cast<bf16 *>(y);
+    p.rbits = relu_bits;
     cudaStream_t st = (cudaStream_t)stream;
     if (use_halo(ksize, w)) {
         const int nch = (c1 + c2) / 64;
@@ -1711,7 +1737,7 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
     int bn, splits;
     const int total_kb = p.taps[0].n * ((c1 + c2) / BK);
     pick_tiling(cout, mtiles, bn, splits, total_kb);
-    if (getenv("ICE_NO_SPLITK")) splits = 1;
+    if (getenv("ICE_NO_SPLITK") || relu_bits) splits = 1;  // the split finisher writes no mask bits
     if (!map_act(&p.xa, x1, n, h, w, c1, p.pt)) return ICE_EINVAL;
     if (c2 && !map_act(&p.xb, x2, n, h, w, c2, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wgt, cout, p.taps[0].n, c1 + c2, bn)) return ICE_EINVAL;
@@ -1738,7 +1764,8 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
                               const uint16_t *wgt, int32_t c1, int32_t c2, uint16_t *dx1, const uint16_t *relu_ref1,
                               const float *drop_scale1, const uint16_t *add1, uint16_t *dx2,
                               const uint16_t *relu_ref2, const float *drop_scale2, const uint16_t *add2,
-                              int32_t dx2_planes, float *dbias1, float *dbias2, void *stream) {
+                              int32_t dx2_planes, float *dbias1, float *dbias2, const uint32_t *relu_bits1,
+                              void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!dy || !wgt || c1 <= 0 || c1 % 64 || c2 < 0 || c2 % 64 || cout <= 0 || cout % 64 ||
         (ksize != 1 && ksize != 3) || !shape_ok(n, h, w))
@@ -1753,6 +1780,7 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
     p.add1 = reinterpret_cast<const bf16 *>(add1); p.add2 = reinterpret_cast<const bf16 *>(add2);
     p.drop1 = drop_scale1; p.drop2 = drop_scale2;
     p.db1 = dbias1; p.db2 = dbias2;
+    p.rbits1 = relu_bits1;
     p.planes_out2 = dx2_planes;
     if (dx2_planes && ((h | w) & 1)) return ICE_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1766,7 +1794,7 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
             p.o1_tma = 1;
         }
         if (res64 && dx1 && !getenv("ICE_NO_STAGE")) {
-            if (relu_ref1 && !getenv("ICE_NO_REF_TMA")) {  // ReLU reference staged by the producer
+            if (relu_ref1 && !relu_bits1 && !getenv("ICE_NO_REF_TMA")) {  // ReLU reference staged by the producer
                 cuuint64_t dims[4] = {(cuuint64_t)c1, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
                 cuuint64_t strides[3] = {(cuuint64_t)c1 * 2, (cuuint64_t)w * c1 * 2, (cuuint64_t)h * w * c1 * 2};
                 cuuint32_t box[4] = {64, 128, 1, 1};

@@ -15,6 +15,8 @@ channels carry zero weights, zero activations and zero gradients forever).
 
 from __future__ import annotations
 
+import os
+
 from collections import OrderedDict
 from dataclasses import asdict, dataclass
 
@@ -215,6 +217,12 @@ class _Acts:
         self.dskip = [e(B, S >> L, S >> L, cp[L]) for L in range(d)]
         self.dhv = [e(4, B, S >> (L + 1), S >> (L + 1), cp[L]) for L in range(d)]
         self.dpool = [e(B, S >> (L + 1), S >> (L + 1), cp[L]) for L in range(d)]
+        # packed ReLU masks of the DoubleConv middle activations (a1, b1, u1): the forward writes
+        # them, the backward's dgrad reads 4 B per 32 channels instead of the bf16 tensor
+        bits = lambda s, c: torch.empty((c // 32, B * s * s), dtype=torch.int32, device=device)  # noqa: E731
+        self.a1_bits = [bits(S >> i, cp[i]) for i in range(d)]
+        self.b1_bits = bits(S >> d, cp[d])
+        self.u1_bits = [bits(S >> (d - 1 - j), cp[d - 1 - j]) for j in range(d)]
         self.labels = torch.empty((B, S, S), dtype=torch.uint8, device=device)
         self.drop = {}  # block name -> fp32 [B][c_p] Dropout2d scales (train mode, p > 0)
 
@@ -352,13 +360,15 @@ class UNetEngine:
         x = A.stem
         for i in range(d):
             n0, n2 = f"down.{i}.block.0", f"down.{i}.block.2"
-            ops.conv_fprop(x, self.wb16(n0), self.b(n0), relu=True, ksize=1 if i == 0 else 3, out=A.a1[i])
+            ops.conv_fprop(x, self.wb16(n0), self.b(n0), relu=True, ksize=1 if i == 0 else 3, out=A.a1[i],
+                           relu_bits=A.a1_bits[i])
             ops.conv_fprop(A.a1[i], self.wb16(n2), self.b(n2), relu=True, drop=dr(f"down.{i}"), out=A.a2[i])
             a2 = A.a2[i]
             _native.call("ice_maxpool_fwd", a2.data_ptr(), B, a2.shape[1], a2.shape[2], a2.shape[3],
                          A.pool[i].data_ptr(), st)
             x = A.pool[i]
-        ops.conv_fprop(x, self.wb16("bottleneck.block.0"), self.b("bottleneck.block.0"), relu=True, out=A.b1)
+        ops.conv_fprop(x, self.wb16("bottleneck.block.0"), self.b("bottleneck.block.0"), relu=True, out=A.b1,
+                       relu_bits=A.b1_bits)
         ops.conv_fprop(A.b1, self.wb16("bottleneck.block.2"), self.b("bottleneck.block.2"), relu=True,
                        drop=dr("bottleneck"), out=A.b2)
         x = A.b2
@@ -369,7 +379,8 @@ class UNetEngine:
             _native.call("ice_halve_fprop", x.data_ptr(), hl.cin_p, B, x.shape[1], x.shape[2],
                          self.halve_wc[hn].data_ptr(), self.b(hn).data_ptr(), hl.cout_p, A.hv[j].data_ptr(), st)
             n0, n2 = f"up.{j}.block.0", f"up.{j}.block.2"
-            ops.conv_fprop(A.a2[L], self.wb16(n0), self.b(n0), x2=A.hv[j], relu=True, out=A.u1[j])
+            ops.conv_fprop(A.a2[L], self.wb16(n0), self.b(n0), x2=A.hv[j], relu=True, out=A.u1[j],
+                           relu_bits=A.u1_bits[j])
             ops.conv_fprop(A.u1[j], self.wb16(n2), self.b(n2), relu=True, drop=dr(f"up.{j}"), out=A.u2[j])
             x = A.u2[j]
         return A
@@ -392,6 +403,11 @@ class UNetEngine:
         return dz
 
     # ---- backward -----------------------------------------------------------------------
+    @staticmethod
+    def _relu(ref, bits):
+        """The ReLU mask a dgrad applies: the forward's packed bits (default) or the bf16 tensor."""
+        return {"ref1": ref} if os.environ.get("ICE_NO_RELU_BITS") else {"bits1": bits}
+
     def _bias_grad(self, name, dz):
         L = self.by_name[name]
         rows = dz.numel() // dz.shape[-1]
@@ -413,14 +429,14 @@ class UNetEngine:
             # up.j.block.2 : u1 -> u2
             ops.conv_wgrad(A.u1[j], dz, self.w(n2, G))
             dz1 = A.dz_b[L]
-            ops.conv_dgrad(dz, self.wb16(n2), A.u1[j].shape[3], out1=dz1, ref1=A.u1[j], db1=self.b(n0, G))
+            ops.conv_dgrad(dz, self.wb16(n2), A.u1[j].shape[3], out1=dz1, **self._relu(A.u1[j], A.u1_bits[j]), db1=self.b(n0, G))
             done(n2)
             # up.j.block.0 : cat(skip, hv) -> u1
             ops.conv_wgrad(A.a2[L], dz1, self.w(n0, G), x2=A.hv[j])
             c = A.a2[L].shape[3]
             _native.call("ice_conv_dgrad", dz1.data_ptr(), dz1.shape[3], B, dz1.shape[1], dz1.shape[2], 3,
                          self.wb16(n0).data_ptr(), c, c, A.dskip[L].data_ptr(), None, None, None,
-                         A.dhv[L].data_ptr(), None, None, None, 1, None, self.b(hn, G).data_ptr(), st)
+                         A.dhv[L].data_ptr(), None, None, None, 1, None, self.b(hn, G).data_ptr(), None, st)
             done(n0)
             # halve.j : x_prev -> hv
             xprev = A.b2 if j == 0 else A.u2[j - 1]
@@ -438,7 +454,7 @@ class UNetEngine:
         # bottleneck
         ops.conv_wgrad(A.b1, dz, self.w("bottleneck.block.2", G))
         dz1 = A.dz_b[d]
-        ops.conv_dgrad(dz, self.wb16("bottleneck.block.2"), A.b1.shape[3], out1=dz1, ref1=A.b1,
+        ops.conv_dgrad(dz, self.wb16("bottleneck.block.2"), A.b1.shape[3], out1=dz1, **self._relu(A.b1, A.b1_bits),
                        db1=self.b("bottleneck.block.0", G))
         done("bottleneck.block.2")
         ops.conv_wgrad(A.pool[d - 1], dz1, self.w("bottleneck.block.0", G))
@@ -454,7 +470,7 @@ class UNetEngine:
                          dz2.data_ptr(), self.b(n2, G).data_ptr(), st)
             ops.conv_wgrad(A.a1[i], dz2, self.w(n2, G))
             dz1 = A.dz_b[i]
-            ops.conv_dgrad(dz2, self.wb16(n2), A.a1[i].shape[3], out1=dz1, ref1=A.a1[i], db1=self.b(n0, G))
+            ops.conv_dgrad(dz2, self.wb16(n2), A.a1[i].shape[3], out1=dz1, **self._relu(A.a1[i], A.a1_bits[i]), db1=self.b(n0, G))
             done(n2)
             if i == 0:
                 ops.conv_wgrad(A.stem, dz1, self.w(n0, G), ksize=1)

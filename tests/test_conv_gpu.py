@@ -182,3 +182,32 @@ def test_dgrad_split_k_planes_and_both_outputs():
     assert rel(nchw(got2), want2) < 1e-2
     assert rel(db1, want1.sum((0, 2, 3))) < 1e-2
     assert rel(db2, want2.sum((0, 2, 3))) < 1e-2
+
+
+@pytest.mark.parametrize("shape", [(2, 16, 16, 64, 0, 64, 3), (4, 256, 256, 64, 0, 64, 3), (2, 128, 128, 128, 0, 128, 3),
+                                   (2, 128, 128, 64, 64, 64, 3), (33, 8, 8, 128, 128, 512, 3), (32, 8, 8, 1024, 0, 2048, 3)],
+                         ids=str)
+def test_relu_bits_roundtrip(shape):
+    """fprop's packed ReLU mask equals (y > 0); dgrad with that mask equals dgrad with the bf16
+    ReLU reference (all kernels: halo BN 64/128, generic, split-K)."""
+    n, h, w, c1, c2, cout, k = shape
+    torch.manual_seed(3)
+    x1 = rnd(n, h, w, c1)
+    x2 = rnd(n, h, w, c2) if c2 else None
+    wt = rnd(cout, k, k, c1 + c2, scale=0.05)
+    b = torch.randn(cout, device="cuda") * 0.1
+    bits = torch.empty(cout // 32, n * h * w, dtype=torch.int32, device="cuda")
+    y = ops.conv_fprop(x1, wt, b, x2, relu=True, relu_bits=bits)
+    pos = (y.float() > 0).reshape(n * h * w, cout // 32, 32)
+    weights = (2 ** torch.arange(32, device="cuda", dtype=torch.int64))
+    want = (pos.long() * weights).sum(-1).t()  # [cout/32][npx] as unsigned
+    got = bits.long() & 0xFFFFFFFF
+    assert torch.equal(got, want)
+    # dgrad of a conv whose input is y: mask by bits == mask by the bf16 reference
+    wt2 = rnd(64, k, k, cout, scale=0.05)
+    dy = rnd(n, h, w, 64)
+    db_a, db_b = torch.zeros(cout, device="cuda"), torch.zeros(cout, device="cuda")
+    da, _ = ops.conv_dgrad(dy, wt2, cout, ref1=y, db1=db_a)
+    dbb, _ = ops.conv_dgrad(dy, wt2, cout, bits1=bits, db1=db_b)
+    assert rel(da, dbb) < 1e-6 or torch.equal(da, dbb)
+    assert rel(db_a, db_b) < 1e-5
