@@ -1607,6 +1607,15 @@ int launch_split(const P &p, long long mtiles, int ncols, int total_kb, int spli
 // transpose the GEMM (M = (tap, cin), N = cout) so no TMEM lane holds a padding row.
 void wgrad_tiles(int ncols, int cout, int &trans, int &mtiles, int &ntiles, int &bn) {
     trans = cout < BM;
+    // 256-wide tiles only exist along the dimension divisible by 256: for (tap, cin) widths like
+    // 9 x 128 = 1152 with cout % 256 == 0, the transposed GEMM gets N = cout in 256-wide tiles
+    if (!trans && ncols % 256 && cout % 256 == 0 && !getenv("ICE_NO_WGRAD_TRANS256")) {
+        trans = 1;
+        mtiles = (ncols + BM - 1) / BM;
+        bn = 256;
+        ntiles = cout / bn;
+        return;
+    }
     if (!trans) {
         mtiles = (cout + BM - 1) / BM;
         bn = ncols % 256 == 0 ? 256 : (ncols % 128 == 0 ? 128 : 64);
