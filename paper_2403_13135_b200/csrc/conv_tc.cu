@@ -33,6 +33,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = one 128-byte swizzle row
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int EPI_WARPS = 8;
+constexpr int STAGE_BYTES = 32 * 64;  // one warp's 32 px x 32 ch bf16 output box (staged TMA stores)
 // single-buffered: with the staged ReLU reference (double-buffered, 32 KB) a second output
 // buffer would overflow the 227 KB of shared memory; a box's store reads smem in well under
 // the time the warp spends on the next tile's TMEM load and math
@@ -258,16 +259,15 @@ struct FpropProb {
                 for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
                 continue;
             }
-            if (!valid) continue;
-            uint4 *dst = reinterpret_cast<uint4 *>(y + ((size_t)((size_t)n * OH + h) * OW + w) * cout + col0);
-            const float *dr = drop ? drop + (size_t)n * cout + col0 : nullptr;
-            uint32_t rb = 0;
+            const bool staged = stage && y_tma;  // warp-uniform
+            if (!valid && !staged) continue;
+            const float *dr = (drop && valid) ? drop + (size_t)n * cout + col0 : nullptr;
+            uint32_t rb = 0, pk[16];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 float bq[8], dq[8];
                 ld8(bias ? bias + col0 + q * 8 : nullptr, 0.f, bq);
                 ld8(dr ? dr + q * 8 : nullptr, 1.f, dq);
-                uint32_t pk[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     float a = v[q * 8 + 2 * e] + bq[2 * e], b = v[q * 8 + 2 * e + 1] + bq[2 * e + 1];
@@ -275,12 +275,27 @@ struct FpropProb {
                         a = fmaxf(a, 0.f);
                         b = fmaxf(b, 0.f);
                     }
-                    pk[e] = tc::pack_bf16(a * dq[2 * e], b * dq[2 * e + 1]);
-                    rb |= pos_bits2(pk[e]) << (8 * q + 2 * e);
+                    pk[4 * q + e] = tc::pack_bf16(a * dq[2 * e], b * dq[2 * e + 1]);
+                    rb |= pos_bits2(pk[4 * q + e]) << (8 * q + 2 * e);
                 }
-                dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
-            if (rbits) rbits[(size_t)(col0 >> 5) * ((size_t)N * OH * OW) + ((size_t)n * OH + h) * OW + w] = rb;
+            if (rbits && valid) rbits[(size_t)(col0 >> 5) * ((size_t)N * OH * OW) + ((size_t)n * OH + h) * OW + w] = rb;
+            if (staged) {
+                const int lane = threadIdx.x & 31;
+                if (lane == 0) tc::bulk_wait_read<0>();
+                __syncwarp();
+                tc::stage_row64(stage, lane, pk);
+                tc::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tc::tma_store_4d(&ym, stage, col0, w, h, n);  // lane 0's pixel starts the box
+                    tc::bulk_commit();
+                }
+                continue;
+            }
+            uint4 *dst = reinterpret_cast<uint4 *>(y + ((size_t)((size_t)n * OH + h) * OW + w) * cout + col0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         }
     }
 };
@@ -732,7 +747,7 @@ __global__ void __launch_bounds__(256) split_finish_dgrad(float *__restrict__ ws
 
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
-    return 1024 + STAGES * (A_BYTES + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16;
+    return 1024 + STAGES * (A_BYTES + BN * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16;
 }
 
 struct TileGrid {  // persistent schedule: tile t -> (m fastest, then n, then split z)
@@ -758,7 +773,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
     constexpr int B_BYTES = BN * BK * 2;
     uint8_t *sa = base;
     uint8_t *sb = base + STAGES * A_BYTES;
-    uint64_t *full = reinterpret_cast<uint64_t *>(sb + STAGES * B_BYTES);
+    uint8_t *sst = sb + STAGES * B_BYTES;  // [EPI_WARPS][STAGE_BYTES] staged output boxes
+    uint64_t *full = reinterpret_cast<uint64_t *>(sst + EPI_WARPS * STAGE_BYTES);
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;  // [2]
     uint64_t *tempty = tfull + 2;      // [2]
@@ -863,12 +879,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
             tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
             tc::tc_fence_after();
             p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z, cc0,
-                                    cc1, bacc, cur);
+                                    cc1, bacc, cur, sst + (warp - 2) * STAGE_BYTES);
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
         if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
+        if (lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -888,7 +905,6 @@ constexpr int HALO_TX = HALO_ROWS * 128;        // bytes a halo load delivers
 constexpr int HALO_BYTES = (HALO_TX + 1023) / 1024 * 1024;
 
 constexpr int TAPS_PER_SLOT = 3;
-constexpr int STAGE_BYTES = 32 * 64;  // one warp's 32 px x 32 ch bf16 output box
 constexpr int REF_BYTES = 128 * 128;  // staged ReLU-reference tile: 128 px x 64 ch bf16  // one kernel row per weight stage: 12 MMAs per barrier wait
 
 template <int BN, int BSTAGES, bool RES>
@@ -1385,6 +1401,19 @@ bool map_act_nb(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, con
 }
 
 // NHWC activation with the row-halo box (64 channels x 130 pixels x 3 rows x 1 image)
+// output box of one epilogue warp for a generic pixel tile: its 32 rows are bw x bh x bn pixels
+bool map_out_tile(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, const PixTile &pt) {
+    const int bw = pt.Wt < 32 ? pt.Wt : 32, bh = (32 / bw) < pt.Ht ? 32 / bw : pt.Ht, bn = 32 / (bw * bh);
+    if (bw * bh * bn != 32 || bn > pt.Nt) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {32, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bn};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(ptr), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool map_out32(CUtensorMap *m, const void *ptr, int N, int H, int W, int C) {
     // NHWC bf16 output, box 32 channels x 32 pixels of one row, SWIZZLE_64B (staged TMA stores)
     cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
@@ -1747,6 +1776,7 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
     const int total_kb = p.taps[0].n * ((c1 + c2) / BK);
     pick_tiling(cout, mtiles, bn, splits, total_kb);
     if (getenv("ICE_NO_SPLITK") || relu_bits) splits = 1;  // the split finisher writes no mask bits
+    if (!getenv("ICE_NO_STAGE") && map_out_tile(&p.ym, y, n, h, w, cout, p.pt)) p.y_tma = 1;  // staged stores
     if (!map_act(&p.xa, x1, n, h, w, c1, p.pt)) return ICE_EINVAL;
     if (c2 && !map_act(&p.xb, x2, n, h, w, c2, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wgt, cout, p.taps[0].n, c1 + c2, bn)) return ICE_EINVAL;
@@ -1829,6 +1859,9 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
     }
     if (!map_act(&p.dym, dy, n, h, w, cout, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wgt, cout, p.taps.n, ct, 64)) return ICE_EINVAL;
+    // staged dx1 stores: the warp's rows must all be valid (no partial image tile)
+    if (dx1 && n % p.pt.Nt == 0 && !getenv("ICE_NO_STAGE") && map_out_tile(&p.o1m, dx1, n, h, w, c1, p.pt))
+        p.o1_tma = 1;
     if (splits > 1) {
         const long long npx = (long long)n * h * w;
         float *ws = split_workspace((size_t)npx * ct * 4, st);
