@@ -1942,6 +1942,19 @@ extern "C" int ice_halve_fprop(const uint16_t *x, int32_t c, int32_t n, int32_t 
     p.bias = bias; p.relu = 0; p.y = reinterpret_cast<bf16 *>(y);
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     const int bn = pick_bn(cout, mtiles * 4);
+    if (p.pt.Wt >= 32 && !getenv("ICE_NO_STAGE")) {
+        // staged stores: a warp's 32 input pixels of one row land on every other output pixel
+        // of row 2h + cy -- a 64-pixel box traversed with element stride 2
+        const int OH = 2 * h, OW = 2 * w;
+        cuuint64_t dims[4] = {(cuuint64_t)cout, (cuuint64_t)OW, (cuuint64_t)OH, (cuuint64_t)n};
+        cuuint64_t strides[3] = {(cuuint64_t)cout * 2, (cuuint64_t)OW * cout * 2, (cuuint64_t)OH * OW * cout * 2};
+        cuuint32_t box[4] = {32, 64, 1, 1};
+        cuuint32_t es[4] = {1, 2, 1, 1};
+        if (encode_fn()(&p.ym, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, y, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+            p.y_tma = 1;
+    }
     if (!map_act(&p.xa, x, n, h, w, c, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wc, cout, 9, c, bn)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, cout / bn, 4);
