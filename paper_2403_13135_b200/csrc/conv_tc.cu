@@ -111,6 +111,7 @@ struct FpropProb {
     Taps taps[4];  // per blockIdx.z (the 4 sub-pixel classes of the halving conv; else 1)
     int N, H, W, c1, c2, cout;
     int omul;      // 1: output pixel = input pixel; 2: output (2h + cy, 2w + cx), z = 2 cy + cx
+    int merged;    // halving conv with the 4 sub-pixel classes side by side in N (class = col / cout)
     const float *bias;
     const float *drop;  // [N][cout] or null
     int relu;
@@ -173,7 +174,7 @@ struct FpropProb {
         for (int ci = 0; ci < 2; ++ci) {
             const int col = nt * BN + (cc0 + ci) * 32 + lane;
             const bool have = cc0 + ci < cc1;
-            pr.b[ci] = (have && bias) ? __ldg(bias + col) : 0.f;
+            pr.b[ci] = (have && bias) ? __ldg(bias + (merged ? col % cout : col)) : 0.f;
             pr.d[ci] = (have && drop && pr.uni) ? __ldg(drop + (size_t)n_first * cout + col) : 1.f;
         }
     }
@@ -187,15 +188,22 @@ struct FpropProb {
         pt.pixel(row, n0, h0, w0, n, h, w);
         const bool valid = n < N;
         const int OH = H * omul, OW = W * omul;
-        if (omul == 2) {
-            h = 2 * h + (z >> 1);
-            w = 2 * w + (z & 1);
+        const int hb = h, wb = w;
+        if (omul == 2 && !merged) {
+            h = 2 * hb + (z >> 1);
+            w = 2 * wb + (z & 1);
         }
 #pragma unroll 1
         for (int cc = cc0; cc < cc1; ++cc) {
             float v[32];
             tc::tmem_ld32(tmem + cc * 32, v);
-            const int col0 = nt * BN + cc * 32;
+            int col0 = nt * BN + cc * 32;
+            if (merged) {  // this 32-column chunk belongs to sub-pixel class col0 / cout
+                const int cls = col0 / cout;
+                col0 -= cls * cout;
+                h = 2 * hb + (cls >> 1);
+                w = 2 * wb + (cls & 1);
+            }
             const int ci = cc - cc0;
             if (ci < 2) {  // warp-uniform: prefetched operands, broadcast through shared memory
                 const float bsrc = ci == 0 ? pr.b[0] : pr.b[1];
@@ -1743,6 +1751,48 @@ int try_hwgrad(const uint16_t *x1, int c1, const uint16_t *x2, int c2, const uin
 }
 }  // namespace
 
+// merged halving-conv weights wm[(cls * cout + co)][t][ci] (t = 2 dy + dx) from the 9 combined
+// slabs wc[co][slab][ci] (ice_halve_prep); taps a class does not use are zero
+__global__ void halve_merge_kernel(const uint16_t *__restrict__ wc, int cout, int c, uint16_t *__restrict__ wm,
+                                   unsigned long long tab) {
+    const long long total = 16LL * cout * c;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int ci = (int)(i % c);
+        const long long r = i / c;
+        const int t = (int)(r % 4), row = (int)(r / 4), cls = row / cout, co = row % cout;
+        const int slab = (int)((tab >> (4 * (cls * 4 + t))) & 15);
+        wm[i] = slab == 15 ? (uint16_t)0 : wc[((size_t)co * 9 + slab) * c + ci];
+    }
+}
+
+// per-process workspace for the merged weights (grown on an eager call, never freed: captured
+// CUDA graphs keep pointing at it)
+uint16_t *halve_merged_weights(const uint16_t *wc, int cout, int c, cudaStream_t st) {
+    static uint16_t *buf = nullptr;
+    static size_t cap = 0;
+    const size_t bytes = 16ull * cout * c * 2;
+    if (bytes > cap) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+        uint16_t *fresh = nullptr;
+        const size_t want = bytes < (4u << 20) ? (4u << 20) : bytes;
+        if (cudaMalloc(&fresh, want) != cudaSuccess) return nullptr;
+        buf = fresh;
+        cap = want;
+    }
+    // class -> tap -> slab (15 = unused), from HALVE_CLS / HALVE_DY / HALVE_DX
+    unsigned long long tab = ~0ull;
+    for (int i = 0; i < 9; ++i) {
+        const int cls = HALVE_CLS[i], t = 2 * HALVE_DY[i] + HALVE_DX[i];
+        tab &= ~(15ull << (4 * (cls * 4 + t)));
+        tab |= (unsigned long long)i << (4 * (cls * 4 + t));
+    }
+    const long long total = 16LL * cout * c;
+    const unsigned grid = (unsigned)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
+    halve_merge_kernel<<<grid, 256, 0, st>>>(wc, cout, c, buf, tab);
+    return buf;
+}
+
 extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2, int32_t n, int32_t h,
                               int32_t w, int32_t ksize, const uint16_t *wgt, const float *bias, int32_t cout,
                               int32_t relu, const float *drop_scale, uint16_t *y, uint32_t *relu_bits, void *stream) {
@@ -1941,6 +1991,35 @@ extern "C" int ice_halve_fprop(const uint16_t *x, int32_t c, int32_t n, int32_t 
     p.N = n; p.H = h; p.W = w; p.c1 = c; p.c2 = 0; p.cout = cout;
     p.bias = bias; p.relu = 0; p.y = reinterpret_cast<bf16 *>(y);
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
+    cudaStream_t st0 = (cudaStream_t)stream;
+    // wide levels: the 4 sub-pixel classes side by side in N (4 x cout columns, 4 taps each, the
+    // class's unused taps zero): 16/9 of the MACs, but one 256-wide tile per 128 pixels instead of
+    // four short-K 64-wide ones (halve.4: 2 + 4 + 4 + 8 K-blocks on 64 columns)
+    if ((4 * cout) % 256 == 0 && cout <= 128 && w >= 64 && p.pt.Wt >= 32 && !getenv("ICE_NO_HALVE_MERGE")) {
+        uint16_t *wm = halve_merged_weights(wc, cout, c, st0);
+        if (wm) {
+            p.merged = 1;
+            p.taps[0].n = 4;
+            for (int t = 0; t < 4; ++t) {
+                p.taps[0].dy[t] = (int8_t)(t >> 1);
+                p.taps[0].dx[t] = (int8_t)(t & 1);
+                p.taps[0].wt[t] = (int8_t)t;
+            }
+            const int OH = 2 * h, OW = 2 * w;
+            cuuint64_t dims[4] = {(cuuint64_t)cout, (cuuint64_t)OW, (cuuint64_t)OH, (cuuint64_t)n};
+            cuuint64_t strides[3] = {(cuuint64_t)cout * 2, (cuuint64_t)OW * cout * 2, (cuuint64_t)OH * OW * cout * 2};
+            cuuint32_t box[4] = {32, 64, 1, 1};
+            cuuint32_t es[4] = {1, 2, 1, 1};
+            if (!getenv("ICE_NO_STAGE") &&
+                encode_fn()(&p.ym, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, y, dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+                p.y_tma = 1;
+            if (!map_act(&p.xa, x, n, h, w, c, p.pt)) return ICE_EINVAL;
+            if (!map_wgt(&p.wm, wm, 4 * cout, 4, c, 256)) return ICE_EINVAL;
+            return launch<256, 4>(p, dim3((unsigned)mtiles, 4 * cout / 256, 1), st0);
+        }
+    }
     const int bn = pick_bn(cout, mtiles * 4);
     if (p.pt.Wt >= 32 && !getenv("ICE_NO_STAGE")) {
         // staged stores: a warp's 32 input pixels of one row land on every other output pixel
