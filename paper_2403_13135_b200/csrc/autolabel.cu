@@ -755,6 +755,11 @@ __device__ __forceinline__ uint32_t rep0(uint32_t w) { return __byte_perm(w, 0, 
 __device__ __forceinline__ uint32_t rep3(uint32_t w) { return __byte_perm(w, 0, 0x3333); }
 __device__ __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) { return __vmaxu4(a, b); }
 __device__ __forceinline__ uint32_t vmin(uint32_t a, uint32_t b) { return __vminu4(a, b); }
+// V = max(r, g, b) per byte; gray words (r == g == b, the sea-ice corpus) skip the emulated
+// byte-wise maxima
+__device__ __forceinline__ uint32_t vmax3(uint32_t r, uint32_t g, uint32_t b) {
+    return ((r ^ g) | (g ^ b)) ? __vmaxu4(r, __vmaxu4(g, b)) : r;
+}
 // per byte: 1 if x > t, else 0; c4 = (255 - t) * 0x01010101, c7f = c4 & 0x7f7f7f7f
 // (x + (255 - t) carries out of the byte  <=>  x > t; carry = majority(x7, c7, carry-in7))
 __device__ __forceinline__ uint32_t gt4(uint32_t x, uint32_t c4, uint32_t c7f) {
@@ -1267,7 +1272,7 @@ __device__ int load_plane(const uint8_t *tile, int ch, uint32_t *dst, uint32_t *
         uint32_t *d = dst + (g >> 4) * WP + 4 * (g & 15);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            d[q] = ch == 3 ? vmax(R[q], vmax(G[q], B[q])) : (ch == 0 ? R[q] : (ch == 1 ? G[q] : B[q]));
+            d[q] = ch == 3 ? vmax3(R[q], G[q], B[q]) : (ch == 0 ? R[q] : (ch == 1 ? G[q] : B[q]));
             if (sh) subhist_add4(sh, d[q]);
             uneq |= (R[q] ^ G[q]) | (G[q] ^ B[q]);
         }
@@ -1284,7 +1289,7 @@ __device__ void channel_hist(const uint8_t *tile, int ch, uint32_t *hist) {
         unpack16(a, b, c, R, G, B);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const uint32_t w = ch == 3 ? vmax(R[q], vmax(G[q], B[q])) : (ch == 0 ? R[q] : (ch == 1 ? G[q] : B[q]));
+            const uint32_t w = ch == 3 ? vmax3(R[q], G[q], B[q]) : (ch == 0 ? R[q] : (ch == 1 ? G[q] : B[q]));
 #pragma unroll
             for (int k = 0; k < 4; ++k) hist_add(hist, (w >> (8 * k)) & 255, true);
         }
@@ -1520,7 +1525,7 @@ __device__ __forceinline__ void process_tile256(const uint8_t *__restrict__ rgb,
             uint32_t sum = 0, e[16];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const uint32_t v = vmax(R[q], vmax(G[q], B[q]));
+                const uint32_t v = vmax3(R[q], G[q], B[q]);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     e[4 * q + k] = s.vlut[(v >> (8 * k)) & 255];
