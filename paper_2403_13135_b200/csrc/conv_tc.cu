@@ -548,6 +548,11 @@ struct WgradProb {
     }
     template <int BN>
     __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
+        load_rows<BN, 2>(kb, sa, sb, bar, mt * BM, nt);
+    }
+    // MB 64-row blocks of the M operand starting at row m0 (MB = 4: the 256-row tiles of conv_gemm_m2)
+    template <int BN, int MB>
+    __device__ void load_rows(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int m0, int nt) const {
         int n0, h0, w0, cls = 0;
         if (halve) {
             const int nblk = pk.tw * pk.th * pk.tn;
@@ -558,10 +563,10 @@ struct WgradProb {
         // one TMA box carries nb consecutive 64-channel blocks ([block][pixel][64 ch] in smem)
         const int bx = nbx, by = nby;
         if (!trans) {
-            for (int j = 0; j < 2; j += by) load_dy(sa + j * 8192, bar, mt * BM + j * 64, cls, n0, h0, w0);
+            for (int j = 0; j < MB; j += by) load_dy(sa + j * 8192, bar, m0 + j * 64, cls, n0, h0, w0);
             for (int j = 0; j < BN / 64; j += bx) load_x(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
         } else {
-            for (int j = 0; j < 2; j += bx) load_x(sa + j * 8192, bar, mt * BM + j * 64, cls, n0, h0, w0);
+            for (int j = 0; j < MB; j += bx) load_x(sa + j * 8192, bar, m0 + j * 64, cls, n0, h0, w0);
             for (int j = 0; j < BN / 64; j += by) load_dy(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
         }
     }
@@ -898,6 +903,108 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
     tc::tc_fence_before();
     __syncthreads();
     if (warp == 1) tc::tmem_dealloc<2 * BN>(tmem);
+}
+
+// 256 x 256 weight-gradient tiles: two 128-row M halves share every B (x / dY) block, so a
+// K-block moves 64 KB through L2 for 2 x 128 x 256 x 64 MACs instead of 96 KB for two
+// 128 x 256 tiles -- the 128-row wgrad is L2-throughput bound (TMA-only replay: 12 TB/s,
+// the LTS cap).  Both halves fill TMEM (2 x 256 columns), so the epilogue drains between
+// tiles instead of overlapping the next one; used where a CTA owns few, long tiles.
+template <int STAGES, class P>
+__global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constant__ P p, const TileGrid g) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int BN = 256, AB = 2 * A_BYTES, B_BYTES = BN * BK * 2;
+    uint8_t *sa = base;
+    uint8_t *sb = base + STAGES * AB;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sb + STAGES * B_BYTES);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 1;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = g.count();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(tfull, 1);
+        tc::mbar_init(tempty, EPI_WARPS);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) p.prefetch();
+    if (warp == 1) tc::tmem_alloc<512>(tslot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int mt, nt, z, kb0, nkb;
+                g.coords(t, mt, nt, z);
+                p.kb_range(z, kb0, nkb);
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    tc::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    tc::mbar_expect_tx(&full[s], AB + B_BYTES);
+                    p.template load_rows<BN, 4>(kb0 + i, sa + s * AB, sb + s * B_BYTES, &full[s], mt * 2 * BM, nt);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, P::A_MN, P::B_MN);
+            int it = 0, local = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+                int mt, nt, z, kb0, nkb;
+                g.coords(t, mt, nt, z);
+                p.kb_range(z, kb0, nkb);
+                tc::mbar_wait(tempty, (local & 1) ^ 1);
+                tc::tc_fence_after();
+                for (int i = 0; i < nkb; ++i, ++it) {
+                    const int s = it % STAGES;
+                    tc::mbar_wait(&full[s], (it / STAGES) & 1);
+                    tc::tc_fence_after();
+                    const uint64_t a0 = tc::sw128_desc(tc::smem_u32(sa + s * AB), P::A_MN ? 8192 : 16, 1024);
+                    const uint64_t a1 = tc::sw128_desc(tc::smem_u32(sa + s * AB + A_BYTES), P::A_MN ? 8192 : 16, 1024);
+                    const uint64_t b0 = tc::sw128_desc(tc::smem_u32(sb + s * B_BYTES), P::B_MN ? 8192 : 16, 1024);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t bk = b0 + (P::B_MN ? 128 : 2) * k;
+                        tc::umma_f16(tmem, a0 + (P::A_MN ? 128 : 2) * k, bk, idesc, (i | k) != 0 ? 1u : 0u);
+                        tc::umma_f16(tmem + BN, a1 + (P::A_MN ? 128 : 2) * k, bk, idesc, (i | k) != 0 ? 1u : 0u);
+                    }
+                    tc::umma_commit(&empty[s]);
+                }
+                tc::umma_commit(tfull);
+            }
+        }
+        __syncwarp();
+    } else {
+        const int sub = warp & 3, half = (warp - 2) >> 2;  // TMEM lane quarter, M half
+        float bacc[4] = {0.f, 0.f, 0.f, 0.f};
+        typename P::Pre pre;
+        int local = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+            int mt, nt, z;
+            g.coords(t, mt, nt, z);
+            tc::mbar_wait(tfull, local & 1);
+            tc::tc_fence_after();
+            p.template epilogue<BN>(tmem + half * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, 2 * mt + half,
+                                    nt, z, 0, BN / 32, bacc, pre);
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tempty);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc<512>(tmem);
 }
 
 // Row-halo variant for 3x3 convs on wide images (W % 128 == 0; U-Net levels 0-1, where
@@ -1573,6 +1680,22 @@ int launch(const P &p, dim3 tiles, cudaStream_t st) {
     return (int)cudaGetLastError();
 }
 
+template <int STAGES, class P>
+int launch_m2(const P &p, dim3 tiles, cudaStream_t st) {
+    constexpr int smem = 1024 + STAGES * (2 * A_BYTES + 256 * BK * 2) + (2 * STAGES + 2) * 8 + 16;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(conv_gemm_m2<STAGES, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return (int)e;
+        attr = true;
+    }
+    TileGrid g{(int)tiles.x, (int)tiles.y, (int)tiles.z};
+    const long long total = (long long)tiles.x * tiles.y * tiles.z;
+    const int grid = (int)(total < num_sms() ? total : num_sms());
+    conv_gemm_m2<STAGES, P><<<grid, NTHREADS, smem, st>>>(p, g);
+    return (int)cudaGetLastError();
+}
+
 int pick_bn(int ntot, long long m_tiles) {
     // largest tile that still gives >= one wave of CTAs; 64 as the floor
     const int cands[3] = {256, 128, 64};
@@ -1662,6 +1785,14 @@ void wgrad_tiles(int ncols, int cout, int &trans, int &mtiles, int &ntiles, int 
         bn = 64;  // cout is a multiple of 64 below 128
         ntiles = cout / bn;
     }
+}
+
+// 256-row weight-gradient tiles (conv_gemm_m2) when the M extent pairs up
+bool wgrad_m2(int mtiles, int bn, int total_kb) {
+    const char *e = getenv("ICE_WG_M2");
+    if (bn != 256 || mtiles % 2) return false;
+    (void)total_kb;  // measured faster at every wgrad shape of the model, 32 K-blocks included
+    return !e || atoi(e) != 0;
 }
 
 // K-blocks per split.  The persistent grid runs ceil(units / SMs) rounds of equal-size
@@ -1950,12 +2081,15 @@ extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2
     int mtiles, ntiles, bn;
     wgrad_tiles(ncols, cout, p.trans, mtiles, ntiles, bn);
     p.total_kb = p.pk.tw * p.pk.th * p.pk.tn;
+    const bool m2 = wgrad_m2(mtiles, bn, p.total_kb);
+    if (m2) mtiles /= 2;
     p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles);
     const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
     // channel blocks per TMA box: as many consecutive 64-blocks as the tile reads from one
-    // (tap, source) run; dY supplies 2 blocks (A, M = 128) or BN/64 (B, transposed)
+    // (tap, source) run; the M operand supplies 2 blocks (4 for 256-row tiles), B BN/64
     {
-        const int want_x = p.trans ? 2 : bn / 64, want_y = p.trans ? bn / 64 : 2;
+        const int mb = m2 ? 4 : 2;
+        const int want_x = p.trans ? mb : bn / 64, want_y = p.trans ? bn / 64 : mb;
         int nbx = want_x;
         while (nbx > 1 && ((c1 % (64 * nbx)) || (c2 % (64 * nbx)))) nbx >>= 1;
         int nby = want_y;
@@ -1968,6 +2102,7 @@ extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2
     if (c2 && !map_act_nb(&p.xb, x2, n, h, w, c2, p.pk, p.nbx)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
     cudaStream_t st = (cudaStream_t)stream;
+    if (m2) return launch_m2<3>(p, grid, st);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
     return launch<64, 8>(p, grid, st);
@@ -2096,10 +2231,13 @@ extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_
     int mtiles, ntiles, bn;
     wgrad_tiles(ncols, cout, p.trans, mtiles, ntiles, bn);
     p.total_kb = 4 * p.pk.tw * p.pk.th * p.pk.tn;
+    const bool m2 = wgrad_m2(mtiles, bn, p.total_kb);
+    if (m2) mtiles /= 2;
     p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles);
     const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
     {
-        const int want_x = p.trans ? 2 : bn / 64, want_y = p.trans ? bn / 64 : 2;
+        const int mb = m2 ? 4 : 2;
+        const int want_x = p.trans ? mb : bn / 64, want_y = p.trans ? bn / 64 : mb;
         int nbx = want_x;
         while (nbx > 1 && (c % (64 * nbx))) nbx >>= 1;
         int nby = want_y;
@@ -2111,6 +2249,7 @@ extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_
     if (!map_act_nb(&p.xa, x, n, h, w, c, p.pk, p.nbx)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
     cudaStream_t st = (cudaStream_t)stream;
+    if (m2) return launch_m2<3>(p, grid, st);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
     return launch<64, 8>(p, grid, st);
