@@ -140,6 +140,17 @@ struct FpropProb {
         else tc::tma_load_4d(sa, &xb, bar, c - c1, w0 + tp.dx[t], h0 + tp.dy[t], n0);
         tc::tma_load_3d(sb, &wm, bar, c, tp.wt[t], nt * BN);
     }
+    // 256-row tile mt = pixel tiles 2 mt and 2 mt + 1 over one 256-column weight block
+    __device__ void load_m2(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int z) const {
+        load<256>(kb, sa, sb, bar, 2 * mt, nt, z);
+        const Taps &tp = taps[z];
+        const int cch = (c1 + c2) / BK;
+        const int t = kb / cch, c = (kb % cch) * BK;
+        int n0, h0, w0;
+        pt.origin(2 * mt + 1, n0, h0, w0);
+        if (c < c1) tc::tma_load_4d(sa + A_BYTES, &xa, bar, c, w0 + tp.dx[t], h0 + tp.dy[t], n0);
+        else tc::tma_load_4d(sa + A_BYTES, &xb, bar, c - c1, w0 + tp.dx[t], h0 + tp.dy[t], n0);
+    }
     // ---- row-halo path (3x3, W % 128 == 0): one 3 x 130-pixel slab per 64-channel chunk
     __device__ int halo_chunks() const { return (c1 + c2) / BK; }
     __device__ void load_halo(int chunk, uint8_t *dst, uint64_t *bar, int mt) const {
@@ -347,6 +358,15 @@ struct DgradProb {
 #pragma unroll
         for (int j = 0; j < BN / 64; ++j) tc::tma_load_3d(sb + j * 8192, &wm, bar, nt * BN + j * 64, taps.wt[t], c);
     }
+    __device__ void load_m2(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int z) const {
+        load<256>(kb, sa, sb, bar, 2 * mt, nt, z);
+        const int cch = cout / BK;
+        const int t = kb / cch, c = (kb % cch) * BK;
+        int n0, h0, w0;
+        pt.origin(2 * mt + 1, n0, h0, w0);
+        if (planes_in) tc::tma_load_5d(sa + A_BYTES, &dym, bar, c, w0 - taps.dx[t], h0 - taps.dy[t], n0, taps.plane[t]);
+        else tc::tma_load_4d(sa + A_BYTES, &dym, bar, c, w0 - taps.dx[t], h0 - taps.dy[t], n0);
+    }
     // ---- row-halo path: slab of dY around the tile; tap t reads dY[p - shift_t]
     __device__ int halo_chunks() const { return cout / BK; }
     // the tile's ReLU-reference rows (64 channels x 128 pixels, SWIZZLE_128B) for the epilogue
@@ -549,6 +569,9 @@ struct WgradProb {
     template <int BN>
     __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
         load_rows<BN, 2>(kb, sa, sb, bar, mt * BM, nt);
+    }
+    __device__ void load_m2(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
+        load_rows<256, 4>(kb, sa, sb, bar, mt * 2 * BM, nt);
     }
     // MB 64-row blocks of the M operand starting at row m0 (MB = 4: the 256-row tiles of conv_gemm_m2)
     template <int BN, int MB>
@@ -905,11 +928,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
     if (warp == 1) tc::tmem_dealloc<2 * BN>(tmem);
 }
 
-// 256 x 256 weight-gradient tiles: two 128-row M halves share every B (x / dY) block, so a
-// K-block moves 64 KB through L2 for 2 x 128 x 256 x 64 MACs instead of 96 KB for two
-// 128 x 256 tiles -- the 128-row wgrad is L2-throughput bound (TMA-only replay: 12 TB/s,
-// the LTS cap).  Both halves fill TMEM (2 x 256 columns), so the epilogue drains between
-// tiles instead of overlapping the next one; used where a CTA owns few, long tiles.
+// 256 x 256 tiles: two 128-row M halves share every B block, so a K-block moves 64 KB
+// through L2 for 2 x 128 x 256 x 64 MACs instead of 96 KB for two 128 x 256 tiles.  The
+// 128-row wgrad is L2-throughput bound (a TMA-only replay of it streams 12 TB/s, the LTS
+// cap; its MMA-only replay runs at 1.84 PFLOP/s).  Both halves fill TMEM (2 x 256 columns),
+// so the epilogue drains between tiles instead of overlapping the next one: used where a
+// CTA owns few, long tiles.  Each epilogue warp drains its 32 TMEM lanes of one M half in
+// two 128-column passes (the problems' epilogues take 4 chunks per call).
+template <int STAGES>
+constexpr int m2_smem_bytes() {
+    return 1024 + STAGES * (2 * A_BYTES + 256 * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 2) * 8 + 16;
+}
+
 template <int STAGES, class P>
 __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constant__ P p, const TileGrid g) {
     extern __shared__ uint8_t smem_raw[];
@@ -917,7 +947,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
     constexpr int BN = 256, AB = 2 * A_BYTES, B_BYTES = BN * BK * 2;
     uint8_t *sa = base;
     uint8_t *sb = base + STAGES * AB;
-    uint64_t *full = reinterpret_cast<uint64_t *>(sb + STAGES * B_BYTES);
+    uint8_t *sst = sb + STAGES * B_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sst + EPI_WARPS * STAGE_BYTES);
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 1;
@@ -952,7 +983,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
                     const int s = it % STAGES;
                     tc::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     tc::mbar_expect_tx(&full[s], AB + B_BYTES);
-                    p.template load_rows<BN, 4>(kb0 + i, sa + s * AB, sb + s * B_BYTES, &full[s], mt * 2 * BM, nt);
+                    p.load_m2(kb0 + i, sa + s * AB, sb + s * B_BYTES, &full[s], mt, nt, z);
                 }
             }
         }
@@ -987,20 +1018,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
         __syncwarp();
     } else {
         const int sub = warp & 3, half = (warp - 2) >> 2;  // TMEM lane quarter, M half
-        float bacc[4] = {0.f, 0.f, 0.f, 0.f};
-        typename P::Pre pre;
-        int local = 0;
+        const int row = sub * 32 + lane;
+        const uint32_t tm = tmem + half * BN + ((uint32_t)(sub * 32) << 16);
+        uint8_t *stage = sst + (warp - 2) * STAGE_BYTES;
+        float bacc0[4] = {0.f, 0.f, 0.f, 0.f}, bacc1[4] = {0.f, 0.f, 0.f, 0.f};
+        int cur_nt = -1, local = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
             int mt, nt, z;
             g.coords(t, mt, nt, z);
+            if (nt != cur_nt) {
+                if (cur_nt >= 0) {
+                    p.template flush_bias<BN>(cur_nt, 0, 4, bacc0);
+                    p.template flush_bias<BN>(cur_nt, 4, 8, bacc1);
+                }
+                cur_nt = nt;
+            }
+            typename P::Pre pre0, pre1;  // operands issued before the wait (hidden by the mainloop)
+            p.template pre_load<BN>(pre0, row, 2 * mt + half, nt, z, 0, 4);
+            p.template pre_load<BN>(pre1, row, 2 * mt + half, nt, z, 4, 8);
             tc::mbar_wait(tfull, local & 1);
             tc::tc_fence_after();
-            p.template epilogue<BN>(tmem + half * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, 2 * mt + half,
-                                    nt, z, 0, BN / 32, bacc, pre);
+            p.template epilogue<BN>(tm, row, 2 * mt + half, nt, z, 0, 4, bacc0, pre0, stage);
+            p.template epilogue<BN>(tm, row, 2 * mt + half, nt, z, 4, 8, bacc1, pre1, stage);
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(tempty);
         }
+        if (cur_nt >= 0) {
+            p.template flush_bias<BN>(cur_nt, 0, 4, bacc0);
+            p.template flush_bias<BN>(cur_nt, 4, 8, bacc1);
+        }
+        if (lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -1682,7 +1730,7 @@ int launch(const P &p, dim3 tiles, cudaStream_t st) {
 
 template <int STAGES, class P>
 int launch_m2(const P &p, dim3 tiles, cudaStream_t st) {
-    constexpr int smem = 1024 + STAGES * (2 * A_BYTES + 256 * BK * 2) + (2 * STAGES + 2) * 8 + 16;
+    constexpr int smem = m2_smem_bytes<STAGES>();
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(conv_gemm_m2<STAGES, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1785,6 +1833,21 @@ void wgrad_tiles(int ncols, int cout, int &trans, int &mtiles, int &ntiles, int 
         bn = 64;  // cout is a multiple of 64 below 128
         ntiles = cout / bn;
     }
+}
+
+// 256-row fprop / dgrad tiles (conv_gemm_m2) for unsplit 256-wide tilings (ICE_CONV_M2=0/1
+// overrides).  Measured per shape in the train step: they gain 8-20% on long K (>= 72
+// K-blocks) when halving the tile count does not worsen the last wave, and lose up to 40%
+// otherwise (short K exposes the drain; 64x64 levels drop from 99% to 87% wave fill).
+bool conv_m2(long long mtiles, int ncols, int bn, int splits, int total_kb) {
+    if (bn != 256 || splits != 1 || mtiles % 2) return false;
+    const char *e = getenv("ICE_CONV_M2");
+    if (e) return atoi(e) != 0;
+    const long long sms = num_sms(), t1 = mtiles * (ncols / 256), t2 = t1 / 2;
+    if (t2 * 5 < sms * 4 || total_kb < 72) return false;
+    const double e1 = (double)t1 / (double)(((t1 + sms - 1) / sms) * sms);
+    const double e2 = (double)t2 / (double)(((t2 + sms - 1) / sms) * sms);
+    return e2 >= e1 - 0.01;
 }
 
 // 256-row weight-gradient tiles (conv_gemm_m2) when the M extent pairs up
@@ -1974,6 +2037,7 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
             return (int)cudaGetLastError();
         }
     }
+    if (conv_m2(mtiles, cout, bn, splits, total_kb)) return launch_m2<3>(p, dim3((unsigned)(mtiles / 2), cout / 256, 1), st);
     dim3 grid((unsigned)mtiles, cout / bn, 1);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
@@ -2054,6 +2118,7 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
             return (int)cudaGetLastError();
         }
     }
+    if (conv_m2(mtiles, ct, bn, splits, total_kb)) return launch_m2<3>(p, dim3((unsigned)(mtiles / 2), ct / 256, 1), st);
     dim3 grid((unsigned)mtiles, ct / bn, 1);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
@@ -2204,8 +2269,10 @@ extern "C" int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t 
     const int bn = pick_bn(c, mtiles);
     if (!map_planes(&p.dym, dy_planes, n, h, w, cout, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wc, cout, 9, c, 64)) return ICE_EINVAL;
-    dim3 grid((unsigned)mtiles, c / bn, 1);
     cudaStream_t st = (cudaStream_t)stream;
+    if (conv_m2(mtiles, c, bn, 1, 9 * (cout / BK)))
+        return launch_m2<3>(p, dim3((unsigned)(mtiles / 2), c / 256, 1), st);
+    dim3 grid((unsigned)mtiles, c / bn, 1);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
     return launch<64, 8>(p, grid, st);
