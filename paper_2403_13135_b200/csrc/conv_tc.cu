@@ -40,22 +40,27 @@ constexpr int STAGE_BYTES = 32 * 64;  // one warp's 32 px x 32 ch bf16 output bo
 constexpr int STAGE_BUFS = 1;  // two warps per TMEM lane quarter, each draining half the columns
 constexpr int NTHREADS = 64 + 32 * EPI_WARPS;
 
-struct PixTile {  // a box of Wt x Ht x Nt pixels, and how many boxes tile (W, H, N)
+// a box of Wt x Ht x Nt pixels, and how many boxes tile (W, H, N).  Every entry point
+// requires power-of-two H and W (shape_ok), so Wt, Ht, Nt, tw, th are powers of two and the
+// index math is shifts and masks (the epilogue runs it per tile; integer division by a
+// runtime value costs ~25 instructions and dominated the short-K epilogues).
+__device__ __forceinline__ int lg2(int v) { return __ffs(v) - 1; }
+struct PixTile {
     int Wt, Ht, Nt, tw, th, tn;
     __device__ __forceinline__ void origin(int t, int &n0, int &h0, int &w0) const {
-        int wi = t % tw;
-        t /= tw;
-        int hi = t % th;
-        int ni = t / th;
+        const int wi = t & (tw - 1);
+        t >>= lg2(tw);
+        const int hi = t & (th - 1);
+        const int ni = t >> lg2(th);
         w0 = wi * Wt;
         h0 = hi * Ht;
         n0 = ni * Nt;
     }
     __device__ __forceinline__ void pixel(int row, int n0, int h0, int w0, int &n, int &h, int &w) const {
-        w = w0 + row % Wt;
-        int r = row / Wt;
-        h = h0 + r % Ht;
-        n = n0 + r / Ht;
+        w = w0 + (row & (Wt - 1));
+        const int r = row >> lg2(Wt);
+        h = h0 + (r & (Ht - 1));
+        n = n0 + (r >> lg2(Ht));
     }
 };
 
@@ -786,16 +791,28 @@ constexpr int smem_bytes() {
     return 1024 + STAGES * (A_BYTES + BN * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16;
 }
 
+// exact t / d for 0 <= t < 2^24 from a float reciprocal and one correction step
+__device__ __forceinline__ int fdiv(int t, int d, float inv) {
+    int q = __float2int_rz((float)t * inv);
+    int r = t - q * d;
+    if (r < 0) --q;
+    else if (r >= d) ++q;
+    return q;
+}
 struct TileGrid {  // persistent schedule: tile t -> (m fastest, then n, then split z)
     int tm, tn, tz;
+    float itm, itn;  // 1 / tm, 1 / tn (tile_grid)
     __device__ __forceinline__ int count() const { return tm * tn * tz; }
     __device__ __forceinline__ void coords(int t, int &mt, int &nt, int &z) const {
-        mt = t % tm;
-        t /= tm;
-        nt = t % tn;
-        z = t / tn;
+        int q = fdiv(t, tm, itm);
+        mt = t - q * tm;
+        z = fdiv(q, tn, itn);
+        nt = q - z * tn;
     }
 };
+TileGrid tile_grid(dim3 tiles) {
+    return TileGrid{(int)tiles.x, (int)tiles.y, (int)tiles.z, 1.f / (float)tiles.x, 1.f / (float)tiles.y};
+}
 
 // Persistent, warp-specialised tcgen05 GEMM.  One CTA per SM walks the tile list; the
 // TMA producer streams K-blocks through a STAGES-deep smem ring across tile boundaries,
@@ -1682,7 +1699,7 @@ int launch_halo(const P &p, dim3 tiles, cudaStream_t st) {
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }
-    TileGrid g{(int)tiles.x, (int)tiles.y, (int)tiles.z};
+    const TileGrid g = tile_grid(tiles);
     const long long total = (long long)tiles.x * tiles.y * tiles.z;
     const int grid = (int)(total < num_sms() ? total : num_sms());
     halo_gemm<BN, BSTAGES, RES, P, DUAL><<<grid, NTHREADS + (DUAL ? 32 : 0), smem, st>>>(p, g);
@@ -1721,7 +1738,7 @@ int launch(const P &p, dim3 tiles, cudaStream_t st) {
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }
-    TileGrid g{(int)tiles.x, (int)tiles.y, (int)tiles.z};
+    const TileGrid g = tile_grid(tiles);
     const long long total = (long long)tiles.x * tiles.y * tiles.z;
     const int grid = (int)(total < num_sms() ? total : num_sms());
     conv_gemm<BN, STAGES, P><<<grid, NTHREADS, smem, st>>>(p, g);
@@ -1737,7 +1754,7 @@ int launch_m2(const P &p, dim3 tiles, cudaStream_t st) {
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }
-    TileGrid g{(int)tiles.x, (int)tiles.y, (int)tiles.z};
+    const TileGrid g = tile_grid(tiles);
     const long long total = (long long)tiles.x * tiles.y * tiles.z;
     const int grid = (int)(total < num_sms() ? total : num_sms());
     conv_gemm_m2<STAGES, P><<<grid, NTHREADS, smem, st>>>(p, g);
