@@ -190,7 +190,7 @@ struct FpropProb {
         for (int ci = 0; ci < 2; ++ci) {
             const int col = nt * BN + (cc0 + ci) * 32 + lane;
             const bool have = cc0 + ci < cc1;
-            pr.b[ci] = (have && bias) ? __ldg(bias + (merged ? col % cout : col)) : 0.f;
+            pr.b[ci] = (have && bias) ? __ldg(bias + (merged ? col & (cout - 1) : col)) : 0.f;
             pr.d[ci] = (have && drop && pr.uni) ? __ldg(drop + (size_t)n_first * cout + col) : 1.f;
         }
     }
@@ -215,7 +215,7 @@ struct FpropProb {
             tc::tmem_ld32(tmem + cc * 32, v);
             int col0 = nt * BN + cc * 32;
             if (merged) {  // this 32-column chunk belongs to sub-pixel class col0 / cout
-                const int cls = col0 / cout;
+                const int cls = col0 >> lg2(cout);  // merged: cout is 64 or 128
                 col0 -= cls * cout;
                 h = 2 * hb + (cls >> 1);
                 w = 2 * wb + (cls & 1);
@@ -1434,8 +1434,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                     const int s = it % STAGES;
                     tc::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     tc::mbar_expect_tx(&full[s], TX);
-                    const int seg = kb % segs, row = kb / segs;
-                    const int h = row % p.H, n = row / p.H, w0 = seg * 64;
+                    const int seg = kb & (segs - 1), row = kb >> lg2(segs);  // W, H powers of two
+                    const int h = row & (p.H - 1), n = row >> lg2(p.H), w0 = seg * 64;
                     uint8_t *st = base + s * STAGE;
 #pragma unroll
                     for (int c = 0; c < NCH; ++c)
