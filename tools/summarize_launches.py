@@ -18,6 +18,7 @@ ap.add_argument("csv")
 ap.add_argument("--steps", type=int, default=0, help="0: count head_ce_kernel launches (one per step)")
 ap.add_argument("--out", default=None)
 ap.add_argument("--traffic", default=None)
+ap.add_argument("--al-tiles", type=int, default=1024, help="tiles per autolabel256 launch (bench --corpus)")
 a = ap.parse_args()
 
 launch = collections.OrderedDict()
@@ -66,5 +67,12 @@ if a.traffic and wg and any(g["dram_bytes"] for g in wg):
     tr = {"ice_conv_wgrad": round(sum(g["dram_bytes"] for g in wg) / n),
           "_note": "DRAM read+write bytes per launch, average over the wgrad family (conv_gemm<..,WgradProb> "
                    "+ hwgrad_kernel) of one train step, from " + a.csv}
-    json.dump(tr, open(a.traffic, "w"), indent=1)
-    print("traffic:", tr)
+    old = json.load(open(a.traffic)) if os.path.exists(a.traffic) else {}
+    old.update(tr)
+    al = [g for k, g in agg.items() if "autolabel256" in k]
+    if al and al[0]["dram_bytes"]:
+        old["ice_autolabel_bytes_per_tile"] = round(al[0]["dram_bytes"] / al[0]["launches"] / a.al_tiles)
+        old["_note_autolabel"] = (f"fastk::autolabel256_kernel over the {a.al_tiles}-tile corpus (one launch), DRAM "
+                                  "read+write / tiles; algorithmic 458,752 B/tile")
+    json.dump(old, open(a.traffic, "w"), indent=1)
+    print("traffic:", old)
