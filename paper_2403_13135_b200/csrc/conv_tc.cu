@@ -146,8 +146,9 @@ struct FpropProb {
         tc::tma_load_3d(sb, &wm, bar, c, tp.wt[t], nt * BN);
     }
     // 256-row tile mt = pixel tiles 2 mt and 2 mt + 1 over one 256-column weight block
+    template <int BN>
     __device__ void load_m2(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int z) const {
-        load<256>(kb, sa, sb, bar, 2 * mt, nt, z);
+        load<BN>(kb, sa, sb, bar, 2 * mt, nt, z);
         const Taps &tp = taps[z];
         const int cch = (c1 + c2) / BK;
         const int t = kb / cch, c = (kb % cch) * BK;
@@ -363,8 +364,9 @@ struct DgradProb {
 #pragma unroll
         for (int j = 0; j < BN / 64; ++j) tc::tma_load_3d(sb + j * 8192, &wm, bar, nt * BN + j * 64, taps.wt[t], c);
     }
+    template <int BN>
     __device__ void load_m2(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int z) const {
-        load<256>(kb, sa, sb, bar, 2 * mt, nt, z);
+        load<BN>(kb, sa, sb, bar, 2 * mt, nt, z);
         const int cch = cout / BK;
         const int t = kb / cch, c = (kb % cch) * BK;
         int n0, h0, w0;
@@ -575,8 +577,9 @@ struct WgradProb {
     __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
         load_rows<BN, 2>(kb, sa, sb, bar, mt * BM, nt);
     }
+    template <int BN>
     __device__ void load_m2(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
-        load_rows<256, 4>(kb, sa, sb, bar, mt * 2 * BM, nt);
+        load_rows<BN, 4>(kb, sa, sb, bar, mt * 2 * BM, nt);
     }
     // MB 64-row blocks of the M operand starting at row m0 (MB = 4: the 256-row tiles of conv_gemm_m2)
     template <int BN, int MB>
@@ -951,25 +954,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
 // cap; its MMA-only replay runs at 1.84 PFLOP/s).  Both halves fill TMEM (2 x 256 columns),
 // so the epilogue drains between tiles instead of overlapping the next one: used where a
 // CTA owns few, long tiles.  Each epilogue warp drains its 32 TMEM lanes of one M half in
-// two 128-column passes (the problems' epilogues take 4 chunks per call).
-template <int STAGES>
+// two 128-column passes (the problems' epilogues take 4 chunks per call).  BN = 128 (layers
+// with 128 output columns): 256 x 128 tiles move 48 KB per K-block for 256 x 128 x 64 MACs
+// (a 128 x 128 tile: 32 KB for half of that) and two accumulator pairs fit TMEM, so the
+// epilogue overlaps the next tile as in conv_gemm.
+template <int BN, int STAGES>
 constexpr int m2_smem_bytes() {
-    return 1024 + STAGES * (2 * A_BYTES + 256 * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 2) * 8 + 16;
+    return 1024 + STAGES * (2 * A_BYTES + BN * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16;
 }
 
-template <int STAGES, class P>
+template <int BN, int STAGES, class P>
 __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constant__ P p, const TileGrid g) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    constexpr int BN = 256, AB = 2 * A_BYTES, B_BYTES = BN * BK * 2;
+    constexpr int AB = 2 * A_BYTES, B_BYTES = BN * BK * 2;
+    constexpr int NACC = 4 * BN <= 512 ? 2 : 1;  // BN = 128: two accumulator pairs, epilogue overlapped
     uint8_t *sa = base;
     uint8_t *sb = base + STAGES * AB;
     uint8_t *sst = sb + STAGES * B_BYTES;
     uint64_t *full = reinterpret_cast<uint64_t *>(sst + EPI_WARPS * STAGE_BYTES);
     uint64_t *empty = full + STAGES;
-    uint64_t *tfull = empty + STAGES;
-    uint64_t *tempty = tfull + 1;
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 1);
+    uint64_t *tfull = empty + STAGES;  // [2]
+    uint64_t *tempty = tfull + 2;      // [2]
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = g.count();
@@ -978,8 +985,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 1);
         }
-        tc::mbar_init(tfull, 1);
-        tc::mbar_init(tempty, EPI_WARPS);
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(&tfull[a], 1);
+            tc::mbar_init(&tempty[a], EPI_WARPS);
+        }
         tc::fence_barrier_init();
     }
     if (warp == 0 && lane == 0) p.prefetch();
@@ -1000,7 +1009,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
                     const int s = it % STAGES;
                     tc::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     tc::mbar_expect_tx(&full[s], AB + B_BYTES);
-                    p.load_m2(kb0 + i, sa + s * AB, sb + s * B_BYTES, &full[s], mt, nt, z);
+                    p.template load_m2<BN>(kb0 + i, sa + s * AB, sb + s * B_BYTES, &full[s], mt, nt, z);
                 }
             }
         }
@@ -1012,8 +1021,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
                 int mt, nt, z, kb0, nkb;
                 g.coords(t, mt, nt, z);
                 p.kb_range(z, kb0, nkb);
-                tc::mbar_wait(tempty, (local & 1) ^ 1);
+                const int acc = local % NACC;
+                tc::mbar_wait(&tempty[acc], ((local / NACC) & 1) ^ 1);
                 tc::tc_fence_after();
+                const uint32_t d = tmem + acc * 2 * BN;
                 for (int i = 0; i < nkb; ++i, ++it) {
                     const int s = it % STAGES;
                     tc::mbar_wait(&full[s], (it / STAGES) & 1);
@@ -1024,19 +1035,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
                         const uint64_t bk = b0 + (P::B_MN ? 128 : 2) * k;
-                        tc::umma_f16(tmem, a0 + (P::A_MN ? 128 : 2) * k, bk, idesc, (i | k) != 0 ? 1u : 0u);
-                        tc::umma_f16(tmem + BN, a1 + (P::A_MN ? 128 : 2) * k, bk, idesc, (i | k) != 0 ? 1u : 0u);
+                        tc::umma_f16(d, a0 + (P::A_MN ? 128 : 2) * k, bk, idesc, (i | k) != 0 ? 1u : 0u);
+                        tc::umma_f16(d + BN, a1 + (P::A_MN ? 128 : 2) * k, bk, idesc, (i | k) != 0 ? 1u : 0u);
                     }
                     tc::umma_commit(&empty[s]);
                 }
-                tc::umma_commit(tfull);
+                tc::umma_commit(&tfull[acc]);
             }
         }
         __syncwarp();
     } else {
         const int sub = warp & 3, half = (warp - 2) >> 2;  // TMEM lane quarter, M half
         const int row = sub * 32 + lane;
-        const uint32_t tm = tmem + half * BN + ((uint32_t)(sub * 32) << 16);
+        constexpr int NCH = BN / 32, PER = (NCH + 1) / 2;  // two passes of PER chunks
         uint8_t *stage = sst + (warp - 2) * STAGE_BYTES;
         float bacc0[4] = {0.f, 0.f, 0.f, 0.f}, bacc1[4] = {0.f, 0.f, 0.f, 0.f};
         int cur_nt = -1, local = 0;
@@ -1045,25 +1056,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
             g.coords(t, mt, nt, z);
             if (nt != cur_nt) {
                 if (cur_nt >= 0) {
-                    p.template flush_bias<BN>(cur_nt, 0, 4, bacc0);
-                    p.template flush_bias<BN>(cur_nt, 4, 8, bacc1);
+                    p.template flush_bias<BN>(cur_nt, 0, PER, bacc0);
+                    p.template flush_bias<BN>(cur_nt, PER, NCH, bacc1);
                 }
                 cur_nt = nt;
             }
             typename P::Pre pre0, pre1;  // operands issued before the wait (hidden by the mainloop)
-            p.template pre_load<BN>(pre0, row, 2 * mt + half, nt, z, 0, 4);
-            p.template pre_load<BN>(pre1, row, 2 * mt + half, nt, z, 4, 8);
-            tc::mbar_wait(tfull, local & 1);
+            p.template pre_load<BN>(pre0, row, 2 * mt + half, nt, z, 0, PER);
+            p.template pre_load<BN>(pre1, row, 2 * mt + half, nt, z, PER, NCH);
+            const int acc = local % NACC;
+            tc::mbar_wait(&tfull[acc], (local / NACC) & 1);
             tc::tc_fence_after();
-            p.template epilogue<BN>(tm, row, 2 * mt + half, nt, z, 0, 4, bacc0, pre0, stage);
-            p.template epilogue<BN>(tm, row, 2 * mt + half, nt, z, 4, 8, bacc1, pre1, stage);
+            const uint32_t tm = tmem + acc * 2 * BN + half * BN + ((uint32_t)(sub * 32) << 16);
+            p.template epilogue<BN>(tm, row, 2 * mt + half, nt, z, 0, PER, bacc0, pre0, stage);
+            p.template epilogue<BN>(tm, row, 2 * mt + half, nt, z, PER, NCH, bacc1, pre1, stage);
             tc::tc_fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(tempty);
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
         if (cur_nt >= 0) {
-            p.template flush_bias<BN>(cur_nt, 0, 4, bacc0);
-            p.template flush_bias<BN>(cur_nt, 4, 8, bacc1);
+            p.template flush_bias<BN>(cur_nt, 0, PER, bacc0);
+            p.template flush_bias<BN>(cur_nt, PER, NCH, bacc1);
         }
         if (lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
     }
@@ -1745,19 +1758,19 @@ int launch(const P &p, dim3 tiles, cudaStream_t st) {
     return (int)cudaGetLastError();
 }
 
-template <int STAGES, class P>
+template <int BN, int STAGES, class P>
 int launch_m2(const P &p, dim3 tiles, cudaStream_t st) {
-    constexpr int smem = m2_smem_bytes<STAGES>();
+    constexpr int smem = m2_smem_bytes<BN, STAGES>();
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(conv_gemm_m2<STAGES, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(conv_gemm_m2<BN, STAGES, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }
     const TileGrid g = tile_grid(tiles);
     const long long total = (long long)tiles.x * tiles.y * tiles.z;
     const int grid = (int)(total < num_sms() ? total : num_sms());
-    conv_gemm_m2<STAGES, P><<<grid, NTHREADS, smem, st>>>(p, g);
+    conv_gemm_m2<BN, STAGES, P><<<grid, NTHREADS, smem, st>>>(p, g);
     return (int)cudaGetLastError();
 }
 
@@ -1857,11 +1870,13 @@ void wgrad_tiles(int ncols, int cout, int &trans, int &mtiles, int &ntiles, int 
 // K-blocks) when halving the tile count does not worsen the last wave, and lose up to 40%
 // otherwise (short K exposes the drain; 64x64 levels drop from 99% to 87% wave fill).
 bool conv_m2(long long mtiles, int ncols, int bn, int splits, int total_kb) {
-    if (bn != 256 || splits != 1 || mtiles % 2) return false;
+    if ((bn != 256 && bn != 128) || splits != 1 || mtiles % 2) return false;
     const char *e = getenv("ICE_CONV_M2");
     if (e) return atoi(e) != 0;
-    const long long sms = num_sms(), t1 = mtiles * (ncols / 256), t2 = t1 / 2;
-    if (t2 * 5 < sms * 4 || total_kb < 72) return false;
+    const long long sms = num_sms(), t1 = mtiles * (ncols / bn), t2 = t1 / 2;
+    if (t2 * 5 < sms * 4) return false;
+    if (bn == 128) return true;  // double-buffered accumulators: no exposed drain
+    if (total_kb < 72) return false;
     const double e1 = (double)t1 / (double)(((t1 + sms - 1) / sms) * sms);
     const double e2 = (double)t2 / (double)(((t2 + sms - 1) / sms) * sms);
     return e2 >= e1 - 0.01;
@@ -2054,7 +2069,9 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
             return (int)cudaGetLastError();
         }
     }
-    if (conv_m2(mtiles, cout, bn, splits, total_kb)) return launch_m2<3>(p, dim3((unsigned)(mtiles / 2), cout / 256, 1), st);
+    if (conv_m2(mtiles, cout, bn, splits, total_kb))
+        return bn == 256 ? launch_m2<256, 3>(p, dim3((unsigned)(mtiles / 2), cout / 256, 1), st)
+                         : launch_m2<128, 4>(p, dim3((unsigned)(mtiles / 2), cout / 128, 1), st);
     dim3 grid((unsigned)mtiles, cout / bn, 1);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
@@ -2135,7 +2152,9 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
             return (int)cudaGetLastError();
         }
     }
-    if (conv_m2(mtiles, ct, bn, splits, total_kb)) return launch_m2<3>(p, dim3((unsigned)(mtiles / 2), ct / 256, 1), st);
+    if (conv_m2(mtiles, ct, bn, splits, total_kb))
+        return bn == 256 ? launch_m2<256, 3>(p, dim3((unsigned)(mtiles / 2), ct / 256, 1), st)
+                         : launch_m2<128, 4>(p, dim3((unsigned)(mtiles / 2), ct / 128, 1), st);
     dim3 grid((unsigned)mtiles, ct / bn, 1);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
@@ -2184,7 +2203,7 @@ extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2
     if (c2 && !map_act_nb(&p.xb, x2, n, h, w, c2, p.pk, p.nbx)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
     cudaStream_t st = (cudaStream_t)stream;
-    if (m2) return launch_m2<3>(p, grid, st);
+    if (m2) return launch_m2<256, 3>(p, grid, st);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
     return launch<64, 8>(p, grid, st);
@@ -2288,7 +2307,8 @@ extern "C" int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t 
     if (!map_wgt(&p.wm, wc, cout, 9, c, 64)) return ICE_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     if (conv_m2(mtiles, c, bn, 1, 9 * (cout / BK)))
-        return launch_m2<3>(p, dim3((unsigned)(mtiles / 2), c / 256, 1), st);
+        return bn == 256 ? launch_m2<256, 3>(p, dim3((unsigned)(mtiles / 2), c / 256, 1), st)
+                         : launch_m2<128, 4>(p, dim3((unsigned)(mtiles / 2), c / 128, 1), st);
     dim3 grid((unsigned)mtiles, c / bn, 1);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
@@ -2333,7 +2353,7 @@ extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_
     if (!map_act_nb(&p.xa, x, n, h, w, c, p.pk, p.nbx)) return ICE_EINVAL;
     dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
     cudaStream_t st = (cudaStream_t)stream;
-    if (m2) return launch_m2<3>(p, grid, st);
+    if (m2) return launch_m2<256, 3>(p, grid, st);
     if (bn == 256) return launch<256, 4>(p, grid, st);
     if (bn == 128) return launch<128, 6>(p, grid, st);
     return launch<64, 8>(p, grid, st);

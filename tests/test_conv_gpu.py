@@ -86,6 +86,22 @@ def test_dgrad(shape):
         assert rel(nchw(d2), g[:, c1:]) < 1e-2
 
 
+# 256-row tiles (conv_gemm_m2) forced on, including shapes the size rule would not pick:
+# ragged image counts (padding rows in the second M half), concat inputs, 8x8 levels
+M2_SHAPES = [(33, 8, 8, 128, 128, 512, 3), (8, 8, 8, 256, 256, 512, 3), (6, 16, 16, 256, 0, 512, 3),
+             (3, 32, 32, 128, 0, 256, 3), (5, 16, 16, 512, 512, 512, 3)]
+
+
+@pytest.mark.parametrize("shape", M2_SHAPES, ids=str)
+def test_m2_tiles_forced(shape, monkeypatch):
+    monkeypatch.setenv("ICE_CONV_M2", "1")
+    monkeypatch.setenv("ICE_WG_M2", "1")
+    monkeypatch.setenv("ICE_NO_SPLITK", "1")  # the 256-row path runs unsplit
+    test_fprop(shape)
+    test_dgrad(shape)
+    test_wgrad(shape)
+
+
 @pytest.mark.parametrize("shape", SHAPES, ids=str)
 def test_wgrad(shape):
     n, h, w, c1, c2, cout, k = shape

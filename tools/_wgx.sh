@@ -1,6 +1,7 @@
-timeout 300 python -m pytest tests/test_conv_gpu.py -x -q -k wgrad 2>&1 | tail -3 || exit 1
-for sh in "32 16 16 1024 0 1024" "32 32 32 512 0 512" "32 64 64 256 256 256" "32 16 16 1024 1024 1024" "32 8 8 2048 0 2048" "32 8 8 1024 0 2048"; do
- for m in 0 1; do echo -n "pair=$m "; ICE_WG_PAIR=$m timeout 60 python tools/time_conv.py wgrad $sh; done
-done
-timeout 600 python -m pytest tests/test_conv_gpu.py tests/test_unet_gpu.py -x -q 2>&1 | tail -2
-bash tools/ab_env.sh ICE_WG_PAIR=0 2
+timeout 600 python -m pytest tests/test_conv_gpu.py -x -q 2>&1 | tail -2
+for m in 0 1; do echo -n "m2=$m "; ICE_CONV_M2=$m timeout 60 python tools/time_conv.py dgrad 32 64 64 128 0 256; done
+for m in 0 1; do echo -n "m2=$m "; ICE_CONV_M2=$m timeout 60 python tools/time_conv.py dgrad 32 32 32 128 0 256; done
+timeout 600 python -m pytest tests/test_unet_gpu.py tests/test_graph_gpu.py -x -q 2>&1 | tail -2
+python tools/profile_layers.py > gpurun_out/layers7.txt 2>&1
+ICE_LIB_PATH=paper_2403_13135_b200/_C/base/libicelabel_b200.so python tools/profile_layers.py > gpurun_out/layers7_base.txt 2>&1
+bash tools/ab_bench.sh paper_2403_13135_b200/_C/base/libicelabel_b200.so paper_2403_13135_b200/_C/libicelabel_b200.so 3
