@@ -8,9 +8,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 K="--kernel-name-base demangled"
 timeout 600 ncu --set full --clock-control none --import-source on $K -k "regex:hwgrad_kernel<.int.64, .int.2" -s 1 -c 1 \
   -o gpurun_out/full_hwgrad64 -f python tools/profile_step.py --steps 2 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on $K -k "regex:conv_gemm_m2<.int.3, .*WgradProb" -s 10 -c 2 \
+timeout 600 ncu --set full --clock-control none --import-source on $K -k "regex:conv_gemm_m2<.int.256, .int.3, .*WgradProb" -s 10 -c 2 \
   -o gpurun_out/full_wgrad_m2 -f python tools/profile_step.py --steps 2 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on $K -k "regex:conv_gemm_m2<.int.3, .*DgradProb" -s 2 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on $K -k "regex:conv_gemm_m2<.int.256, .int.3, .*DgradProb" -s 2 -c 1 \
   -o gpurun_out/full_dgrad_m2 -f python tools/profile_step.py --steps 2 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on $K -k "regex:halo_gemm<.int.64, .int.1, .bool.1.*FpropProb" -s 2 -c 1 \
   -o gpurun_out/full_halo_fp64 -f python tools/profile_step.py --steps 2 > /dev/null 2>&1
