@@ -30,33 +30,57 @@ inline unsigned grid_for(long long work, int per_block) {
 
 // ---- stem: train.py:63 (u8 / 255) + im2col of the 3x3x3 first conv, K padded to 64 ----
 // out[p][(r*3+s)*3 + c] = img[p + (r-1, s-1)][c] / 255 (zero outside), out[p][27..63] = 0
-__global__ void stem_im2col_kernel(const uint8_t *__restrict__ img, int n, int h, int w, uint16_t *__restrict__ out) {
+// 8-bit values: the bf16 of v / 255 comes from a 256-entry table built once per block (the
+// same expression, so bit-identical); each warp stages its 32 pixels' 128-B rows in shared
+// memory and writes them as 8 fully coalesced 512-B stores (per-lane 128-B rows would touch 32
+// lines per store instruction).
+__global__ void __launch_bounds__(256) stem_im2col_kernel(const uint8_t *__restrict__ img, int n, int h, int w,
+                                                          uint16_t *__restrict__ out) {
+    __shared__ uint16_t lut[256];
+    __shared__ __align__(16) uint4 stage[8][32 * 8 + 8];  // per warp: 32 px x 128 B (+ pad)
+    lut[threadIdx.x] = to_bf((float)threadIdx.x / 255.0f);
+    __syncthreads();
     const long long npx = (long long)n * h * w;
-    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < npx; p += (long long)gridDim.x * blockDim.x) {
-        const int x = (int)(p % w);
-        const int y = (int)((p / w) % h);
-        const long long img0 = p - (long long)y * w - x;  // first pixel of this image
-        uint16_t v[64];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint4 *st = stage[wid];
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < npx; base += (long long)gridDim.x * blockDim.x) {
+        const long long p = base + threadIdx.x;
+        if (p < npx) {
+            const long long row = p / w;
+            const int x = (int)(p - row * w);
+            const int y = (int)(row % h);
+            const long long img0 = p - (long long)y * w - x;  // first pixel of this image
+            uint16_t v[32];
 #pragma unroll
-        for (int i = 27; i < 64; ++i) v[i] = 0;
+            for (int i = 27; i < 32; ++i) v[i] = 0;
 #pragma unroll
-        for (int t = 0; t < 9; ++t) {
-            const int yy = y + t / 3 - 1, xx = x + t % 3 - 1;
-            const bool in = yy >= 0 && yy < h && xx >= 0 && xx < w;
-            const uint8_t *px = img + 3 * (img0 + (long long)yy * w + xx);
+            for (int t = 0; t < 9; ++t) {
+                const int yy = y + t / 3 - 1, xx = x + t % 3 - 1;
+                const bool in = yy >= 0 && yy < h && xx >= 0 && xx < w;
+                const uint8_t *px = img + 3 * (img0 + (long long)yy * w + xx);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) v[t * 3 + c] = in ? to_bf((float)px[c] / 255.0f) : (uint16_t)0;
+                for (int c = 0; c < 3; ++c) v[t * 3 + c] = in ? lut[px[c]] : (uint16_t)0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // 16-B chunk q of the row, chunks 4-7 are the zero pad
+                uint4 u;
+                u.x = v[q * 8 + 0] | ((uint32_t)v[q * 8 + 1] << 16);
+                u.y = v[q * 8 + 2] | ((uint32_t)v[q * 8 + 3] << 16);
+                u.z = v[q * 8 + 4] | ((uint32_t)v[q * 8 + 5] << 16);
+                u.w = v[q * 8 + 6] | ((uint32_t)v[q * 8 + 7] << 16);
+                st[lane * 8 + ((q + lane) & 7)] = u;  // rotate chunks: conflict-free 16-B stores
+                st[lane * 8 + ((q + 4 + lane) & 7)] = make_uint4(0, 0, 0, 0);
+            }
         }
-        uint4 *dst = reinterpret_cast<uint4 *>(out + p * 64);
+        __syncwarp();
+        const long long p0 = base + (wid << 5);
+        uint4 *dst = reinterpret_cast<uint4 *>(out) + p0 * 8;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            uint4 u;
-            u.x = v[q * 8 + 0] | ((uint32_t)v[q * 8 + 1] << 16);
-            u.y = v[q * 8 + 2] | ((uint32_t)v[q * 8 + 3] << 16);
-            u.z = v[q * 8 + 4] | ((uint32_t)v[q * 8 + 5] << 16);
-            u.w = v[q * 8 + 6] | ((uint32_t)v[q * 8 + 7] << 16);
-            dst[q] = u;
+        for (int k = 0; k < 8; ++k) {
+            const int idx = k * 32 + lane, px = idx >> 3, ch = idx & 7;
+            if (p0 + px < npx) dst[idx] = st[px * 8 + ((ch + px) & 7)];
         }
+        __syncwarp();
     }
 }
 

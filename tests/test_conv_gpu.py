@@ -227,3 +227,22 @@ def test_relu_bits_roundtrip(shape):
     dbb, _ = ops.conv_dgrad(dy, wt2, cout, bits1=bits, db1=db_b)
     assert rel(da, dbb) < 1e-6 or torch.equal(da, dbb)
     assert rel(db_a, db_b) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(3, 8, 16), (2, 5, 7), (1, 256, 256), (4, 33, 64)], ids=str)
+def test_stem_im2col(shape):
+    """ice_stem_im2col: u8 NHWC RGB -> [px][64] bf16 rows of the 27 3x3x3 taps (/255, zero
+    padded; column 3 t + c for tap t = 3 (dy + 1) + (dx + 1)), columns 27-63 zero."""
+    from paper_2403_13135_b200 import _native
+    n, h, w = shape
+    g = torch.Generator().manual_seed(5)
+    img = torch.randint(0, 256, (n, h, w, 3), generator=g, dtype=torch.uint8).cuda()
+    out = torch.full((n * h * w, 64), 7, dtype=torch.int16, device="cuda")
+    _native.call("ice_stem_im2col", img.data_ptr(), n, h, w, out.data_ptr(), _native.stream_handle())
+    torch.cuda.synchronize()
+    x = (img.float() / 255.0).permute(0, 3, 1, 2)
+    cols = F.unfold(x, 3, padding=1)  # [n][c * 9 + t][px]
+    ref = cols.view(n, 3, 9, h * w).permute(0, 3, 2, 1).reshape(n * h * w, 27)
+    want = torch.zeros(n * h * w, 64, dtype=torch.bfloat16, device="cuda")
+    want[:, :27] = ref.to(torch.bfloat16)
+    assert torch.equal(out.view(torch.bfloat16), want)
