@@ -572,7 +572,17 @@ extern "C" int ice_maxpool_bwd(const uint16_t *x, const uint16_t *dpool, const u
     // grid * threads must be a multiple of cv (fixed channels per thread for the bias sums)
     if (cv > threads || threads % cv) return ICE_EINVAL;  // c <= 2048, power-of-two channel groups
     long long blocks = (total + threads - 1) / threads;
-    if (blocks > 148LL * 4) blocks = 148LL * 4;
+    // one wave of resident blocks (72 registers: 3 per SM, not 4 -- a 4th would run as a tail)
+    static int resident = 0;
+    if (!resident && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, maxpool_bwd_kernel, threads, 0) !=
+                          cudaSuccess || resident < 1))
+        resident = 2;
+    int sms = 148;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (blocks > (long long)sms * resident) blocks = (long long)sms * resident;
     maxpool_bwd_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(x, dpool, add, drop, n, h, w, c, dz,
                                                                                 dbias);
     LAUNCH_CHECK();
