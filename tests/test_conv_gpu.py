@@ -229,6 +229,14 @@ def test_relu_bits_roundtrip(shape):
     assert rel(db_a, db_b) < 1e-5
 
 
+@pytest.mark.parametrize("shape", [(32, 32, 32, 512, 256), (32, 64, 64, 128, 64), (16, 16, 16, 1024, 512)], ids=str)
+def test_halve_m2_tiles_forced(shape, monkeypatch):
+    """Halving conv with 256-row tiles forced on (256x256 and 256x128 dgrad tiles, 256-row wgrad)."""
+    monkeypatch.setenv("ICE_CONV_M2", "1")
+    monkeypatch.setenv("ICE_WG_M2", "1")
+    test_halve_fprop_dgrad_wgrad(shape)
+
+
 @pytest.mark.parametrize("shape", [(3, 8, 16), (2, 5, 7), (1, 256, 256), (4, 33, 64)], ids=str)
 def test_stem_im2col(shape):
     """ice_stem_im2col: u8 NHWC RGB -> [px][64] bf16 rows of the 27 3x3x3 taps (/255, zero
