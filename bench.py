@@ -97,14 +97,14 @@ class ClockSampler:
 
 
 def _scene_chunk(args):
-    from paper_2403_13135_b200.icelabel import synth
+    from tests.fixtures import synth
     seed, count, haze, lo, hi = args
     flags = synth.haze_flags(seed, count, haze)
     return np.stack([synth.scene(seed, i, SIZE, bool(flags[i]))[0] for i in range(lo, hi)])
 
 
 def _scene512_chunk(args):
-    from paper_2403_13135_b200.icelabel import synth
+    from tests.fixtures import synth
     seed, count, haze, lo, hi = args
     flags = synth.haze_flags(seed, count, haze)
     out = [synth.scene(seed, i, 512, bool(flags[i])) for i in range(lo, hi)]
@@ -221,7 +221,7 @@ def cpu_reference_step_rate(batch: int, steps: int, warmup: int = 0):
     on the host cores: returns (images/s, threads, seconds)."""
     from oracle import unet_ref
     from paper_2403_13135_b200.icetrain import UNetSpec
-    from paper_2403_13135_b200.icelabel import synth
+    from tests.fixtures import synth
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
     spec = UNetSpec()

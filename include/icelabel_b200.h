@@ -4,7 +4,7 @@
  * One shared library (paper_2403_13135_b200/_C/libicelabel_b200.so, sm_100a only).
  * Conventions for every entry point:
  *   - all array arguments are DEVICE pointers owned by the caller; the library never
- *     allocates caller-visible memory;
+ *     allocates device memory (temporary space comes from caller-owned scratch, below);
  *   - work is enqueued asynchronously on `stream` (a cudaStream_t, NULL = legacy);
  *   - return 0 on success, a negative ICE_E* code for an argument error detected on
  *     the host before any launch, or a positive CUDA error code.
@@ -27,6 +27,21 @@ extern "C" {
 #define ICE_EWINDOW (-2)    /* window k exceeds tile extent (kernels.py:38-39)         */
 #define ICE_ETOOBIG (-3)    /* tile larger than the on-chip plane (256 x 256)         */
 #define ICE_ENODRIVER (-4)  /* cuTensorMapEncodeTiled entry point unavailable          */
+#define ICE_ESCRATCH (-5)   /* caller scratch smaller than the call needs              */
+
+/* Scratch.  Entry points with a (void *scratch, uint64_t *scratch_bytes) pair take their
+ * temporary device space from the caller (split-K partial slices, per-CTA / per-block partial
+ * sums of bias and head gradients, the merged halving-conv weights):
+ *   - scratch == NULL, scratch_bytes != NULL: size query -- *scratch_bytes = bytes this call
+ *     needs; nothing is launched, ICE_OK is returned (CUB-style two-phase call);
+ *   - scratch != NULL: *scratch_bytes is its capacity; a call that needs more returns
+ *     ICE_ESCRATCH before any launch;
+ *   - both NULL: only calls that need no scratch succeed.
+ * Calls sharing one scratch buffer must be ordered (same stream).
+ * Determinism: no fp32 value on the training path is accumulated with atomics.  Partial sums
+ * are stored into scratch and added by finishing kernels in a fixed order, so equal inputs
+ * give bit-identical gradients, losses and weights run to run (the reference's same-seed
+ * reproducibility, pkg/trainer/tests/test_train.py:71-75). */
 
 /* FilterConfig (icelabel/cloudfilter.py:23-66) as a POD. */
 typedef struct {
@@ -100,7 +115,8 @@ int ice_rgb_to_hsv(const uint8_t *rgb, int64_t npx, uint8_t *hsv, void *stream);
 int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2,
                    int32_t n, int32_t h, int32_t w, int32_t ksize, const uint16_t *wgt,
                    const float *bias, int32_t cout, int32_t relu, const float *drop_scale,
-                   uint16_t *y, uint32_t *relu_bits, void *stream);
+                   uint16_t *y, uint32_t *relu_bits, void *scratch, uint64_t *scratch_bytes,
+                   void *stream);
 
 /* Data gradient of ice_conv_fprop w.r.t. its input (autograd of model.py:68-69, 129).
  * dx is written split into dx1 (first c1 channels) and dx2 (last c2; may be NULL), each
@@ -118,13 +134,17 @@ int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32_t h, int32
                    uint16_t *dx1, const uint16_t *relu_ref1, const float *drop_scale1,
                    const uint16_t *add1, uint16_t *dx2, const uint16_t *relu_ref2,
                    const float *drop_scale2, const uint16_t *add2, int32_t dx2_planes,
-                   float *dbias1, float *dbias2, const uint32_t *relu_bits1, void *stream);
+                   float *dbias1, float *dbias2, const uint32_t *relu_bits1,
+                   void *scratch, uint64_t *scratch_bytes, void *stream);
 
 /* Weight gradient: dw[cout][ksize][ksize][c1 + c2] (fp32) += sum over pixels of
- * dy[p][cout] * x[p + tap][c].  dw must be zeroed by the caller before the first call. */
+ * dy[p][cout] * x[p + tap][c].  dw must be zeroed by the caller before the first call.
+ * When the pixel range is split across CTAs, each split's partial goes to scratch and the
+ * splits are added in split order. */
 int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2,
                    const uint16_t *dy, int32_t cout, int32_t n, int32_t h, int32_t w,
-                   int32_t ksize, float *dw, void *stream);
+                   int32_t ksize, float *dw, void *scratch, uint64_t *scratch_bytes,
+                   void *stream);
 
 /* Halving conv forward (model.py:79-88,105,128): y[n][2h][2w][cout] =
  * conv2x2(pad(upsample_nearest_2x(x), (0,1,0,1))) + bias, as four sub-pixel GEMMs over
@@ -132,19 +152,21 @@ int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c
  * ice_halve_prep builds from the 2x2 weights. */
 int ice_halve_fprop(const uint16_t *x, int32_t c, int32_t n, int32_t h, int32_t w,
                     const uint16_t *wc, const float *bias, int32_t cout, uint16_t *y,
-                    void *stream);
+                    void *scratch, uint64_t *scratch_bytes, void *stream);
 
 /* Halving conv data gradient: dx[n][h][w][c] = (sum over sub-pixel classes and taps of
  * dy_planes[cls][n][h - dy][w - dx][cout] * wc^T) * drop_scale[n][c] * [relu_ref > 0];
  * dbias (may be NULL) += column sums of dx (fused bias gradient). */
 int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t n, int32_t h, int32_t w,
                     const uint16_t *wc, int32_t c, uint16_t *dx, const uint16_t *relu_ref,
-                    const float *drop_scale, float *dbias, void *stream);
+                    const float *drop_scale, float *dbias, void *scratch,
+                    uint64_t *scratch_bytes, void *stream);
 
 /* Halving conv weight gradient: dw[cout][2][2][c] (fp32, caller-zeroed) +=
  * sum over classes/pixels of dy_planes[cls][p] (x) x[p + ((cy + a) / 2, (cx + b) / 2)]. */
 int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_planes, int32_t cout,
-                    int32_t n, int32_t h, int32_t w, float *dw, void *stream);
+                    int32_t n, int32_t h, int32_t w, float *dw, void *scratch,
+                    uint64_t *scratch_bytes, void *stream);
 
 /* ---- bandwidth-bound U-Net kernels (unet_ops.cu) ---------------------------------- */
 
@@ -175,7 +197,8 @@ int ice_maxpool_fwd(const uint16_t *x, int32_t n, int32_t h, int32_t w, int32_t 
  * dbias (fp32 [c], may be NULL) += sum of dz over pixels (fused bias gradient). */
 int ice_maxpool_bwd(const uint16_t *x, const uint16_t *dpool, const uint16_t *add,
                     const float *drop, int32_t n, int32_t h, int32_t w, int32_t c,
-                    uint16_t *dz, float *dbias, void *stream);
+                    uint16_t *dz, float *dbias, void *scratch, uint64_t *scratch_bytes,
+                    void *stream);
 
 /* Head (model.py:109,130 out = Conv2d(64, 3, 1)) + nn.CrossEntropyLoss (train.py:89,96).
  * h bf16 [npx][64] (hw pixels per image), labels u8 [npx], w_out fp32 [3][64], b_out [3].
@@ -187,10 +210,11 @@ int ice_maxpool_bwd(const uint16_t *x, const uint16_t *dpool, const uint16_t *ad
 int ice_head_ce(const uint16_t *h, int64_t npx, int32_t hw, const uint8_t *labels,
                 const float *w_out, const float *b_out, const float *drop, float grad_scale,
                 uint16_t *dz, float *dw, float *db, float *stats, float *logits, float *dzbias,
-                void *stream);
+                void *scratch, uint64_t *scratch_bytes, void *stream);
 
 /* Bias gradient: db[c] += sum_rows dz[row][c] (dz bf16 [rows][c], c % 8 == 0, c <= 2048). */
-int ice_bias_grad(const uint16_t *dz, int64_t rows, int32_t c, float *db, void *stream);
+int ice_bias_grad(const uint16_t *dz, int64_t rows, int32_t c, float *db, void *scratch,
+                  uint64_t *scratch_bytes, void *stream);
 
 /* Dropout2d multipliers (model.py:74-75): out[i] = (u_i >= p) / (1 - p), u from a
  * counter-based hash of (seed + f(*step_dev), i); step_dev (may be NULL) is the device step
@@ -246,6 +270,10 @@ int ice_head_argmax(const uint16_t *h, int64_t npx, const float *w_out, const fl
  * k <= 4; pixels with a label >= k are added to *bad instead. */
 int ice_confusion(const uint8_t *pred, const uint8_t *ref, int64_t npx, int32_t k, uint64_t *counts, uint64_t *bad,
                   void *stream);
+
+/* Number of kernels this library has launched in the process so far (host-side count kept
+ * at every launch site, finishing kernels included). */
+uint64_t ice_kernel_launches(void);
 
 #ifdef __cplusplus
 }

@@ -12,9 +12,9 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ICE_LIB_PATH") or os.path.join(_HERE, "_C", "libicelabel_b200.so")
 
-ICE_OK, ICE_EINVAL, ICE_EWINDOW, ICE_ETOOBIG, ICE_ENODRIVER = 0, -1, -2, -3, -4
+ICE_OK, ICE_EINVAL, ICE_EWINDOW, ICE_ETOOBIG, ICE_ENODRIVER, ICE_ESCRATCH = 0, -1, -2, -3, -4, -5
 _ERRNAMES = {ICE_EINVAL: "ICE_EINVAL", ICE_EWINDOW: "ICE_EWINDOW", ICE_ETOOBIG: "ICE_ETOOBIG",
-             ICE_ENODRIVER: "ICE_ENODRIVER"}
+             ICE_ENODRIVER: "ICE_ENODRIVER", ICE_ESCRATCH: "ICE_ESCRATCH"}
 
 
 class NativeError(RuntimeError):
@@ -40,6 +40,8 @@ _V = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
 _F32 = ctypes.c_float
+_U64P = ctypes.POINTER(ctypes.c_uint64)
+_S = [_V, _U64P]  # (scratch, scratch_bytes) before the stream: see include/icelabel_b200.h
 
 # name -> argtypes (restype is always int32).  Kept in sync with include/icelabel_b200.h;
 # tests/test_native_abi.py checks both directions.
@@ -55,27 +57,30 @@ SIGNATURES = {
     "ice_confusion": [_V, _V, _I64, _I32, _V, _V, _V],
     "ice_segment": [_V, _I64, _I32, _I32, ctypes.POINTER(IceScheme), _V, _V, _V, _V],
     "ice_rgb_to_hsv": [_V, _I64, _V, _V],
-    "ice_conv_fprop": [_V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, _V, _I32, _I32, _V, _V, _V, _V],
+    "ice_conv_fprop": [_V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, _V, _I32, _I32, _V, _V, _V, *_S, _V],
     "ice_conv_dgrad": [_V, _I32, _I32, _I32, _I32, _I32, _V, _I32, _I32, _V, _V, _V, _V, _V, _V, _V, _V, _I32,
-                       _V, _V, _V, _V],
-    "ice_halve_fprop": [_V, _I32, _I32, _I32, _I32, _V, _V, _I32, _V, _V],
-    "ice_halve_dgrad": [_V, _I32, _I32, _I32, _I32, _V, _I32, _V, _V, _V, _V, _V],
-    "ice_halve_wgrad": [_V, _I32, _V, _I32, _I32, _I32, _I32, _V, _V],
+                       _V, _V, _V, *_S, _V],
+    "ice_halve_fprop": [_V, _I32, _I32, _I32, _I32, _V, _V, _I32, _V, *_S, _V],
+    "ice_halve_dgrad": [_V, _I32, _I32, _I32, _I32, _V, _I32, _V, _V, _V, _V, *_S, _V],
+    "ice_halve_wgrad": [_V, _I32, _V, _I32, _I32, _I32, _I32, _V, *_S, _V],
     "ice_stem_im2col": [_V, _I32, _I32, _I32, _V, _V],
     "ice_stem_im2col_f32": [_V, _I32, _I32, _I32, _V, _V],
     "ice_pad_weights": [_V, _I32, _I32, _V, _I32, _V],
     "ice_halve_prep": [_V, _I32, _I32, _V, _V],
     "ice_maxpool_fwd": [_V, _I32, _I32, _I32, _I32, _V, _V],
-    "ice_maxpool_bwd": [_V, _V, _V, _V, _I32, _I32, _I32, _I32, _V, _V, _V],
-    "ice_head_ce": [_V, _I64, _I32, _V, _V, _V, _V, _F32, _V, _V, _V, _V, _V, _V, _V],
-    "ice_bias_grad": [_V, _I64, _I32, _V, _V],
+    "ice_maxpool_bwd": [_V, _V, _V, _V, _I32, _I32, _I32, _I32, _V, _V, *_S, _V],
+    "ice_head_ce": [_V, _I64, _I32, _V, _V, _V, _V, _F32, _V, _V, _V, _V, _V, _V, *_S, _V],
+    "ice_bias_grad": [_V, _I64, _I32, _V, *_S, _V],
     "ice_dropout_scale": [_I32, _F32, ctypes.c_uint64, _V, _V, _V],
     "ice_adam": [_V, _V, _V, _V, _I64, _I64, _V, _F32, _F32, _F32, _F32, _V, _V],
     "ice_counter_add": [_V, _I64, _V],
     "ice_cast_bf16": [_V, _I64, _V, _V],
     "ice_fill_f32": [_V, _I64, _F32, _V],
-    "ice_conv_wgrad": [_V, _I32, _V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, _V],
+    "ice_conv_wgrad": [_V, _I32, _V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, *_S, _V],
 }
+
+# entry points taking caller scratch; `call` supplies it (the call sites pass the other args)
+SCRATCH_FNS = frozenset(n for n, a in SIGNATURES.items() if len(a) >= 3 and a[-3:] == [*_S, _V])
 
 _lib = None
 
@@ -92,14 +97,67 @@ def load():
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = _I32
+        lib.ice_kernel_launches.argtypes = []
+        lib.ice_kernel_launches.restype = ctypes.c_uint64
         _lib = lib
     return _lib
 
 
+def kernel_launches() -> int:
+    """Kernels the library has launched in this process (counted at every launch site)."""
+    return int(load().ice_kernel_launches())
+
+
+class Scratch:
+    """Caller-owned device scratch for the entry points in SCRATCH_FNS (the library never
+    allocates): one uint8 buffer per (device, stream), grown on an eager call to the largest
+    size a call has asked for.  A buffer is never freed once replaced -- CUDA graphs captured
+    earlier keep pointing at it -- and growing inside a stream capture is an error (run the
+    step eagerly once first, as every warm-up does).  Sizes come from the library's own query
+    mode (scratch == NULL), cached per call shape."""
+
+    def __init__(self):
+        self.bufs = {}
+        self.retired = []
+        self.sizes = {}
+
+    def need(self, fn, name, core) -> int:
+        key = (name,) + tuple(bool(a) if t is _V else (a if t in (_I32, _I64) else None)
+                              for a, t in zip(core, SIGNATURES[name]))
+        n = self.sizes.get(key)
+        if n is None:
+            q = ctypes.c_uint64(0)
+            rc = fn(*core, None, ctypes.byref(q), None)
+            if rc != ICE_OK:
+                raise NativeError(name, rc)
+            n = self.sizes[key] = int(q.value)
+        return n
+
+    def get(self, stream_handle, nbytes: int):
+        import torch
+        dev = torch.cuda.current_device()
+        key = (dev, stream_handle)
+        buf = self.bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            if torch.cuda.is_current_stream_capturing():
+                raise RuntimeError(f"scratch must grow to {nbytes} B inside a CUDA-graph capture: "
+                                   "run the same step eagerly before capturing")
+            if buf is not None:
+                self.retired.append(buf)
+            size = max(nbytes, 2 * (buf.numel() if buf is not None else 0), 1 << 20)
+            buf = torch.empty(size, dtype=torch.uint8, device=dev)
+            self.bufs[key] = buf
+        return buf
+
+
+scratch = Scratch()
+
+
 class _Counter:
-    """Launch accounting: every ice_* entry point enqueues exactly one kernel.  When
-    `events` is a list, each call is bracketed by CUDA events on the current stream
-    (bench.py's per-kernel breakdown); otherwise only the count is kept."""
+    """Call accounting: `launches` counts ice_* entry-point calls (each enqueues one kernel,
+    plus a fixed-order finishing kernel where it reduces partial sums; kernel_launches() is
+    the library's own kernel count).  When `events` is a list, each call is bracketed by CUDA
+    events on the current stream (bench.py's per-entry-point breakdown)."""
     launches = 0
     events = None
 
@@ -114,7 +172,18 @@ def call(name: str, *args) -> None:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-    rc = getattr(load(), name)(*args)
+    fn = getattr(load(), name)
+    if name in SCRATCH_FNS:
+        core, stream = args[:-1], args[-1]
+        need = scratch.need(fn, name, core)
+        if need:
+            buf = scratch.get(stream, need)
+            cap = ctypes.c_uint64(buf.numel())
+            rc = fn(*core, buf.data_ptr(), ctypes.byref(cap), stream)
+        else:
+            rc = fn(*core, None, None, stream)
+    else:
+        rc = fn(*args)
     if rc != ICE_OK:
         raise NativeError(name, rc)
     counter.launches += 1

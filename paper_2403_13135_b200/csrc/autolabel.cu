@@ -20,6 +20,7 @@
 #include <stdint.h>
 
 #include "icelabel_b200.h"
+#include "reduce.cuh"
 
 #ifdef ICE_AL_PROF
 __device__ unsigned long long g_al_prof[16];
@@ -1669,6 +1670,7 @@ extern "C" int ice_autolabel(const uint8_t *rgb, int64_t n, int32_t h, int32_t w
         }
         fastk::autolabel256_kernel<<<(unsigned)n, fastk::NTF, sizeof(fastk::SmemF), (cudaStream_t)stream>>>(
             rgb, (int)n, n_sm, prm, filtered, label, mask, affected, counts, unmatched);
+        ice::count_launch();
         return (int)cudaGetLastError();
     }
     static bool attr_set = false;
@@ -1680,6 +1682,7 @@ extern "C" int ice_autolabel(const uint8_t *rgb, int64_t n, int32_t h, int32_t w
     }
     autolabel_kernel<<<(unsigned)n, NT, sizeof(Smem), (cudaStream_t)stream>>>(
         rgb, h, w, prm, filtered, label, mask, affected, counts, unmatched);
+    ice::count_launch();
     return (int)cudaGetLastError();
 }
 
@@ -1704,8 +1707,10 @@ extern "C" int ice_segment(const uint8_t *rgb, int64_t n, int32_t h, int32_t w,
         else if (nh && ns) segment_vec_kernel<true, true><<<(unsigned)n, SEG_VNT, 0, st>>>(rgb, npx, *scheme, label, counts, unmatched);
         else if (nh) segment_vec_kernel<true, false><<<(unsigned)n, SEG_VNT, 0, st>>>(rgb, npx, *scheme, label, counts, unmatched);
         else segment_vec_kernel<false, true><<<(unsigned)n, SEG_VNT, 0, st>>>(rgb, npx, *scheme, label, counts, unmatched);
+        ice::count_launch();
     } else {
         segment_kernel<<<(unsigned)n, SEG_NT, 0, st>>>(rgb, npx, *scheme, label, counts, unmatched);
+        ice::count_launch();
     }
     return (int)cudaGetLastError();
 }
@@ -1716,6 +1721,7 @@ extern "C" int ice_rgb_to_hsv(const uint8_t *rgb, int64_t npx, uint8_t *hsv, voi
     int64_t blocks = (npx + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
     hsv_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(rgb, npx, hsv);
+    ice::count_launch();
     return (int)cudaGetLastError();
 }
 

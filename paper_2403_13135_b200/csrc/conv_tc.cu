@@ -24,6 +24,7 @@
 #include <string.h>
 
 #include "icelabel_b200.h"
+#include "reduce.cuh"
 #include "tc_common.cuh"
 
 namespace {
@@ -196,7 +197,7 @@ struct FpropProb {
         }
     }
     template <int BN>
-    __device__ void flush_bias(int, int, int, float *) const {}
+    __device__ void flush_bias(int, int, int, float *, int) const {}
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *,
                              const Pre &pr, uint8_t *stage = nullptr, const uint8_t * = nullptr) const {
@@ -342,6 +343,8 @@ struct DgradProb {
     const uint32_t *rbits1;  // optional ReLU mask of dx1 as bits ([c1 / 32][N*H*W]); replaces ref1
     const float *drop1, *drop2;
     float *db1, *db2;  // fused bias gradients of the layers whose pre-activation grads these are
+    float *bpart;      // their per-CTA partial column sums (scratch), bslots rows per CTA
+    int bslots;
     CUtensorMap o1m;   // dx1 as (c1, W, H, N), box 32 ch x 32 px, SWIZZLE_64B (staged stores)
     int o1_tma;
 
@@ -396,22 +399,18 @@ struct DgradProb {
 
     // lane j of each epilogue warp keeps, per owned 32-column chunk, the running sum of
     // column j over all rows it has stored for the current column tile
+    // ... and at the end of its run over a column tile stores them (no atomics) as row
+    // (blockIdx.x, slot) of the partial matrix bpart[G * bslots][c1 + c2]; colsum_finish adds
+    // the rows in a fixed order (reduce.cuh)
     template <int BN>
-    __device__ void flush_bias(int nt, int cc0, int cc1, float *bacc) const {
+    __device__ void flush_bias(int nt, int cc0, int cc1, float *bacc, int slot) const {
         const int lane = threadIdx.x & 31;
         constexpr int NCH = BN / 32, PER = (NCH + 1) / 2;
+        float *row = bpart ? bpart + ((size_t)blockIdx.x * bslots + slot) * (size_t)(c1 + c2) : nullptr;
 #pragma unroll
         for (int ci = 0; ci < PER; ++ci) {
             const int cc = cc0 + ci;
-            if (cc < cc1) {
-                int col = nt * BN + cc * 32 + lane;
-                float *db = db1;
-                if (col >= c1) {
-                    col -= c1;
-                    db = db2;
-                }
-                if (db && bacc[ci] != 0.f) atomicAdd(db + col, bacc[ci]);
-            }
+            if (cc < cc1 && row) row[nt * BN + cc * 32 + lane] = bacc[ci];
             bacc[ci] = 0.f;
         }
     }
@@ -538,6 +537,8 @@ struct WgradProb {
     int trans;  // narrow cout (< 128): D = [(tap, cin)][cout], A = shifted x, B = dY (no wasted M rows)
     int nbx, nby;  // non-halve: maps are 5-D (64, W, H, N, C/64) and one TMA box carries nb 64-ch blocks
     float *dw;  // [cout][taps][c1+c2]
+    float *ws;  // split-K partials [splits][cout][taps][c1+c2] (scratch) when splits > 1
+    size_t wsize;
 
     __device__ void kb_range(int z, int &kb0, int &nkb) const {
         kb0 = z * kb_per_split;
@@ -605,27 +606,40 @@ struct WgradProb {
     template <int BN>
     __device__ void pre_load(Pre &, int, int, int, int, int, int) const {}
     template <int BN>
-    __device__ void flush_bias(int, int, int, float *) const {}
+    __device__ void flush_bias(int, int, int, float *, int) const {}
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *, const Pre &,
+    // one split: dw += tile (a single writer per element); several: the split's partial tile
+    // is stored into its own slice of ws and splitsum_finish adds the slices in split order
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *, const Pre &,
                              uint8_t * = nullptr, const uint8_t * = nullptr) const {
         const int m = mt * BM + row;
         const int ld = taps.n * (c1 + c2);
+        float *base = ws ? ws + (size_t)z * wsize : dw;
 #pragma unroll 1
         for (int cc = cc0; cc < cc1; ++cc) {
             float v[32];
             tc::tmem_ld32(tmem + cc * 32, v);
             if (!trans) {
                 if (m >= cout) continue;
-                float *dst = dw + (size_t)m * ld + nt * BN + cc * 32;
+                float *dst = base + (size_t)m * ld + nt * BN + cc * 32;
+                if (ws) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) tc::red_add_v4(dst + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    for (int q = 0; q < 8; ++q)
+                        __stcg(reinterpret_cast<float4 *>(dst) + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) tc::red_add_v4(dst + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                }
             } else {
                 if (m >= ld) continue;
                 const int o0 = nt * BN + cc * 32;  // output channels; lanes hold consecutive (tap, cin)
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (o0 + j < cout) atomicAdd(dw + (size_t)(o0 + j) * ld + m, v[j]);
+                for (int j = 0; j < 32; ++j) {
+                    if (o0 + j >= cout) continue;
+                    float *dst = base + (size_t)(o0 + j) * ld + m;
+                    if (ws) __stcg(dst, v[j]);
+                    else *dst += v[j];
+                }
             }
         }
     }
@@ -635,15 +649,16 @@ struct WgradProb {
 // ------------------------------------------------------------------------------------
 // Split-K wrapper for fprop / dgrad problems whose (M, N) tile grid is smaller than one wave
 // of SMs (the 8 x 8 and 16 x 16 U-Net levels at batch 32: 16-64 M tiles).  Split z covers
-// K-blocks [z kps, (z+1) kps); the epilogue red.adds the fp32 partial tile into a row-major
-// [pixel][column] workspace, and a finishing kernel (split_finish_*) applies the problem's
-// own epilogue (bias / ReLU / Dropout2d, or gradient-sum / ReLU-backward / split / planes /
-// bias gradient) and re-zeroes the workspace.
+// K-blocks [z kps, (z+1) kps); the epilogue stores the fp32 partial tile into slice z of a
+// row-major [split][pixel][column] scratch buffer, and a finishing kernel (split_finish_*)
+// adds the slices in split order (deterministic) and applies the problem's own epilogue
+// (bias / ReLU / Dropout2d, or gradient-sum / ReLU-backward / split / planes / bias gradient).
 template <class P>
 struct SplitK {
     static constexpr bool A_MN = P::A_MN, B_MN = P::B_MN;
     P p;
     float *ws;
+    size_t zstride;  // floats per split slice (pixels x ld)
     int ld, kps, total_kb;
     __device__ void kb_range(int z, int &kb0, int &nkb) const {
         kb0 = z * kps;
@@ -658,15 +673,15 @@ struct SplitK {
     template <int BN>
     __device__ void pre_load(Pre &, int, int, int, int, int, int) const {}
     template <int BN>
-    __device__ void flush_bias(int, int, int, float *) const {}
+    __device__ void flush_bias(int, int, int, float *, int) const {}
     template <int BN>
-    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *, const Pre &,
+    __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *, const Pre &,
                              uint8_t * = nullptr, const uint8_t * = nullptr) const {
         int n0, h0, w0, n, h, w;
         p.pt.origin(mt, n0, h0, w0);
         p.pt.pixel(row, n0, h0, w0, n, h, w);
         const bool valid = n < p.N;
-        float *dst = ws + (((size_t)n * p.H + h) * p.W + w) * ld + nt * BN;
+        float *dst = ws + (size_t)z * zstride + (((size_t)n * p.H + h) * p.W + w) * ld + nt * BN;
 #pragma unroll 1
         for (int cc = cc0; cc < cc1; ++cc) {
             float v[32];
@@ -674,24 +689,36 @@ struct SplitK {
             if (!valid) continue;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-                tc::red_add_v4(dst + cc * 32 + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                __stcg(reinterpret_cast<float4 *>(dst + cc * 32) + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
         }
     }
 };
 
-// y = act(ws + bias) * drop, bf16; ws re-zeroed.  One thread per 8 columns of one pixel.
-__global__ void split_finish_fprop(float *__restrict__ ws, long long npx, int hw, int cout, const float *__restrict__ bias,
-                                   const float *__restrict__ drop, int relu, bf16 *__restrict__ y) {
+// sum of the nsplit partial slices of 8 consecutive floats, in split order
+__device__ __forceinline__ void split_sum8(const float *ws, int nsplit, size_t zstride, size_t off, float (&v)[8]) {
+    const float4 *s0 = reinterpret_cast<const float4 *>(ws + off);
+    float4 a = __ldcg(s0), b = __ldcg(s0 + 1);
+    for (int z = 1; z < nsplit; ++z) {
+        const float4 *sz = reinterpret_cast<const float4 *>(ws + z * zstride + off);
+        const float4 c = __ldcg(sz), d = __ldcg(sz + 1);
+        a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+        b.x += d.x; b.y += d.y; b.z += d.z; b.w += d.w;
+    }
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// y = act(sum_z ws[z] + bias) * drop, bf16.  One thread per 8 columns of one pixel.
+__global__ void split_finish_fprop(const float *__restrict__ ws, int nsplit, long long npx, int hw, int cout,
+                                   const float *__restrict__ bias, const float *__restrict__ drop, int relu,
+                                   bf16 *__restrict__ y) {
     const int groups = cout / 8;
     const long long total = npx * groups;
+    const size_t zstride = (size_t)npx * cout;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
         const long long px = i / groups;
         const int col = (int)(i - px * groups) * 8;
-        float4 *src = reinterpret_cast<float4 *>(ws + px * cout + col);
-        const float4 a = src[0], b = src[1];
-        src[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-        src[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}, bq[8], dq[8];
+        float v[8], bq[8], dq[8];
+        split_sum8(ws, nsplit, zstride, (size_t)px * cout + col, v);
         ld8(bias ? bias + col : nullptr, 0.f, bq);
         ld8(drop ? drop + (px / hw) * cout + col : nullptr, 1.f, dq);
         uint32_t pk[4];
@@ -708,12 +735,13 @@ __global__ void split_finish_fprop(float *__restrict__ ws, long long npx, int hw
     }
 }
 
-// dgrad finish: the DgradProb epilogue on the reduced sums.  Block = 256 columns (32
+// dgrad finish: the DgradProb epilogue on the split-ordered sums.  Block = 256 columns (32
 // column groups of 8, one per lane) x FIN_STRIP pixels (8 warps, interleaved rows); the bias
-// gradient column sums reduce through shared memory, one atomic per column per block.
+// gradient column sums reduce through shared memory into row `strip` of p.bpart ([strips][ct]),
+// which colsum_finish adds in strip order.
 constexpr int FIN_STRIP = 64;
-__global__ void __launch_bounds__(256) split_finish_dgrad(float *__restrict__ ws, int npx, int N, int H, int W,
-                                                          DgradProb p) {
+__global__ void __launch_bounds__(256) split_finish_dgrad(const float *__restrict__ ws, int nsplit, int npx, int N,
+                                                          int H, int W, DgradProb p) {
     __shared__ float red[8][32][9];
     const int ct = p.c1 + p.c2, cblocks = ct / 256;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -736,12 +764,9 @@ __global__ void __launch_bounds__(256) split_finish_dgrad(float *__restrict__ ws
     float dsum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const int px0 = strip * FIN_STRIP, px1 = min(npx, px0 + FIN_STRIP);
     for (int px = px0 + wid; px < px1; px += 8) {
-        float4 *src = reinterpret_cast<float4 *>(ws + (size_t)px * ct + cg * 8);
-        const float4 a = src[0], b = src[1];
-        src[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-        src[1] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (!out) continue;
-        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        float v[8];
+        split_sum8(ws, nsplit, (size_t)npx * ct, (size_t)px * ct + cg * 8, v);
         const int n = px / (H * W), hw = px - n * H * W, h = hw / W, w = hw - h * W;
         size_t pix = (size_t)px;
         if (second && p.planes_out2)
@@ -785,8 +810,7 @@ __global__ void __launch_bounds__(256) split_finish_dgrad(float *__restrict__ ws
     float t = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) t += red[k][g][e];
-    const int gcol = (cb * 32 + g) * 8 + e - (second ? p.c1 : 0);
-    atomicAdd(db + gcol, t);
+    p.bpart[(size_t)strip * ct + (cb * 32 + g) * 8 + e] = t;
 }
 
 template <int BN, int STAGES>
@@ -922,7 +946,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
             int mt, nt, z;
             g.coords(t, mt, nt, z);
             if (nt != cur_nt) {
-                if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
+                if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc, sub);
                 cur_nt = nt;
             }
             const typename P::Pre cur = pre;
@@ -940,7 +964,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
-        if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
+        if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc, sub);
         if (lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
     }
     tc::tc_fence_before();
@@ -1056,8 +1080,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
             g.coords(t, mt, nt, z);
             if (nt != cur_nt) {
                 if (cur_nt >= 0) {
-                    p.template flush_bias<BN>(cur_nt, 0, PER, bacc0);
-                    p.template flush_bias<BN>(cur_nt, PER, NCH, bacc1);
+                    p.template flush_bias<BN>(cur_nt, 0, PER, bacc0, half * 4 + sub);
+                    p.template flush_bias<BN>(cur_nt, PER, NCH, bacc1, half * 4 + sub);
                 }
                 cur_nt = nt;
             }
@@ -1075,8 +1099,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
         if (cur_nt >= 0) {
-            p.template flush_bias<BN>(cur_nt, 0, PER, bacc0);
-            p.template flush_bias<BN>(cur_nt, PER, NCH, bacc1);
+            p.template flush_bias<BN>(cur_nt, 0, PER, bacc0, half * 4 + sub);
+            p.template flush_bias<BN>(cur_nt, PER, NCH, bacc1, half * 4 + sub);
         }
         if (lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
     }
@@ -1320,7 +1344,7 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
             int mt, nt, z;
             g.coords(t, mt, nt, z);
             if (nt != cur_nt) {
-                if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
+                if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc, sub);
                 cur_nt = nt;
             }
             const typename P::Pre cur = pre;
@@ -1346,7 +1370,7 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
                 if (REFS && stage_ref) tc::mbar_arrive(&rempty[acc]);
             }
         }
-        if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc);
+        if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc, sub);
         if (STAGE && lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
     }
     tc::tc_fence_before();
@@ -1369,6 +1393,8 @@ struct HWgrad {
     int N, H, W, ct, cout, nchx;
     int total_kb, kb_per_split, groups, G, total_mt;
     float *dw;  // [cout][9][ct]
+    float *ws;  // split partials [splits][cout][9][ct] (scratch) when there are several splits
+    size_t wsize;
 };
 
 // HALVE variant (2x2 halving conv, model.py:79-88): dW[(a,b), c] accumulates, for each of
@@ -1512,8 +1538,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
         const int ld = G::TAPS * p.ct;
         int local = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
-            const int grp = u % p.groups;
+            const int grp = u % p.groups, split = u / p.groups;
             const int mt0 = grp * p.G, mt1 = min(p.total_mt, mt0 + p.G);
+            float *base = p.ws ? p.ws + (size_t)split * p.wsize : p.dw;
             tc::mbar_wait(tfull, local & 1);
             tc::tc_fence_after();
             for (int mt = mt0; mt < mt1; ++mt) {
@@ -1528,14 +1555,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                 const int b = 2 * mt + second;
                 const bool valid = b < NBLK && !(second == 1 && b1 == b0);
                 const int tap = b / NCH, c = (b % NCH) * 64 + (r & 63);
-                float *dst = p.dw + (size_t)tap * p.ct + c;
+                // one split: dw += (single writer); several: store the split's slice of ws
+                // (lanes hold consecutive channels: 128-B coalesced stores), summed in split
+                // order by splitsum_finish
+                float *dst = base + (size_t)tap * p.ct + c;
 #pragma unroll
                 for (int cc = half * PER; cc < min(NCC, (half + 1) * PER); ++cc) {
                     float v[32];
                     tc::tmem_ld32(tmem + (mt - mt0) * COUT + cc * 32 + ((uint32_t)(sub * 32) << 16), v);
                     if (!valid) continue;
+                    if (p.ws) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) atomicAdd(dst + (size_t)(cc * 32 + j) * ld, v[j]);
+                        for (int j = 0; j < 32; ++j) __stcg(dst + (size_t)(cc * 32 + j) * ld, v[j]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) dst[(size_t)(cc * 32 + j) * ld] += v[j];
+                    }
                 }
             }
             tc::tc_fence_before();
@@ -1701,6 +1736,49 @@ const int8_t HALVE_CLS[9] = {0, 1, 1, 2, 2, 3, 3, 3, 3};
 const int8_t HALVE_DY[9] = {0, 0, 0, 0, 1, 0, 0, 1, 1};
 const int8_t HALVE_DX[9] = {0, 0, 1, 0, 0, 0, 1, 0, 1};
 
+// A/B switches of the tiling heuristics (test / tuning hooks), read once when the library is
+// first used; the defaults are the measured-best choices.
+struct Knobs {
+    bool no_dual, no_stage, no_splitk, no_wgrad_trans256, no_ref_tma, no_halo_wgrad, no_halve_merge;
+    int conv_m2, wg_m2;  // -1 = automatic, 0 / 1 forced
+};
+const Knobs &knobs() {
+    static const Knobs k = [] {
+        auto flag = [](const char *n) { return getenv(n) != nullptr; };
+        auto tri = [](const char *n) {
+            const char *e = getenv(n);
+            return e ? (atoi(e) != 0 ? 1 : 0) : -1;
+        };
+        Knobs r;
+        r.no_dual = flag("ICE_NO_DUAL");
+        r.no_stage = flag("ICE_NO_STAGE");
+        r.no_splitk = flag("ICE_NO_SPLITK");
+        r.no_wgrad_trans256 = flag("ICE_NO_WGRAD_TRANS256");
+        r.no_ref_tma = flag("ICE_NO_REF_TMA");
+        r.no_halo_wgrad = flag("ICE_NO_HALO_WGRAD");
+        r.no_halve_merge = flag("ICE_NO_HALVE_MERGE");
+        r.conv_m2 = tri("ICE_CONV_M2");
+        r.wg_m2 = tri("ICE_WG_M2");
+        return r;
+    }();
+    return k;
+}
+
+// (settle the scratch arena: answer a size query or reject a too-small buffer before any launch)
+#define ICE_SETTLE(ar)                                           \
+    do {                                                         \
+        const int q_ = (ar).settle(scratch_bytes);               \
+        if (q_) return q_ > 0 ? ICE_OK : ICE_ESCRATCH;           \
+    } while (0)
+
+int persist_grid(long long total) { return (int)(total < num_sms() ? total : num_sms()); }
+
+// The persistent schedule a launch used (for the bias-gradient finisher's row validity).
+ice::RowSched sched(dim3 tiles, int bn, int slots) {
+    const long long total = (long long)tiles.x * tiles.y * tiles.z;
+    return ice::RowSched{persist_grid(total), slots, (int)tiles.x, (int)total, bn};
+}
+
 template <int BN, int BSTAGES, bool RES, class P, bool DUAL = false>
 int launch_halo(const P &p, dim3 tiles, cudaStream_t st) {
     constexpr int smem = halo_smem_bytes<BN, BSTAGES, RES>(P::STAGE_REF);
@@ -1714,8 +1792,8 @@ int launch_halo(const P &p, dim3 tiles, cudaStream_t st) {
     }
     const TileGrid g = tile_grid(tiles);
     const long long total = (long long)tiles.x * tiles.y * tiles.z;
-    const int grid = (int)(total < num_sms() ? total : num_sms());
-    halo_gemm<BN, BSTAGES, RES, P, DUAL><<<grid, NTHREADS + (DUAL ? 32 : 0), smem, st>>>(p, g);
+    halo_gemm<BN, BSTAGES, RES, P, DUAL><<<persist_grid(total), NTHREADS + (DUAL ? 32 : 0), smem, st>>>(p, g);
+    ice::count_launch();
     return (int)cudaGetLastError();
 }
 
@@ -1724,20 +1802,27 @@ int launch_halo(const P &p, dim3 tiles, cudaStream_t st) {
 // 64-column problem keeps its 9 weight taps resident instead.
 int halo_bn(int nch, int ncols) { return ncols % 128 == 0 ? 128 : 64; }
 
-// halo-path dispatch
+struct HaloPlan {
+    int kind;  // 0: BN 64, resident weights (dual issuers when ncols == 64); 1: BN 128; 2: BN 64 streamed
+    int bn;
+    dim3 tiles;
+};
+HaloPlan halo_plan(int nch, int ncols, unsigned mtiles) {
+    HaloPlan h;
+    h.bn = halo_bn(nch, ncols);
+    h.kind = (h.bn == 64 && nch == 1) ? 0 : (h.bn == 128 ? 1 : 2);
+    h.tiles = dim3(mtiles, ncols / h.bn, 1);
+    return h;
+}
+
 template <class P>
-int run_halo(const P &p, int nch, int ncols, dim3 tiles_m, cudaStream_t st) {
-    if (halo_bn(nch, ncols) == 64 && nch == 1) {  // all 9 weight taps resident
-        dim3 tiles(tiles_m.x, ncols / 64, 1);
-        if (ncols == 64 && !getenv("ICE_NO_DUAL")) return launch_halo<64, 1, true, P, true>(p, tiles, st);
-        return launch_halo<64, 1, true>(p, tiles, st);
+int run_halo(const P &p, const HaloPlan &h, int ncols, cudaStream_t st) {
+    if (h.kind == 0) {
+        if (ncols == 64 && !knobs().no_dual) return launch_halo<64, 1, true, P, true>(p, h.tiles, st);
+        return launch_halo<64, 1, true>(p, h.tiles, st);
     }
-    if (halo_bn(nch, ncols) == 128) {  // N = 128 halves the smem bytes per MMA FLOP
-        dim3 tiles(tiles_m.x, ncols / 128, 1);
-        return launch_halo<128, 2, false>(p, tiles, st);
-    }
-    dim3 tiles(tiles_m.x, ncols / 64, 1);
-    return launch_halo<64, 5, false>(p, tiles, st);
+    if (h.kind == 1) return launch_halo<128, 2, false>(p, h.tiles, st);
+    return launch_halo<64, 5, false>(p, h.tiles, st);
 }
 
 bool use_halo(int ksize, int w) { return ksize == 3 && w >= 128 && w % 128 == 0; }
@@ -1752,9 +1837,8 @@ int launch(const P &p, dim3 tiles, cudaStream_t st) {
         attr = true;
     }
     const TileGrid g = tile_grid(tiles);
-    const long long total = (long long)tiles.x * tiles.y * tiles.z;
-    const int grid = (int)(total < num_sms() ? total : num_sms());
-    conv_gemm<BN, STAGES, P><<<grid, NTHREADS, smem, st>>>(p, g);
+    conv_gemm<BN, STAGES, P><<<persist_grid((long long)tiles.x * tiles.y * tiles.z), NTHREADS, smem, st>>>(p, g);
+    ice::count_launch();
     return (int)cudaGetLastError();
 }
 
@@ -1768,10 +1852,21 @@ int launch_m2(const P &p, dim3 tiles, cudaStream_t st) {
         attr = true;
     }
     const TileGrid g = tile_grid(tiles);
-    const long long total = (long long)tiles.x * tiles.y * tiles.z;
-    const int grid = (int)(total < num_sms() ? total : num_sms());
-    conv_gemm_m2<BN, STAGES, P><<<grid, NTHREADS, smem, st>>>(p, g);
+    conv_gemm_m2<BN, STAGES, P><<<persist_grid((long long)tiles.x * tiles.y * tiles.z), NTHREADS, smem, st>>>(p, g);
+    ice::count_launch();
     return (int)cudaGetLastError();
+}
+
+// one-column-tile-width dispatch of the 128-row kernel
+template <class P>
+int launch_bn(const P &p, int bn, dim3 tiles, cudaStream_t st) {
+    if (bn == 256) return launch<256, 4>(p, tiles, st);
+    if (bn == 128) return launch<128, 6>(p, tiles, st);
+    return launch<64, 8>(p, tiles, st);
+}
+template <class P>
+int launch_bn_m2(const P &p, int bn, dim3 tiles, cudaStream_t st) {
+    return bn == 256 ? launch_m2<256, 3>(p, tiles, st) : launch_m2<128, 4>(p, tiles, st);
 }
 
 int pick_bn(int ntot, long long m_tiles) {
@@ -1790,7 +1885,7 @@ bool shape_ok(int N, int H, int W) { return N > 0 && pow2(H) && pow2(W); }
 // fprop / dgrad tiling for the non-halo path.  N = 256 tiles run at ~95% of the MMA peak,
 // N = 128 tiles at ~60% (their A + B operand stream per FLOP is 1.5x larger and becomes
 // L2-bound), so 256-wide tiles are kept even when they give fewer tiles than SMs; below
-// 80% of a wave the K range is split (fp32 workspace + split_finish_*).
+// 80% of a wave the K range is split (fp32 partial slices + split_finish_*).
 void pick_tiling(int ntot, long long m_tiles, int &bn, int &splits, int total_kb) {
     splits = 1;
     if (ntot % 256) {
@@ -1810,34 +1905,21 @@ void pick_tiling(int ntot, long long m_tiles, int &bn, int &splits, int total_kb
     }
 }
 
-// Split-K workspace: one fp32 [pixels][columns] buffer per process, grown on an eager call
-// (never inside stream capture), kept zeroed by the finishing kernels.  A grown buffer never
-// frees its predecessor: CUDA graphs captured earlier keep pointing at it.  Calls that split
-// must not run concurrently on different streams (the U-Net issues convs on one stream).
-float *split_workspace(size_t bytes, cudaStream_t st) {
-    static float *ws = nullptr;
-    static size_t cap = 0;
-    if (bytes <= cap) return ws;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-    size_t want = bytes < ((size_t)32 << 20) ? ((size_t)32 << 20) : 2 * bytes;
-    float *fresh = nullptr;
-    if (cudaMalloc(&fresh, want) != cudaSuccess) return nullptr;
-    if (cudaMemsetAsync(fresh, 0, want, st) != cudaSuccess) return nullptr;
-    ws = fresh;  // the previous buffer stays allocated (referenced by captured graphs)
-    cap = want;
-    return ws;
+// K-blocks per split and the number of non-empty splits it gives
+void split_shape(int total_kb, int splits, int &kps, int &z) {
+    kps = (total_kb + splits - 1) / splits;
+    z = (total_kb + kps - 1) / kps;
 }
 
 template <class P>
-int launch_split(const P &p, long long mtiles, int ncols, int total_kb, int splits, cudaStream_t st, float *ws) {
+int launch_split(const P &p, long long mtiles, int ncols, int total_kb, int kps, int z, float *ws, cudaStream_t st) {
     SplitK<P> q;
     q.p = p;
     q.ws = ws;
     q.ld = ncols;
-    q.kps = (total_kb + splits - 1) / splits;
+    q.kps = kps;
     q.total_kb = total_kb;
-    const int z = (total_kb + q.kps - 1) / q.kps;
+    q.zstride = (size_t)p.N * p.H * p.W * ncols;
     return launch<256, 4>(q, dim3((unsigned)mtiles, ncols / 256, (unsigned)z), st);
 }
 
@@ -1847,7 +1929,7 @@ void wgrad_tiles(int ncols, int cout, int &trans, int &mtiles, int &ntiles, int 
     trans = cout < BM;
     // 256-wide tiles only exist along the dimension divisible by 256: for (tap, cin) widths like
     // 9 x 128 = 1152 with cout % 256 == 0, the transposed GEMM gets N = cout in 256-wide tiles
-    if (!trans && ncols % 256 && cout % 256 == 0 && !getenv("ICE_NO_WGRAD_TRANS256")) {
+    if (!trans && ncols % 256 && cout % 256 == 0 && !knobs().no_wgrad_trans256) {
         trans = 1;
         mtiles = (ncols + BM - 1) / BM;
         bn = 256;
@@ -1871,8 +1953,7 @@ void wgrad_tiles(int ncols, int cout, int &trans, int &mtiles, int &ntiles, int 
 // otherwise (short K exposes the drain; 64x64 levels drop from 99% to 87% wave fill).
 bool conv_m2(long long mtiles, int ncols, int bn, int splits, int total_kb) {
     if ((bn != 256 && bn != 128) || splits != 1 || mtiles % 2) return false;
-    const char *e = getenv("ICE_CONV_M2");
-    if (e) return atoi(e) != 0;
+    if (knobs().conv_m2 >= 0) return knobs().conv_m2 != 0;
     const long long sms = num_sms(), t1 = mtiles * (ncols / bn), t2 = t1 / 2;
     if (t2 * 5 < sms * 4) return false;
     if (bn == 128) return true;  // double-buffered accumulators: no exposed drain
@@ -1884,15 +1965,14 @@ bool conv_m2(long long mtiles, int ncols, int bn, int splits, int total_kb) {
 
 // 256-row weight-gradient tiles (conv_gemm_m2) when the M extent pairs up
 bool wgrad_m2(int mtiles, int bn, int total_kb) {
-    const char *e = getenv("ICE_WG_M2");
     if (bn != 256 || mtiles % 2) return false;
     (void)total_kb;  // measured faster at every wgrad shape of the model, 32 K-blocks included
-    return !e || atoi(e) != 0;
+    return knobs().wg_m2 != 0;
 }
 
 // K-blocks per split.  The persistent grid runs ceil(units / SMs) rounds of equal-size
 // units (units = tiles * splits), so pick the split count whose last round is fullest
-// (>= 4 K-blocks per split); fewer splits (fewer fp32 atomics) win ties.
+// (>= 4 K-blocks per split); fewer splits (less partial-slice traffic) win ties.
 int split_k(int total_kb, long long tiles) {
     const long long sms = num_sms();
     int best = 1;
@@ -1914,7 +1994,6 @@ int split_k(int total_kb, long long tiles) {
     return (total_kb + best - 1) / best;
 }
 
-
 bool map_halo_box(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, int c0, int cols, int rows) {
     // halo box (64 ch, cols px, rows rows, 1 image) starting at channel c0 of a C-channel NHWC tensor
     const char *base = reinterpret_cast<const char *>(ptr) + (size_t)c0 * 2;
@@ -1928,7 +2007,7 @@ bool map_halo_box(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, i
 }
 
 template <int COUT, int NCH, int STAGES, bool HALVE>
-int launch_hwgrad(HWgrad &p, cudaStream_t st) {
+int launch_hwgrad(const HWgrad &p, int grid, cudaStream_t st) {
     constexpr int smem = hw_smem_bytes<COUT, NCH, STAGES, HALVE>();
     static_assert(smem <= 232448, "hwgrad smem");
     static bool attr = false;
@@ -1938,21 +2017,16 @@ int launch_hwgrad(HWgrad &p, cudaStream_t st) {
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }
-    p.total_mt = (HWGeom<HALVE>::TAPS * NCH + 1) / 2;
-    const int gmax = 512 / COUT;
-    p.groups = (p.total_mt + gmax - 1) / gmax;
-    p.G = (p.total_mt + p.groups - 1) / p.groups;
-    p.kb_per_split = split_k(p.total_kb, p.groups);
-    const long long units = (long long)p.groups * ((p.total_kb + p.kb_per_split - 1) / p.kb_per_split);
-    const int grid = (int)(units < num_sms() ? units : num_sms());
     hwgrad_kernel<COUT, NCH, STAGES, HALVE><<<grid, NTHREADS, smem, st>>>(p);
+    ice::count_launch();
     return (int)cudaGetLastError();
 }
 
 // halo weight-gradient path: 3x3 (or the 2x2 halving conv with HALVE), W % 64 == 0,
-// cout in {64, 128}, cin / 64 in {1, 2}.  Returns 1 when not applicable.
+// cout in {64, 128}, cin / 64 in {1, 2}.  Returns 1 when not applicable (nothing taken from
+// the arena, nothing launched).
 int try_hwgrad(const uint16_t *x1, int c1, const uint16_t *x2, int c2, const uint16_t *dy, int cout, int n, int h,
-               int w, float *dw, cudaStream_t st, bool halve = false) {
+               int w, float *dw, ice::Arena &ar, uint64_t *scratch_bytes, cudaStream_t st, bool halve = false) {
     const int nch = (c1 + c2) / 64;
     if (w % 64 || w < 64 || (cout != 64 && cout != 128) || (nch != 1 && nch != 2)) return 1;
     if (halve && cout != 64) return 1;
@@ -1969,11 +2043,65 @@ int try_hwgrad(const uint16_t *x1, int c1, const uint16_t *x2, int c2, const uin
     }
     PixTile seg{64, 1, 1, w / 64, h, (halve ? 4 : 1) * n};
     if (!map_act_nb(&p.dym, dy, (halve ? 4 : 1) * n, h, w, cout, seg, cout / 64)) return ICE_EINVAL;
-    if (halve) return nch == 1 ? launch_hwgrad<64, 1, 3, true>(p, st) : launch_hwgrad<64, 2, 3, true>(p, st);
-    if (cout == 64 && nch == 1) return launch_hwgrad<64, 1, 6, false>(p, st);
-    if (cout == 64) return launch_hwgrad<64, 2, 3, false>(p, st);
-    if (nch == 1) return launch_hwgrad<128, 1, 5, false>(p, st);
-    return launch_hwgrad<128, 2, 3, false>(p, st);
+    // work split: M tile groups (G x cout <= 512 TMEM columns) x pixel splits
+    p.total_mt = ((halve ? 4 : 9) * nch + 1) / 2;
+    const int gmax = 512 / cout;
+    p.groups = (p.total_mt + gmax - 1) / gmax;
+    p.G = (p.total_mt + p.groups - 1) / p.groups;
+    p.kb_per_split = split_k(p.total_kb, p.groups);
+    const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
+    const long long units = (long long)p.groups * splits;
+    p.wsize = (size_t)cout * (halve ? 4 : 9) * p.ct;
+    if (splits > 1) p.ws = ar.take<float>((size_t)splits * p.wsize * 4);
+    ICE_SETTLE(ar);
+    const int grid = persist_grid(units);
+    int rc;
+    if (halve) rc = nch == 1 ? launch_hwgrad<64, 1, 3, true>(p, grid, st) : launch_hwgrad<64, 2, 3, true>(p, grid, st);
+    else if (cout == 64 && nch == 1) rc = launch_hwgrad<64, 1, 6, false>(p, grid, st);
+    else if (cout == 64) rc = launch_hwgrad<64, 2, 3, false>(p, grid, st);
+    else if (nch == 1) rc = launch_hwgrad<128, 1, 5, false>(p, grid, st);
+    else rc = launch_hwgrad<128, 2, 3, false>(p, grid, st);
+    if (rc || splits == 1) return rc;
+    return ice::splitsum_finish(p.ws, splits, p.wsize, p.wsize, dw, st);
+}
+
+// The non-halo weight gradient (WgradProb on conv_gemm / conv_gemm_m2), split over pixels
+// when the tile grid is below a wave: partial slices in scratch + splitsum_finish.
+int run_wgrad(WgradProb &p, int ncols, int mtiles, int ntiles, int bn, bool m2, ice::Arena &ar,
+              uint64_t *scratch_bytes, cudaStream_t st) {
+    const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
+    p.wsize = (size_t)p.cout * ncols;
+    p.ws = splits > 1 ? ar.take<float>((size_t)splits * p.wsize * 4) : nullptr;
+    ICE_SETTLE(ar);
+    dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
+    const int rc = m2 ? launch_m2<256, 3>(p, grid, st) : launch_bn(p, bn, grid, st);
+    if (rc || splits == 1) return rc;
+    return ice::splitsum_finish(p.ws, splits, p.wsize, p.wsize, p.dw, st);
+}
+
+// channel blocks per TMA box: as many consecutive 64-blocks as the tile reads from one
+// (tap, source) run; the M operand supplies 2 blocks (4 for 256-row tiles), B BN/64
+void wgrad_boxes(WgradProb &p, bool m2, int bn) {
+    const int mb = m2 ? 4 : 2;
+    const int want_x = p.trans ? mb : bn / 64, want_y = p.trans ? bn / 64 : mb;
+    int nbx = want_x;
+    while (nbx > 1 && ((p.c1 % (64 * nbx)) || (p.c2 % (64 * nbx)))) nbx >>= 1;
+    int nby = want_y;
+    while (nby > 1 && (p.cout % (64 * nby))) nby >>= 1;
+    p.nbx = nbx;
+    p.nby = nby;
+}
+
+// dgrad bias gradients: rows of per-CTA partial column sums taken from the arena
+void take_bias_rows(DgradProb &p, const ice::RowSched &s, ice::Arena &ar) {
+    if (!p.db1 && !p.db2) return;
+    p.bslots = s.slots;
+    p.bpart = ar.take<float>((size_t)s.G * s.slots * (p.c1 + p.c2) * 4);
+}
+int finish_bias(const DgradProb &p, const ice::RowSched &s, cudaStream_t st) {
+    if (!p.db1 && !p.db2) return 0;
+    const ice::ColSegs segs{{p.db1, p.db2, nullptr, nullptr}, {p.c1, p.c2, 0, 0}};
+    return ice::colsum_finish(p.bpart, s.G * s.slots, p.c1 + p.c2, p.c1 + p.c2, segs, s, st);
 }
 }  // namespace
 
@@ -1991,21 +2119,8 @@ __global__ void halve_merge_kernel(const uint16_t *__restrict__ wc, int cout, in
     }
 }
 
-// per-process workspace for the merged weights (grown on an eager call, never freed: captured
-// CUDA graphs keep pointing at it)
-uint16_t *halve_merged_weights(const uint16_t *wc, int cout, int c, cudaStream_t st) {
-    static uint16_t *buf = nullptr;
-    static size_t cap = 0;
-    const size_t bytes = 16ull * cout * c * 2;
-    if (bytes > cap) {
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-        uint16_t *fresh = nullptr;
-        const size_t want = bytes < (4u << 20) ? (4u << 20) : bytes;
-        if (cudaMalloc(&fresh, want) != cudaSuccess) return nullptr;
-        buf = fresh;
-        cap = want;
-    }
+// builds the merged weights into buf (scratch, 16 * cout * c bf16)
+int halve_merged_weights(const uint16_t *wc, int cout, int c, uint16_t *buf, cudaStream_t st) {
     // class -> tap -> slab (15 = unused), from HALVE_CLS / HALVE_DY / HALVE_DX
     unsigned long long tab = ~0ull;
     for (int i = 0; i < 9; ++i) {
@@ -2016,16 +2131,19 @@ uint16_t *halve_merged_weights(const uint16_t *wc, int cout, int c, cudaStream_t
     const long long total = 16LL * cout * c;
     const unsigned grid = (unsigned)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
     halve_merge_kernel<<<grid, 256, 0, st>>>(wc, cout, c, buf, tab);
-    return buf;
+    ice::count_launch();
+    return (int)cudaGetLastError();
 }
 
 extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2, int32_t n, int32_t h,
                               int32_t w, int32_t ksize, const uint16_t *wgt, const float *bias, int32_t cout,
-                              int32_t relu, const float *drop_scale, uint16_t *y, uint32_t *relu_bits, void *stream) {
+                              int32_t relu, const float *drop_scale, uint16_t *y, uint32_t *relu_bits, void *scratch,
+                              uint64_t *scratch_bytes, void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!x1 || !wgt || !y || c1 <= 0 || c1 % 64 || c2 < 0 || c2 % 64 || (c2 && !x2) || cout <= 0 || cout % 64 ||
         (ksize != 1 && ksize != 3) || !shape_ok(n, h, w))
         return ICE_EINVAL;
+    ice::Arena ar(scratch, scratch_bytes);
     FpropProb p;
     memset(&p, 0, sizeof p);
     p.pt = pix_tile(n, h, w, BM);
@@ -2035,47 +2153,46 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
     p.bias = bias; p.drop = drop_scale; p.relu = relu; p.y = reinterpret_cast<bf16 *>(y);
     p.rbits = relu_bits;
     cudaStream_t st = (cudaStream_t)stream;
+    const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     if (use_halo(ksize, w)) {
         const int nch = (c1 + c2) / 64;
-        const int bn = halo_bn(nch, cout);
+        const HaloPlan hp = halo_plan(nch, cout, (unsigned)mtiles);
         if (!map_halo(&p.xa, x1, n, h, w, c1)) return ICE_EINVAL;
         if (c2 && !map_halo(&p.xb, x2, n, h, w, c2)) return ICE_EINVAL;
-        if (!map_wgt(&p.wm, wgt, cout, 9, c1 + c2, bn)) return ICE_EINVAL;
-        if (((nch == 1 && cout == 64) || bn == 128) && !getenv("ICE_NO_STAGE")) {  // staged TMA stores
+        if (!map_wgt(&p.wm, wgt, cout, 9, c1 + c2, hp.bn)) return ICE_EINVAL;
+        if (((nch == 1 && cout == 64) || hp.bn == 128) && !knobs().no_stage) {  // staged TMA stores
             if (!map_out32(&p.ym, y, n, h, w, cout)) return ICE_EINVAL;
             p.y_tma = 1;
         }
-        return run_halo(p, nch, cout, dim3((unsigned)(p.pt.tw * p.pt.th * p.pt.tn)), st);
+        ICE_SETTLE(ar);
+        return run_halo(p, hp, cout, st);
     }
-    const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     int bn, splits;
     const int total_kb = p.taps[0].n * ((c1 + c2) / BK);
     pick_tiling(cout, mtiles, bn, splits, total_kb);
-    if (getenv("ICE_NO_SPLITK") || relu_bits) splits = 1;  // the split finisher writes no mask bits
-    if (!getenv("ICE_NO_STAGE") && map_out_tile(&p.ym, y, n, h, w, cout, p.pt)) p.y_tma = 1;  // staged stores
+    if (knobs().no_splitk || relu_bits) splits = 1;  // the split finisher writes no mask bits
+    if (!knobs().no_stage && map_out_tile(&p.ym, y, n, h, w, cout, p.pt)) p.y_tma = 1;  // staged stores
     if (!map_act(&p.xa, x1, n, h, w, c1, p.pt)) return ICE_EINVAL;
     if (c2 && !map_act(&p.xb, x2, n, h, w, c2, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wgt, cout, p.taps[0].n, c1 + c2, bn)) return ICE_EINVAL;
     if (splits > 1) {
         const long long npx = (long long)n * h * w;
-        float *ws = split_workspace((size_t)npx * cout * 4, st);
-        if (ws) {
-            int rc = launch_split(p, mtiles, cout, total_kb, splits, st, ws);
-            if (rc) return rc;
-            const long long work = npx * (cout / 8), nblk = (work + 255) / 256;
-            const unsigned fgrid = (unsigned)(nblk < 148 * 16 ? nblk : 148 * 16);
-            split_finish_fprop<<<fgrid, 256, 0, st>>>(
-                ws, npx, h * w, cout, bias, drop_scale, relu, p.y);
-            return (int)cudaGetLastError();
-        }
+        int kps, z;
+        split_shape(total_kb, splits, kps, z);
+        float *ws = ar.take<float>((size_t)z * npx * cout * 4);
+        ICE_SETTLE(ar);
+        int rc = launch_split(p, mtiles, cout, total_kb, kps, z, ws, st);
+        if (rc) return rc;
+        const long long work = npx * (cout / 8), nblk = (work + 255) / 256;
+        const unsigned fgrid = (unsigned)(nblk < 148 * 16 ? nblk : 148 * 16);
+        split_finish_fprop<<<fgrid, 256, 0, st>>>(ws, z, npx, h * w, cout, bias, drop_scale, relu, p.y);
+        ice::count_launch();
+        return (int)cudaGetLastError();
     }
+    ICE_SETTLE(ar);
     if (conv_m2(mtiles, cout, bn, splits, total_kb))
-        return bn == 256 ? launch_m2<256, 3>(p, dim3((unsigned)(mtiles / 2), cout / 256, 1), st)
-                         : launch_m2<128, 4>(p, dim3((unsigned)(mtiles / 2), cout / 128, 1), st);
-    dim3 grid((unsigned)mtiles, cout / bn, 1);
-    if (bn == 256) return launch<256, 4>(p, grid, st);
-    if (bn == 128) return launch<128, 6>(p, grid, st);
-    return launch<64, 8>(p, grid, st);
+        return launch_bn_m2(p, bn, dim3((unsigned)(mtiles / 2), cout / bn, 1), st);
+    return launch_bn(p, bn, dim3((unsigned)mtiles, cout / bn, 1), st);
 }
 
 extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32_t h, int32_t w, int32_t ksize,
@@ -2083,11 +2200,12 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
                               const float *drop_scale1, const uint16_t *add1, uint16_t *dx2,
                               const uint16_t *relu_ref2, const float *drop_scale2, const uint16_t *add2,
                               int32_t dx2_planes, float *dbias1, float *dbias2, const uint32_t *relu_bits1,
-                              void *stream) {
+                              void *scratch, uint64_t *scratch_bytes, void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!dy || !wgt || c1 <= 0 || c1 % 64 || c2 < 0 || c2 % 64 || cout <= 0 || cout % 64 ||
         (ksize != 1 && ksize != 3) || !shape_ok(n, h, w))
         return ICE_EINVAL;
+    ice::Arena ar(scratch, scratch_bytes);
     DgradProb p;
     memset(&p, 0, sizeof p);
     p.pt = pix_tile(n, h, w, BM);
@@ -2097,40 +2215,44 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
     p.ref1 = reinterpret_cast<const bf16 *>(relu_ref1); p.ref2 = reinterpret_cast<const bf16 *>(relu_ref2);
     p.add1 = reinterpret_cast<const bf16 *>(add1); p.add2 = reinterpret_cast<const bf16 *>(add2);
     p.drop1 = drop_scale1; p.drop2 = drop_scale2;
-    p.db1 = dbias1; p.db2 = dbias2;
+    p.db1 = dx1 ? dbias1 : nullptr; p.db2 = dx2 ? dbias2 : nullptr;
     p.rbits1 = relu_bits1;
     p.planes_out2 = dx2_planes;
     if (dx2_planes && ((h | w) & 1)) return ICE_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     const int ct = c1 + c2;
+    const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     if (use_halo(ksize, w)) {  // the epilogue picks dx1/dx2 (and the plane layout) per 32-column chunk
+        const HaloPlan hp = halo_plan(cout / 64, ct, (unsigned)mtiles);
         if (!map_halo(&p.dym, dy, n, h, w, cout)) return ICE_EINVAL;
         if (!map_wgt(&p.wm, wgt, cout, 9, ct, 64)) return ICE_EINVAL;
         const bool res64 = cout == 64 && ct == 64 && c2 == 0;  // resident-weight BN = 64 tiles
-        if ((res64 || halo_bn(cout / 64, ct) == 128) && dx1 && !getenv("ICE_NO_STAGE")) {  // staged TMA stores
+        if ((res64 || hp.bn == 128) && dx1 && !knobs().no_stage) {  // staged TMA stores
             if (!map_out32(&p.o1m, dx1, n, h, w, c1)) return ICE_EINVAL;
             p.o1_tma = 1;
         }
-        if (res64 && dx1 && !getenv("ICE_NO_STAGE")) {
-            if (relu_ref1 && !relu_bits1 && !getenv("ICE_NO_REF_TMA")) {  // ReLU reference staged by the producer
-                cuuint64_t dims[4] = {(cuuint64_t)c1, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
-                cuuint64_t strides[3] = {(cuuint64_t)c1 * 2, (cuuint64_t)w * c1 * 2, (cuuint64_t)h * w * c1 * 2};
-                cuuint32_t box[4] = {64, 128, 1, 1};
-                cuuint32_t es[4] = {1, 1, 1, 1};
-                if (encode_fn()(&p.refm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t *>(relu_ref1), dims,
-                                strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-                    return ICE_EINVAL;
-                p.ref_tma = 1;
-            }
+        if (res64 && dx1 && !knobs().no_stage && relu_ref1 && !relu_bits1 && !knobs().no_ref_tma) {
+            // ReLU reference staged by the producer
+            cuuint64_t dims[4] = {(cuuint64_t)c1, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+            cuuint64_t strides[3] = {(cuuint64_t)c1 * 2, (cuuint64_t)w * c1 * 2, (cuuint64_t)h * w * c1 * 2};
+            cuuint32_t box[4] = {64, 128, 1, 1};
+            cuuint32_t es[4] = {1, 1, 1, 1};
+            if (encode_fn()(&p.refm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t *>(relu_ref1), dims,
+                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return ICE_EINVAL;
+            p.ref_tma = 1;
         }
-        return run_halo(p, cout / 64, ct, dim3((unsigned)(p.pt.tw * p.pt.th * p.pt.tn)), st);
+        const ice::RowSched s = sched(hp.tiles, hp.bn, 4);
+        take_bias_rows(p, s, ar);
+        ICE_SETTLE(ar);
+        const int rc = run_halo(p, hp, ct, st);
+        return rc ? rc : finish_bias(p, s, st);
     }
-    const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     int bn, splits;
     const int total_kb = p.taps.n * (cout / BK);
     pick_tiling(ct, mtiles, bn, splits, total_kb);
-    if (getenv("ICE_NO_SPLITK")) splits = 1;
+    if (knobs().no_splitk) splits = 1;
     // a column tile must not straddle the dx1 / dx2 split
     while (bn > 64 && (c1 % bn)) {
         bn >>= 1;
@@ -2139,37 +2261,45 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
     if (!map_act(&p.dym, dy, n, h, w, cout, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wgt, cout, p.taps.n, ct, 64)) return ICE_EINVAL;
     // staged dx1 stores: the warp's rows must all be valid (no partial image tile)
-    if (dx1 && n % p.pt.Nt == 0 && !getenv("ICE_NO_STAGE") && map_out_tile(&p.o1m, dx1, n, h, w, c1, p.pt))
+    if (dx1 && n % p.pt.Nt == 0 && !knobs().no_stage && map_out_tile(&p.o1m, dx1, n, h, w, c1, p.pt))
         p.o1_tma = 1;
     if (splits > 1) {
         const long long npx = (long long)n * h * w;
-        float *ws = split_workspace((size_t)npx * ct * 4, st);
-        if (ws) {
-            int rc = launch_split(p, mtiles, ct, total_kb, splits, st, ws);
-            if (rc) return rc;
-            const int blocks = (ct / 256) * (int)((npx + FIN_STRIP - 1) / FIN_STRIP);
-            split_finish_dgrad<<<blocks, 256, 0, st>>>(ws, (int)npx, n, h, w, p);
-            return (int)cudaGetLastError();
-        }
+        int kps, z;
+        split_shape(total_kb, splits, kps, z);
+        float *ws = ar.take<float>((size_t)z * npx * ct * 4);
+        const int strips = (int)((npx + FIN_STRIP - 1) / FIN_STRIP);
+        if (p.db1 || p.db2) p.bpart = ar.take<float>((size_t)strips * ct * 4);
+        ICE_SETTLE(ar);
+        int rc = launch_split(p, mtiles, ct, total_kb, kps, z, ws, st);
+        if (rc) return rc;
+        split_finish_dgrad<<<(ct / 256) * strips, 256, 0, st>>>(ws, z, (int)npx, n, h, w, p);
+        ice::count_launch();
+        rc = (int)cudaGetLastError();
+        if (rc || (!p.db1 && !p.db2)) return rc;
+        const ice::ColSegs segs{{p.db1, p.db2, nullptr, nullptr}, {c1, c2, 0, 0}};
+        return ice::colsum_finish(p.bpart, strips, ct, ct, segs, ice::RowSched{1, 1, 1, 1, 0}, st);
     }
-    if (conv_m2(mtiles, ct, bn, splits, total_kb))
-        return bn == 256 ? launch_m2<256, 3>(p, dim3((unsigned)(mtiles / 2), ct / 256, 1), st)
-                         : launch_m2<128, 4>(p, dim3((unsigned)(mtiles / 2), ct / 128, 1), st);
-    dim3 grid((unsigned)mtiles, ct / bn, 1);
-    if (bn == 256) return launch<256, 4>(p, grid, st);
-    if (bn == 128) return launch<128, 6>(p, grid, st);
-    return launch<64, 8>(p, grid, st);
+    const bool m2 = conv_m2(mtiles, ct, bn, splits, total_kb);
+    const dim3 tiles = m2 ? dim3((unsigned)(mtiles / 2), ct / bn, 1) : dim3((unsigned)mtiles, ct / bn, 1);
+    const ice::RowSched s = sched(tiles, bn, m2 ? 8 : 4);
+    take_bias_rows(p, s, ar);
+    ICE_SETTLE(ar);
+    const int rc = m2 ? launch_bn_m2(p, bn, tiles, st) : launch_bn(p, bn, tiles, st);
+    return rc ? rc : finish_bias(p, s, st);
 }
 
 extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2, int32_t c2, const uint16_t *dy,
-                              int32_t cout, int32_t n, int32_t h, int32_t w, int32_t ksize, float *dw,
-                              void *stream) {
+                              int32_t cout, int32_t n, int32_t h, int32_t w, int32_t ksize, float *dw, void *scratch,
+                              uint64_t *scratch_bytes, void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!x1 || !dy || !dw || c1 <= 0 || c1 % 64 || c2 < 0 || c2 % 64 || (c2 && !x2) || cout <= 0 || cout % 64 ||
         (ksize != 1 && ksize != 3) || !shape_ok(n, h, w))
         return ICE_EINVAL;
-    if (ksize == 3 && !getenv("ICE_NO_HALO_WGRAD")) {
-        const int rc = try_hwgrad(x1, c1, x2, c2, dy, cout, n, h, w, dw, (cudaStream_t)stream);
+    ice::Arena ar(scratch, scratch_bytes);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ksize == 3 && !knobs().no_halo_wgrad) {
+        const int rc = try_hwgrad(x1, c1, x2, c2, dy, cout, n, h, w, dw, ar, scratch_bytes, st);
         if (rc <= 0) return rc;  // 1 = not applicable
     }
     WgradProb p;
@@ -2185,34 +2315,19 @@ extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2
     const bool m2 = wgrad_m2(mtiles, bn, p.total_kb);
     if (m2) mtiles /= 2;
     p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles);
-    const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
-    // channel blocks per TMA box: as many consecutive 64-blocks as the tile reads from one
-    // (tap, source) run; the M operand supplies 2 blocks (4 for 256-row tiles), B BN/64
-    {
-        const int mb = m2 ? 4 : 2;
-        const int want_x = p.trans ? mb : bn / 64, want_y = p.trans ? bn / 64 : mb;
-        int nbx = want_x;
-        while (nbx > 1 && ((c1 % (64 * nbx)) || (c2 % (64 * nbx)))) nbx >>= 1;
-        int nby = want_y;
-        while (nby > 1 && (cout % (64 * nby))) nby >>= 1;
-        p.nbx = nbx;
-        p.nby = nby;
-    }
+    wgrad_boxes(p, m2, bn);
     if (!map_act_nb(&p.dym, dy, n, h, w, cout, p.pk, p.nby)) return ICE_EINVAL;
     if (!map_act_nb(&p.xa, x1, n, h, w, c1, p.pk, p.nbx)) return ICE_EINVAL;
     if (c2 && !map_act_nb(&p.xb, x2, n, h, w, c2, p.pk, p.nbx)) return ICE_EINVAL;
-    dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
-    cudaStream_t st = (cudaStream_t)stream;
-    if (m2) return launch_m2<256, 3>(p, grid, st);
-    if (bn == 256) return launch<256, 4>(p, grid, st);
-    if (bn == 128) return launch<128, 6>(p, grid, st);
-    return launch<64, 8>(p, grid, st);
+    return run_wgrad(p, ncols, mtiles, ntiles, bn, m2, ar, scratch_bytes, st);
 }
 
 extern "C" int ice_halve_fprop(const uint16_t *x, int32_t c, int32_t n, int32_t h, int32_t w, const uint16_t *wc,
-                               const float *bias, int32_t cout, uint16_t *y, void *stream) {
+                               const float *bias, int32_t cout, uint16_t *y, void *scratch, uint64_t *scratch_bytes,
+                               void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!x || !wc || !y || c <= 0 || c % 64 || cout <= 0 || cout % 64 || !shape_ok(n, h, w)) return ICE_EINVAL;
+    ice::Arena ar(scratch, scratch_bytes);
     FpropProb p;
     memset(&p, 0, sizeof p);
     p.pt = pix_tile(n, h, w, BM);
@@ -2227,64 +2342,57 @@ extern "C" int ice_halve_fprop(const uint16_t *x, int32_t c, int32_t n, int32_t 
     p.N = n; p.H = h; p.W = w; p.c1 = c; p.c2 = 0; p.cout = cout;
     p.bias = bias; p.relu = 0; p.y = reinterpret_cast<bf16 *>(y);
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
-    cudaStream_t st0 = (cudaStream_t)stream;
-    // wide levels: the 4 sub-pixel classes side by side in N (4 x cout columns, 4 taps each, the
-    // class's unused taps zero): 16/9 of the MACs, but one 256-wide tile per 128 pixels instead of
-    // four short-K 64-wide ones (halve.4: 2 + 4 + 4 + 8 K-blocks on 64 columns)
-    if ((4 * cout) % 256 == 0 && cout <= 128 && w >= 64 && p.pt.Wt >= 32 && !getenv("ICE_NO_HALVE_MERGE")) {
-        uint16_t *wm = halve_merged_weights(wc, cout, c, st0);
-        if (wm) {
-            p.merged = 1;
-            p.taps[0].n = 4;
-            for (int t = 0; t < 4; ++t) {
-                p.taps[0].dy[t] = (int8_t)(t >> 1);
-                p.taps[0].dx[t] = (int8_t)(t & 1);
-                p.taps[0].wt[t] = (int8_t)t;
-            }
-            const int OH = 2 * h, OW = 2 * w;
-            cuuint64_t dims[4] = {(cuuint64_t)cout, (cuuint64_t)OW, (cuuint64_t)OH, (cuuint64_t)n};
-            cuuint64_t strides[3] = {(cuuint64_t)cout * 2, (cuuint64_t)OW * cout * 2, (cuuint64_t)OH * OW * cout * 2};
-            cuuint32_t box[4] = {32, 64, 1, 1};
-            cuuint32_t es[4] = {1, 2, 1, 1};
-            if (!getenv("ICE_NO_STAGE") &&
-                encode_fn()(&p.ym, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, y, dims, strides, box, es,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
-                p.y_tma = 1;
-            if (!map_act(&p.xa, x, n, h, w, c, p.pt)) return ICE_EINVAL;
-            if (!map_wgt(&p.wm, wm, 4 * cout, 4, c, 256)) return ICE_EINVAL;
-            return launch<256, 4>(p, dim3((unsigned)mtiles, 4 * cout / 256, 1), st0);
-        }
-    }
-    const int bn = pick_bn(cout, mtiles * 4);
-    if (p.pt.Wt >= 32 && !getenv("ICE_NO_STAGE")) {
-        // staged stores: a warp's 32 input pixels of one row land on every other output pixel
-        // of row 2h + cy -- a 64-pixel box traversed with element stride 2
+    cudaStream_t st = (cudaStream_t)stream;
+    // staged stores: a warp's 32 input pixels of one row land on every other output pixel of
+    // row 2h + cy -- a 64-pixel box traversed with element stride 2
+    auto map_y = [&]() {
         const int OH = 2 * h, OW = 2 * w;
         cuuint64_t dims[4] = {(cuuint64_t)cout, (cuuint64_t)OW, (cuuint64_t)OH, (cuuint64_t)n};
         cuuint64_t strides[3] = {(cuuint64_t)cout * 2, (cuuint64_t)OW * cout * 2, (cuuint64_t)OH * OW * cout * 2};
         cuuint32_t box[4] = {32, 64, 1, 1};
         cuuint32_t es[4] = {1, 2, 1, 1};
-        if (encode_fn()(&p.ym, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, y, dims, strides, box, es,
+        if (!knobs().no_stage &&
+            encode_fn()(&p.ym, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, y, dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
             p.y_tma = 1;
+    };
+    // wide levels: the 4 sub-pixel classes side by side in N (4 x cout columns, 4 taps each, the
+    // class's unused taps zero): 16/9 of the MACs, but one 256-wide tile per 128 pixels instead of
+    // four short-K 64-wide ones (halve.4: 2 + 4 + 4 + 8 K-blocks on 64 columns)
+    if ((4 * cout) % 256 == 0 && cout <= 128 && w >= 64 && p.pt.Wt >= 32 && !knobs().no_halve_merge) {
+        uint16_t *wm = ar.take<uint16_t>(16ull * cout * c * 2);
+        p.merged = 1;
+        p.taps[0].n = 4;
+        for (int t = 0; t < 4; ++t) {
+            p.taps[0].dy[t] = (int8_t)(t >> 1);
+            p.taps[0].dx[t] = (int8_t)(t & 1);
+            p.taps[0].wt[t] = (int8_t)t;
+        }
+        map_y();
+        if (!map_act(&p.xa, x, n, h, w, c, p.pt)) return ICE_EINVAL;
+        ICE_SETTLE(ar);
+        if (!map_wgt(&p.wm, wm, 4 * cout, 4, c, 256)) return ICE_EINVAL;
+        const int rc = halve_merged_weights(wc, cout, c, wm, st);
+        if (rc) return rc;
+        return launch<256, 4>(p, dim3((unsigned)mtiles, 4 * cout / 256, 1), st);
     }
+    const int bn = pick_bn(cout, mtiles * 4);
+    if (p.pt.Wt >= 32) map_y();
     if (!map_act(&p.xa, x, n, h, w, c, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wc, cout, 9, c, bn)) return ICE_EINVAL;
-    dim3 grid((unsigned)mtiles, cout / bn, 4);
-    cudaStream_t st = (cudaStream_t)stream;
-    if (bn == 256) return launch<256, 4>(p, grid, st);
-    if (bn == 128) return launch<128, 6>(p, grid, st);
-    return launch<64, 8>(p, grid, st);
+    ICE_SETTLE(ar);
+    return launch_bn(p, bn, dim3((unsigned)mtiles, cout / bn, 4), st);
 }
 
 extern "C" int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t n, int32_t h, int32_t w,
                                const uint16_t *wc, int32_t c, uint16_t *dx, const uint16_t *relu_ref,
-                               const float *drop_scale, float *dbias, void *stream) {
+                               const float *drop_scale, float *dbias, void *scratch, uint64_t *scratch_bytes,
+                               void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!dy_planes || !wc || !dx || c <= 0 || c % 64 || cout <= 0 || cout % 64 || !shape_ok(n, h, w))
         return ICE_EINVAL;
+    ice::Arena ar(scratch, scratch_bytes);
     DgradProb p;
     memset(&p, 0, sizeof p);
     p.pt = pix_tile(n, h, w, BM);
@@ -2306,22 +2414,24 @@ extern "C" int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t 
     if (!map_planes(&p.dym, dy_planes, n, h, w, cout, p.pt)) return ICE_EINVAL;
     if (!map_wgt(&p.wm, wc, cout, 9, c, 64)) return ICE_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    if (conv_m2(mtiles, c, bn, 1, 9 * (cout / BK)))
-        return bn == 256 ? launch_m2<256, 3>(p, dim3((unsigned)(mtiles / 2), c / 256, 1), st)
-                         : launch_m2<128, 4>(p, dim3((unsigned)(mtiles / 2), c / 128, 1), st);
-    dim3 grid((unsigned)mtiles, c / bn, 1);
-    if (bn == 256) return launch<256, 4>(p, grid, st);
-    if (bn == 128) return launch<128, 6>(p, grid, st);
-    return launch<64, 8>(p, grid, st);
+    const bool m2 = conv_m2(mtiles, c, bn, 1, 9 * (cout / BK));
+    const dim3 tiles = m2 ? dim3((unsigned)(mtiles / 2), c / bn, 1) : dim3((unsigned)mtiles, c / bn, 1);
+    const ice::RowSched s = sched(tiles, bn, m2 ? 8 : 4);
+    take_bias_rows(p, s, ar);
+    ICE_SETTLE(ar);
+    const int rc = m2 ? launch_bn_m2(p, bn, tiles, st) : launch_bn(p, bn, tiles, st);
+    return rc ? rc : finish_bias(p, s, st);
 }
 
 extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_planes, int32_t cout, int32_t n,
-                               int32_t h, int32_t w, float *dw, void *stream) {
+                               int32_t h, int32_t w, float *dw, void *scratch, uint64_t *scratch_bytes, void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!x || !dy_planes || !dw || c <= 0 || c % 64 || cout <= 0 || cout % 64 || !shape_ok(n, h, w))
         return ICE_EINVAL;
-    if (!getenv("ICE_NO_HALO_WGRAD")) {
-        const int rc = try_hwgrad(x, c, nullptr, 0, dy_planes, cout, n, h, w, dw, (cudaStream_t)stream, true);
+    ice::Arena ar(scratch, scratch_bytes);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!knobs().no_halo_wgrad) {
+        const int rc = try_hwgrad(x, c, nullptr, 0, dy_planes, cout, n, h, w, dw, ar, scratch_bytes, st, true);
         if (rc <= 0) return rc;  // 1 = not applicable
     }
     WgradProb p;
@@ -2338,23 +2448,8 @@ extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_
     const bool m2 = wgrad_m2(mtiles, bn, p.total_kb);
     if (m2) mtiles /= 2;
     p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles);
-    const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
-    {
-        const int mb = m2 ? 4 : 2;
-        const int want_x = p.trans ? mb : bn / 64, want_y = p.trans ? bn / 64 : mb;
-        int nbx = want_x;
-        while (nbx > 1 && (c % (64 * nbx))) nbx >>= 1;
-        int nby = want_y;
-        while (nby > 1 && (cout % (64 * nby))) nby >>= 1;
-        p.nbx = nbx;
-        p.nby = nby;
-    }
+    wgrad_boxes(p, m2, bn);
     if (!map_act_nb(&p.dym, dy_planes, 4 * n, h, w, cout, p.pk, p.nby)) return ICE_EINVAL;
     if (!map_act_nb(&p.xa, x, n, h, w, c, p.pk, p.nbx)) return ICE_EINVAL;
-    dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
-    cudaStream_t st = (cudaStream_t)stream;
-    if (m2) return launch_m2<256, 3>(p, grid, st);
-    if (bn == 256) return launch<256, 4>(p, grid, st);
-    if (bn == 128) return launch<128, 6>(p, grid, st);
-    return launch<64, 8>(p, grid, st);
+    return run_wgrad(p, ncols, mtiles, ntiles, bn, m2, ar, scratch_bytes, st);
 }

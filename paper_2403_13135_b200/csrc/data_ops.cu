@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include "icelabel_b200.h"
+#include "reduce.cuh"
 
 namespace {
 
@@ -134,6 +135,7 @@ extern "C" int ice_cut_tiles(const uint8_t *img, int32_t h, int32_t w, int32_t c
     const int rows = (h + size - 1) / size, cols = (w + size - 1) / size;
     const long long total = (long long)rows * cols * size * size * c;
     cut_kernel<<<grid_for(total), NT, 0, (cudaStream_t)stream>>>(img, h, w, c, size, cols, total, tiles);
+    ice::count_launch();
     return (int)cudaGetLastError();
 }
 
@@ -143,6 +145,7 @@ extern "C" int ice_stitch_tiles(const uint8_t *tiles, int32_t cols, int32_t size
     if (cols <= 0) cols = (w + size - 1) / size;
     if ((long long)cols * size < w) return ICE_EINVAL;
     stitch_kernel<<<grid_for((long long)h * w * c), NT, 0, (cudaStream_t)stream>>>(tiles, cols, size, c, h, w, out);
+    ice::count_launch();
     return (int)cudaGetLastError();
 }
 
@@ -152,6 +155,7 @@ extern "C" int ice_encode_labels(const uint8_t *mask, int64_t npx, const uint8_t
     if (npx == 0) return ICE_OK;
     encode_kernel<<<grid_for(npx), NT, 0, (cudaStream_t)stream>>>(mask, npx, colors, ncls, rgb,
                                                                   reinterpret_cast<unsigned long long *>(first_bad));
+    ice::count_launch();
     return (int)cudaGetLastError();
 }
 
@@ -161,6 +165,7 @@ extern "C" int ice_decode_labels(const uint8_t *rgb, int64_t npx, const uint8_t 
     if (npx == 0) return ICE_OK;
     decode_kernel<<<grid_for(npx), NT, 0, (cudaStream_t)stream>>>(rgb, npx, colors, ncls, mask,
                                                                   reinterpret_cast<unsigned long long *>(first_bad));
+    ice::count_launch();
     return (int)cudaGetLastError();
 }
 
@@ -169,6 +174,7 @@ extern "C" int ice_head_argmax(const uint16_t *h, int64_t npx, const float *w_ou
     if (npx < 0 || (npx > 0 && (!h || !w_out || !b_out || !mask))) return ICE_EINVAL;
     if (npx == 0) return ICE_OK;
     head_argmax_kernel<<<grid_for(npx), NT, 0, (cudaStream_t)stream>>>(h, npx, w_out, b_out, mask);
+    ice::count_launch();
     return (int)cudaGetLastError();
 }
 
@@ -178,5 +184,6 @@ extern "C" int ice_confusion(const uint8_t *pred, const uint8_t *ref, int64_t np
     if (npx == 0) return ICE_OK;
     confusion_kernel<<<grid_for(npx), NT, 0, (cudaStream_t)stream>>>(
         pred, ref, npx, k, reinterpret_cast<unsigned long long *>(counts), reinterpret_cast<unsigned long long *>(bad));
+    ice::count_launch();
     return (int)cudaGetLastError();
 }

@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #include "icelabel_b200.h"
+#include "reduce.cuh"
 
 namespace {
 
@@ -178,10 +179,11 @@ __global__ void maxpool_fwd_kernel(const uint16_t *__restrict__ x, int n, int h,
 // dz = (add + maxpool_backward(dpool)) * drop[n][c] * [x > 0]: the fused backward of
 // "ReLU -> Dropout2d -> {skip, MaxPool2d}" for a down block's output x (model.py:115-118).
 // The grid-stride is a multiple of c/8, so each thread always owns the same 8 channels and
-// keeps their bias-gradient partial sums (sum of dz) in registers.
+// keeps their bias-gradient partial sums (sum of dz) in registers; each block stores its
+// channel sums as row blockIdx.x of bpart[blocks][c] (colsum_finish adds the rows in order).
 __global__ void maxpool_bwd_kernel(const uint16_t *__restrict__ x, const uint16_t *__restrict__ dpool,
                                    const uint16_t *__restrict__ add, const float *__restrict__ drop, int n, int h, int w,
-                                   int c, uint16_t *__restrict__ dz, float *__restrict__ dbias) {
+                                   int c, uint16_t *__restrict__ dz, float *__restrict__ bpart) {
     const int ho = h / 2, wo = w / 2, cv = c / 8;
     const long long total = (long long)n * ho * wo * cv;
     float bsum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -225,7 +227,7 @@ __global__ void maxpool_bwd_kernel(const uint16_t *__restrict__ x, const uint16_
 #pragma unroll
         for (int k = 0; k < 4; ++k) reinterpret_cast<uint4 *>(dz)[idx[k]] = out[k];
     }
-    if (dbias) {  // block reduction per channel (thread t owns channel group t % cv), then atomics
+    if (bpart) {  // block reduction per channel (thread t owns channel group t % cv)
         __shared__ float red[256 * 8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) red[threadIdx.x * 8 + e] = bsum[e];
@@ -234,7 +236,7 @@ __global__ void maxpool_bwd_kernel(const uint16_t *__restrict__ x, const uint16_
             const int cg = ch >> 3, e = ch & 7;
             float acc = 0.f;
             for (int t = cg; t < (int)blockDim.x; t += cv) acc += red[t * 8 + e];
-            if (acc != 0.f) atomicAdd(&dbias[ch], acc);
+            bpart[(size_t)blockIdx.x * c + ch] = acc;
         }
     }
 }
@@ -244,16 +246,19 @@ __global__ void maxpool_bwd_kernel(const uint16_t *__restrict__ x, const uint16_
 // loss, argmax hit.  Backward: dlogits = (p - onehot) * scale; dz = (dlogits W) * drop *
 // [h > 0] (the ReLU/Dropout2d of up.{d-1}'s output); dW[k][c] = sum_p dlogits_k h_c via a
 // per-warp smem stage (lane l owns channels 2l, 2l+1 of all 32 staged pixels), db and
-// loss/hit counts via warp reductions; one atomic per lane per block at the end.  h is read
-// and dz written with coalesced 16 B accesses through the same per-warp stage.
+// loss/hit counts via warp reductions; at the end the block's sums (warps added in order) are
+// stored as row blockIdx.x of part[blocks][HEAD_LD] = [dW 192 | db 3 | dz bias 64 | loss, hits]
+// and colsum_finish adds the rows in order (no atomics: bit-reproducible).  h is read and dz
+// written with coalesced 16 B accesses through the same per-warp stage.
 constexpr int HEAD_NT = 256;
 constexpr int HC = 64;
+constexpr int HEAD_COLS = 3 * HC + 3 + HC + 2, HEAD_LD = 264;
 
 __global__ void __launch_bounds__(HEAD_NT, 4) head_ce_kernel(
     const uint16_t *__restrict__ hact, long long npx, int hw, const uint8_t *__restrict__ labels,
     const float *__restrict__ w_out, const float *__restrict__ b_out, const float *__restrict__ drop, float grad_scale,
-    uint16_t *__restrict__ dz, float *__restrict__ dw, float *__restrict__ db, float *__restrict__ stats,
-    float *__restrict__ logits_out, float *__restrict__ dzbias) {
+    uint16_t *__restrict__ dz, bool train, bool zsum,
+    float *__restrict__ logits_out, float *__restrict__ part) {
     __shared__ float sw[3 * HC];
     __shared__ float sdrop[HC];
     // per-warp staging of 32 pixels x 128 B (row pitch 144 B: conflict-free 16 B row reads)
@@ -264,7 +269,6 @@ __global__ void __launch_bounds__(HEAD_NT, 4) head_ce_kernel(
     const int lane = threadIdx.x & 31;
     uint8_t *wst = stage[threadIdx.x >> 5];
     long long cur_img = -1;
-    const bool train = dw != nullptr;
     float accw[6] = {0, 0, 0, 0, 0, 0};
     float accz0 = 0.f, accz1 = 0.f;  // bias gradient of the conv that produced h: sum of dz
     float accb0 = 0.f, accb1 = 0.f, accb2 = 0.f, loss_sum = 0.f, correct = 0.f;
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(HEAD_NT, 4) head_ce_kernel(
                 *reinterpret_cast<uint4 *>(wst + lane * 144 + q * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
             __syncwarp();
-            if (dzbias) {  // lane l sums channels 2l, 2l+1 of the 32 staged dz rows
+            if (zsum) {  // lane l sums channels 2l, 2l+1 of the 32 staged dz rows
 #pragma unroll 4
                 for (int q = 0; q < 32; ++q) {
                     const uint32_t zv = *reinterpret_cast<const uint32_t *>(wst + q * 144 + lane * 4);
@@ -404,30 +408,37 @@ __global__ void __launch_bounds__(HEAD_NT, 4) head_ce_kernel(
         accb1 += __shfl_xor_sync(0xffffffffu, accb1, o);
         accb2 += __shfl_xor_sync(0xffffffffu, accb2, o);
     }
-    if (train) {
+    // per warp: its row of the block's sums (in the staging buffer, free once all warps are done)
+    __syncthreads();
+    float(*wsum)[HEAD_LD] = reinterpret_cast<float(*)[HEAD_LD]>(&stage[0][0]);
+    static_assert(sizeof(stage) >= sizeof(float) * (HEAD_NT / 32) * HEAD_LD, "head partial rows");
+    float *row = wsum[threadIdx.x >> 5];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            atomicAdd(&dw[k * HC + 2 * lane], accw[2 * k]);
-            atomicAdd(&dw[k * HC + 2 * lane + 1], accw[2 * k + 1]);
-        }
-        if (lane == 0) {
-            atomicAdd(&db[0], accb0);
-            atomicAdd(&db[1], accb1);
-            atomicAdd(&db[2], accb2);
-        }
-        if (dzbias && dz) {
-            atomicAdd(&dzbias[2 * lane], accz0);
-            atomicAdd(&dzbias[2 * lane + 1], accz1);
-        }
+    for (int k = 0; k < 3; ++k) {
+        row[k * HC + 2 * lane] = accw[2 * k];
+        row[k * HC + 2 * lane + 1] = accw[2 * k + 1];
     }
-    if (lane == 0 && stats) {
-        atomicAdd(&stats[0], loss_sum);
-        atomicAdd(&stats[1], correct);
+    row[3 * HC + 3 + 2 * lane] = accz0;
+    row[3 * HC + 3 + 2 * lane + 1] = accz1;
+    if (lane == 0) {
+        row[3 * HC] = accb0;
+        row[3 * HC + 1] = accb1;
+        row[3 * HC + 2] = accb2;
+        row[4 * HC + 3] = loss_sum;
+        row[4 * HC + 4] = correct;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < HEAD_COLS; i += HEAD_NT) {
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < HEAD_NT / 32; ++k) s += wsum[k][i];
+        part[(size_t)blockIdx.x * HEAD_LD + i] = s;
     }
 }
 
 // ---- bias gradient: db[c] += sum over rows of dz[row][c] --------------------------------
-__global__ void bias_grad_kernel(const uint16_t *__restrict__ dz, long long rows, int c, float *__restrict__ db) {
+// (block sums stored as row blockIdx.x of part[blocks][c], added in order by colsum_finish)
+__global__ void bias_grad_kernel(const uint16_t *__restrict__ dz, long long rows, int c, float *__restrict__ part) {
     extern __shared__ float red[];
     const int groups = c / 8;               // 16-byte vectors per row
     const int rows_per_iter = blockDim.x / groups;
@@ -447,7 +458,7 @@ __global__ void bias_grad_kernel(const uint16_t *__restrict__ dz, long long rows
         const int gg = i / 8, j = i % 8;
         float s = 0.f;
         for (int rr = 0; rr < rows_per_iter; ++rr) s += red[(rr * groups + gg) * 8 + j];
-        atomicAdd(&db[i], s);
+        part[(size_t)blockIdx.x * c + i] = s;
     }
 }
 
@@ -535,24 +546,28 @@ __global__ void fill_f32_kernel(float *__restrict__ dst, long long n, float v) {
 extern "C" int ice_stem_im2col(const uint8_t *img, int32_t n, int32_t h, int32_t w, uint16_t *out, void *stream) {
     if (!img || !out || n < 1 || h < 1 || w < 1) return ICE_EINVAL;
     stem_im2col_kernel<<<grid_for((long long)n * h * w, 256), 256, 0, (cudaStream_t)stream>>>(img, n, h, w, out);
+    ice::count_launch();
     LAUNCH_CHECK();
 }
 
 extern "C" int ice_stem_im2col_f32(const float *img, int32_t n, int32_t h, int32_t w, uint16_t *out, void *stream) {
     if (!img || !out || n < 1 || h < 1 || w < 1) return ICE_EINVAL;
     stem_im2col_f32_kernel<<<grid_for((long long)n * h * w, 256), 256, 0, (cudaStream_t)stream>>>(img, n, h, w, out);
+    ice::count_launch();
     LAUNCH_CHECK();
 }
 
 extern "C" int ice_pad_weights(const float *src, int32_t rows, int32_t k, uint16_t *dst, int32_t kp, void *stream) {
     if (!src || !dst || rows < 1 || k < 1 || kp < k) return ICE_EINVAL;
     pad_weights_kernel<<<grid_for((long long)rows * kp, 256), 256, 0, (cudaStream_t)stream>>>(src, rows, k, dst, kp);
+    ice::count_launch();
     LAUNCH_CHECK();
 }
 
 extern "C" int ice_halve_prep(const float *w, int32_t cout, int32_t c, uint16_t *wc, void *stream) {
     if (!w || !wc || cout < 1 || c < 1) return ICE_EINVAL;
     halve_prep_kernel<<<grid_for((long long)cout * c, 256), 256, 0, (cudaStream_t)stream>>>(w, cout, c, wc);
+    ice::count_launch();
     LAUNCH_CHECK();
 }
 
@@ -561,12 +576,21 @@ extern "C" int ice_maxpool_fwd(const uint16_t *x, int32_t n, int32_t h, int32_t 
     if (!x || !y || n < 1 || h < 2 || w < 2 || (h | w) & 1 || c % 8) return ICE_EINVAL;
     maxpool_fwd_kernel<<<grid_for((long long)n * (h / 2) * (w / 2) * (c / 8), 256), 256, 0, (cudaStream_t)stream>>>(
         x, n, h, w, c, y);
+    ice::count_launch();
     LAUNCH_CHECK();
 }
 
+#define ICE_SETTLE(ar)                                 \
+    do {                                               \
+        const int q_ = (ar).settle(scratch_bytes);     \
+        if (q_) return q_ > 0 ? ICE_OK : ICE_ESCRATCH; \
+    } while (0)
+
 extern "C" int ice_maxpool_bwd(const uint16_t *x, const uint16_t *dpool, const uint16_t *add, const float *drop,
-                               int32_t n, int32_t h, int32_t w, int32_t c, uint16_t *dz, float *dbias, void *stream) {
+                               int32_t n, int32_t h, int32_t w, int32_t c, uint16_t *dz, float *dbias, void *scratch,
+                               uint64_t *scratch_bytes, void *stream) {
     if (!x || !dpool || !dz || n < 1 || h < 2 || w < 2 || (h | w) & 1 || c % 8) return ICE_EINVAL;
+    ice::Arena ar(scratch, scratch_bytes);
     const long long total = (long long)n * (h / 2) * (w / 2) * (c / 8);
     const int cv = c / 8, threads = 256;
     // grid * threads must be a multiple of cv (fixed channels per thread for the bias sums)
@@ -583,32 +607,58 @@ extern "C" int ice_maxpool_bwd(const uint16_t *x, const uint16_t *dpool, const u
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     if (blocks > (long long)sms * resident) blocks = (long long)sms * resident;
-    maxpool_bwd_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(x, dpool, add, drop, n, h, w, c, dz,
-                                                                                dbias);
-    LAUNCH_CHECK();
+    float *part = dbias ? ar.take<float>((size_t)blocks * c * 4) : nullptr;
+    ICE_SETTLE(ar);
+    cudaStream_t st = (cudaStream_t)stream;
+    maxpool_bwd_kernel<<<(unsigned)blocks, threads, 0, st>>>(x, dpool, add, drop, n, h, w, c, dz, part);
+    ice::count_launch();
+    const int rc = (int)cudaGetLastError();
+    if (rc || !dbias) return rc;
+    return ice::colsum_finish(part, (int)blocks, c, c, ice::ColSegs{{dbias, nullptr, nullptr, nullptr}, {c, 0, 0, 0}},
+                              ice::RowSched{1, 1, 1, 1, 0}, st);
 }
 
 extern "C" int ice_head_ce(const uint16_t *h, int64_t npx, int32_t hw, const uint8_t *labels, const float *w_out,
                            const float *b_out, const float *drop, float grad_scale, uint16_t *dz, float *dw, float *db,
-                           float *stats, float *logits, float *dzbias, void *stream) {
+                           float *stats, float *logits, float *dzbias, void *scratch, uint64_t *scratch_bytes,
+                           void *stream) {
     if (!h || !labels || !w_out || !b_out || npx < 0 || hw < 1 || ((dw == nullptr) != (db == nullptr))) return ICE_EINVAL;
-    if (npx == 0) return ICE_OK;
+    ice::Arena ar(scratch, scratch_bytes);
     unsigned blocks = grid_for(npx, HEAD_NT);
     if (blocks > 148 * 4) blocks = 148 * 4;
-    head_ce_kernel<<<blocks, HEAD_NT, 0, (cudaStream_t)stream>>>(h, npx, hw, labels, w_out, b_out, drop, grad_scale,
-                                                                 dz, dw, db, stats, logits, dzbias);
-    LAUNCH_CHECK();
+    const bool train = dw != nullptr, zsum = train && dz && dzbias;
+    const bool need = train || stats;
+    float *part = need ? ar.take<float>((size_t)blocks * HEAD_LD * 4) : nullptr;
+    ICE_SETTLE(ar);
+    if (npx == 0) return ICE_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    head_ce_kernel<<<blocks, HEAD_NT, 0, st>>>(h, npx, hw, labels, w_out, b_out, drop, grad_scale, dz, train, zsum,
+                                               logits, part);
+    ice::count_launch();
+    const int rc = (int)cudaGetLastError();
+    if (rc || !need) return rc;
+    const ice::ColSegs segs{{dw, db, zsum ? dzbias : nullptr, stats}, {3 * HC, 3, HC, 2}};
+    return ice::colsum_finish(part, (int)blocks, HEAD_LD, HEAD_COLS, segs, ice::RowSched{1, 1, 1, 1, 0}, st);
 }
 
-extern "C" int ice_bias_grad(const uint16_t *dz, int64_t rows, int32_t c, float *db, void *stream) {
+extern "C" int ice_bias_grad(const uint16_t *dz, int64_t rows, int32_t c, float *db, void *scratch,
+                             uint64_t *scratch_bytes, void *stream) {
     if (!dz || !db || rows < 0 || c < 8 || c % 8 || c / 8 > 256) return ICE_EINVAL;
-    if (rows == 0) return ICE_OK;
+    ice::Arena ar(scratch, scratch_bytes);
     const int threads = 256;
     const int rows_per_iter = threads / (c / 8);
     unsigned blocks = grid_for(rows, rows_per_iter * 64);
     if (blocks > 148 * 4) blocks = 148 * 4;
-    bias_grad_kernel<<<blocks, threads, threads * 8 * sizeof(float), (cudaStream_t)stream>>>(dz, rows, c, db);
-    LAUNCH_CHECK();
+    float *part = ar.take<float>((size_t)blocks * c * 4);
+    ICE_SETTLE(ar);
+    if (rows == 0) return ICE_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    bias_grad_kernel<<<blocks, threads, threads * 8 * sizeof(float), st>>>(dz, rows, c, part);
+    ice::count_launch();
+    const int rc = (int)cudaGetLastError();
+    if (rc) return rc;
+    return ice::colsum_finish(part, (int)blocks, c, c, ice::ColSegs{{db, nullptr, nullptr, nullptr}, {c, 0, 0, 0}},
+                              ice::RowSched{1, 1, 1, 1, 0}, st);
 }
 
 extern "C" int ice_dropout_scale(int32_t count, float p, uint64_t seed, const int64_t *step_dev, float *out,
@@ -617,6 +667,7 @@ extern "C" int ice_dropout_scale(int32_t count, float p, uint64_t seed, const in
     if (count == 0) return ICE_OK;
     dropout_scale_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(
         count, p, seed, reinterpret_cast<const long long *>(step_dev), out);
+    ice::count_launch();
     LAUNCH_CHECK();
 }
 
@@ -631,6 +682,7 @@ extern "C" int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64
     adam_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, (cudaStream_t)stream>>>(
         p, g, m, v, n, (float)(lr / bc1), beta1, beta2, eps, (float)sqrt(bc2), out_bf16,
         reinterpret_cast<const long long *>(step_dev), lr);
+    ice::count_launch();
     LAUNCH_CHECK();
 }
 
@@ -639,6 +691,7 @@ __global__ void counter_add_kernel(long long *c, long long d) { *c += d; }
 extern "C" int ice_counter_add(int64_t *counter, int64_t delta, void *stream) {
     if (!counter) return ICE_EINVAL;
     counter_add_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<long long *>(counter), delta);
+    ice::count_launch();
     LAUNCH_CHECK();
 }
 
@@ -646,6 +699,7 @@ extern "C" int ice_cast_bf16(const float *src, int64_t n, uint16_t *dst, void *s
     if (!src || !dst || n < 0) return ICE_EINVAL;
     if (n == 0) return ICE_OK;
     cast_bf16_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(src, n, dst);
+    ice::count_launch();
     LAUNCH_CHECK();
 }
 
@@ -653,5 +707,6 @@ extern "C" int ice_fill_f32(float *dst, int64_t n, float value, void *stream) {
     if (!dst || n < 0) return ICE_EINVAL;
     if (n == 0) return ICE_OK;
     fill_f32_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(dst, n, value);
+    ice::count_launch();
     LAUNCH_CHECK();
 }

@@ -64,6 +64,17 @@ def phys(c: int) -> int:
     return (c + 63) // 64 * 64
 
 
+def check_tile(h: int, w: int, depth: int) -> None:
+    """Tile sides the B200 engine runs: divisible by 2^depth (the reference's own rule,
+    model.py:42-45,116-119) and powers of two (the conv kernels' shift/mask index math)."""
+    step = 2 ** depth
+    if h % step or w % step:
+        raise ValueError(f"spatial dims {(h, w)} not divisible by {step}")
+    if h & (h - 1) or w & (w - 1):
+        raise ValueError(f"tile sides {(h, w)} must be powers of two on the B200 engine "
+                         "(the reference accepts any multiple of 2^depth)")
+
+
 def check_supported(spec: UNetSpec) -> None:
     """Limits of the B200 kernels (the reference accepts more; those raise loudly here)."""
     if spec.in_channels != 3:
@@ -186,44 +197,37 @@ def init_reference_params(spec: UNetSpec) -> "OrderedDict[str, torch.Tensor]":
 
 
 class _Acts:
-    """Per-batch-shape activation / gradient buffers (NHWC bf16)."""
+    """Per-batch-shape activation / gradient buffers (NHWC bf16) for B tiles of H x W."""
 
-    def __init__(self, spec: UNetSpec, B: int, S: int, device):
+    def __init__(self, spec: UNetSpec, B: int, H: int, W: int, device):
         d = spec.depth
         chans = [spec.base_channels * 2 ** i for i in range(d + 1)]
         cp = [phys(c) for c in chans]
         e = lambda *shape: torch.empty(shape, dtype=torch.bfloat16, device=device)  # noqa: E731
-        self.B, self.S = B, S
-        self.stem = e(B, S, S, 64)
-        self.a1, self.a2, self.pool = [], [], []
-        for i in range(d):
-            s = S >> i
-            self.a1.append(e(B, s, s, cp[i]))
-            self.a2.append(e(B, s, s, cp[i]))
-            self.pool.append(e(B, s // 2, s // 2, cp[i]))
-        sb = S >> d
-        self.b1, self.b2 = e(B, sb, sb, cp[d]), e(B, sb, sb, cp[d])
-        self.hv, self.u1, self.u2 = [], [], []
-        for j in range(d):
-            L = d - 1 - j
-            s = S >> L
-            self.hv.append(e(B, s, s, cp[L]))
-            self.u1.append(e(B, s, s, cp[L]))
-            self.u2.append(e(B, s, s, cp[L]))
+        lv = lambda L, c, n=B: e(n, H >> L, W >> L, c)  # noqa: E731  (level-L tensor)
+        self.B, self.H, self.W = B, H, W
+        self.stem = e(B, H, W, 64)
+        self.a1 = [lv(i, cp[i]) for i in range(d)]
+        self.a2 = [lv(i, cp[i]) for i in range(d)]
+        self.pool = [lv(i + 1, cp[i]) for i in range(d)]
+        self.b1, self.b2 = lv(d, cp[d]), lv(d, cp[d])
+        self.hv = [lv(d - 1 - j, cp[d - 1 - j]) for j in range(d)]
+        self.u1 = [lv(d - 1 - j, cp[d - 1 - j]) for j in range(d)]
+        self.u2 = [lv(d - 1 - j, cp[d - 1 - j]) for j in range(d)]
         # backward scratch, per level: two dZ ping-pong buffers, the skip gradient, the
         # halving-conv output gradient (sub-pixel planes) and the pooled gradient
-        self.dz_a = [e(B, S >> L, S >> L, cp[L]) for L in range(d + 1)]
-        self.dz_b = [e(B, S >> L, S >> L, cp[L]) for L in range(d + 1)]
-        self.dskip = [e(B, S >> L, S >> L, cp[L]) for L in range(d)]
-        self.dhv = [e(4, B, S >> (L + 1), S >> (L + 1), cp[L]) for L in range(d)]
-        self.dpool = [e(B, S >> (L + 1), S >> (L + 1), cp[L]) for L in range(d)]
+        self.dz_a = [lv(L, cp[L]) for L in range(d + 1)]
+        self.dz_b = [lv(L, cp[L]) for L in range(d + 1)]
+        self.dskip = [lv(L, cp[L]) for L in range(d)]
+        self.dhv = [e(4, B, H >> (L + 1), W >> (L + 1), cp[L]) for L in range(d)]
+        self.dpool = [lv(L + 1, cp[L]) for L in range(d)]
         # packed ReLU masks of the DoubleConv middle activations (a1, b1, u1): the forward writes
         # them, the backward's dgrad reads 4 B per 32 channels instead of the bf16 tensor
-        bits = lambda s, c: torch.empty((c // 32, B * s * s), dtype=torch.int32, device=device)  # noqa: E731
-        self.a1_bits = [bits(S >> i, cp[i]) for i in range(d)]
-        self.b1_bits = bits(S >> d, cp[d])
-        self.u1_bits = [bits(S >> (d - 1 - j), cp[d - 1 - j]) for j in range(d)]
-        self.labels = torch.empty((B, S, S), dtype=torch.uint8, device=device)
+        bits = lambda L, c: torch.empty((c // 32, B * (H >> L) * (W >> L)), dtype=torch.int32, device=device)  # noqa: E731
+        self.a1_bits = [bits(i, cp[i]) for i in range(d)]
+        self.b1_bits = bits(d, cp[d])
+        self.u1_bits = [bits(d - 1 - j, cp[d - 1 - j]) for j in range(d)]
+        self.labels = torch.empty((B, H, W), dtype=torch.uint8, device=device)
         self.drop = {}  # block name -> fp32 [B][c_p] Dropout2d scales (train mode, p > 0)
 
 
@@ -312,13 +316,15 @@ class UNetEngine:
             _native.call("ice_halve_prep", self.w(name).data_ptr(), L.cout_p, L.cin_p, wc.data_ptr(), st)
 
     # ---- buffers ---------------------------------------------------------------------------
-    def ensure(self, B: int, S: int) -> _Acts:
-        key = (B, S)
+    def ensure(self, B: int, H: int, W: int = None) -> _Acts:
+        W = H if W is None else W
+        check_tile(H, W, self.spec.depth)
+        key = (B, H, W)
         if key not in self._acts_cache:
             if len(self._acts_cache) >= 4:  # ragged tails etc.: keep a few shapes resident
                 self._acts_cache.pop(next(iter(self._acts_cache)))
                 torch.cuda.empty_cache()
-            acts = _Acts(self.spec, B, S, self.device)
+            acts = _Acts(self.spec, B, H, W, self.device)
             acts.stats = self.stats
             self._acts_cache[key] = acts
         self.acts = self._acts_cache[key]
@@ -345,16 +351,16 @@ class UNetEngine:
 
     # ---- forward ------------------------------------------------------------------------
     def forward(self, images, train: bool, seed: int = 0, float_input: bool = False) -> _Acts:
-        """images: u8 [B, S, S, 3] (or fp32 in [0,1] with float_input) device tensor."""
+        """images: u8 [B, H, W, 3] (or fp32 in [0,1] with float_input) device tensor."""
         spec = self.spec
         d = spec.depth
-        B, S = images.shape[0], images.shape[1]
-        A = self.ensure(B, S)
+        B, H, W = images.shape[0], images.shape[1], images.shape[2]
+        A = self.ensure(B, H, W)
         st = _native.stream_handle()
         if float_input:
-            _native.call("ice_stem_im2col_f32", images.data_ptr(), B, S, S, A.stem.data_ptr(), st)
+            _native.call("ice_stem_im2col_f32", images.data_ptr(), B, H, W, A.stem.data_ptr(), st)
         else:
-            _native.call("ice_stem_im2col", images.data_ptr(), B, S, S, A.stem.data_ptr(), st)
+            _native.call("ice_stem_im2col", images.data_ptr(), B, H, W, A.stem.data_ptr(), st)
         self._drop_masks(A, seed, train)
         dr = A.drop.get
         x = A.stem
@@ -390,10 +396,10 @@ class UNetEngine:
         correct) and, in training, the head gradients and dZ of up.{d-1}.block.2."""
         d = self.spec.depth
         h = A.u2[d - 1]
-        B, S = h.shape[0], h.shape[1]
+        B, hw = h.shape[0], h.shape[1] * h.shape[2]
         st = _native.stream_handle()
         dz = A.dz_a[0] if train else None
-        _native.call("ice_head_ce", h.data_ptr(), B * S * S, S * S, labels.data_ptr(),
+        _native.call("ice_head_ce", h.data_ptr(), B * hw, hw, labels.data_ptr(),
                      self.w("out").data_ptr(), self.b("out").data_ptr(),
                      _native.ptr(A.drop.get(f"up.{d - 1}")) if train else None, float(grad_scale),
                      _native.ptr(dz), _native.ptr(self.w("out", self.grads)) if train else None,
@@ -549,11 +555,7 @@ class UNet:
     def _check(self, x):
         if x.ndim != 4 or x.shape[1] != self.spec.in_channels:
             raise ValueError(f"expected (n, {self.spec.in_channels}, h, w) input, got {tuple(x.shape)}")
-        step = 2 ** self.spec.depth
-        if x.shape[2] % step or x.shape[3] % step:
-            raise ValueError(f"spatial dims {tuple(x.shape[2:])} not divisible by {step}")
-        if x.shape[2] != x.shape[3]:
-            raise ValueError("the B200 engine expects square tiles")
+        check_tile(x.shape[2], x.shape[3], self.spec.depth)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         """Class logits (n, classes, h, w) fp32, on x's device.  Inference semantics
@@ -561,10 +563,10 @@ class UNet:
         self._check(x)
         dev = x.device
         xin = x.detach().to(self.engine.device, torch.float32).permute(0, 2, 3, 1).contiguous()
-        n, s = xin.shape[0], xin.shape[1]
+        n, h, w = xin.shape[0], xin.shape[1], xin.shape[2]
         A = self.engine.forward(xin, train=False, float_input=True)
-        logits = torch.empty((n, s, s, 3), dtype=torch.float32, device=self.engine.device)
-        labels = torch.zeros((n, s, s), dtype=torch.uint8, device=self.engine.device)
+        logits = torch.empty((n, h, w, 3), dtype=torch.float32, device=self.engine.device)
+        labels = torch.zeros((n, h, w), dtype=torch.uint8, device=self.engine.device)
         A.stats.zero_()
         self.engine.head(A, labels, train=False, logits=logits)
         return logits.permute(0, 3, 1, 2).contiguous().to(dev)

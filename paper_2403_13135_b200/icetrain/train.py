@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from .data import train_val_split
-from .model import UNet, UNetSpec
+from .model import UNet, UNetSpec, check_tile
 from .optim import Adam
 
 BATCH_CHOICES = (16, 32, 64)
@@ -155,11 +155,11 @@ def device_step(model, optimizer, x, y, union_count: int, bucketer=None) -> None
     bucketer is given), fused Adam.  x: u8 NHWC [n, S, S, 3], y: u8 [n, S, S].
     The step's loss sum / hit count accumulate in model.engine.stats."""
     engine = model.engine
-    S = x.shape[1]
+    hw = x.shape[1] * x.shape[2]
     # dropout masks: per-rank seed + the engine's device step counter (graph-replay safe)
     dist = _dist()
     A = engine.forward(x, train=model.training, seed=1 + (dist.get_rank() if dist else 0))
-    dz = engine.head(A, y, train=True, grad_scale=1.0 / (union_count * S * S))
+    dz = engine.head(A, y, train=True, grad_scale=1.0 / (union_count * hw))
     fused = bucketer is not None and bucketer.optimizer is optimizer
     if fused:
         bucketer.begin()
@@ -216,13 +216,17 @@ def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
     device = engine.device
     counts = [len(x) for x, _ in shards]
     local = sum(counts)
+    # union sample count and pixels per tile (tiles of one corpus share a shape; a rank with
+    # an empty shard learns the tile size from the others)
+    local_hw = next((x.shape[1] * x.shape[2] if x.shape[-1] == 3 else x.shape[2] * x.shape[3]
+                     for x, _ in shards if len(x)), 0)
     dist = _dist()
     if dist is not None:
-        t = torch.tensor([float(local)], device=device)
+        t = torch.tensor([float(local), float(local * local_hw)], dtype=torch.float64, device=device)
         dist.all_reduce(t)
-        total = int(t.item())
+        total, pixels = int(t[0].item()), int(t[1].item())
     else:
-        total = local
+        total, pixels = local, local * local_hw
     if total == 0:
         raise ValueError("synchronized step got only empty shards")
     A = None
@@ -242,27 +246,24 @@ def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
     live = [(k, s) for k, s in enumerate(shards) if counts[k] > 0]
     for idx, (k, (x, y)) in enumerate(live):
         xin, is_float = _as_nhwc(x, device)
-        S = xin.shape[1]
         A = engine.forward(xin, train=models[0].training, seed=rank_seed + k, float_input=is_float)
         if idx == 0:
             A.stats.zero_()
         A.labels.copy_(y.to(device, non_blocking=True), non_blocking=True)
-        dz = engine.head(A, A.labels, train=True, grad_scale=1.0 / (total * S * S))
+        dz = engine.head(A, A.labels, train=True, grad_scale=1.0 / pixels)
         last = idx == len(live) - 1
         engine.backward(A, dz, on_layer_done=bucketer.on_layer_done if (bucketer and last) else None)
     if A is None:  # this rank had no samples: contribute zeros
-        engine.ensure(1, models[0].spec.input_size).stats.zero_()
-        A = engine.acts
+        engine.stats.zero_()
         if bucketer:
             for _, _, last in bucketer.buckets:
                 bucketer.on_layer_done(last)
     if bucketer:
         bucketer.finish()
-    stats = A.stats
+    stats = engine.stats
     if dist is not None:
         dist.all_reduce(stats)
-    S = models[0].spec.input_size if A.S is None else A.S
-    mean_loss = float(stats[0].item()) / (total * S * S)
+    mean_loss = float(stats[0].item()) / pixels
     if not fused:
         for m in models[1:]:
             m.engine.grads.copy_(engine.grads)
@@ -292,6 +293,7 @@ def _validate_pairs(pairs: list, spec: UNetSpec) -> None:
     if shape[2] != spec.in_channels or shape[0] % step or shape[1] % step:
         raise ValueError(f"tile shape {shape} does not fit the model "
                          f"(needs {spec.in_channels} channels, dims divisible by {step})")
+    check_tile(shape[0], shape[1], spec.depth)  # the B200 engine's own limit, raised up front
 
 
 def _device_corpus(pairs: list, device):

@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from paper_2403_13135_b200.icelabel import synth
+from tests.fixtures import synth
 
 
 def _gray(seed, count, haze, i, size=256):

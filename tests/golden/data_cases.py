@@ -3,6 +3,8 @@ import numpy as np
 
 SIZES = [(300, 517), (256, 256), (17, 40), (513, 255)]
 TILE = 256
+# train_val_split cases (n, val_fraction, seed): BASELINE corpus, tiny corpora, zero fraction
+SPLITS = [(4224, 0.2, 0), (64, 0.2, 0), (10, 0.2, 9), (3, 0.5, 1), (1, 0.2, 0), (50, 0.0, 3), (97, 0.35, 7)]
 
 
 def scene(h, w, seed=5):

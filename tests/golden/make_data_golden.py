@@ -4,7 +4,8 @@
 
 Records sha256 digests of the reference's cut_tiles / stitch_tiles / encode_labels /
 decode_labels (pkg/trainer/src/icetrain/data.py:35-80) outputs, and its confusion counts and
-report (pkg/src/icelabel/metrics.py:108-142), on the seeded inputs of tests/golden/data_cases.py.
+report (pkg/src/icelabel/metrics.py:108-142), and its train_val_split (data.py:125-136), on the
+seeded inputs of tests/golden/data_cases.py.
 """
 import hashlib
 import json
@@ -18,7 +19,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, "/root/reference/pkg/trainer/src")
 
-from icetrain.data import cut_tiles, decode_labels, encode_labels, stitch_tiles  # noqa: E402  (reference)
+from icetrain.data import cut_tiles, decode_labels, encode_labels, stitch_tiles, train_val_split  # noqa: E402  (reference)
 from icelabel.metrics import confusion, report  # noqa: E402
 from icelabel.raster import LabelMask  # noqa: E402
 
@@ -57,5 +58,10 @@ cm = confusion(LabelMask(pred), LabelMask(ref))
 out["confusion"] = cm.counts.tolist()
 out["report"] = report(cm, 0.5).to_dict()
 out["report_csv"] = report(cm).to_csv()
+out["train_val_split"] = []
+for n, frac, seed in dc.SPLITS:
+    tr, va = train_val_split(list(range(n)), frac, seed)
+    out["train_val_split"].append({"n": n, "frac": frac, "seed": seed, "train": sha(np.array(tr, np.int64)),
+                                   "val": sha(np.array(va, np.int64)), "n_val": len(va)})
 json.dump(out, open(os.path.join(os.path.dirname(__file__), "data_golden.json"), "w"), indent=1)
 print("ok")

@@ -1,0 +1,86 @@
+"""tests/golden/desk_trajectory.pt: the reference trainer's loss over 200 synchronized_step
+calls at SURVEY.md 8(d).4's parity config -- UNetSpec(256, base_channels=16, dropout=0.0),
+batch 8, seed 0, on T-gray tiles labelled by the reference auto-labeler (north_star: "loss
+after 200 steps on the same seed and batch order must agree within 2%").
+
+Also records the reference's OWN sensitivity at this config: the same 200 steps from initial
+weights perturbed by 1e-6 (relative, fp32 rounding scale) with a few seeds.  The GPU test
+compares against the unperturbed run and reports the spread beside it.
+
+Run in the build container (/root/reference present; ~10 min on 8 cores):
+
+    python tests/golden/make_desk_trajectory.py [--spread N]
+"""
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, "/root/reference/pkg/trainer/src")
+
+from icelabel.cloudfilter import FilterConfig  # noqa: E402  (reference)
+from icelabel.engine import process_tile  # noqa: E402
+from icelabel.raster import Tile  # noqa: E402
+from icelabel.segmentation import ROSS_SEA_SUMMER  # noqa: E402
+from icelabel.synth import generate_corpus  # noqa: E402
+from icetrain.model import UNet, UNetSpec  # noqa: E402
+from icetrain.train import synchronized_step  # noqa: E402
+
+from tests.golden.desk_trajectory_data import N_TILES, SEED, SPEC, batch_order  # noqa: E402
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def reference_corpus():
+    tiles, labels = [], []
+    for s in generate_corpus(101, N_TILES, 0.3):
+        res = process_tile(Tile(s.raster, "t", 0, 0), FilterConfig(), ROSS_SEA_SUMMER)
+        assert res.ok, res.error
+        tiles.append(s.raster.data)
+        labels.append(res.label)
+    return np.stack(tiles), np.stack(labels)
+
+
+def run(x, y, perturb_seed=None):
+    torch.manual_seed(SEED)
+    model = UNet(UNetSpec(**SPEC))
+    if perturb_seed is not None:
+        g = torch.Generator().manual_seed(perturb_seed)
+        with torch.no_grad():
+            for p in model.parameters():
+                p.mul_(1 + 1e-6 * torch.randn(p.shape, generator=g))
+    opt = torch.optim.Adam(model.parameters(), lr=1e-3)
+    losses = []
+    t0 = time.time()
+    for k, idx in enumerate(batch_order()):
+        losses.append(synchronized_step([model], [opt], [(x[idx], y[idx])])[0])
+        if k % 20 == 0:
+            print(f"  step {k} loss {losses[-1]:.5f} ({time.time() - t0:.0f} s)", flush=True)
+    return losses
+
+
+def main():
+    torch.set_num_threads(os.cpu_count())
+    spread = int(sys.argv[sys.argv.index("--spread") + 1]) if "--spread" in sys.argv else 2
+    x_u8, y = reference_corpus()
+    x = torch.from_numpy(x_u8).permute(0, 3, 1, 2).float() / 255.0
+    yt = torch.from_numpy(y.astype(np.int64))
+    losses = run(x, yt)
+    spreads = [run(x, yt, perturb_seed=1000 + k) for k in range(spread)]
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "desk_trajectory.pt")
+    torch.save({"spec": SPEC, "seed": SEED, "losses": losses, "perturbed": spreads,
+                "tiles_sha": sha(x_u8), "labels_sha": sha(y)}, path)
+    print("wrote", path, "first", losses[0], "last", losses[-1],
+          "perturbed last", [s[-1] for s in spreads])
+
+
+if __name__ == "__main__":
+    main()

@@ -24,7 +24,7 @@ sys.path.insert(0, "/root/reference/pkg/trainer/src")
 from icetrain.model import UNet, UNetSpec  # noqa: E402  (reference)
 from icetrain.train import synchronized_step  # noqa: E402
 
-from paper_2403_13135_b200.icelabel import synth  # noqa: E402
+from tests.fixtures import synth  # noqa: E402
 
 
 def corpus(n, size):

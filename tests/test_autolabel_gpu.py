@@ -15,7 +15,7 @@ torch = pytest.importorskip("torch")
 
 from oracle import autolabel as orc
 from paper_2403_13135_b200 import icelabel as il
-from paper_2403_13135_b200.icelabel import synth
+from tests.fixtures import synth
 from tests.golden.cases import all_cases
 
 pytestmark = pytest.mark.gpu

@@ -36,3 +36,16 @@ def test_codec_oracle_matches_reference():
 def test_confusion_oracle_matches_reference():
     pred, ref = dc.pred_ref()
     assert orc.confusion(pred, ref).tolist() == GOLDEN["confusion"]
+
+
+def test_train_val_split_matches_reference():
+    """trainer data.py:125-136 on the BASELINE corpus size and edge cases (tiny corpora keep
+    at least one training pair; val_fraction 0 gives an empty validation side)."""
+    from paper_2403_13135_b200.icetrain.data import train_val_split
+    for rec in GOLDEN["train_val_split"]:
+        tr, va = train_val_split(list(range(rec["n"])), rec["frac"], rec["seed"])
+        assert len(va) == rec["n_val"] and len(tr) + len(va) == rec["n"]
+        assert sha(np.array(tr, np.int64)) == rec["train"] and sha(np.array(va, np.int64)) == rec["val"], rec["n"]
+    import pytest
+    with pytest.raises(ValueError, match="val_fraction"):
+        train_val_split([1, 2], 1.0, 0)

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from oracle import autolabel as orc
-from paper_2403_13135_b200.icelabel import synth
+from tests.fixtures import synth
 from tests.golden.cases import all_cases
 
 GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "autolabel_golden.json")))

@@ -143,7 +143,7 @@ def test_paper_spec_step_matches_oracle():
     gradients are ~1e-6 of the head's and their bf16 error is dominated by ReLU-mask flips
     of near-zero activations; there the bound is 2e-2 or 2x torch's own bf16-autocast
     error on the same step, and on average over tensors within 1.5x of torch's."""
-    from paper_2403_13135_b200.icelabel import synth
+    from tests.fixtures import synth
     spec = UNetSpec(dropout=0.0)
     tiles = synth.corpus(101, 2, 0.5)
     imgs = torch.from_numpy(__import__("numpy").stack([t for t, _ in tiles]))

@@ -13,7 +13,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2403_13135_b200 import icelabel as il  # noqa: E402
-from paper_2403_13135_b200.icelabel import synth  # noqa: E402
+from tests.fixtures import synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--tiles", type=int, default=1184)

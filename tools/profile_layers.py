@@ -12,7 +12,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2403_13135_b200 import _native  # noqa: E402
-from paper_2403_13135_b200.icelabel import synth  # noqa: E402
+from tests.fixtures import synth  # noqa: E402
 from paper_2403_13135_b200.icetrain import Adam, UNet, UNetSpec  # noqa: E402
 from paper_2403_13135_b200.icetrain.train import GradBucketer, device_step  # noqa: E402
 

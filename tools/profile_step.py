@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
 
-from paper_2403_13135_b200.icelabel import synth  # noqa: E402
+from tests.fixtures import synth  # noqa: E402
 from paper_2403_13135_b200.icetrain import Adam, UNet, UNetSpec  # noqa: E402
 from paper_2403_13135_b200.icetrain.train import device_step  # noqa: E402
 
