@@ -110,7 +110,9 @@ def kernel_launches() -> int:
 
 class Scratch:
     """Caller-owned device scratch for the entry points in SCRATCH_FNS (the library never
-    allocates): one uint8 buffer per (device, stream), grown on an eager call to the largest
+    allocates): one uint8 buffer per device, shared by calls that are stream-ordered (the
+    U-Net issues every scratch-using op on its compute stream; the gradient-bucket side
+    stream runs only Adam), grown on an eager call to the largest
     size a call has asked for.  A buffer is never freed once replaced -- CUDA graphs captured
     earlier keep pointing at it -- and growing inside a stream capture is an error (run the
     step eagerly once first, as every warm-up does).  Sizes come from the library's own query
@@ -136,7 +138,7 @@ class Scratch:
     def get(self, stream_handle, nbytes: int):
         import torch
         dev = torch.cuda.current_device()
-        key = (dev, stream_handle)
+        key = dev
         buf = self.bufs.get(key)
         if buf is None or buf.numel() < nbytes:
             if torch.cuda.is_current_stream_capturing():

@@ -537,7 +537,7 @@ struct WgradProb {
     int trans;  // narrow cout (< 128): D = [(tap, cin)][cout], A = shifted x, B = dY (no wasted M rows)
     int nbx, nby;  // non-halve: maps are 5-D (64, W, H, N, C/64) and one TMA box carries nb 64-ch blocks
     float *dw;  // [cout][taps][c1+c2]
-    float *ws;  // split-K partials [splits][cout][taps][c1+c2] (scratch) when splits > 1
+    float *ws;  // partials of splits 1.. [splits - 1][cout][taps][c1+c2] (scratch) when splits > 1
     size_t wsize;
 
     __device__ void kb_range(int z, int &kb0, int &nkb) const {
@@ -608,13 +608,15 @@ struct WgradProb {
     template <int BN>
     __device__ void flush_bias(int, int, int, float *, int) const {}
     template <int BN>
-    // one split: dw += tile (a single writer per element); several: the split's partial tile
-    // is stored into its own slice of ws and splitsum_finish adds the slices in split order
+    // split 0: dw += tile (the only writer of these elements in the launch); split z > 0 stores
+    // its partial tile into slice z - 1 of ws and splitsum_finish then adds the slices in split
+    // order: dw = (dw + p0) + ((p1 + p2) + ...), a fixed association -> bit-reproducible
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *, const Pre &,
                              uint8_t * = nullptr, const uint8_t * = nullptr) const {
         const int m = mt * BM + row;
         const int ld = taps.n * (c1 + c2);
-        float *base = ws ? ws + (size_t)z * wsize : dw;
+        const bool part = z > 0;
+        float *base = part ? ws + (size_t)(z - 1) * wsize : dw;
 #pragma unroll 1
         for (int cc = cc0; cc < cc1; ++cc) {
             float v[32];
@@ -622,7 +624,7 @@ struct WgradProb {
             if (!trans) {
                 if (m >= cout) continue;
                 float *dst = base + (size_t)m * ld + nt * BN + cc * 32;
-                if (ws) {
+                if (part) {
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
                         __stcg(reinterpret_cast<float4 *>(dst) + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
@@ -637,7 +639,7 @@ struct WgradProb {
                 for (int j = 0; j < 32; ++j) {
                     if (o0 + j >= cout) continue;
                     float *dst = base + (size_t)(o0 + j) * ld + m;
-                    if (ws) __stcg(dst, v[j]);
+                    if (part) __stcg(dst, v[j]);
                     else *dst += v[j];
                 }
             }
@@ -1393,7 +1395,7 @@ struct HWgrad {
     int N, H, W, ct, cout, nchx;
     int total_kb, kb_per_split, groups, G, total_mt;
     float *dw;  // [cout][9][ct]
-    float *ws;  // split partials [splits][cout][9][ct] (scratch) when there are several splits
+    float *ws;  // partials of splits 1.. [splits - 1][cout][9][ct] (scratch)
     size_t wsize;
 };
 
@@ -1540,7 +1542,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
             const int grp = u % p.groups, split = u / p.groups;
             const int mt0 = grp * p.G, mt1 = min(p.total_mt, mt0 + p.G);
-            float *base = p.ws ? p.ws + (size_t)split * p.wsize : p.dw;
+            const bool part = split > 0;
+            float *base = part ? p.ws + (size_t)(split - 1) * p.wsize : p.dw;
             tc::mbar_wait(tfull, local & 1);
             tc::tc_fence_after();
             for (int mt = mt0; mt < mt1; ++mt) {
@@ -1555,16 +1558,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                 const int b = 2 * mt + second;
                 const bool valid = b < NBLK && !(second == 1 && b1 == b0);
                 const int tap = b / NCH, c = (b % NCH) * 64 + (r & 63);
-                // one split: dw += (single writer); several: store the split's slice of ws
-                // (lanes hold consecutive channels: 128-B coalesced stores), summed in split
-                // order by splitsum_finish
+                // split 0: dw += (its only writer in the launch); split s > 0: store slice s - 1
+                // of ws (lanes hold consecutive channels: 128-B coalesced stores), added in
+                // split order by splitsum_finish
                 float *dst = base + (size_t)tap * p.ct + c;
 #pragma unroll
                 for (int cc = half * PER; cc < min(NCC, (half + 1) * PER); ++cc) {
                     float v[32];
                     tc::tmem_ld32(tmem + (mt - mt0) * COUT + cc * 32 + ((uint32_t)(sub * 32) << 16), v);
                     if (!valid) continue;
-                    if (p.ws) {
+                    if (part) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) __stcg(dst + (size_t)(cc * 32 + j) * ld, v[j]);
                     } else {
@@ -1972,8 +1975,11 @@ bool wgrad_m2(int mtiles, int bn, int total_kb) {
 
 // K-blocks per split.  The persistent grid runs ceil(units / SMs) rounds of equal-size
 // units (units = tiles * splits), so pick the split count whose last round is fullest
-// (>= 4 K-blocks per split); fewer splits (less partial-slice traffic) win ties.
-int split_k(int total_kb, long long tiles) {
+// (>= 4 K-blocks per split, at most max_units units); fewer splits win ties.  Every split
+// beyond the first writes a partial slice of the weight gradient (fixed-order reduction,
+// reduce.cuh), so the GEMM path caps the units at one round: its layers' weights are MBs and
+// 80-split slices cost GBs of traffic; the halo path's weights are 0.15-0.6 MB.
+int split_k(int total_kb, long long tiles, long long max_units = 8LL * 148) {
     const long long sms = num_sms();
     int best = 1;
     double best_eff = -1.0;
@@ -1985,6 +1991,7 @@ int split_k(int total_kb, long long tiles) {
         const long long rounds = (units + sms - 1) / sms;
         double eff = (double)units / (double)(rounds * sms);
         eff *= (double)total_kb / ((double)kps * s);  // short last split
+        if (units > max_units && s > 1) break;
         if (eff > best_eff + 1e-3) {
             best_eff = eff;
             best = s;
@@ -2052,7 +2059,7 @@ int try_hwgrad(const uint16_t *x1, int c1, const uint16_t *x2, int c2, const uin
     const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
     const long long units = (long long)p.groups * splits;
     p.wsize = (size_t)cout * (halve ? 4 : 9) * p.ct;
-    if (splits > 1) p.ws = ar.take<float>((size_t)splits * p.wsize * 4);
+    if (splits > 1) p.ws = ar.take<float>((size_t)(splits - 1) * p.wsize * 4);
     ICE_SETTLE(ar);
     const int grid = persist_grid(units);
     int rc;
@@ -2062,7 +2069,7 @@ int try_hwgrad(const uint16_t *x1, int c1, const uint16_t *x2, int c2, const uin
     else if (nch == 1) rc = launch_hwgrad<128, 1, 5, false>(p, grid, st);
     else rc = launch_hwgrad<128, 2, 3, false>(p, grid, st);
     if (rc || splits == 1) return rc;
-    return ice::splitsum_finish(p.ws, splits, p.wsize, p.wsize, dw, st);
+    return ice::splitsum_finish(p.ws, splits - 1, p.wsize, p.wsize, dw, st);
 }
 
 // The non-halo weight gradient (WgradProb on conv_gemm / conv_gemm_m2), split over pixels
@@ -2071,12 +2078,12 @@ int run_wgrad(WgradProb &p, int ncols, int mtiles, int ntiles, int bn, bool m2, 
               uint64_t *scratch_bytes, cudaStream_t st) {
     const int splits = (p.total_kb + p.kb_per_split - 1) / p.kb_per_split;
     p.wsize = (size_t)p.cout * ncols;
-    p.ws = splits > 1 ? ar.take<float>((size_t)splits * p.wsize * 4) : nullptr;
+    p.ws = splits > 1 ? ar.take<float>((size_t)(splits - 1) * p.wsize * 4) : nullptr;
     ICE_SETTLE(ar);
     dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
     const int rc = m2 ? launch_m2<256, 3>(p, grid, st) : launch_bn(p, bn, grid, st);
     if (rc || splits == 1) return rc;
-    return ice::splitsum_finish(p.ws, splits, p.wsize, p.wsize, p.dw, st);
+    return ice::splitsum_finish(p.ws, splits - 1, p.wsize, p.wsize, p.dw, st);
 }
 
 // channel blocks per TMA box: as many consecutive 64-blocks as the tile reads from one
@@ -2314,7 +2321,7 @@ extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2
     p.total_kb = p.pk.tw * p.pk.th * p.pk.tn;
     const bool m2 = wgrad_m2(mtiles, bn, p.total_kb);
     if (m2) mtiles /= 2;
-    p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles);
+    p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles, num_sms());
     wgrad_boxes(p, m2, bn);
     if (!map_act_nb(&p.dym, dy, n, h, w, cout, p.pk, p.nby)) return ICE_EINVAL;
     if (!map_act_nb(&p.xa, x1, n, h, w, c1, p.pk, p.nbx)) return ICE_EINVAL;
@@ -2447,7 +2454,7 @@ extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_
     p.total_kb = 4 * p.pk.tw * p.pk.th * p.pk.tn;
     const bool m2 = wgrad_m2(mtiles, bn, p.total_kb);
     if (m2) mtiles /= 2;
-    p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles);
+    p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles, num_sms());
     wgrad_boxes(p, m2, bn);
     if (!map_act_nb(&p.dym, dy_planes, 4 * n, h, w, cout, p.pk, p.nby)) return ICE_EINVAL;
     if (!map_act_nb(&p.xa, x, n, h, w, c, p.pk, p.nbx)) return ICE_EINVAL;
