@@ -40,6 +40,7 @@ constexpr int STAGE_BYTES = 32 * 64;  // one warp's 32 px x 32 ch bf16 output bo
 // the time the warp spends on the next tile's TMEM load and math
 constexpr int STAGE_BUFS = 1;  // two warps per TMEM lane quarter, each draining half the columns
 constexpr int NTHREADS = 64 + 32 * EPI_WARPS;
+constexpr int BIAS_SLOTS = 8;  // shared-memory rows of the fused bias-gradient column sums
 
 // a box of Wt x Ht x Nt pixels, and how many boxes tile (W, H, N).  Every entry point
 // requires power-of-two H and W (shape_ok), so Wt, Ht, Nt, tw, th are powers of two and the
@@ -197,7 +198,9 @@ struct FpropProb {
         }
     }
     template <int BN>
-    __device__ void flush_bias(int, int, int, float *, int) const {}
+    __device__ void stash_bias(int, int, float *, int, float *) const {}
+    template <int BN>
+    __device__ void commit_bias(int, float *) const {}
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *,
                              const Pre &pr, uint8_t *stage = nullptr, const uint8_t * = nullptr) const {
@@ -399,20 +402,36 @@ struct DgradProb {
 
     // lane j of each epilogue warp keeps, per owned 32-column chunk, the running sum of
     // column j over all rows it has stored for the current column tile
-    // ... and at the end of its run over a column tile stores them (no atomics) as row
-    // (blockIdx.x, slot) of the partial matrix bpart[G * bslots][c1 + c2]; colsum_finish adds
-    // the rows in a fixed order (reduce.cuh)
+    // ... and at the end of its run over a column tile stashes them in shared memory (row
+    // `slot` of sb[bslots][BN]: the TMEM lane quarter, x the M half for 256-row tiles); the
+    // commit then adds the slots in slot order and stores the CTA's column sums as row
+    // blockIdx.x of bpart[G][c1 + c2] (no atomics); colsum_finish adds the rows of the CTAs
+    // that visited the column tile, in CTA order (reduce.cuh).  Every epilogue warp reaches
+    // each stash/commit at the same tile, so the commit's named barrier (id 1, the 256
+    // epilogue threads) is uniform.
     template <int BN>
-    __device__ void flush_bias(int nt, int cc0, int cc1, float *bacc, int slot) const {
+    __device__ void stash_bias(int cc0, int cc1, float *bacc, int slot, float *sb) const {
         const int lane = threadIdx.x & 31;
         constexpr int NCH = BN / 32, PER = (NCH + 1) / 2;
-        float *row = bpart ? bpart + ((size_t)blockIdx.x * bslots + slot) * (size_t)(c1 + c2) : nullptr;
 #pragma unroll
         for (int ci = 0; ci < PER; ++ci) {
             const int cc = cc0 + ci;
-            if (cc < cc1 && row) row[nt * BN + cc * 32 + lane] = bacc[ci];
+            if (cc < cc1) sb[slot * BN + cc * 32 + lane] = bacc[ci];
             bacc[ci] = 0.f;
         }
+    }
+    template <int BN>
+    __device__ void commit_bias(int nt, float *sb) const {
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+        if (bpart) {
+            float *row = bpart + (size_t)blockIdx.x * (c1 + c2) + nt * BN;
+            for (int j = threadIdx.x - 64; j < BN; j += 32 * EPI_WARPS) {
+                float s = 0.f;
+                for (int k = 0; k < bslots; ++k) s += sb[k * BN + j];
+                row[j] = s;
+            }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
     }
     // (register prefetch of the next tile's ReLU-reference rows measured slower: the
     // extra in-flight loads contend with the epilogue's stores)
@@ -606,11 +625,14 @@ struct WgradProb {
     template <int BN>
     __device__ void pre_load(Pre &, int, int, int, int, int, int) const {}
     template <int BN>
-    __device__ void flush_bias(int, int, int, float *, int) const {}
+    __device__ void stash_bias(int, int, float *, int, float *) const {}
     template <int BN>
-    // split 0: dw += tile (the only writer of these elements in the launch); split z > 0 stores
-    // its partial tile into slice z - 1 of ws and splitsum_finish then adds the slices in split
-    // order: dw = (dw + p0) + ((p1 + p2) + ...), a fixed association -> bit-reproducible
+    __device__ void commit_bias(int, float *) const {}
+    template <int BN>
+    // split 0: dw += tile with fire-and-forget reductions (RED) -- the launch's only
+    // contribution to these elements, so the result does not depend on timing; split z > 0
+    // stores its partial tile into slice z - 1 of ws and splitsum_finish then adds the slices in
+    // split order: dw = (dw + p0) + ((p1 + p2) + ...), a fixed association -> bit-reproducible
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *, const Pre &,
                              uint8_t * = nullptr, const uint8_t * = nullptr) const {
         const int m = mt * BM + row;
@@ -640,7 +662,7 @@ struct WgradProb {
                     if (o0 + j >= cout) continue;
                     float *dst = base + (size_t)(o0 + j) * ld + m;
                     if (part) __stcg(dst, v[j]);
-                    else *dst += v[j];
+                    else atomicAdd(dst, v[j]);  // RED, fire-and-forget; one contribution per element
                 }
             }
         }
@@ -675,7 +697,9 @@ struct SplitK {
     template <int BN>
     __device__ void pre_load(Pre &, int, int, int, int, int, int) const {}
     template <int BN>
-    __device__ void flush_bias(int, int, int, float *, int) const {}
+    __device__ void stash_bias(int, int, float *, int, float *) const {}
+    template <int BN>
+    __device__ void commit_bias(int, float *) const {}
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *, const Pre &,
                              uint8_t * = nullptr, const uint8_t * = nullptr) const {
@@ -817,7 +841,8 @@ __global__ void __launch_bounds__(256) split_finish_dgrad(const float *__restric
 
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
-    return 1024 + STAGES * (A_BYTES + BN * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16;
+    return 1024 + STAGES * (A_BYTES + BN * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16 +
+           BIAS_SLOTS * BN * 4;
 }
 
 // exact t / d for 0 <= t < 2^24 from a float reciprocal and one correction step
@@ -861,6 +886,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
     uint64_t *tfull = empty + STAGES;  // [2]
     uint64_t *tempty = tfull + 2;      // [2]
     uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
+    float *sbias = reinterpret_cast<float *>(tslot + 4);  // [BIAS_SLOTS][BN] (DgradProb)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = g.count();
@@ -948,7 +974,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
             int mt, nt, z;
             g.coords(t, mt, nt, z);
             if (nt != cur_nt) {
-                if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc, sub);
+                if (cur_nt >= 0) {
+                    p.template stash_bias<BN>(cc0, cc1, bacc, sub, sbias);
+                    p.template commit_bias<BN>(cur_nt, sbias);
+                }
                 cur_nt = nt;
             }
             const typename P::Pre cur = pre;
@@ -966,7 +995,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
-        if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc, sub);
+        if (cur_nt >= 0) {
+            p.template stash_bias<BN>(cc0, cc1, bacc, sub, sbias);
+            p.template commit_bias<BN>(cur_nt, sbias);
+        }
         if (lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
     }
     tc::tc_fence_before();
@@ -986,7 +1018,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
 // epilogue overlaps the next tile as in conv_gemm.
 template <int BN, int STAGES>
 constexpr int m2_smem_bytes() {
-    return 1024 + STAGES * (2 * A_BYTES + BN * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16;
+    return 1024 + STAGES * (2 * A_BYTES + BN * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16 +
+           BIAS_SLOTS * BN * 4;
 }
 
 template <int BN, int STAGES, class P>
@@ -1003,6 +1036,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
     uint64_t *tfull = empty + STAGES;  // [2]
     uint64_t *tempty = tfull + 2;      // [2]
     uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
+    float *sbias = reinterpret_cast<float *>(tslot + 4);  // [BIAS_SLOTS][BN] (DgradProb)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = g.count();
@@ -1082,8 +1116,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
             g.coords(t, mt, nt, z);
             if (nt != cur_nt) {
                 if (cur_nt >= 0) {
-                    p.template flush_bias<BN>(cur_nt, 0, PER, bacc0, half * 4 + sub);
-                    p.template flush_bias<BN>(cur_nt, PER, NCH, bacc1, half * 4 + sub);
+                    p.template stash_bias<BN>(0, PER, bacc0, half * 4 + sub, sbias);
+                    p.template stash_bias<BN>(PER, NCH, bacc1, half * 4 + sub, sbias);
+                    p.template commit_bias<BN>(cur_nt, sbias);
                 }
                 cur_nt = nt;
             }
@@ -1101,8 +1136,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
         if (cur_nt >= 0) {
-            p.template flush_bias<BN>(cur_nt, 0, PER, bacc0, half * 4 + sub);
-            p.template flush_bias<BN>(cur_nt, PER, NCH, bacc1, half * 4 + sub);
+            p.template stash_bias<BN>(0, PER, bacc0, half * 4 + sub, sbias);
+            p.template stash_bias<BN>(PER, NCH, bacc1, half * 4 + sub, sbias);
+            p.template commit_bias<BN>(cur_nt, sbias);
         }
         if (lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
     }
@@ -1131,7 +1167,7 @@ constexpr int halo_smem_bytes(bool refs = false) {
     return 1024 + 2 * HALO_BYTES + (RES ? 9 : BSTAGES * TAPS_PER_SLOT) * BN * BK * 2 +
            (((BN == 64 && RES) || BN == 128) ? EPI_WARPS * STAGE_BUFS * STAGE_BYTES : 0) +
            ((BN == 64 && RES && refs) ? 2 * REF_BYTES : 0) +
-           (2 * 2 + 2 * BSTAGES + 6 + 4) * 8 + 16;
+           (2 * 2 + 2 * BSTAGES + 6 + 4) * 8 + 16 + BIAS_SLOTS * BN * 4;
 }
 
 // RES (resident weights): single-chunk problems (64 input channels) keep all 9 weight taps
@@ -1162,6 +1198,7 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
     uint64_t *rfull = tempty + 2;   // [2]
     uint64_t *rempty = rfull + 2;   // [2]
     uint32_t *tslot = reinterpret_cast<uint32_t *>(rempty + 2);
+    float *sbias = reinterpret_cast<float *>(tslot + 4);  // [BIAS_SLOTS][BN] (DgradProb)
     const bool stage_ref = REFS && p.ref_tma;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1346,7 +1383,10 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
             int mt, nt, z;
             g.coords(t, mt, nt, z);
             if (nt != cur_nt) {
-                if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc, sub);
+                if (cur_nt >= 0) {
+                    p.template stash_bias<BN>(cc0, cc1, bacc, sub, sbias);
+                    p.template commit_bias<BN>(cur_nt, sbias);
+                }
                 cur_nt = nt;
             }
             const typename P::Pre cur = pre;
@@ -1372,7 +1412,10 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
                 if (REFS && stage_ref) tc::mbar_arrive(&rempty[acc]);
             }
         }
-        if (cur_nt >= 0) p.template flush_bias<BN>(cur_nt, cc0, cc1, bacc, sub);
+        if (cur_nt >= 0) {
+            p.template stash_bias<BN>(cc0, cc1, bacc, sub, sbias);
+            p.template commit_bias<BN>(cur_nt, sbias);
+        }
         if (STAGE && lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
     }
     tc::tc_fence_before();
@@ -1570,9 +1613,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                     if (part) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) __stcg(dst + (size_t)(cc * 32 + j) * ld, v[j]);
-                    } else {
+                    } else {  // RED (fire-and-forget): the launch's one contribution per element
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) dst[(size_t)(cc * 32 + j) * ld] += v[j];
+                        for (int j = 0; j < 32; ++j) atomicAdd(dst + (size_t)(cc * 32 + j) * ld, v[j]);
                     }
                 }
             }
@@ -2099,16 +2142,17 @@ void wgrad_boxes(WgradProb &p, bool m2, int bn) {
     p.nby = nby;
 }
 
-// dgrad bias gradients: rows of per-CTA partial column sums taken from the arena
+// dgrad bias gradients: one row of per-CTA column sums per CTA, taken from the arena
+// (s.slots = the shared-memory slots the CTA adds first: 4 lane quarters, x2 M halves in m2)
 void take_bias_rows(DgradProb &p, const ice::RowSched &s, ice::Arena &ar) {
     if (!p.db1 && !p.db2) return;
     p.bslots = s.slots;
-    p.bpart = ar.take<float>((size_t)s.G * s.slots * (p.c1 + p.c2) * 4);
+    p.bpart = ar.take<float>((size_t)s.G * (p.c1 + p.c2) * 4);
 }
 int finish_bias(const DgradProb &p, const ice::RowSched &s, cudaStream_t st) {
     if (!p.db1 && !p.db2) return 0;
     const ice::ColSegs segs{{p.db1, p.db2, nullptr, nullptr}, {p.c1, p.c2, 0, 0}};
-    return ice::colsum_finish(p.bpart, s.G * s.slots, p.c1 + p.c2, p.c1 + p.c2, segs, s, st);
+    return ice::colsum_finish(p.bpart, s.G, p.c1 + p.c2, p.c1 + p.c2, segs, s, st);
 }
 }  // namespace
 

@@ -50,10 +50,12 @@ struct ColSegs {
     int len[4];
 };
 
-// Which partial rows are valid.  bn == 0: all rows.  Otherwise rows are (CTA b, slot s) of a
-// persistent GEMM (row = b * slots + s; tile t -> (m = t % tm, n = (t / tm)) walked as
-// t = b, b + G, ...) and column c lives in tile column c / bn: CTA b holds a partial for it
-// only if it visited a tile of that column.
+// Which partial rows a column adds.  bn == 0: all rows.  Otherwise row b is the column sums
+// of CTA b of a persistent GEMM with G CTAs walking tiles t = b, b + G, ... (tile t ->
+// m = t % tm, n = t / tm); column c lives in tile column c / bn and only the CTAs that
+// visited a tile of it wrote that part of their row: the cyclic range (lo + k) mod G,
+// k < min(G, hi - lo), lo = n * tm, hi = min(lo + tm, ntiles), added in k order.
+// (slots: how many shared-memory rows each CTA added before storing -- informational.)
 struct RowSched {
     int G, slots, tm, ntiles, bn;
 };
