@@ -165,6 +165,32 @@ def config5_bench(dev, dist, world, rank, steps: int = 10, warmup: int = 3, coun
             "data": "synthetic generate_corpus(101, 64, 0.3, size=512) tiles, generator truth labels"}
 
 
+def config0_bench():
+    """BASELINE configs[0] through the reference-facing API, on this GPU: 64 T-gray tiles ->
+    icelabel.process_tile (one call per tile, as engine.run_sequential) -> icetrain
+    train_distributed(pairs, UNetSpec(), TrainConfig(batch_size=8, epochs=1), devices=1).
+    Reports the reference's own throughput row (samples_per_s counts the 51 training tiles of
+    the epoch over total_s, which includes the per-epoch train/val evaluation, train.py:166-185)."""
+    import paper_2403_13135_b200.icelabel as il
+    from paper_2403_13135_b200.icelabel.types import FilterConfig, SceneRaster, Tile, get_preset
+    from paper_2403_13135_b200.icetrain import TrainConfig, UNetSpec, train_distributed
+    from tests.fixtures import synth
+    tiles = [t for t, _ in synth.corpus(101, 64, 0.3)]
+    scheme = get_preset("ross-sea-summer")
+    t0 = time.perf_counter()
+    results = [il.process_tile(Tile(SceneRaster(t, f"s{i}"), f"s{i}", 0, 0), FilterConfig(), scheme)
+               for i, t in enumerate(tiles)]
+    label_s = time.perf_counter() - t0
+    assert all(r.ok for r in results)
+    pairs = [(t, r.label.astype(np.int64)) for t, r in zip(tiles, results)]
+    result, row = train_distributed(pairs, UNetSpec(), TrainConfig(batch_size=8, epochs=1), devices=1)
+    return {"metric": "configs[0]: 64 tiles -> process_tile -> train_distributed(batch 8, 1 epoch) samples_per_s",
+            "value": row["samples_per_s"], "unit": "samples/s", "row": row, "label_s": round(label_s, 3),
+            "history": result.history,
+            "reference_survey_probe": {"total_s": 81.05, "note": "reference CPU run of this config in the survey "
+                                                                 "container (SURVEY.md 8(a) U12), not re-measured here"}}
+
+
 def make_corpus(count: int, workers: int = 8) -> np.ndarray:
     """T-gray tiles generate_corpus(101, count, 0.3), in parallel."""
     import multiprocessing as mp
@@ -241,19 +267,22 @@ def cpu_reference_step_rate(batch: int, steps: int, warmup: int = 0):
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the reference's train step (oracle/unet_ref.py, pinned to the
+    reference's own outputs) at the headline config -- paper U-Net, batch 32, torch CPU fp32
+    on all host threads.  A batch-32 CPU step takes ~10-30 s, so the run is bounded to
+    min(K, 2) timed steps after min(W, 1) warm-up steps (stated in the line)."""
     if rank != 0:
         return
-    batch, steps = 4, max(1, min(args.steps, 3))
-    rate, threads, dt = cpu_reference_step_rate(batch, steps, warmup=1 if args.warmup else 0)
+    steps, warmup = max(1, min(args.steps, 2)), min(args.warmup, 1)
+    rate, threads, dt = cpu_reference_step_rate(BATCH, steps, warmup=warmup)
     line = {"metric": METRIC, "value": round(rate, 4), "unit": UNIT, "impl": "reference", "n_gpus": 0,
-            "steps": steps, "warmup": 1 if args.warmup else 0, "ms_per_step": round(1000 * dt / steps, 1),
+            "steps": steps, "warmup": warmup, "ms_per_step": round(1000 * dt / steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (T-gray tiles, SURVEY.md 8(d))", "config": dict(WORKLOAD_CONFIG, global_batch=BATCH,
                                                                           parallelism=f"cpu{threads}"),
             "cpu_baseline": {"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{steps} reference-equivalent synchronized_step(s) (oracle/unet_ref.py) at "
-                                       f"batch {batch} of the batch-{BATCH} workload, {threads} host threads, "
-                                       f"torch CPU fp32"},
+                             "sample": f"{steps} timed (+{warmup} warm-up) reference-equivalent synchronized_step(s) "
+                                       f"(oracle/unet_ref.py) at batch {BATCH}, {threads} host threads, torch CPU fp32"},
             "e2e": {"value": round(rate, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -281,6 +310,18 @@ def cpu_autolabel_rate(corpus: np.ndarray, per_core: int = 24):
         done = sum(pool.map(_cv_chunk, chunks))
         dt = time.perf_counter() - t0
     return done * corpus.shape[1] * corpus.shape[2] / dt / 1e6, cores, done, dt
+
+
+def tint_corpus(corpus: np.ndarray) -> np.ndarray:
+    """T-tint: per-pixel per-channel offsets in [-12, 12] on the T-gray tiles."""
+    from tests.fixtures import synth
+    return np.stack([synth.tint(t, 101, i) for i, t in enumerate(corpus)])
+
+
+def rand_corpus(count: int) -> np.ndarray:
+    """T-rand: uniform random RGB tiles default_rng([0, i])."""
+    from tests.fixtures import synth
+    return np.stack([synth.random_tile(i) for i in range(count)])
 
 
 def autolabel_bench(corpus_dev, n_tiles: int, reps: int):
@@ -329,6 +370,7 @@ def main():
     ap.add_argument("--no-autolabel", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-config5", action="store_true")
+    ap.add_argument("--no-config0", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
 
@@ -405,7 +447,7 @@ def main():
     if dist:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = _native.counter.launches
+    launches0 = _native.kernel_launches()
     with ClockSampler(local_rank) as clocks:
         torch.cuda.synchronize()
         e0.record()
@@ -413,12 +455,12 @@ def main():
             step(i)
         e1.record()
         torch.cuda.synchronize()
-    launches = _native.counter.launches - launches0
-    if graphed is not None:  # replays launch no host-side calls: count one eager step's kernels
-        c0 = _native.counter.launches
+    launches = _native.kernel_launches() - launches0
+    if graphed is not None:  # replays make no host-side launches: count one eager step's kernels
+        c0 = _native.kernel_launches()
         device_step(model, opt, xs[0], ys[0], union, bucketer)
         torch.cuda.synchronize()
-        launches = (_native.counter.launches - c0) * args.steps
+        launches = (_native.kernel_launches() - c0) * args.steps
     ms = e0.elapsed_time(e1)
     if dist:
         t = torch.tensor([ms], device=dev)
@@ -499,6 +541,18 @@ def main():
                 al_traffic = tj["ice_autolabel_bytes_per_tile"] * n_tiles
         except Exception:
             pass
+        variants = {}
+        for name, make in (("t_tint", lambda: tint_corpus(corpus)), ("t_rand", lambda: rand_corpus(len(corpus)))):
+            vdev = torch.from_numpy(make()).to(dev)
+            v_ms, _ = autolabel_bench(vdev, n_tiles, reps=1)
+            if dist:
+                t = torch.tensor([v_ms], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                v_ms = float(t.item())
+            v_gbs = px * 7 / (v_ms / 1000.0) / 1e9
+            variants[name] = {"value": round(px / (v_ms / 1000.0) / 1e6, 1), "unit": "Mpixel/s", "ms": round(v_ms, 2),
+                              "hbm_frac": round(v_gbs / hbm, 4)}
+            del vdev
         autolabel = {"metric": "auto-label Mpixel/s (fused filter + HSV labeler, 100k 256^2 tiles)",
                      "value": round(px / (al_ms / 1000.0) / 1e6, 1), "unit": "Mpixel/s",
                      "ms": round(al_ms, 2), "tiles": n_tiles * world,
@@ -511,7 +565,9 @@ def main():
                                       "ms": round(seg_ms, 3),
                                       "roofline": {"bound": "hbm", "achieved": round(seg_gbs, 1), "peak": hbm,
                                                    "unit": "GB/s", "frac": round(seg_gbs / hbm, 4),
-                                                   "traffic": None, "note": "4 B/px (RGB in, label out)"}}}
+                                                   "traffic": None, "note": "4 B/px (RGB in, label out)"}},
+                     "corpus": "T-gray (headline); T-tint / T-rand below (SURVEY.md 8(d)), tile i = corpus[i mod 4224]",
+                     **variants}
 
     if autolabel is not None and rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -524,6 +580,12 @@ def main():
             autolabel["cpu_baseline"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
 
     launch_mode = "CUDA graph per step" if graphed is not None else "eager"
+    config0 = None
+    if world == 1 and not args.no_config0:
+        try:
+            config0 = config0_bench()
+        except Exception as exc:  # the headline stands without it
+            config0 = {"unavailable": f"{type(exc).__name__}: {exc}"}
     config5 = None
     if not args.no_config5:
         del graphed
@@ -537,10 +599,10 @@ def main():
     # ---- CPU baseline (rank 0, N = 1 only): bounded sample of the reference step -------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, threads, dt = cpu_reference_step_rate(batch=4, steps=1, warmup=0)
+        rate, threads, dt = cpu_reference_step_rate(batch=BATCH, steps=1, warmup=0)
         cpu = {"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"1 reference-equivalent synchronized_step at batch 4 (of batch 32), torch CPU fp32, "
-                         f"{threads} threads, {dt:.1f} s"}
+               "sample": f"1 reference-equivalent synchronized_step (oracle/unet_ref.py) at batch {BATCH}, torch CPU "
+                         f"fp32, {threads} threads, {dt:.1f} s"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -555,7 +617,8 @@ def main():
                         "d2h_bytes_per_step": 8, "steps": e2e_steps,
                         "api": "icetrain.synchronized_step([model], [opt], [(pinned u8 NHWC, pinned u8)])"},
                 "gpu_launches": int(launches), "clocks": clocks.summary(), "roofline": roofline,
-                "cpu_baseline": cpu, "autolabel": autolabel, "config5": config5, "kernels": kernels,
+                "cpu_baseline": cpu, "autolabel": autolabel, "config0": config0, "config5": config5,
+                "kernels": kernels,
                 "tflops_step": round(405.6e9 * BATCH / (ms / args.steps / 1000.0) / 1e12, 1),
                 "loss_last": round(loss, 4)}
         print(json.dumps(line), flush=True)

@@ -4,10 +4,12 @@ batch 8, seed 0, on T-gray tiles labelled by the reference auto-labeler (north_s
 after 200 steps on the same seed and batch order must agree within 2%").
 
 Also records the reference's OWN sensitivity at this config: the same 200 steps from initial
-weights perturbed by 1e-6 (relative, fp32 rounding scale) with a few seeds.  The GPU test
-compares against the unperturbed run and reports the spread beside it.
+weights perturbed by 1e-6 (relative, fp32 rounding scale) with 8 seeds.  The reference is
+chaotic here: its own perturbed runs leave the 2% band around the unperturbed losses after
+~16 steps, so the GPU test holds the early steps to 2% and the late-training level (mean of
+the last 50 step losses, final whole-corpus eval loss) to the reference's own spread.
 
-Run in the build container (/root/reference present; ~10 min on 8 cores):
+Run in the build container (/root/reference present; ~25 min on 8 cores):
 
     python tests/golden/make_desk_trajectory.py [--spread N]
 """
@@ -62,24 +64,29 @@ def run(x, y, perturb_seed=None):
     t0 = time.time()
     for k, idx in enumerate(batch_order()):
         losses.append(synchronized_step([model], [opt], [(x[idx], y[idx])])[0])
-        if k % 20 == 0:
+        if k % 50 == 0:
             print(f"  step {k} loss {losses[-1]:.5f} ({time.time() - t0:.0f} s)", flush=True)
-    return losses
+    model.eval()
+    with torch.no_grad():  # whole-corpus loss of the trained model (eval mode), in batches of 32
+        tot = sum(float(torch.nn.functional.cross_entropy(model(x[i:i + 32]), y[i:i + 32], reduction="sum"))
+                  for i in range(0, len(x), 32))
+    return losses, tot / y.numel()
 
 
 def main():
     torch.set_num_threads(os.cpu_count())
-    spread = int(sys.argv[sys.argv.index("--spread") + 1]) if "--spread" in sys.argv else 2
+    spread = int(sys.argv[sys.argv.index("--spread") + 1]) if "--spread" in sys.argv else 8
     x_u8, y = reference_corpus()
     x = torch.from_numpy(x_u8).permute(0, 3, 1, 2).float() / 255.0
     yt = torch.from_numpy(y.astype(np.int64))
-    losses = run(x, yt)
+    losses, eval_loss = run(x, yt)
     spreads = [run(x, yt, perturb_seed=1000 + k) for k in range(spread)]
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "desk_trajectory.pt")
-    torch.save({"spec": SPEC, "seed": SEED, "losses": losses, "perturbed": spreads,
+    torch.save({"spec": SPEC, "seed": SEED, "losses": losses, "eval_loss": eval_loss,
+                "perturbed": [s[0] for s in spreads], "perturbed_eval": [s[1] for s in spreads],
                 "tiles_sha": sha(x_u8), "labels_sha": sha(y)}, path)
-    print("wrote", path, "first", losses[0], "last", losses[-1],
-          "perturbed last", [s[-1] for s in spreads])
+    print("wrote", path, "first", losses[0], "last", losses[-1], "eval", eval_loss,
+          "perturbed last", [s[0][-1] for s in spreads], "perturbed eval", [s[1] for s in spreads])
 
 
 if __name__ == "__main__":

@@ -184,49 +184,47 @@ def test_checkpoint_layout_is_the_reference_layout(tmp_path):
         assert torch.equal(v, payload["state"][k])
 
 
-def test_loss_trajectory_200_steps():
-    """north_star: loss after 200 steps on the same seed and batch order vs the reference CPU
-    fp32 trainer (tests/golden/unet_trajectory.pt: the reference's own toy parity setup).
+def test_loss_after_200_steps_desk_config():
+    """north_star: "loss after 200 steps on the same seed and batch order must agree within 2%",
+    at SURVEY.md 8(d).4's parity config -- UNetSpec(256, base_channels=16, dropout=0.0), batch 8,
+    seed 0, 256 T-gray tiles labelled by the auto-labeler -- against the reference CPU fp32
+    trainer (tests/golden/desk_trajectory.pt, made by tests/golden/make_desk_trajectory.py from
+    /root/reference).  One run, no retries: the B200 train step is bit-reproducible.
 
-    Batch-4 training of this toy net is chaotic: once the loss starts falling, rounding
-    differences alone change which plateau each step lands on.  Perturbing the reference's
-    own initial weights by 1e-6 (relative) spreads ITS final eval loss over 0.014-0.057 and
-    its last-50-step train loss over 0.017-0.19 (measured, 8 runs, oracle/unet_ref.py on the
-    CPU); our weight gradients reduce split-K partials with fp32 atomics, so every run is such
-    a perturbation and a minority of runs (~20%) hit a late Adam spike.  So the test asserts
-      * step-by-step agreement within 2% for the first 20 steps (observed: ~0.3%), and
-      * after 200 steps, the whole-corpus eval loss reaches the reference's level: in the best
-        of up to three runs (same seed and batch order) the best of the last 10 steps is
-        within 3x of the reference's final eval loss, with >= 98% pixel accuracy."""
+    The reference is chaotic at this config: from initial weights perturbed by 1e-6 (fp32
+    rounding scale) its own runs leave the 2% band after ~16 steps and end 5-20% apart (the
+    golden records 8 such runs).  So: the first 10 steps within 2%; the late-training level --
+    the mean of the last 50 step losses and the final whole-corpus eval loss -- within 2% or,
+    where the reference's own perturbed runs scatter wider, within that scatter."""
+    import hashlib
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(__file__)))
+    from paper_2403_13135_b200 import icelabel as il
     from paper_2403_13135_b200.icetrain.train import evaluate
-    from tests.golden.trajectory_data import SEED, batch_order, corpus
-    gold = torch.load(os.path.join(os.path.dirname(__file__), "golden", "unet_trajectory.pt"))
-    spec = UNetSpec(**gold["spec"])
-    x_u8, y = corpus()
-    x = torch.from_numpy(x_u8)
-    yt = torch.from_numpy(y.astype("uint8"))
-    xc, yc = x.cuda(), yt.cuda()
+    from tests.fixtures import synth
+    from tests.golden.desk_trajectory_data import N_TILES, SEED, SPEC, batch_order
+    gold = torch.load(os.path.join(os.path.dirname(__file__), "golden", "desk_trajectory.pt"))
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    tiles = np.stack([t for t, _ in synth.corpus(101, N_TILES, 0.3)])
+    assert sha(tiles) == gold["tiles_sha"]  # the reference's corpus, byte for byte
+    x = torch.from_numpy(tiles).cuda()
+    y = il.autolabel(x)["label"]
+    assert sha(y.cpu().numpy()) == gold["labels_sha"]  # the reference's labels, byte for byte
+    torch.manual_seed(SEED)
+    model = UNet(UNetSpec(**SPEC))
+    opt = Adam(model.parameters(), lr=1e-3)
+    ours = [synchronized_step([model], [opt], [(x[idx.cuda()], y[idx.cuda()])])[0] for idx in batch_order()]
     ref = gold["losses"]
-    order = batch_order()
-    runs = []
-    for attempt in range(3):
-        torch.manual_seed(SEED)
-        model = UNet(spec)
-        opt = Adam(model.parameters(), lr=1e-3)
-        ours, evals = [], []
-        for k, idx in enumerate(order):
-            ours.append(synchronized_step([model], [opt], [(x[idx], yt[idx])])[0])
-            if k >= len(order) - 10:
-                evals.append(evaluate(model, xc, yc, 32))
-        for k in range(20):
-            assert abs(ours[k] - ref[k]) / ref[k] < 0.02, (attempt, k, ours[k], ref[k])
-        best = min(evals)
-        runs.append(best)
-        if best[0] <= 3.0 * gold["eval_loss"] and best[1] >= 0.98:
-            return
-    raise AssertionError((runs, gold["eval_loss"]))
+    for k in range(10):
+        assert abs(ours[k] - ref[k]) / ref[k] < 0.02, (k, ours[k], ref[k])
+    late = lambda ls: float(np.mean(ls[-50:]))  # noqa: E731
+    ref_late = late(ref)
+    band = max([0.02 * ref_late] + [abs(late(p) - ref_late) for p in gold["perturbed"]])
+    assert abs(late(ours) - ref_late) <= band, (late(ours), ref_late, band)
+    ev = evaluate(model, x, y, 32)[0]
+    ref_ev = gold["eval_loss"]
+    band_ev = max([0.02 * ref_ev] + [abs(p - ref_ev) for p in gold["perturbed_eval"]])
+    assert abs(ev - ref_ev) <= band_ev, (ev, ref_ev, band_ev)
 
 
 def test_config5_512_tiles_forward_and_grads_match_oracle():
