@@ -266,6 +266,18 @@ int ice_decode_labels(const uint8_t *rgb, int64_t npx, const uint8_t *colors, in
 int ice_head_argmax(const uint16_t *h, int64_t npx, const float *w_out, const float *b_out, uint8_t *mask,
                     void *stream);
 
+/* parse_labels(snap=True) (icelabel/segmentation.py:140-157): RGB u8 [npx][3] -> class index of
+ * the nearest colour of colors u8 [ncls][3] in squared RGB distance (ties: earlier class). */
+int ice_snap_labels(const uint8_t *rgb, int64_t npx, const uint8_t *colors, int32_t ncls, uint8_t *mask,
+                    void *stream);
+
+/* ssim (icelabel/metrics.py:153-172): a, b u8 [h][w][3]; window = the 11 x 11 normalised Gaussian
+ * (float64, DEVICE memory); sums[c] (float64, device) = sum over the valid positions of channel c
+ * of num / den in float64 (the caller divides by (h - 10) * (w - 10) and averages the channels).
+ * Block sums are added in a fixed order (deterministic).  Needs scratch (see above). */
+int ice_ssim(const uint8_t *a, const uint8_t *b, int32_t h, int32_t w, const double *window, double c1,
+             double c2, double *sums, void *scratch, uint64_t *scratch_bytes, void *stream);
+
 /* confusion (icelabel/metrics.py:108-113): counts u64 [k][k] += #(pred == a, ref == b),
  * k <= 4; pixels with a label >= k are added to *bad instead. */
 int ice_confusion(const uint8_t *pred, const uint8_t *ref, int64_t npx, int32_t k, uint64_t *counts, uint64_t *bad,

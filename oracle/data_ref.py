@@ -46,3 +46,28 @@ def decode_labels(img):  # icetrain/data.py:35-44 (returns -1 at unknown colours
 
 def confusion(pred, ref, n=3):  # icelabel/metrics.py:108-113
     return np.bincount(pred.astype(np.int64).ravel() * n + ref.ravel(), minlength=n * n).reshape(n, n)
+
+
+def snap_labels(img):  # icelabel/segmentation.py:138-157 with snap=True
+    colors = np.asarray(CLASS_COLORS, np.int64)
+    flat = img.reshape(-1, 3).astype(np.int64)
+    dist = ((flat[:, None, :] - colors[None, :, :]) ** 2).sum(axis=2)
+    return dist.argmin(axis=1).reshape(img.shape[:2]).astype(np.uint8)
+
+
+def ssim(a, b, window=11, sigma=1.5):  # icelabel/metrics.py:145-172
+    from scipy.signal import convolve2d
+    x = np.arange(window) - (window - 1) / 2
+    g = np.exp(-(x ** 2) / (2 * sigma ** 2))
+    k = np.outer(g, g)
+    k = k / k.sum()
+    c1, c2 = (0.01 * 255) ** 2, (0.03 * 255) ** 2
+    scores = []
+    for ch in range(3):
+        p, q = a[:, :, ch].astype(np.float64), b[:, :, ch].astype(np.float64)
+        mx, my = convolve2d(p, k, mode="valid"), convolve2d(q, k, mode="valid")
+        vx = convolve2d(p * p, k, mode="valid") - mx ** 2
+        vy = convolve2d(q * q, k, mode="valid") - my ** 2
+        cov = convolve2d(p * q, k, mode="valid") - mx * my
+        scores.append(float(np.mean((2 * mx * my + c1) * (2 * cov + c2) / ((mx ** 2 + my ** 2 + c1) * (vx + vy + c2)))))
+    return float(np.mean(scores))

@@ -55,6 +55,8 @@ SIGNATURES = {
     "ice_decode_labels": [_V, _I64, _V, _I32, _V, _V, _V],
     "ice_head_argmax": [_V, _I64, _V, _V, _V, _V],
     "ice_confusion": [_V, _V, _I64, _I32, _V, _V, _V],
+    "ice_snap_labels": [_V, _I64, _V, _I32, _V, _V],
+    "ice_ssim": [_V, _V, _I32, _I32, _V, ctypes.c_double, ctypes.c_double, _V, *_S, _V],
     "ice_segment": [_V, _I64, _I32, _I32, ctypes.POINTER(IceScheme), _V, _V, _V, _V],
     "ice_rgb_to_hsv": [_V, _I64, _V, _V],
     "ice_conv_fprop": [_V, _I32, _V, _I32, _I32, _I32, _I32, _I32, _V, _V, _I32, _I32, _V, _V, _V, *_S, _V],

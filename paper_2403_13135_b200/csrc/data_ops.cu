@@ -127,7 +127,127 @@ __global__ void confusion_kernel(const uint8_t *__restrict__ pred, const uint8_t
     if (threadIdx.x == 16 && h[16]) atomicAdd(bad, (unsigned long long)h[16]);
 }
 
+// parse_labels(snap=True) (segmentation.py:140-157): nearest colormap colour in squared RGB
+// distance, ties to the earlier class (argmin keeps the first minimum)
+__global__ void snap_kernel(const uint8_t *__restrict__ rgb, long long npx, const uint8_t *__restrict__ colors,
+                            int ncls, uint8_t *__restrict__ mask) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < npx; p += (long long)gridDim.x * blockDim.x) {
+        const int r = rgb[3 * p], g = rgb[3 * p + 1], b = rgb[3 * p + 2];
+        int best = 0, bd = 0x7fffffff;
+        for (int i = 0; i < ncls; ++i) {
+            const int dr = r - colors[3 * i], dg = g - colors[3 * i + 1], db = b - colors[3 * i + 2];
+            const int d = dr * dr + dg * dg + db * db;
+            if (d < bd) {
+                bd = d;
+                best = i;
+            }
+        }
+        mask[p] = (uint8_t)best;
+    }
+}
+
+// ---- SSIM (icelabel/metrics.py:145-172): single-scale, 11 x 11 Gaussian window (sigma 1.5),
+// "valid" positions, per channel mean of num / den, float64 like the reference.  Block =
+// SSIM_TX x SSIM_TY valid output positions of one channel: the (TX + 10) x (TY + 10) input
+// patches of both images are staged in shared memory, each thread forms the five windowed
+// moments of its position with the 121 weights (host-computed in float64, as numpy does), and
+// the block's sum of num/den goes to part[blockIdx] (fixed-order finish: deterministic).
+constexpr int SSIM_K = 11, SSIM_TX = 32, SSIM_TY = 8;
+__constant__ double c_ssim_w[SSIM_K * SSIM_K];
+
+__global__ void __launch_bounds__(SSIM_TX * SSIM_TY) ssim_kernel(const uint8_t *__restrict__ a,
+                                                                 const uint8_t *__restrict__ b, int h, int w,
+                                                                 double c1, double c2, double *__restrict__ part) {
+    __shared__ double sa[SSIM_TY + SSIM_K - 1][SSIM_TX + SSIM_K - 1];
+    __shared__ double sb[SSIM_TY + SSIM_K - 1][SSIM_TX + SSIM_K - 1];
+    __shared__ double red[SSIM_TX * SSIM_TY / 32];
+    const int ch = blockIdx.z;
+    const int x0 = blockIdx.x * SSIM_TX, y0 = blockIdx.y * SSIM_TY;
+    const int vw = w - SSIM_K + 1, vh = h - SSIM_K + 1;  // valid output extent
+    for (int i = threadIdx.x; i < (SSIM_TY + SSIM_K - 1) * (SSIM_TX + SSIM_K - 1); i += blockDim.x) {
+        const int yy = i / (SSIM_TX + SSIM_K - 1), xx = i % (SSIM_TX + SSIM_K - 1);
+        const int gy = min(y0 + yy, h - 1), gx = min(x0 + xx, w - 1);
+        const size_t o = ((size_t)gy * w + gx) * 3 + ch;
+        sa[yy][xx] = (double)a[o];
+        sb[yy][xx] = (double)b[o];
+    }
+    __syncthreads();
+    const int tx = threadIdx.x % SSIM_TX, ty = threadIdx.x / SSIM_TX;
+    double v = 0.0;
+    if (x0 + tx < vw && y0 + ty < vh) {
+        double mx = 0, my = 0, xx2 = 0, yy2 = 0, xy = 0;
+        for (int i = 0; i < SSIM_K; ++i)
+#pragma unroll
+            for (int j = 0; j < SSIM_K; ++j) {
+                const double k = c_ssim_w[i * SSIM_K + j];
+                const double p = sa[ty + i][tx + j], q = sb[ty + i][tx + j];
+                mx += k * p;
+                my += k * q;
+                xx2 += k * (p * p);
+                yy2 += k * (q * q);
+                xy += k * (p * q);
+            }
+        const double vx = xx2 - mx * mx, vy = yy2 - my * my, cov = xy - mx * my;
+        const double num = (2 * mx * my + c1) * (2 * cov + c2);
+        const double den = (mx * mx + my * my + c1) * (vx + vy + c2);
+        v = num / den;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < SSIM_TX * SSIM_TY / 32; ++k) t += red[k];
+        part[((size_t)ch * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+// per channel: sum of the block partials in block order
+__global__ void ssim_finish(const double *__restrict__ part, int blocks_per_ch, double *__restrict__ sums) {
+    __shared__ double red[256];
+    const int ch = blockIdx.x;
+    double t = 0.0;
+    for (int i = threadIdx.x; i < blocks_per_ch; i += 256) t += part[(size_t)ch * blocks_per_ch + i];
+    red[threadIdx.x] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int k = 0; k < 256; ++k) s += red[k];
+        sums[ch] = s;
+    }
+}
+
 }  // namespace
+
+extern "C" int ice_snap_labels(const uint8_t *rgb, int64_t npx, const uint8_t *colors, int32_t ncls, uint8_t *mask,
+                               void *stream) {
+    if (npx < 0 || ncls < 1 || ncls > 255 || (npx > 0 && (!mask || !colors || !rgb))) return ICE_EINVAL;
+    if (npx == 0) return ICE_OK;
+    snap_kernel<<<grid_for(npx), NT, 0, (cudaStream_t)stream>>>(rgb, npx, colors, ncls, mask);
+    ice::count_launch();
+    return (int)cudaGetLastError();
+}
+
+extern "C" int ice_ssim(const uint8_t *a, const uint8_t *b, int32_t h, int32_t w, const double *window, double c1,
+                        double c2, double *sums, void *scratch, uint64_t *scratch_bytes, void *stream) {
+    if (!a || !b || !window || !sums || h < SSIM_K || w < SSIM_K) return ICE_EINVAL;
+    ice::Arena ar(scratch, scratch_bytes);
+    const dim3 grid((w - SSIM_K + 1 + SSIM_TX - 1) / SSIM_TX, (h - SSIM_K + 1 + SSIM_TY - 1) / SSIM_TY, 3);
+    const int per_ch = (int)(grid.x * grid.y);
+    double *part = ar.take<double>((size_t)3 * per_ch * 8);
+    const int q = ar.settle(scratch_bytes);
+    if (q) return q > 0 ? ICE_OK : ICE_ESCRATCH;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyToSymbolAsync(c_ssim_w, window, sizeof(double) * SSIM_K * SSIM_K, 0,
+                                            cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return (int)e;
+    ssim_kernel<<<grid, SSIM_TX * SSIM_TY, 0, st>>>(a, b, h, w, c1, c2, part);
+    ice::count_launch();
+    ssim_finish<<<3, 256, 0, st>>>(part, per_ch, sums);
+    ice::count_launch();
+    return (int)cudaGetLastError();
+}
 
 extern "C" int ice_cut_tiles(const uint8_t *img, int32_t h, int32_t w, int32_t c, int32_t size, uint8_t *tiles,
                              void *stream) {

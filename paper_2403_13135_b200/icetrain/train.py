@@ -320,16 +320,45 @@ def evaluate(model: UNet, x: torch.Tensor, y: torch.Tensor, batch: int) -> tuple
     return loss_sum / pixels, correct / pixels
 
 
-def _fit(pairs: list, spec: UNetSpec, config: TrainConfig, replicas: int) -> tuple:
-    _validate_pairs(pairs, spec)
+def _validate_device(x, y, spec: UNetSpec) -> None:
+    """_validate_pairs for a device corpus: u8 [n, h, w, 3] tiles, [n, h, w] class ids."""
+    if x.ndim != 4 or len(x) == 0:
+        raise ValueError("training corpus is empty" if x.ndim == 4 else f"expected (n, h, w, 3) tiles, got {tuple(x.shape)}")
+    if x.dtype != torch.uint8 or not x.is_cuda:
+        raise ValueError("device corpus tiles must be a uint8 CUDA tensor")
+    if tuple(y.shape) != tuple(x.shape[:3]):
+        raise ValueError(f"labels {tuple(y.shape)} do not match tiles {tuple(x.shape)}")
+    step = 2 ** spec.depth
+    if x.shape[3] != spec.in_channels or x.shape[1] % step or x.shape[2] % step:
+        raise ValueError(f"tile shape {tuple(x.shape[1:])} does not fit the model "
+                         f"(needs {spec.in_channels} channels, dims divisible by {step})")
+    if int(y.max()) >= spec.classes or (y.dtype.is_signed and int(y.min()) < 0):
+        raise ValueError(f"class index out of range for {spec.classes} classes")
+    check_tile(x.shape[1], x.shape[2], spec.depth)
+
+
+def _fit(pairs, spec: UNetSpec, config: TrainConfig, replicas: int, device_corpus=None) -> tuple:
+    """train.py:137-185.  `pairs` (host (tile, mask) list, the reference's input) or
+    `device_corpus` = (u8 [n, h, w, 3], [n, h, w]) already resident in HBM (K1 output)."""
+    device = torch.device("cuda", torch.cuda.current_device())
+    if device_corpus is None:
+        _validate_pairs(pairs, spec)
+    else:
+        _validate_device(*device_corpus, spec)
     torch.manual_seed(config.seed)
-    train_pairs, val_pairs = train_val_split(pairs, config.val_fraction, config.seed)
+    if device_corpus is None:
+        train_pairs, val_pairs = train_val_split(pairs, config.val_fraction, config.seed)
+        x_train, y_train = _device_corpus(train_pairs, device)
+        x_val, y_val = _device_corpus(val_pairs, device) if val_pairs else (None, None)
+    else:  # the same seeded split, on indices; the tiles never leave the GPU
+        x_all, y_all = device_corpus
+        tr, va = train_val_split(list(range(len(x_all))), config.val_fraction, config.seed)
+        pick = lambda t, idx: t[torch.as_tensor(idx, device=t.device)].contiguous()  # noqa: E731
+        x_train, y_train = pick(x_all, tr), pick(y_all, tr).to(torch.uint8)
+        x_val, y_val = (pick(x_all, va), pick(y_all, va).to(torch.uint8)) if va else (None, None)
     dist = _dist()
     rank = dist.get_rank() if dist else 0
     world = dist.get_world_size() if dist else 1
-    device = torch.device("cuda", torch.cuda.current_device())
-    x_train, y_train = _device_corpus(train_pairs, device)
-    x_val, y_val = _device_corpus(val_pairs, device) if val_pairs else (None, None)
 
     local = replicas if dist is None else 1
     models = [UNet(spec, device)]
@@ -380,6 +409,14 @@ def _fit(pairs: list, spec: UNetSpec, config: TrainConfig, replicas: int) -> tup
 def train(pairs: list, spec: UNetSpec, config: TrainConfig) -> TrainResult:
     result, _ = _fit(pairs, spec, config, replicas=1)
     return result
+
+
+def train_device(tiles, labels, spec: UNetSpec, config: TrainConfig, devices: int = 1) -> tuple:
+    """train / train_distributed on a corpus already in HBM -- e.g. icelabel.autolabel's
+    labels of icelabel.tiling.split_scene_device tiles (K1 -> training
+    with no host round trip).  Same split, shuffle, steps and history as train() on the
+    equivalent host pairs.  Returns (TrainResult, throughput row)."""
+    return _fit(None, spec, config, _available_replicas(config, devices), device_corpus=(tiles, labels))
 
 
 def _available_replicas(config: TrainConfig, requested: int) -> int:

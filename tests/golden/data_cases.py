@@ -22,3 +22,23 @@ def pred_ref(seed=7, n=4096):
     flip = rng.random(ref.shape) < 0.3
     pred[flip] = rng.integers(0, 3, int(flip.sum())).astype(np.uint8)
     return pred, ref
+
+
+def noisy_colors(h, w, seed=8):
+    """Colormap colours with +-60 per-channel noise (parse_labels snap=True / error cases)."""
+    rng = np.random.default_rng([seed, h, w])
+    cols = np.array([(255, 0, 0), (0, 0, 255), (0, 255, 0)], np.int16)
+    img = cols[rng.integers(0, 3, (h, w))] + rng.integers(-60, 61, (h, w, 3))
+    img[0, :3] = [(128, 128, 0), (0, 128, 128), (128, 0, 128)]  # equidistant ties
+    return np.clip(img, 0, 255).astype(np.uint8)
+
+
+def ssim_pairs():
+    """(name, a, b) u8 images for SSIM: identical, noisy copy, unrelated, minimum size."""
+    a = scene(64, 80, seed=11)
+    rng = np.random.default_rng(12)
+    noisy = np.clip(a.astype(np.int16) + rng.integers(-20, 21, a.shape), 0, 255).astype(np.uint8)
+    smooth = np.repeat(np.repeat(scene(8, 10, seed=13), 8, axis=0), 8, axis=1)
+    return [("same", a, a.copy()), ("noisy", a, noisy), ("unrelated", a, scene(64, 80, seed=14)),
+            ("smooth", smooth, np.clip(smooth.astype(np.int16) + 3, 0, 255).astype(np.uint8)),
+            ("min", scene(11, 11, seed=15), scene(11, 11, seed=16))]

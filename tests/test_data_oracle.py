@@ -49,3 +49,17 @@ def test_train_val_split_matches_reference():
     import pytest
     with pytest.raises(ValueError, match="val_fraction"):
         train_val_split([1, 2], 1.0, 0)
+
+
+def test_snap_and_ssim_oracle_match_reference():
+    assert sha(orc.snap_labels(dc.noisy_colors(64, 48))) == GOLDEN["parse_snap"]
+    for rec, (name, a, b) in zip(GOLDEN["ssim"], dc.ssim_pairs()):
+        assert rec["case"] == name
+        assert abs(orc.ssim(a, b) - rec["value"]) <= 1e-12, name
+
+
+def test_split_scene_oracle_matches_reference():
+    for rec in GOLDEN["split_scene"]:
+        tiles = orc.cut_tiles(dc.scene(rec["h"], rec["w"]), rec["tile_size"])
+        assert [[sha(t), r, c] for t, r, c in tiles] == [x[:3] for x in rec["tiles"]]
+        assert (rec["rows"], rec["cols"]) == (1 + tiles[-1][1], 1 + tiles[-1][2])
