@@ -58,8 +58,9 @@ def install(engine, chunk_size: int = DEFAULT_CHUNK):
     """Point a reference `icelabel.engine` module (or any namespace with the same names) at the
     GPU executor: `process_tile` becomes the GPU drop-in and `run_sequential(job)` labels the
     job's tiles in chunks.  Returns the replaced attributes, for `uninstall`."""
-    saved = {"process_tile": getattr(engine, "process_tile", None),
-             "run_sequential": getattr(engine, "run_sequential", None)}
+    missing = object()
+    saved = {n: getattr(engine, n, missing) for n in ("process_tile", "run_sequential")}
+    saved = {n: (v is not missing, None if v is missing else v) for n, v in saved.items()}
     engine.process_tile = process_tile
     load_tiles, timing_cls, outcome_cls = (getattr(engine, n, None) for n in ("load_tiles", "PhaseTiming",
                                                                                "RunOutcome"))
@@ -80,6 +81,9 @@ def install(engine, chunk_size: int = DEFAULT_CHUNK):
 
 
 def uninstall(engine, saved: dict) -> None:
-    for name, value in saved.items():
-        if value is not None:
+    """Restore what `install` replaced (attributes it created are removed)."""
+    for name, (present, value) in saved.items():
+        if present:
             setattr(engine, name, value)
+        elif hasattr(engine, name):
+            delattr(engine, name)
