@@ -514,6 +514,31 @@ class UNetEngine:
         return L.w_off, L.b_off + L.cout_p
 
 
+class ParamList(list):
+    """UNet.parameters(): one torch.nn.Parameter per reference parameter (state_dict order),
+    each a VIEW of the engine's flat fp32 master buffer in its physical layout (KRSC, channels
+    padded to 64 -- padded entries are zero and get zero gradients), with `.grad` a view of the
+    flat gradient buffer.  So any torch optimizer can step them in place
+    (`torch.optim.SGD(m.parameters(), lr)` as in the reference's own tests); synchronized_step
+    then refreshes the bf16 working weights.  `.engine` lets the fused Adam find its buffers."""
+
+    def __init__(self, engine):
+        super().__init__()
+        self.engine = engine
+        for L in engine.layers:
+            for view, grad in ((engine.w(L.name), engine.w(L.name, engine.grads)),
+                               (engine.b(L.name), engine.b(L.name, engine.grads))):
+                prm = torch.nn.Parameter(view, requires_grad=True)
+                prm.grad = grad
+                self.append(prm)
+        self._grads = [p.grad for p in self]
+
+    def attach_grads(self) -> None:
+        """Re-point every .grad at its flat-buffer view (after a zero_grad(set_to_none=True))."""
+        for prm, g in zip(self, self._grads):
+            prm.grad = g
+
+
 class UNet:
     """Drop-in for icetrain.model.UNet (model.py:91-137) running on the B200 engine."""
 
@@ -524,6 +549,7 @@ class UNet:
         self.engine = UNetEngine(spec, device)
         self.engine.load_state_dict(params)
         self.training = True
+        self._params = None
 
     # nn.Module-like surface
     def train(self, mode: bool = True):
@@ -546,8 +572,18 @@ class UNet:
                                f"unexpected keys {unexpected}")
         self.engine.load_state_dict(sd)
 
-    def parameters(self):
-        return [self.engine]
+    def parameters(self) -> ParamList:
+        if self._params is None:
+            self._params = ParamList(self.engine)
+        return self._params
+
+    def zero_grad(self, set_to_none: bool = True) -> None:
+        """nn.Module.zero_grad: the engine accumulates into one flat buffer, which is zeroed."""
+        self.engine.zero_grad()
+
+    def named_parameters(self):
+        names = [L.name + s for L in self.engine.layers for s in (".weight", ".bias")]
+        return list(zip(names, self.parameters()))
 
     def conv_layer_count(self) -> int:
         return len(self.engine.layers)
@@ -558,13 +594,17 @@ class UNet:
         check_tile(x.shape[2], x.shape[3], self.spec.depth)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        """Class logits (n, classes, h, w) fp32, on x's device.  Inference semantics
-        (Dropout2d only acts in train mode, as in the reference's model.train())."""
+        """Class logits (n, classes, h, w) fp32, on x's device (model.py:111-130).  In train mode
+        (the default, as an nn.Module) Dropout2d drops whole (sample, channel) planes with a
+        mask seeded from torch's default generator (so torch.manual_seed fixes it); eval()
+        makes the forward deterministic, as the reference's model.eval()."""
         self._check(x)
         dev = x.device
         xin = x.detach().to(self.engine.device, torch.float32).permute(0, 2, 3, 1).contiguous()
         n, h, w = xin.shape[0], xin.shape[1], xin.shape[2]
-        A = self.engine.forward(xin, train=False, float_input=True)
+        drop = self.training and self.spec.dropout > 0
+        seed = int(torch.randint(0, 2 ** 62, (1,)).item()) if drop else 0
+        A = self.engine.forward(xin, train=drop, seed=seed, float_input=True)
         logits = torch.empty((n, h, w, 3), dtype=torch.float32, device=self.engine.device)
         labels = torch.zeros((n, h, w), dtype=torch.uint8, device=self.engine.device)
         A.stats.zero_()

