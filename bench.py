@@ -137,7 +137,7 @@ def config5_bench(dev, dist, world, rank, steps: int = 10, warmup: int = 3, coun
            for _ in range(warmup + steps)]
     xs = [x_all[i].contiguous() for i in idx]
     ys = [y_all[i].contiguous() for i in idx]
-    graphed = GraphedStep(model, opt, xs[0], ys[0], union, bucketer) if world == 1 else None
+    graphed = GraphedStep(model, opt, xs[0], ys[0], union, bucketer) if not os.environ.get("ICE_NO_GRAPH") else None
     run = (lambda i: graphed(xs[i], ys[i])) if graphed else (lambda i: device_step(model, opt, xs[i], ys[i], union, bucketer))
     for i in range(warmup):
         run(i)
@@ -394,6 +394,9 @@ def main():
     if world > 1:
         import torch.distributed as tdist
         backend = os.environ.get("ICE_DIST_BACKEND", "nccl")
+        # NCCL's init lines (ranks, channels, NVLS / NVLink transport) on stderr as evidence
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         tdist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
         dist = tdist
     _native.require_cuda()
@@ -415,7 +418,9 @@ def main():
     # optimizer-in-backward: each gradient bucket is (all-reduced and) Adam-stepped on a side
     # stream as soon as backward completes it
     bucket_mb = int(os.environ.get("ICE_BUCKET_MB", "64" if dist else str(SINGLE_GPU_BUCKET >> 20)))
-    bucketer = GradBucketer(model.engine, bucket_bytes=bucket_mb << 20, optimizer=opt)
+    comm_bf16 = bool(os.environ.get("ICE_COMM_BF16"))
+    bucketer = GradBucketer(model.engine, bucket_bytes=bucket_mb << 20, optimizer=opt,
+                            comm_dtype=torch.bfloat16 if comm_bf16 else None)
     union = BATCH * world
     gen = torch.Generator().manual_seed(1234)
 
@@ -428,9 +433,9 @@ def main():
     ys = [labels_dev[b].contiguous() for b in batches]
 
     graphed = None
-    if world == 1 and not os.environ.get("ICE_NO_GRAPH"):
-        # one CUDA graph per step (launch overhead off the critical path); batches are copied
-        # into the graph's static inputs before each replay
+    if not os.environ.get("ICE_NO_GRAPH"):
+        # one CUDA graph per step, the NCCL bucket all-reduces included at N > 1 (launch
+        # overhead off the critical path); batches are copied into the graph's static inputs
         from paper_2403_13135_b200.icetrain.train import GraphedStep
         graphed = GraphedStep(model, opt, xs[0], ys[0], union, bucketer)
 
@@ -611,6 +616,8 @@ def main():
                 "data": f"synthetic (T-gray tiles generate_corpus(101, {args.corpus}, 0.3), labels by K1 on GPU)",
                 "config": {**WORKLOAD_CONFIG,
                            "global_batch": union, "parallelism": f"dp{world}",
+                           "grad_allreduce": (f"NCCL SUM, {bucket_mb} MB buckets, "
+                                              f"{'bf16' if comm_bf16 else 'fp32'} on the wire") if world > 1 else None,
                            "l2": "per-step working set (activations, 124M params) >> 126 MB L2; no flush",
                            "launch": launch_mode},
                 "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
