@@ -135,6 +135,7 @@ class GradBucketer:
         for b in self.buckets:
             self.by_last.setdefault(b[2], []).append(b)
         self._wire = None
+        self._comm_used = False
         if self.cuda and comm_dtype is not None:
             longest = max(stop - start for start, stop, _ in self.buckets)
             self._wire = torch.empty(longest, dtype=comm_dtype, device=dev)
@@ -158,6 +159,7 @@ class GradBucketer:
             ev.record(torch.cuda.current_stream())
             done = None
             if self._collective():
+                self._comm_used = True
                 with torch.cuda.stream(self.comm_stream):
                     self.comm_stream.wait_event(ev)
                     if self._wire is None:
@@ -178,11 +180,16 @@ class GradBucketer:
         if not self.cuda:
             return
         cur = torch.cuda.current_stream()
+        # join only streams that carry this step's work (a capture must not wait on a stream
+        # with no captured work)
+        comm, self._comm_used = self._comm_used, False
         if self.optimizer is not None:
-            self.opt_stream.wait_stream(self.comm_stream)
+            if comm:
+                self.opt_stream.wait_stream(self.comm_stream)
             self.engine.prep_halves(self.opt_stream)
             cur.wait_stream(self.opt_stream)
-        cur.wait_stream(self.comm_stream)
+        if comm:
+            cur.wait_stream(self.comm_stream)
 
 
 def device_step(model, optimizer, x, y, union_count: int, bucketer=None) -> None:
