@@ -81,6 +81,9 @@ def main(argv):
                 dur_ns *= 1e3
             elif dur_ns is not None and units[hdr.index("gpu__time_duration.sum")] in ("msecond", "ms"):
                 dur_ns *= 1e6
+            ops = to_num(r[hdr.index(UTC + ".sum")]) if UTC + ".sum" in hdr else None
+            if ops and dur_ns:
+                d["utc_bf16_tflops_executed"] = round(ops / dur_ns * 1e-3, 1)  # MMA ops actually issued / time
             for key, gflop in flops.items():
                 if key in name and dur_ns:
                     d["algorithmic_gflop"] = gflop
