@@ -122,13 +122,22 @@ def stitch_tiles_device(tiles_dev, height: int, width: int, cols: int = 0):
     return out
 
 
+def _check_byte_range(a: np.ndarray, who: str) -> None:
+    """The GPU cut/stitch kernels move bytes: integer data in 0..255 round-trips exactly through
+    them; anything else (float probabilities, wide integers) would be silently truncated, so it
+    is refused instead (the reference keeps any dtype; labels and RGB tiles are all it cuts)."""
+    if not (np.issubdtype(a.dtype, np.integer) or a.dtype == np.bool_):
+        raise TypeError(f"{who}: integer data in 0..255 expected, got {a.dtype}")
+    if a.size and (a.min() < 0 or a.max() > 255):
+        raise ValueError(f"{who}: values outside 0..255")
+
+
 def cut_tiles(img: np.ndarray, size: int) -> list:
     """(tile, row, col) squares covering the image, zero-padded at the ragged edges; works
     for (h, w, 3) images and (h, w) masks (data.py:55-66)."""
     img = np.asarray(img)
     if img.dtype != np.uint8:  # int64 class masks: values 0..2 travel as bytes
-        if img.size and (img.min() < 0 or img.max() > 255):
-            raise ValueError("cut_tiles: values outside 0..255")
+        _check_byte_range(img, "cut_tiles")
         tiles, rows, cols = cut_tiles_device(_dev(img.astype(np.uint8)), size)
         host = tiles.cpu().numpy().astype(img.dtype)
     else:
@@ -148,6 +157,8 @@ def stitch_tiles(tiles: list, height: int, width: int) -> np.ndarray:
     dtype = tiles[0][0].dtype
     grid = np.zeros((rows * cols,) + tiles[0][0].shape, np.uint8)
     for tile, r, c in tiles:
+        if dtype != np.uint8:
+            _check_byte_range(np.asarray(tile), "stitch_tiles")
         grid[r * cols + c] = tile
     height, width = min(height, rows * size), min(width, cols * size)  # canvas[:height, :width]
     out = stitch_tiles_device(_dev(grid), height, width, cols)

@@ -4,6 +4,7 @@ import json
 import os
 
 import numpy as np
+import pytest
 
 from oracle import data_ref as orc
 from tests.golden import data_cases as dc
@@ -63,3 +64,17 @@ def test_split_scene_oracle_matches_reference():
         tiles = orc.cut_tiles(dc.scene(rec["h"], rec["w"]), rec["tile_size"])
         assert [[sha(t), r, c] for t, r, c in tiles] == [x[:3] for x in rec["tiles"]]
         assert (rec["rows"], rec["cols"]) == (1 + tiles[-1][1], 1 + tiles[-1][2])
+
+
+def test_cut_stitch_refuse_non_byte_data():
+    """The GPU cut / stitch kernels move bytes; float or out-of-range data is refused before any
+    device work (it would otherwise be silently truncated)."""
+    from paper_2403_13135_b200.icetrain import data as D
+    with pytest.raises(TypeError, match="cut_tiles: integer data"):
+        D.cut_tiles(np.zeros((8, 8), np.float32), 4)
+    with pytest.raises(ValueError, match="cut_tiles: values outside"):
+        D.cut_tiles(np.full((8, 8), 300, np.int64), 4)
+    with pytest.raises(TypeError, match="stitch_tiles: integer data"):
+        D.stitch_tiles([(np.zeros((4, 4), np.float64), 0, 0)], 4, 4)
+    with pytest.raises(ValueError, match="stitch_tiles: values outside"):
+        D.stitch_tiles([(np.full((4, 4), -1, np.int64), 0, 0)], 4, 4)
