@@ -25,7 +25,7 @@ extern "C" {
 #define ICE_OK 0
 #define ICE_EINVAL (-1)     /* bad size / pointer / configuration                     */
 #define ICE_EWINDOW (-2)    /* window k exceeds tile extent (kernels.py:38-39)         */
-#define ICE_ETOOBIG (-3)    /* tile larger than the on-chip plane (256 x 256)         */
+#define ICE_ETOOBIG (-3)    /* extent beyond what the entry point handles             */
 #define ICE_ENODRIVER (-4)  /* cuTensorMapEncodeTiled entry point unavailable          */
 #define ICE_ESCRATCH (-5)   /* caller scratch smaller than the call needs              */
 
@@ -81,10 +81,26 @@ int ice_autolabel(const uint8_t *rgb, int64_t n, int32_t h, int32_t w,
                   uint32_t *affected, uint32_t *counts, int32_t *unmatched,
                   void *stream);
 
+/* ice_autolabel for any extent: whole scenes (cloudfilter.apply_filter as cli.py:112-125
+ * calls it) and tiles larger than 256 x 256 (BASELINE configs[4]'s 512^2 tiles).  Extents
+ * <= 256 go to ice_autolabel (no scratch).  Larger ones run the multi-CTA region path:
+ * cores of <= (256 - 2 * halo)^2 pixels with their halo (halo = bg_dilate_k / 2 +
+ * bg_median_k / 2), image-global statistics (d histogram -> stretch -> Otsu, channel
+ * medians) in per-image scratch counters; 4 kernels + one memset.  Bit-exact like
+ * ice_autolabel.  Scratch (see above): n * (4152 + h * w) bytes, rounded up.
+ * ICE_ETOOBIG: h * w >= 2^31, or windows so large that a core would be < 16 pixels. */
+int ice_autolabel_scene(const uint8_t *rgb, int64_t n, int32_t h, int32_t w,
+                        const IceFilterCfg *cfg, const IceScheme *scheme,
+                        uint8_t *filtered, uint8_t *label, uint8_t *mask,
+                        uint32_t *affected, uint32_t *counts, int32_t *unmatched,
+                        void *scratch, uint64_t *scratch_bytes, void *stream);
+
 /* Kernel selection for ice_autolabel (test hook, process-wide): 0 = automatic (the SWAR
  * 256 x 256 kernel for 256 x 256 tiles with the default windows 7/21/3, the generic
  * kernel otherwise), 1 = generic kernel only, 2 = SWAR kernel only (ICE_EINVAL when the
- * call does not qualify).  Both kernels are exact; the hook lets tests compare them. */
+ * call does not qualify), 3 = ice_autolabel_scene takes the region path at every extent
+ * with cores of <= 40 x 40 pixels (exercises the halo logic on small inputs).  All paths
+ * are exact; the hook lets tests compare them. */
 int ice_autolabel_set_path(int32_t mode);
 
 /* Segment-only kernel (K1s): replaces segmentation.segment (segmentation.py:118-128)

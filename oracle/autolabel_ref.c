@@ -96,6 +96,35 @@ void or_minmax_normalize(const uint8_t *src, size_t n, uint8_t *dst) {
 }
 
 /* kernels.py:77-110: exact integer between-class variance argmax, smallest t on ties */
+/* z[0..nx+ny) = x * y, little-endian 64-bit limbs (schoolbook) */
+static void mul_limbs(const uint64_t *x, int nx, const uint64_t *y, int ny, uint64_t *z) {
+    for (int i = 0; i < nx + ny; ++i) z[i] = 0;
+    for (int i = 0; i < nx; ++i) {
+        unsigned __int128 carry = 0;
+        for (int j = 0; j < ny; ++j) {
+            unsigned __int128 t = (unsigned __int128)x[i] * y[j] + z[i + j] + carry;
+            z[i + j] = (uint64_t)t;
+            carry = t >> 64;
+        }
+        z[i + ny] = (uint64_t)carry;
+    }
+}
+
+/* a1^2 * d2 > a2^2 * d1, exactly: the reference compares Python big ints
+ * (num * best_den > best_num * den, kernels.py:104-106); for scenes beyond ~2^19 pixels
+ * these products exceed 128 bits (a <= 255 * n0 * n1 < 2^128, d = n0 * n1 < 2^64). */
+static int sq_ratio_greater(unsigned __int128 a1, uint64_t d1, unsigned __int128 a2, uint64_t d2) {
+    uint64_t x1[2] = {(uint64_t)a1, (uint64_t)(a1 >> 64)}, x2[2] = {(uint64_t)a2, (uint64_t)(a2 >> 64)};
+    uint64_t sq1[4], sq2[4], l[5], r[5];
+    mul_limbs(x1, 2, x1, 2, sq1);
+    mul_limbs(x2, 2, x2, 2, sq2);
+    mul_limbs(sq1, 4, &d2, 1, l);
+    mul_limbs(sq2, 4, &d1, 1, r);
+    for (int i = 4; i >= 0; --i)
+        if (l[i] != r[i]) return l[i] > r[i];
+    return 0;
+}
+
 int or_otsu_threshold(const uint8_t *src, size_t n) {
     int64_t counts[256] = {0};
     for (size_t i = 0; i < n; ++i) counts[src[i]]++;
@@ -105,7 +134,8 @@ int or_otsu_threshold(const uint8_t *src, size_t n) {
         s_total += (__int128)t * counts[t];
     }
     int best_t = 0;
-    unsigned __int128 best_num = 0, best_den = 1;
+    unsigned __int128 best_a = 0; /* best_num = best_a^2 */
+    uint64_t best_den = 1;
     __int128 n0 = 0, s0 = 0;
     for (int t = 0; t < 256; ++t) {
         n0 += counts[t];
@@ -114,11 +144,10 @@ int or_otsu_threshold(const uint8_t *src, size_t n) {
         if (n0 == 0 || n1 == 0) continue;
         __int128 s1 = s_total - s0;
         __int128 diff = s0 * n1 - s1 * n0;
-        unsigned __int128 num = (unsigned __int128)(diff < 0 ? -diff : diff);
-        num = num * num;
-        unsigned __int128 den = (unsigned __int128)(n0 * n1);
-        if (num * best_den > best_num * den) {
-            best_num = num;
+        unsigned __int128 a = (unsigned __int128)(diff < 0 ? -diff : diff);
+        uint64_t den = (uint64_t)(n0 * n1);
+        if (sq_ratio_greater(a, den, best_a, best_den)) {
+            best_a = a;
             best_den = den;
             best_t = t;
         }

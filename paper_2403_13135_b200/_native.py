@@ -49,6 +49,8 @@ SIGNATURES = {
     "ice_autolabel": [_V, _I64, _I32, _I32, ctypes.POINTER(IceFilterCfg), ctypes.POINTER(IceScheme),
                       _V, _V, _V, _V, _V, _V, _V],
     "ice_autolabel_set_path": [_I32],
+    "ice_autolabel_scene": [_V, _I64, _I32, _I32, ctypes.POINTER(IceFilterCfg), ctypes.POINTER(IceScheme),
+                            _V, _V, _V, _V, _V, _V, *_S, _V],
     "ice_cut_tiles": [_V, _I32, _I32, _I32, _I32, _V, _V],
     "ice_stitch_tiles": [_V, _I32, _I32, _I32, _I32, _I32, _V, _V],
     "ice_encode_labels": [_V, _I64, _V, _I32, _V, _V, _V],
@@ -188,6 +190,8 @@ def call(name: str, *args) -> None:
             rc = fn(*core, None, None, stream)
     else:
         rc = fn(*args)
+    if name == "ice_autolabel_set_path":
+        scratch.sizes.clear()  # the region path's scratch need depends on the mode
     if rc != ICE_OK:
         raise NativeError(name, rc)
     counter.launches += 1

@@ -548,6 +548,378 @@ autolabel_kernel(const uint8_t *__restrict__ rgb, int h, int w, Params prm,
     }
 }
 
+// =====================================================================================
+// Region path: tiles and whole scenes larger than one CTA's 256 x 256 planes
+// (cloudfilter.apply_filter on a scene, cli.py:112-125; 512^2 tiles of BASELINE configs[4]).
+// The image is cut into cores of at most (256 - 2 * halo)^2 pixels, halo = dilate radius +
+// background-median radius (>= noise-median radius).  Each CTA loads its core plus the halo
+// clipped to the image, so:
+//   * at an image border the region border IS the image border: the clamped indices of
+//     dilate_plane / median_plane replicate exactly as cv2's BORDER_REPLICATE does;
+//   * at an interior region border, dilated values within dilate-radius of the edge are
+//     wrong, but the background median of a core pixel only reads dilated values within
+//     median-radius of the core, i.e. >= dilate-radius inside the region.
+// The image-global quantities become three launches:
+//   1. region_d_kernel      d = |median_noise(V) - median(dilate(V))| [truncated] of the core
+//                           -> u8 d plane in scratch; integer histograms of d and of each
+//                           channel added into per-image counters (integer atomics: exact,
+//                           order-free);
+//   2. region_stats_kernel  per image: min/max of d, the exact stretch, Otsu (192-bit exact
+//                           compare: scenes beyond ~2^19 pixels overflow 128-bit products),
+//                           masked-pixel count, the three channel medians;
+//   3. region_out_kernel    mask of the core; per-channel backgrounds only when the core holds
+//                           masked pixels; repair, HSV segmentation, per-class counts and the
+//                           first unmatched pixel (integer atomics).
+//   + region_finish_kernel  per-image outputs.
+struct RegionGeom {
+    int h, w;          // image extent
+    int ny, nx;        // regions per column / row
+    int cs_y, cs_x;    // core extent (the last row / column of cores may be shorter)
+    int halo;
+};
+
+struct RegionBox {
+    int cy0, cx0, ch, cw;  // core, image coordinates
+    int ry0, rx0, rh, rw;  // core + halo clipped to the image
+};
+
+struct RegionStats {       // per image, in caller scratch
+    uint32_t hist_d[256];
+    uint32_t hist_c[3][256];
+    int lo, range, thr, masked;
+    int center[3];
+    uint32_t counts[3];
+    int first;
+    int pad[3];
+};
+static_assert(sizeof(RegionStats) == 4152, "documented in icelabel_b200.h");
+
+__device__ __forceinline__ RegionBox region_box(const RegionGeom &g, int r) {
+    RegionBox b;
+    const int by = r / g.nx, bx = r - by * g.nx;
+    b.cy0 = by * g.cs_y;
+    b.ch = min(g.cs_y, g.h - b.cy0);
+    b.cx0 = bx * g.cs_x;
+    b.cw = min(g.cs_x, g.w - b.cx0);
+    b.ry0 = max(b.cy0 - g.halo, 0);
+    b.rh = min(b.cy0 + b.ch + g.halo, g.h) - b.ry0;
+    b.rx0 = max(b.cx0 - g.halo, 0);
+    b.rw = min(b.cx0 + b.cw + g.halo, g.w) - b.rx0;
+    return b;
+}
+
+// channel ch (3 = V = max(r, g, b), cloudfilter.py:89) of the region -> plane
+__device__ void load_region(const uint8_t *img, int w_img, int ch, const RegionBox &b, uint8_t *dst) {
+    for (int i = threadIdx.x; i < b.rh * b.rw; i += NT) {
+        const int y = i / b.rw, x = i - y * b.rw;
+        const uint8_t *px = img + 3 * ((size_t)(b.ry0 + y) * w_img + b.rx0 + x);
+        dst[y * PITCH + x] = (uint8_t)(ch == 3 ? max(px[0], max(px[1], px[2])) : px[ch]);
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void flush_hist(const uint32_t *sh, uint32_t *gh) {
+    for (int i = threadIdx.x; i < 256; i += NT)
+        if (sh[i]) atomicAdd(&gh[i], sh[i]);
+}
+
+__global__ void __launch_bounds__(NT, 1)
+region_d_kernel(const uint8_t *__restrict__ rgb, RegionGeom g, IceFilterCfg cfg, int regions,
+                uint8_t *__restrict__ dplanes, RegionStats *__restrict__ st) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    Smem &s = *reinterpret_cast<Smem *>(smem_raw);
+    const int img = blockIdx.x / regions;
+    const RegionBox b = region_box(g, blockIdx.x - img * regions);
+    const size_t npx = (size_t)g.h * g.w;
+    const uint8_t *im = rgb + img * npx * 3;
+    uint8_t *dp = dplanes + img * npx;
+    RegionStats &S = st[img];
+    uint8_t *P0 = s.p[0], *P1 = s.p[1], *P2 = s.p[2];
+    // background of V over the region (cloudfilter.py:82-84, 89)
+    load_region(im, g.w, 3, b, P0);
+    dilate_plane(P0, P2, P1, b.rh, b.rw, cfg.bg_dilate_k);
+    median_plane(P1, P2, P0, b.rh, b.rw, cfg.bg_median_k, s);
+    load_region(im, g.w, 3, b, P1);
+    for (int i = threadIdx.x; i < 256; i += NT) s.hist[i] = 0;
+    uint32_t *hc = reinterpret_cast<uint32_t *>(P2);  // 3 channel histograms (P2 is free now)
+    for (int i = threadIdx.x; i < 3 * 256; i += NT) hc[i] = 0;
+    __syncthreads();
+    const int oy = b.cy0 - b.ry0, ox = b.cx0 - b.rx0, cn = b.ch * b.cw;
+    for (int base = 0; base < cn; base += NT) {
+        const int i = base + threadIdx.x;
+        const bool act = i < cn;
+        int d = 0, r = 0, gr = 0, bl = 0;
+        if (act) {
+            const int y = i / b.cw, x = i - y * b.cw, ly = oy + y, lx = ox + x;
+            const int sm = cfg.noise_median_k == 3 ? median3x3_at(P1, b.rh, b.rw, ly, lx)
+                                                   : median_at(P1, b.rh, b.rw, ly, lx, cfg.noise_median_k);
+            d = abs(sm - (int)P0[ly * PITCH + lx]);
+            if (cfg.diff_truncate) d = min(d, cfg.truncate_t);
+            const size_t gi = (size_t)(b.cy0 + y) * g.w + b.cx0 + x;
+            dp[gi] = (uint8_t)d;
+            const uint8_t *px = im + 3 * gi;
+            r = px[0];
+            gr = px[1];
+            bl = px[2];
+        }
+        hist_add(s.hist, d, act);
+        hist_add(hc, r, act);
+        hist_add(hc + 256, gr, act);
+        hist_add(hc + 512, bl, act);
+    }
+    __syncthreads();
+    flush_hist(s.hist, S.hist_d);
+    for (int c = 0; c < 3; ++c) flush_hist(hc + 256 * c, S.hist_c[c]);
+}
+
+// a1^2 * d2 > a2^2 * d1 exactly (320-bit products; kernels.py:104-106 compares Python ints)
+__device__ bool sq_ratio_greater(unsigned __int128 a1, uint64_t d1, unsigned __int128 a2, uint64_t d2) {
+    uint64_t x1[2] = {(uint64_t)a1, (uint64_t)(a1 >> 64)}, x2[2] = {(uint64_t)a2, (uint64_t)(a2 >> 64)};
+    uint64_t q1[4] = {0, 0, 0, 0}, q2[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        unsigned __int128 c1 = 0, c2 = 0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            c1 += (unsigned __int128)x1[i] * x1[j] + q1[i + j];
+            q1[i + j] = (uint64_t)c1;
+            c1 >>= 64;
+            c2 += (unsigned __int128)x2[i] * x2[j] + q2[i + j];
+            q2[i + j] = (uint64_t)c2;
+            c2 >>= 64;
+        }
+        q1[i + 2] = (uint64_t)c1;
+        q2[i + 2] = (uint64_t)c2;
+    }
+    uint64_t l[5], r[5];
+    unsigned __int128 cl = 0, cr = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        cl += (unsigned __int128)q1[i] * d2;
+        l[i] = (uint64_t)cl;
+        cl >>= 64;
+        cr += (unsigned __int128)q2[i] * d1;
+        r[i] = (uint64_t)cr;
+        cr >>= 64;
+    }
+    l[4] = (uint64_t)cl;
+    r[4] = (uint64_t)cr;
+#pragma unroll
+    for (int i = 4; i >= 0; --i)
+        if (l[i] != r[i]) return l[i] > r[i];
+    return false;
+}
+
+// Otsu (kernels.py:77-110) for any pixel count < 2^32: warp 0, lane l owns bins [8l, 8l+8)
+__device__ int otsu_wide(const uint32_t *hist) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long n_loc = 0, s_loc = 0;
+    for (int j = 0; j < 8; ++j) {
+        n_loc += hist[8 * lane + j];
+        s_loc += (unsigned long long)(8 * lane + j) * hist[8 * lane + j];
+    }
+    unsigned long long n_pre = n_loc, s_pre = s_loc;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long a = __shfl_up_sync(0xffffffffu, n_pre, o);
+        const unsigned long long c = __shfl_up_sync(0xffffffffu, s_pre, o);
+        if (lane >= o) { n_pre += a; s_pre += c; }
+    }
+    const unsigned long long n_tot = __shfl_sync(0xffffffffu, n_pre, 31);
+    const unsigned long long s_tot = __shfl_sync(0xffffffffu, s_pre, 31);
+    unsigned long long n0 = n_pre - n_loc, s0 = s_pre - s_loc;
+    int best_t = -1;
+    unsigned __int128 best_a = 0;
+    unsigned long long best_den = 1;
+    for (int j = 0; j < 8; ++j) {
+        const int t = 8 * lane + j;
+        n0 += hist[t];
+        s0 += (unsigned long long)t * hist[t];
+        const unsigned long long n1 = n_tot - n0;
+        if (n0 == 0 || n1 == 0) continue;
+        const unsigned long long s1 = s_tot - s0;
+        const unsigned __int128 p = (unsigned __int128)s0 * n1, q = (unsigned __int128)s1 * n0;
+        const unsigned __int128 a = p > q ? p - q : q - p;
+        const unsigned long long den = n0 * n1;
+        if (best_t < 0 || sq_ratio_greater(a, den, best_a, best_den)) {
+            best_t = t; best_a = a; best_den = den;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const int ot = __shfl_xor_sync(0xffffffffu, best_t, o);
+        const unsigned long long alo = __shfl_xor_sync(0xffffffffu, (unsigned long long)best_a, o);
+        const unsigned long long ahi = __shfl_xor_sync(0xffffffffu, (unsigned long long)(best_a >> 64), o);
+        const unsigned long long od = __shfl_xor_sync(0xffffffffu, best_den, o);
+        const unsigned __int128 oa = ((unsigned __int128)ahi << 64) | alo;
+        bool take;
+        if (ot < 0) take = false;
+        else if (best_t < 0) take = true;
+        else take = sq_ratio_greater(oa, od, best_a, best_den) ||
+                    (!sq_ratio_greater(best_a, best_den, oa, od) && ot < best_t);
+        if (take) { best_t = ot; best_a = oa; best_den = od; }
+    }
+    if (best_t < 0 || best_a == 0) best_t = 0;  // ratio 0 never beats the initial (0, 1)
+    return best_t;
+}
+
+__device__ __forceinline__ int stretch(int d, int lo, int range) {  // kernels.py:66-74, exact
+    return range == 0 ? 0 : (510 * (d - lo) + range) / (2 * range);
+}
+
+__global__ void __launch_bounds__(256)
+region_stats_kernel(RegionStats *__restrict__ st, int npx, IceFilterCfg cfg) {
+    __shared__ uint32_t hn[256];
+    __shared__ int slo, shi, sthr;
+    __shared__ uint32_t smasked;
+    RegionStats &S = st[blockIdx.x];
+    const int t = threadIdx.x;
+    if (t == 0) { slo = 255; shi = 0; smasked = 0; }
+    hn[t] = 0;
+    __syncthreads();
+    const uint32_t c = S.hist_d[t];
+    if (c) { atomicMin(&slo, t); atomicMax(&shi, t); }
+    __syncthreads();
+    const int lo = slo, range = shi - slo;
+    const int dn = stretch(t, lo, range);
+    if (c) atomicAdd(&hn[dn], c);
+    __syncthreads();
+    if (t < 32) {
+        const int thr = cfg.mask_mode_fixed ? cfg.fixed_t : otsu_wide(hn);
+        if (t == 0) sthr = thr;
+    }
+    __syncthreads();
+    if (c && dn > sthr) atomicAdd(&smasked, c);
+    if (t < 3) S.center[t] = center_from_hist(S.hist_c[t], npx);
+    __syncthreads();
+    if (t == 0) {
+        S.lo = lo; S.range = range; S.thr = sthr; S.masked = (int)smasked;
+        S.counts[0] = S.counts[1] = S.counts[2] = 0;
+        S.first = 0x7fffffff;
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1)
+region_out_kernel(const uint8_t *__restrict__ rgb, RegionGeom g, Params prm, int regions,
+                  const uint8_t *__restrict__ dplanes, RegionStats *__restrict__ st,
+                  uint8_t *__restrict__ filtered, uint8_t *__restrict__ label, uint8_t *__restrict__ maskout) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    Smem &s = *reinterpret_cast<Smem *>(smem_raw);
+    const IceFilterCfg &cfg = prm.cfg;
+    const int img = blockIdx.x / regions;
+    const RegionBox b = region_box(g, blockIdx.x - img * regions);
+    const size_t npx = (size_t)g.h * g.w;
+    const uint8_t *im = rgb + img * npx * 3;
+    const uint8_t *dp = dplanes + img * npx;
+    uint8_t *fim = filtered + img * npx * 3;
+    RegionStats &S = st[img];
+    const int lo = S.lo, range = S.range, thr = S.thr;
+    uint8_t *P0 = s.p[0], *P1 = s.p[1], *P2 = s.p[2];
+    const int oy = b.cy0 - b.ry0, ox = b.cx0 - b.rx0, cn = b.ch * b.cw;
+    // 1. the core's mask (cloudfilter.py:94-96 on the image-global stretch and threshold)
+    int cnt = 0;
+    for (int base = 0; base < cn; base += NT) {
+        const int i = base + threadIdx.x;
+        bool m = false;
+        if (i < cn) {
+            const int y = i / b.cw, x = i - y * b.cw;
+            m = stretch(dp[(size_t)(b.cy0 + y) * g.w + b.cx0 + x], lo, range) > thr;
+        }
+        const unsigned bits = __ballot_sync(0xffffffffu, m);
+        if ((threadIdx.x & 31) == 0 && base + (threadIdx.x & ~31) < cn) s.maskbits[(base + threadIdx.x) >> 5] = bits;
+        cnt += m;
+    }
+    const bool repair = block_sum(cnt, s) > 0;
+    // 2. per-channel backgrounds of the region, only where the core has masked pixels
+    bool gray = true;
+    if (repair) {
+        int unequal = 0;
+        for (int i = threadIdx.x; i < b.rh * b.rw; i += NT) {
+            const int y = i / b.rw, x = i - y * b.rw;
+            const uint8_t *px = im + 3 * ((size_t)(b.ry0 + y) * g.w + b.rx0 + x);
+            unequal |= (px[0] != px[1]) | (px[1] != px[2]);
+        }
+        gray = block_sum(unequal, s) == 0;
+        if (gray) {  // R == G == B over the region: every channel's background is V's (in P0)
+            load_region(im, g.w, 3, b, P1);
+            dilate_plane(P1, P0, P2, b.rh, b.rw, cfg.bg_dilate_k);
+            median_plane(P2, P1, P0, b.rh, b.rw, cfg.bg_median_k, s);
+        } else {
+            for (int ch = 0; ch < 3; ++ch) {
+                load_region(im, g.w, ch, b, P1);
+                dilate_plane(P1, P0, P2, b.rh, b.rw, cfg.bg_dilate_k);
+                median_plane(P2, P1, P0, b.rh, b.rw, cfg.bg_median_k, s);
+                const int cc = S.center[ch];
+                for (int i = threadIdx.x; i < cn; i += NT) {
+                    if (s.maskbits[i >> 5] >> (i & 31) & 1) {
+                        const int y = i / b.cw, x = i - y * b.cw;
+                        const size_t gi = (size_t)(b.cy0 + y) * g.w + b.cx0 + x;
+                        fim[3 * gi + ch] = (uint8_t)clampi((int)im[3 * gi + ch] - (int)P0[(oy + y) * PITCH + ox + x] + cc, 0, 255);
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    // 3. output: filtered core, mask, HSV segmentation, counts, first unmatched
+    int c0 = 0, c1 = 0, c2 = 0, first = 0x7fffffff;
+    uint8_t *lim = label + img * npx;
+    uint8_t *mim = maskout ? maskout + img * npx : nullptr;
+    const SchemeR scr(prm.scheme);
+    for (int i = threadIdx.x; i < cn; i += NT) {
+        const int y = i / b.cw, x = i - y * b.cw;
+        const size_t gi = (size_t)(b.cy0 + y) * g.w + b.cx0 + x;
+        int R = im[3 * gi], G = im[3 * gi + 1], B = im[3 * gi + 2];
+        const bool mk = repair && (s.maskbits[i >> 5] >> (i & 31) & 1);
+        if (mim) mim[gi] = mk ? 255 : 0;
+        if (mk) {
+            if (gray) {
+                const int bg = P0[(oy + y) * PITCH + ox + x];
+                R = clampi(R - bg + S.center[0], 0, 255);
+                G = clampi(G - bg + S.center[1], 0, 255);
+                B = clampi(B - bg + S.center[2], 0, 255);
+            } else {
+                R = fim[3 * gi];
+                G = fim[3 * gi + 1];
+                B = fim[3 * gi + 2];
+            }
+        }
+        fim[3 * gi] = (uint8_t)R;
+        fim[3 * gi + 1] = (uint8_t)G;
+        fim[3 * gi + 2] = (uint8_t)B;
+        const int cls = prm.v_only ? classify<false, false>(R, G, B, scr) : classify(R, G, B, scr);
+        lim[gi] = (uint8_t)cls;
+        c0 += cls == 0;
+        c1 += cls == 1;
+        c2 += cls == 2;
+        if (cls == 255) first = min(first, (int)gi);
+    }
+    c0 = block_sum(c0, s);
+    c1 = block_sum(c1, s);
+    c2 = block_sum(c2, s);
+    for (int o = 16; o; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s.red_i[threadIdx.x >> 5] = first;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NT / 32; ++i) first = min(first, s.red_i[i]);
+        if (c0) atomicAdd(&S.counts[0], (uint32_t)c0);
+        if (c1) atomicAdd(&S.counts[1], (uint32_t)c1);
+        if (c2) atomicAdd(&S.counts[2], (uint32_t)c2);
+        if (first != 0x7fffffff) atomicMin(&S.first, first);
+    }
+}
+
+__global__ void region_finish_kernel(const RegionStats *__restrict__ st, int n, uint32_t *__restrict__ affected,
+                                     uint32_t *__restrict__ counts, int32_t *__restrict__ unmatched) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const RegionStats &S = st[i];
+    affected[i] = (uint32_t)S.masked;
+    counts[3 * i] = S.counts[0];
+    counts[3 * i + 1] = S.counts[1];
+    counts[3 * i + 2] = S.counts[2];
+    unmatched[i] = S.first == 0x7fffffff ? -1 : S.first;
+}
+
 // K1s: segment only.  One CTA per tile, any size.
 constexpr int SEG_NT = 256;
 __global__ void __launch_bounds__(SEG_NT)
@@ -1687,9 +2059,77 @@ extern "C" int ice_autolabel(const uint8_t *rgb, int64_t n, int32_t h, int32_t w
 }
 
 extern "C" int ice_autolabel_set_path(int32_t mode) {
-    if (mode < 0 || mode > 2) return ICE_EINVAL;
+    if (mode < 0 || mode > 3) return ICE_EINVAL;
     g_autolabel_path = mode;
     return ICE_OK;
+}
+
+extern "C" int ice_autolabel_scene(const uint8_t *rgb, int64_t n, int32_t h, int32_t w,
+                                   const IceFilterCfg *cfg, const IceScheme *scheme,
+                                   uint8_t *filtered, uint8_t *label, uint8_t *mask,
+                                   uint32_t *affected, uint32_t *counts, int32_t *unmatched,
+                                   void *scratch, uint64_t *scratch_bytes, void *stream) {
+    if (!cfg || !scheme || n < 0 || h < 1 || w < 1) return ICE_EINVAL;
+    const bool region = h > MAXD || w > MAXD || g_autolabel_path == 3;
+    if (!region) {  // one CTA per tile: no scratch
+        if (!scratch && scratch_bytes) {
+            *scratch_bytes = 0;
+            return ICE_OK;
+        }
+        return ice_autolabel(rgb, n, h, w, cfg, scheme, filtered, label, mask, affected, counts, unmatched, stream);
+    }
+    if ((int64_t)h * w > 0x7fffffff || n > 0x7fffffff) return ICE_ETOOBIG;
+    if (!window_ok(cfg->noise_median_k, h, w) || !window_ok(cfg->bg_dilate_k, h, w) ||
+        !window_ok(cfg->bg_median_k, h, w))
+        return ICE_EWINDOW;
+    const int halo = max(cfg->bg_dilate_k / 2 + cfg->bg_median_k / 2, cfg->noise_median_k / 2);
+    int cmax = MAXD - 2 * halo;
+    if (g_autolabel_path == 3) cmax = min(cmax, 40);  // test hook: many small regions
+    if (cmax < 16) return ICE_ETOOBIG;
+    RegionGeom g;
+    g.h = h;
+    g.w = w;
+    g.halo = halo;
+    g.ny = (h + cmax - 1) / cmax;
+    g.nx = (w + cmax - 1) / cmax;
+    g.cs_y = (h + g.ny - 1) / g.ny;
+    g.cs_x = (w + g.nx - 1) / g.nx;
+    const int regions = g.ny * g.nx;
+    const uint64_t stats_bytes = ((uint64_t)n * sizeof(RegionStats) + 255) & ~(uint64_t)255;
+    const uint64_t need = stats_bytes + (((uint64_t)n * h * w + 255) & ~(uint64_t)255);
+    if (!scratch) {
+        if (!scratch_bytes) return ICE_ESCRATCH;
+        *scratch_bytes = need;
+        return ICE_OK;
+    }
+    if (!scratch_bytes || *scratch_bytes < need) return ICE_ESCRATCH;
+    if (n == 0) return ICE_OK;
+    if (!rgb || !filtered || !label || !affected || !counts || !unmatched) return ICE_EINVAL;
+    if ((int64_t)n * regions > 0x7fffffff) return ICE_ETOOBIG;
+    Params prm;
+    prm.cfg = *cfg;
+    prm.scheme = *scheme;
+    prm.v_only = full_hue(*scheme) && full_sat(*scheme);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(region_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(region_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+        if (e != cudaSuccess) return (int)e;
+        attr_set = true;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    RegionStats *stats = reinterpret_cast<RegionStats *>(scratch);
+    uint8_t *dplanes = reinterpret_cast<uint8_t *>(scratch) + stats_bytes;
+    cudaError_t e = cudaMemsetAsync(stats, 0, (size_t)n * sizeof(RegionStats), st);
+    if (e != cudaSuccess) return (int)e;
+    const unsigned grid = (unsigned)(n * regions);
+    region_d_kernel<<<grid, NT, sizeof(Smem), st>>>(rgb, g, *cfg, regions, dplanes, stats);
+    region_stats_kernel<<<(unsigned)n, 256, 0, st>>>(stats, h * w, *cfg);
+    region_out_kernel<<<grid, NT, sizeof(Smem), st>>>(rgb, g, prm, regions, dplanes, stats, filtered, label, mask);
+    region_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stats, (int)n, affected, counts, unmatched);
+    for (int k = 0; k < 4; ++k) ice::count_launch();
+    return (int)cudaGetLastError();
 }
 
 extern "C" int ice_segment(const uint8_t *rgb, int64_t n, int32_t h, int32_t w,

@@ -47,7 +47,7 @@ def check_windows(cfg: FilterConfig, h: int, w: int) -> None:
 
 def autolabel(rgb, cfg: FilterConfig | None = None, scheme: SegmentationScheme = ROSS_SEA_SUMMER,
               want_mask: bool = False, out=None, stream=None):
-    """Fused filter + segmentation for a device batch rgb u8 [n, h, w, 3] (K1)."""
+    """Fused filter + segmentation for a device batch rgb u8 [n, h, w, 3] (K1), any extent."""
     import torch
     cfg = cfg or FilterConfig()
     if rgb.dtype != torch.uint8 or rgb.ndim != 4 or rgb.shape[3] != 3:
@@ -64,7 +64,9 @@ def autolabel(rgb, cfg: FilterConfig | None = None, scheme: SegmentationScheme =
         out["mask"] = torch.empty((n, h, w), dtype=torch.uint8, device=dev) if want_mask else None
     c = native_cfg(cfg)
     s = native_scheme(scheme)
-    _native.call("ice_autolabel", _native.ptr(rgb.contiguous()), n, h, w, c, s,
+    # ice_autolabel_scene: one CTA per tile up to 256 x 256 (ice_autolabel), the multi-CTA
+    # region path beyond (whole scenes, 512^2 tiles) with caller scratch
+    _native.call("ice_autolabel_scene", _native.ptr(rgb.contiguous()), n, h, w, c, s,
                  _native.ptr(out["filtered"]), _native.ptr(out["label"]), _native.ptr(out.get("mask")),
                  _native.ptr(out["affected"]), _native.ptr(out["counts"]), _native.ptr(out["unmatched"]),
                  _native.stream_handle(stream))

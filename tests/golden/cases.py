@@ -95,4 +95,25 @@ def all_cases():
                       make=lambda: _rand(8, (40, 40, 3))))
     cases.append(dict(name="pt_satonly_rand", op="process_tile", scheme="sat-only",
                       make=lambda: _rand(9, (64, 64, 3))))
+    # beyond one 256 x 256 CTA (round 2): whole-scene apply_filter and 512^2 tiles run the
+    # multi-CTA region path; 1024^2 and 2048^2 also need Otsu's > 128-bit exact compare
+    for i in range(4):
+        cases.append(dict(name=f"large_gray_512_{i}", op="process_tile",
+                          make=lambda i=i: synth.scene(101, i, 512, i % 2 == 0)[0]))
+    for i in range(2):
+        cases.append(dict(name=f"large_tint_512_{i}", op="process_tile",
+                          make=lambda i=i: synth.tint(synth.scene(101, i, 512, True)[0], 101, i)))
+    cases.append(dict(name="large_rand_512", op="process_tile", make=lambda: synth.random_tile(3, 512)))
+    cases.append(dict(name="large_flat_512", op="process_tile", make=lambda: _flat(140, 512)))
+    cases.append(dict(name="large_edge_512", op="process_tile", make=lambda: _edge(512)))
+    for shp in ((300, 517, 3), (40, 700, 3), (257, 256, 3), (700, 33, 3)):
+        cases.append(dict(name=f"large_filter_{shp[0]}x{shp[1]}", op="apply_filter",
+                          make=lambda s=shp: _rand(4000 + s[0] + s[1], s)))
+    cases.append(dict(name="large_scene_1024", op="apply_filter",
+                      make=lambda: synth.scene(7, 0, 1024, True)[0]))
+    cases.append(dict(name="large_scene_2048", op="apply_filter",
+                      make=lambda: synth.scene(7, 1, 2048, True)[0]))
+    for j, cfg in enumerate(variants):
+        cases.append(dict(name=f"large_cfg_{j}", op="apply_filter", cfg=cfg,
+                          make=lambda j=j: synth.scene(11, j, 384, True)[0][:320]))
     return cases

@@ -290,3 +290,66 @@ def test_autolabel_sharded_single_rank_totals():
     assert totals[:3].tolist() == ref["counts"].to(torch.int64).sum(0).tolist()
     assert int(totals[3]) == int(ref["affected"].sum())
     assert torch.equal(out["label"], ref["label"])
+
+
+# ---- region path (ice_autolabel_scene): extents beyond one CTA's 256 x 256 planes ----------
+
+def _oracle_check(out, tiles, cfg=None):
+    ocfg = None
+    if cfg is not None:
+        ocfg = orc.make_cfg(**{k: getattr(cfg, k) for k in cfg.__dataclass_fields__})
+    for i, t in enumerate(tiles):
+        f, m, a = orc.apply_filter(t, ocfg) if ocfg is not None else orc.apply_filter(t)
+        lbl, first = orc.segment(f)
+        assert np.array_equal(out["filtered"][i], f), i
+        assert np.array_equal(out["mask"][i], m), i
+        assert out["affected"][i] == a, i
+        assert np.array_equal(out["label"][i], lbl), i
+        assert out["unmatched"][i] == first, i
+        assert out["counts"][i].tolist() == np.bincount(lbl.ravel(), minlength=256)[:3].tolist(), i
+
+
+@pytest.mark.parametrize("cfg", [il.FilterConfig(), il.FilterConfig(mask_mode="fixed", fixed_t=40),
+                                 il.FilterConfig(diff_truncate=True, truncate_t=9),
+                                 il.FilterConfig(noise_median_k=5, bg_median_k=9, bg_dilate_k=5)],
+                         ids=["default", "fixed40", "trunc9", "windows"])
+def test_region_path_forced_matches_one_cta_kernels(cfg):
+    """Mode 3 cuts even 256^2 tiles into <= 40 x 40 cores with halos: every core border is
+    interior, so the halo logic is exercised everywhere; outputs equal the one-CTA kernels."""
+    tiles = [rgb for rgb, _ in synth.corpus(13, 6, 0.5)]
+    tiles += [synth.tint(t, 13, i) for i, t in enumerate(tiles[:3])]
+    tiles += [synth.random_tile(310)] + _edge_tiles()
+    one = _run_path(tiles, 0, cfg)
+    reg = _run_path(tiles, 3, cfg)
+    for k in one:
+        for i in range(len(tiles)):
+            assert np.array_equal(one[k][i], reg[k][i]), (k, i)
+
+
+@pytest.mark.parametrize("shape", [(100, 37), (37, 100), (129, 131), (64, 300)])
+def test_region_path_ragged_vs_oracle(shape):
+    rng = np.random.default_rng(shape[0] * 1000 + shape[1])
+    h, w = shape
+    smooth = np.repeat(np.repeat(rng.integers(0, 256, (h // 8 + 1, w // 8 + 1, 3)), 8, 0), 8, 1)
+    tiles = [rng.integers(0, 256, (h, w, 3), dtype=np.uint8), smooth[:h, :w].astype(np.uint8)]
+    _oracle_check(_run_path(tiles, 3), tiles)
+
+
+def test_region_path_512_tiles_vs_oracle():
+    """BASELINE configs[4] geometry: 512^2 T-gray / T-tint / T-rand tiles (3 x 3 regions)."""
+    tiles = [synth.scene(31, i, 512, i % 2 == 0)[0] for i in range(4)]
+    tiles += [synth.tint(tiles[0], 31, 0), synth.random_tile(41, 512)]
+    _oracle_check(_run_path(tiles, 0), tiles)
+
+
+def test_region_path_hsv_scheme_and_scene_size():
+    """Whole-scene apply_filter (1000 x 1400, no tiling) and a hue/saturation scheme."""
+    scene = synth.tint(np.ascontiguousarray(synth.scene(5, 2, 1400, True)[0][:1000]), 5, 2)
+    out = _run_path([scene], 0, None, SAT_ONLY)
+    f, m, a = orc.apply_filter(scene)
+    assert np.array_equal(out["filtered"][0], f)
+    assert np.array_equal(out["mask"][0], m)
+    assert out["affected"][0] == a
+    lbl, first = orc.segment(f, _ranges(SAT_ONLY))
+    assert np.array_equal(out["label"][0], lbl)
+    assert out["unmatched"][0] == first

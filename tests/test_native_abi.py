@@ -54,3 +54,24 @@ def test_argument_errors_are_reported_before_launch():
     assert lib.ice_autolabel(None, -1, 16, 16, cfg, sc, None, None, None, None, None, None, None) == -1
     assert lib.ice_autolabel(1, 1, 16, 16, cfg, sc, 1, 1, None, 1, 1, 1, None) == -2
     assert lib.ice_autolabel(1, 1, 300, 300, cfg, sc, 1, 1, None, 1, 1, 1, None) == -3
+
+
+def test_autolabel_scene_scratch_query_and_errors():
+    """ice_autolabel_scene (region path beyond 256 x 256): CUB-style scratch query and the
+    host-side argument checks, all before any device work."""
+    import ctypes
+    lib = _native.load()
+    cfg = _native.IceFilterCfg(7, 21, 3, 0, 128, 0, 16)
+    sc = _native.IceScheme()
+    q = ctypes.c_uint64(123)
+    args = (None, None, None, None, None, None)
+    assert lib.ice_autolabel_scene(None, 2, 512, 512, cfg, sc, *args, None, ctypes.byref(q), None) == 0
+    assert q.value == ((2 * 4152 + 255) // 256) * 256 + 2 * 512 * 512
+    assert lib.ice_autolabel_scene(None, 3, 64, 64, cfg, sc, *args, None, ctypes.byref(q), None) == 0
+    assert q.value == 0  # <= 256 x 256: one CTA per tile, no scratch
+    assert lib.ice_autolabel_scene(None, 1, 300, 10, cfg, sc, *args, None, ctypes.byref(q), None) == -2
+    small = ctypes.c_uint64(1000)
+    assert lib.ice_autolabel_scene(1, 1, 600, 600, cfg, sc, 1, 1, None, 1, 1, 1, 1, ctypes.byref(small), None) == -5
+    big = _native.IceFilterCfg(7, 241, 3, 0, 128, 0, 16)  # halo 123: cores would be < 16 px
+    assert lib.ice_autolabel_scene(None, 1, 600, 600, big, sc, *args, None, ctypes.byref(q), None) == -3
+    assert lib.ice_autolabel_set_path(4) == -1

@@ -21,14 +21,15 @@ ap.add_argument("--uniq", type=int, default=296)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--kind", default="tgray")
 ap.add_argument("--path", type=int, default=0)
+ap.add_argument("--size", type=int, default=256)
 ap.add_argument("--prof", action="store_true", help="needs ICE_LIB_PATH=.../_C/prof/libicelabel_b200.so")
 a = ap.parse_args()
 if a.kind == "trand":
-    u = np.stack([synth.random_tile(i) for i in range(a.uniq)])
+    u = np.stack([synth.random_tile(i, a.size) for i in range(a.uniq)])
 elif a.kind == "tint":
-    u = np.stack([synth.tint(t, 101, i) for i, (t, _) in enumerate(synth.corpus(101, a.uniq, 0.3))])
+    u = np.stack([synth.tint(t, 101, i) for i, (t, _) in enumerate(synth.corpus(101, a.uniq, 0.3, a.size))])
 else:
-    u = np.stack([t for t, _ in synth.corpus(101, a.uniq, 0.3)])
+    u = np.stack([t for t, _ in synth.corpus(101, a.uniq, 0.3, a.size)])
 x = torch.from_numpy(u).cuda()[torch.arange(a.tiles) % a.uniq]
 _native.call("ice_autolabel_set_path", a.path)
 out = il.autolabel(x)
@@ -53,6 +54,6 @@ if a.prof:
           "share:", [round(buf[i] / tot, 3) for i in range(8)])
     print("per tile: distinct values %.1f, passes %.1f, active col blocks/pass %.1f" %
           (buf[8] / a.tiles, buf[9] / a.tiles, buf[10] / max(1, buf[9])))
-px = a.tiles * 65536
-print(f"{a.kind} path={a.path} tiles={a.tiles}: {ms:.2f} ms  {px / ms / 1e6:.1f} Gpx/s  "
+px = a.tiles * a.size * a.size
+print(f"{a.kind} {a.size}^2 path={a.path} tiles={a.tiles}: {ms:.2f} ms  {px / ms / 1e6:.1f} Gpx/s  "
       f"{px * 7 / ms / 1e6:.1f} GB/s  us/tile/SM={ms * 1000 * 148 / a.tiles:.1f}")
