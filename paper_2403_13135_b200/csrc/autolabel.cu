@@ -1369,7 +1369,10 @@ __device__ __forceinline__ uint32_t col_pass(const uint32_t *tmp, uint32_t *acc,
 //   3. median = s_R through a byte LUT.
 // A row-pass warp runs only when one of the blocks it feeds (+-10 rows) runs the pass.
 // Value mode (> 128 distinct values): one pass per distinct value, acc += gap.
-constexpr int CG = 8;  // coarse group (ranks per bucket)
+#ifndef ICE_AL_CG
+#define ICE_AL_CG 6
+#endif
+constexpr int CG = ICE_AL_CG;  // coarse group (ranks per bucket)
 #ifndef ICE_AL_COARSE_V
 #define ICE_AL_COARSE_V false
 #endif
@@ -1653,22 +1656,6 @@ __device__ int load_plane(const uint8_t *tile, int ch, uint32_t *dst, uint32_t *
     return uneq != 0;
 }
 
-// 256-bin histogram of a tile channel read from global memory (ch = 3: V)
-__device__ void channel_hist(const uint8_t *tile, int ch, uint32_t *hist) {
-    const uint4 *t4 = reinterpret_cast<const uint4 *>(tile);
-    for (int g = threadIdx.x; g < 4096; g += NTF) {
-        const uint4 a = __ldg(t4 + 3 * g), b = __ldg(t4 + 3 * g + 1), c = __ldg(t4 + 3 * g + 2);
-        uint32_t R[4], G[4], B[4];
-        unpack16(a, b, c, R, G, B);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t w = ch == 3 ? vmax3(R[q], G[q], B[q]) : (ch == 0 ? R[q] : (ch == 1 ? G[q] : B[q]));
-#pragma unroll
-            for (int k = 0; k < 4; ++k) hist_add(hist, (w >> (8 * k)) & 255, true);
-        }
-    }
-}
-
 __device__ __forceinline__ int block_sum_f(int v, SmemF &s) {
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     __syncthreads();
@@ -1801,10 +1788,11 @@ __device__ __forceinline__ void process_tile256(const uint8_t *__restrict__ rgb,
             }
             __syncthreads();
             for (int ch = 0; ch < 3; ++ch) {
-                if (threadIdx.x < 256) s.hist[threadIdx.x] = 0;
+                subhist_zero(P2);
                 __syncthreads();
-                load_plane(tile, ch, P0);
-                channel_hist(tile, ch, s.hist);
+                load_plane(tile, ch, P0, P2);  // + its histogram in 64 bank-spread copies (P2)
+                __syncthreads();
+                subhist_reduce(P2, s.hist);
                 __syncthreads();
                 const int c_ch = center_from_hist(s.hist, NPX);
                 dilate7(P0, P1, P2, s);
