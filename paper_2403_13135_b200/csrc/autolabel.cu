@@ -1117,6 +1117,7 @@ struct SmemF {
     int act[16];            // median21 block activity, [band][half]
     int kmin[16], kmax[16]; // median21 coarse buckets per block
     unsigned int done_bits; // median21: blocks whose current bucket is final
+    unsigned int need_bits; // blocks holding masked pixels (the channel repair needs bg_c only there)
     uint32_t hist_v[256];   // histogram of V (channel median of the gray repair)
 };
 
@@ -1360,17 +1361,17 @@ __device__ __forceinline__ uint32_t col_pass(const uint32_t *tmp, uint32_t *acc,
 //
 // Rank mode (<= 128 distinct values; src rewritten as 0x80 | rank): the median's rank R(p) =
 // #{i : median > s_i} accumulates in acc, coarse-to-fine:
-//   1. coarse passes at ranks 8k+7 give the bucket K(p) = floor(R / 8) of every pixel; a
+//   1. coarse passes at ranks CG*k + CG-1 give the bucket K(p) = floor(R / CG) of every pixel; a
 //      (32-row x 128-px) block whose pixels all stopped is skipped from then on (counts are
 //      monotone in the threshold), and the loop ends when no block is active;
-//   2. acc becomes 8K; each block then runs only the fine ranks of the buckets its pixels
+//   2. acc becomes CG*K; each block then runs only the fine ranks of the buckets its pixels
 //      occupy ([Kmin, Kmax] of the block), adding a pass's bit only where acc <= i (pixels of
-//      higher buckets have bit 1 there and are already counted by 8K);
+//      higher buckets have bit 1 there and are already counted by CG*K);
 //   3. median = s_R through a byte LUT.
 // A row-pass warp runs only when one of the blocks it feeds (+-10 rows) runs the pass.
 // Value mode (> 128 distinct values): one pass per distinct value, acc += gap.
 #ifndef ICE_AL_CG
-#define ICE_AL_CG 6
+#define ICE_AL_CG 8
 #endif
 constexpr int CG = ICE_AL_CG;  // coarse group (ranks per bucket)
 #ifndef ICE_AL_COARSE_V
@@ -1380,7 +1381,10 @@ constexpr int CG = ICE_AL_CG;  // coarse group (ranks per bucket)
 #define ICE_AL_COARSE_C true
 #endif
 
-__device__ void median21(uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s, bool coarse) {
+// `need`: 16-bit block mask; blocks outside it start inactive and are never computed (their
+// acc words are left unspecified) -- the channel repair reads bg_c only at masked pixels.
+__device__ void median21(uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s, bool coarse,
+                         uint32_t need = 0xffffu) {
     const int nd = collect_values(s);
 #ifdef ICE_AL_PROF
     if (threadIdx.x == 0) atomicAdd(&g_al_prof[8], (unsigned long long)nd);
@@ -1392,7 +1396,7 @@ __device__ void median21(uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s, 
     const bool two_level = rank_mode && coarse;
     const uint32_t v0 = two_level ? 0u : s.vals[0] * 0x01010101u;
     for (int y = band * 32; y < band * 32 + 32; ++y) acc[y * WP + c] = v0;
-    if (threadIdx.x < 16) s.act[threadIdx.x] = 1;
+    if (threadIdx.x < 16) s.act[threadIdx.x] = (need >> threadIdx.x) & 1;
     // 16-bit block mask (bit 2*band + half) -> does this row-pass warp feed an active block?
     const uint32_t feed = (1u << (2 * rwarp + rhalf)) | (rwarp > 0 ? 1u << (2 * (rwarp - 1) + rhalf) : 0u) |
                           (rwarp < 7 ? 1u << (2 * (rwarp + 1) + rhalf) : 0u);
@@ -1462,14 +1466,14 @@ __device__ void median21(uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s, 
         }
     }
     __syncthreads();
-    // 2. buckets: per-block [Kmin, Kmax], acc = 8K
+    // 2. buckets: per-block [Kmin, Kmax], acc = CG*K
     {
         uint32_t mn = 0xffffffffu, mx = 0;
         for (int y = band * 32; y < band * 32 + 32; ++y) {
             const uint32_t a = acc[y * WP + c];
             mn = vmin(mn, a);
             mx = vmax(mx, a);
-            acc[y * WP + c] = a << 3;  // K <= 15: no byte overflow
+            acc[y * WP + c] = a * (uint32_t)CG;  // per byte CG*K <= nd - 1 < 128: no carry
         }
         int kmn = min(min(mn & 255, (mn >> 8) & 255), min((mn >> 16) & 255, mn >> 24));
         int kmx = max(max(mx & 255, (mx >> 8) & 255), max((mx >> 16) & 255, mx >> 24));
@@ -1487,12 +1491,12 @@ __device__ void median21(uint32_t *src, uint32_t *tmp, uint32_t *acc, SmemF &s, 
     for (int i = 0; i + 1 < nd; ++i) {
         if (i % cg == cg - 1) continue;  // coarse rank: counted
         const int k = i / cg;
-        if (i % cg == 0) {  // new bucket: static masks, clear the done set (rare: <= nd / 8 times)
+        if (i % cg == 0) {  // new bucket: static masks, clear the done set (rare: <= nd / CG times)
             span = 0;
             top = 0;
 #pragma unroll
             for (int b2 = 0; b2 < 16; ++b2) {
-                span |= (s.kmin[b2] <= k && k <= s.kmax[b2] ? 1u : 0u) << b2;
+                span |= (s.kmin[b2] <= k && k <= s.kmax[b2] && (need >> b2 & 1) ? 1u : 0u) << b2;
                 top |= (s.kmax[b2] == k ? 1u : 0u) << b2;
             }
             __syncthreads();
@@ -1692,6 +1696,7 @@ __device__ __forceinline__ void process_tile256(const uint8_t *__restrict__ rgb,
         s.hist[threadIdx.x] = 0;
         s.hist2[threadIdx.x] = 0;
     }
+    if (threadIdx.x == 0) s.need_bits = 0;
     subhist_zero(P2);
     __syncthreads();
     // 1. V plane (cloudfilter.py:89) + its histogram, D = dilate7(V) (cloudfilter.py:84)
@@ -1785,8 +1790,10 @@ __device__ __forceinline__ void process_tile256(const uint8_t *__restrict__ rgb,
                     bits |= ((g & 1) | ((g >> 7) & 2) | ((g >> 14) & 4) | ((g >> 21) & 8)) << (4 * q);
                 }
                 s.maskbits[w] = bits;
+                if (bits) atomicOr(&s.need_bits, 1u << (2 * (y >> 5) + ((w & 7) >> 2)));
             }
             __syncthreads();
+            const uint32_t need = s.need_bits;
             for (int ch = 0; ch < 3; ++ch) {
                 subhist_zero(P2);
                 __syncthreads();
@@ -1796,7 +1803,7 @@ __device__ __forceinline__ void process_tile256(const uint8_t *__restrict__ rgb,
                 __syncthreads();
                 const int c_ch = center_from_hist(s.hist, NPX);
                 dilate7(P0, P1, P2, s);
-                median21(P2, P0, P1, s, ICE_AL_COARSE_C);  // bg_c in P1
+                median21(P2, P0, P1, s, ICE_AL_COARSE_C, need);  // bg_c in P1 (blocks in need)
                 load_plane(tile, ch, P0);  // the channel again (L2-resident re-read)
                 __syncthreads();
 #pragma unroll 2
