@@ -63,6 +63,17 @@ typedef struct {
     uint8_t pad[5];
 } IceScheme;
 
+/* Deferred finishing.  ice_finish_defer(1): from now on the fixed-order finishers of the
+ * gradient reductions (split-K weight-gradient slice sums, bias-gradient column sums of
+ * ice_conv_dgrad / ice_halve_dgrad / ice_maxpool_bwd / ice_bias_grad) are recorded instead of
+ * launched; ice_finish_flush(stream) runs every recorded finisher in ONE kernel launch (same
+ * partition and summation order as the immediate path: bit-identical results), ordered after
+ * the work already on `stream`.  While deferring, the caller must keep each call's scratch
+ * untouched until the flush (give every call its own scratch slice).  ice_finish_defer(0)
+ * stops recording and drops anything not yet flushed.  Process-wide; not thread-safe. */
+int ice_finish_defer(int32_t on);
+int ice_finish_flush(void *stream);
+
 /* Fused auto-label kernel (K1): replaces engine.process_tile (engine.py:145-160) =
  * cloudfilter.apply_filter (cloudfilter.py:99-117) + segmentation.segment
  * (segmentation.py:118-128) over a batch of n tiles, plus per-class counts (new).

@@ -49,6 +49,8 @@ SIGNATURES = {
     "ice_autolabel": [_V, _I64, _I32, _I32, ctypes.POINTER(IceFilterCfg), ctypes.POINTER(IceScheme),
                       _V, _V, _V, _V, _V, _V, _V],
     "ice_autolabel_set_path": [_I32],
+    "ice_finish_defer": [_I32],
+    "ice_finish_flush": [_V],
     "ice_autolabel_scene": [_V, _I64, _I32, _I32, ctypes.POINTER(IceFilterCfg), ctypes.POINTER(IceScheme),
                             _V, _V, _V, _V, _V, _V, *_S, _V],
     "ice_cut_tiles": [_V, _I32, _I32, _I32, _I32, _V, _V],
@@ -126,6 +128,44 @@ class Scratch:
         self.bufs = {}
         self.retired = []
         self.sizes = {}
+        self.bump = None  # bump mode: {dev: [chunk, offset, used_this_pass]}
+
+    def begin_bump(self) -> None:
+        """Every call until end_bump() gets its OWN slice (deferred finishers read the partial
+        sums of earlier calls at flush time, so their scratch must not be reused)."""
+        self.bump = {}
+
+    def end_bump(self) -> None:
+        """Leave bump mode; if a pass spilled into more than one chunk, the next pass gets a
+        single chunk of the whole pass's size (steady state: one chunk, nothing allocated)."""
+        import torch
+        for dev, (chunk, _, used) in (self.bump or {}).items():
+            base = self.bufs[("bump", dev)]
+            if (chunk is not base or used > base.numel()) and not torch.cuda.is_current_stream_capturing():
+                self.retired.append(base)
+                self.bufs[("bump", dev)] = torch.empty(used, dtype=torch.uint8, device=dev)
+        self.bump = None
+
+    def _bump_get(self, nbytes: int):
+        import torch
+        dev = torch.cuda.current_device()
+        st = self.bump.get(dev)
+        if st is None:
+            chunk = self.bufs.get(("bump", dev))
+            if chunk is None:
+                chunk = self.bufs[("bump", dev)] = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+            st = self.bump[dev] = [chunk, 0, 0]
+        off = (st[1] + 255) & ~255
+        if off + nbytes > st[0].numel():  # spill: a new chunk; earlier slices stay valid
+            if torch.cuda.is_current_stream_capturing():
+                raise RuntimeError("bump scratch must grow inside a CUDA-graph capture: run the same "
+                                   "step eagerly before capturing")
+            self.retired.append(st[0])
+            st[0] = torch.empty(max(nbytes, 2 * st[0].numel()), dtype=torch.uint8, device=dev)
+            off = 0
+        st[1] = off + nbytes
+        st[2] += nbytes + 256
+        return st[0][off:off + nbytes]
 
     def need(self, fn, name, core) -> int:
         key = (name,) + tuple(bool(a) if t is _V else (a if t in (_I32, _I64) else None)
@@ -141,6 +181,8 @@ class Scratch:
 
     def get(self, stream_handle, nbytes: int):
         import torch
+        if self.bump is not None:
+            return self._bump_get(nbytes)
         dev = torch.cuda.current_device()
         key = dev
         buf = self.bufs.get(key)

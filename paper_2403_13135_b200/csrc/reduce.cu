@@ -3,6 +3,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <utility>
+#include <vector>
 
 #include "reduce.cuh"
 
@@ -128,6 +130,185 @@ __global__ void splitsum_kernel1(const float *__restrict__ ws, int nsplit, size_
     }
 }
 
+// ---- deferred finishing (ice_finish_defer / ice_finish_flush) ------------------------------
+// While deferral is on, colsum_finish / splitsum_finish record their work instead of
+// launching; ice_finish_flush launches ONE kernel that runs every recorded reduction (each
+// item keeps the exact partition and summation order of its stand-alone kernel, so results
+// are bit-identical to the immediate path).  The ~50 small finishers of a backward pass
+// become one launch.
+enum FKind : int { F_COLSUM = 0, F_SEQ4 = 1, F_WIDE4 = 2, F_SEQ1 = 3 };
+struct FItem {
+    int kind, blocks;
+    const float *src;
+    int rows, ld, cols;  // colsum
+    ColSegs segs;
+    RowSched sch;
+    int nsplit;          // splitsum
+    size_t stride, n;    // in float4 (F_SEQ4 / F_WIDE4) or float (F_SEQ1) units
+    float *dst;
+};
+constexpr int MAXF = 40;
+struct FBatch {
+    int n;
+    int start[MAXF + 1];
+    FItem it[MAXF];
+};
+constexpr int FNT = 1024;
+
+__global__ void __launch_bounds__(FNT) flush_kernel(const __grid_constant__ FBatch b) {
+    __shared__ float4 red4[32][33];
+    int i = 0;
+    while (i + 1 < b.n && b.start[i + 1] <= (int)blockIdx.x) ++i;
+    const FItem &f = b.it[i];
+    const int lb = (int)blockIdx.x - b.start[i];
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    if (f.kind == F_COLSUM) {  // == colsum_kernel
+        float(*red)[33] = reinterpret_cast<float(*)[33]>(&red4[0][0]);
+        const int col = lb * 32 + lane;
+        float s = 0.f;
+        if (col < f.cols) {
+            int count = f.rows, r0 = 0, G = f.rows;
+            if (f.sch.bn) {
+                const int lo = (col / f.sch.bn) * f.sch.tm;
+                const int hi = min(lo + f.sch.tm, f.sch.ntiles);
+                G = f.sch.G;
+                count = min(G, hi - lo);
+                r0 = lo % G;
+            }
+            const float *p = f.src + col;
+#pragma unroll 4
+            for (int k = g; k < count; k += 32) {
+                int r = r0 + k;
+                if (r >= G) r -= G;
+                s += __ldcg(p + (size_t)r * f.ld);
+            }
+        }
+        red[g][lane] = s;
+        __syncthreads();
+        if (g == 0 && col < f.cols) {
+            float t = 0.f;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) t += red[k][lane];
+            int c = col;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (c < f.segs.len[q]) {
+                    if (f.segs.dst[q]) f.segs.dst[q][c] += t;
+                    break;
+                }
+                c -= f.segs.len[q];
+            }
+        }
+    } else if (f.kind == F_WIDE4) {  // == splitsum_wide_kernel
+        const float4 *ws = reinterpret_cast<const float4 *>(f.src);
+        const size_t j = (size_t)lb * 32 + lane;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < f.n) {
+#pragma unroll 4
+            for (int z = g; z < f.nsplit; z += 32) {
+                const float4 v = __ldcg(ws + z * f.stride + j);
+                a.x += v.x;
+                a.y += v.y;
+                a.z += v.z;
+                a.w += v.w;
+            }
+        }
+        red4[g][lane] = a;
+        __syncthreads();
+        if (g == 0 && j < f.n) {
+            float4 t = red4[0][lane];
+            for (int k = 1; k < 32; ++k) {
+                const float4 v = red4[k][lane];
+                t.x += v.x;
+                t.y += v.y;
+                t.z += v.z;
+                t.w += v.w;
+            }
+            float4 *d = reinterpret_cast<float4 *>(f.dst) + j;
+            float4 o = *d;
+            o.x += t.x;
+            o.y += t.y;
+            o.z += t.z;
+            o.w += t.w;
+            *d = o;
+        }
+    } else if (f.kind == F_SEQ4) {  // == splitsum_kernel4: slices added in z order, then dst +=
+        const float4 *ws = reinterpret_cast<const float4 *>(f.src);
+        const size_t j = (size_t)lb * FNT + threadIdx.x;
+        if (j < f.n) {
+            float4 a = __ldcg(ws + j);
+            for (int z0 = 1; z0 < f.nsplit; z0 += 4) {
+                float4 v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (z0 + q < f.nsplit) v[q] = __ldcg(ws + (z0 + q) * f.stride + j);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (z0 + q < f.nsplit) {
+                        a.x += v[q].x;
+                        a.y += v[q].y;
+                        a.z += v[q].z;
+                        a.w += v[q].w;
+                    }
+            }
+            float4 *d = reinterpret_cast<float4 *>(f.dst) + j;
+            float4 o = *d;
+            o.x += a.x;
+            o.y += a.y;
+            o.z += a.z;
+            o.w += a.w;
+            *d = o;
+        }
+    } else {  // F_SEQ1 == splitsum_kernel1
+        const size_t j = (size_t)lb * FNT + threadIdx.x;
+        if (j < f.n) {
+            float a = __ldcg(f.src + j);
+            for (int z = 1; z < f.nsplit; ++z) a += __ldcg(f.src + z * f.stride + j);
+            f.dst[j] += a;
+        }
+    }
+}
+
+struct Deferred {
+    bool on = false;
+    std::vector<FItem> items;
+};
+Deferred g_def;
+
+// destination ranges of an item ([lo, hi) byte addresses), for the overlap check
+void dst_ranges(const FItem &f, std::vector<std::pair<uintptr_t, uintptr_t>> &out) {
+    if (f.kind == F_COLSUM) {
+        for (int q = 0; q < 4; ++q)
+            if (f.segs.dst[q] && f.segs.len[q] > 0)
+                out.emplace_back(reinterpret_cast<uintptr_t>(f.segs.dst[q]),
+                                 reinterpret_cast<uintptr_t>(f.segs.dst[q] + f.segs.len[q]));
+    } else {
+        const size_t elems = f.kind == F_SEQ1 ? f.n : 4 * f.n;
+        out.emplace_back(reinterpret_cast<uintptr_t>(f.dst), reinterpret_cast<uintptr_t>(f.dst + elems));
+    }
+}
+
+int launch_batch(const std::vector<FItem> &v, size_t lo, size_t hi, cudaStream_t st) {
+    FBatch b;
+    b.n = (int)(hi - lo);
+    int blocks = 0;
+    for (size_t k = lo; k < hi; ++k) {
+        b.start[k - lo] = blocks;
+        b.it[k - lo] = v[k];
+        blocks += v[k].blocks;
+    }
+    b.start[hi - lo] = blocks;
+    if (blocks == 0) return 0;
+    flush_kernel<<<(unsigned)blocks, FNT, 0, st>>>(b);
+    count_launch();
+    return (int)cudaGetLastError();
+}
+
+int push_or_launch(const FItem &f) {
+    g_def.items.push_back(f);
+    return 0;
+}
+
 }  // namespace
 
 static std::atomic<unsigned long long> g_launches{0};
@@ -136,6 +317,18 @@ void count_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memo
 int colsum_finish(const float *P, int rows, int ld, int cols, const ColSegs &segs, const RowSched &sch,
                   cudaStream_t st) {
     if (rows <= 0 || cols <= 0) return 0;
+    if (g_def.on) {
+        FItem f{};
+        f.kind = F_COLSUM;
+        f.blocks = (cols + 31) / 32;
+        f.src = P;
+        f.rows = rows;
+        f.ld = ld;
+        f.cols = cols;
+        f.segs = segs;
+        f.sch = sch;
+        return push_or_launch(f);
+    }
     colsum_kernel<<<(cols + 31) / 32, 1024, 0, st>>>(P, rows, ld, cols, segs, sch);
     count_launch();
     return (int)cudaGetLastError();
@@ -150,6 +343,24 @@ int splitsum_finish(const float *ws, int nsplit, size_t stride, size_t n, float 
     };
     const float4 *w4 = reinterpret_cast<const float4 *>(ws);
     float4 *d4 = reinterpret_cast<float4 *>(dst);
+    if (g_def.on) {
+        FItem f{};
+        f.src = ws;
+        f.dst = dst;
+        f.nsplit = nsplit;
+        if (!v4) {
+            f.kind = F_SEQ1;
+            f.stride = stride;
+            f.n = n;
+            f.blocks = (int)((n + FNT - 1) / FNT);
+        } else {
+            f.kind = nsplit <= 16 ? F_SEQ4 : F_WIDE4;
+            f.stride = stride / 4;
+            f.n = n / 4;
+            f.blocks = (int)(f.kind == F_SEQ4 ? (f.n + FNT - 1) / FNT : (f.n + 31) / 32);
+        }
+        return push_or_launch(f);
+    }
     if (!v4)
         splitsum_kernel1<<<grid(n), 256, 0, st>>>(ws, nsplit, stride, n, dst);
     else if (nsplit <= 4)
@@ -167,3 +378,38 @@ int splitsum_finish(const float *ws, int nsplit, size_t stride, size_t n, float 
 // Kernels this library has launched in this process (every launch site counts itself): the
 // evidence bench.py reports as gpu_launches.
 extern "C" uint64_t ice_kernel_launches(void) { return ice::g_launches.load(std::memory_order_relaxed); }
+
+// Deferred finishing of gradient reductions (see include/icelabel_b200.h).
+extern "C" int ice_finish_defer(int32_t on) {
+    if (on != 0 && on != 1) return -1;
+    if (!on) ice::g_def.items.clear();  // pending items are dropped (flush first to keep them)
+    ice::g_def.on = on != 0;
+    return 0;
+}
+
+extern "C" int ice_finish_flush(void *stream) {
+    using namespace ice;
+    std::vector<FItem> v;
+    v.swap(g_def.items);
+    cudaStream_t st = (cudaStream_t)stream;
+    // batches of <= MAXF items whose destinations do not overlap (items touching the same
+    // gradient keep their recorded order across batches)
+    size_t lo = 0;
+    std::vector<std::pair<uintptr_t, uintptr_t>> seen, mine;
+    for (size_t k = 0; k < v.size(); ++k) {
+        mine.clear();
+        dst_ranges(v[k], mine);
+        bool clash = k - lo >= (size_t)MAXF;
+        for (const auto &a : mine)
+            for (const auto &b : seen)
+                if (a.first < b.second && b.first < a.second) clash = true;
+        if (clash) {
+            const int rc = launch_batch(v, lo, k, st);
+            if (rc) return rc;
+            lo = k;
+            seen.clear();
+        }
+        seen.insert(seen.end(), mine.begin(), mine.end());
+    }
+    return v.size() > lo ? launch_batch(v, lo, v.size(), st) : 0;
+}

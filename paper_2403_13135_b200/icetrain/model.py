@@ -420,9 +420,31 @@ class UNetEngine:
         _native.call("ice_bias_grad", dz.data_ptr(), rows, dz.shape[-1], self.b(name, self.grads).data_ptr(),
                      _native.stream_handle())
 
+    # Deferred finishing (ice_finish_defer): the ~50 fixed-order finishers of the weight / bias
+    # gradient reductions run as ONE kernel per flush instead of one launch each (bit-identical
+    # results); every backward call then gets its own scratch slice (bump mode).
+    defer_finish = True
+
     def backward(self, A: _Acts, dz, on_layer_done=None) -> None:
         """Accumulate parameter gradients into self.grads (dz: dZ of up.{d-1}.block.2).
-        on_layer_done(name) fires after each layer's gradient is complete (DP buckets)."""
+        on_layer_done(name) fires after each layer's gradient is complete (DP buckets); a
+        callback that reads gradients before backward returns calls flush_deferred() first."""
+        if not self.defer_finish:
+            return self._backward(A, dz, on_layer_done)
+        _native.call("ice_finish_defer", 1)
+        _native.scratch.begin_bump()
+        try:
+            self._backward(A, dz, on_layer_done)
+            self.flush_deferred()
+        finally:
+            _native.call("ice_finish_defer", 0)
+            _native.scratch.end_bump()
+
+    def flush_deferred(self, stream=None) -> None:
+        """Run the gradient finishers recorded so far (one launch; no-op when none)."""
+        _native.call("ice_finish_flush", _native.stream_handle(stream))
+
+    def _backward(self, A: _Acts, dz, on_layer_done=None) -> None:
         d = self.spec.depth
         B = A.B
         st = _native.stream_handle()

@@ -150,6 +150,8 @@ class GradBucketer:
 
     def on_layer_done(self, name: str) -> None:
         dist = _dist()
+        if self.cuda and name in self.by_last and hasattr(self.engine, "flush_deferred"):
+            self.engine.flush_deferred()  # the bucket's deferred gradient finishers, first
         for start, stop, _ in self.by_last.get(name, ()):
             g = self.engine.grads[start:stop]
             if not self.cuda:

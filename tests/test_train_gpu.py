@@ -114,6 +114,35 @@ def test_paper_spec_step_is_bit_reproducible():
     assert float(g0.abs().sum()) > 0
 
 
+def test_deferred_finishers_match_immediate_bit_for_bit():
+    """ice_finish_defer / ice_finish_flush: the gradient finishers of a paper-spec backward run
+    as one batched launch with the same partitions and summation orders, so the gradients are
+    bit-identical to launching each finisher on its own -- with far fewer launches."""
+    from paper_2403_13135_b200 import _native
+    spec = UNetSpec(dropout=0.1)
+    rng = np.random.default_rng(12)
+    x = torch.from_numpy(rng.integers(0, 256, (8, 256, 256, 3), dtype=np.uint8)).cuda()
+    y = torch.from_numpy(rng.integers(0, 3, (8, 256, 256), dtype=np.uint8)).cuda()
+    torch.manual_seed(0)
+    eng = UNet(spec).engine
+    res = {}
+    for defer in (False, True, True):
+        eng.defer_finish = defer
+        eng.grads.zero_()
+        A = eng.forward(x, train=True, seed=5)
+        dz = eng.head(A, y, train=True, grad_scale=1.0 / y.numel())
+        torch.cuda.synchronize()
+        k0 = _native.kernel_launches()
+        eng.backward(A, dz)
+        torch.cuda.synchronize()
+        res.setdefault(defer, []).append((eng.grads.clone(), _native.kernel_launches() - k0))
+    eng.defer_finish = True
+    (g_imm, n_imm), = res[False]
+    (g_def, n_def), (g_def2, _) = res[True]
+    assert torch.equal(g_imm, g_def) and torch.equal(g_def, g_def2)
+    assert n_def <= n_imm - 30, (n_def, n_imm)
+
+
 def test_synchronized_step_same_inputs_same_bits():
     """synchronized_step twice from the same state (two lockstep replicas, ragged shards)."""
     spec = UNetSpec(input_size=64, base_channels=16, depth=4, dropout=0.0)

@@ -18,7 +18,7 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int CG, int M, int N>
+template <int CG, int M, int N, int NACC>
 __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long *cycles) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long *c
         tc::fence_barrier_init();
     }
     tc::fence_proxy_async_smem();
-    constexpr int COLS = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
+    constexpr int NC = N * NACC;
+    constexpr int COLS = NC <= 32 ? 32 : (NC <= 64 ? 64 : (NC <= 128 ? 128 : (NC <= 256 ? 256 : 512)));
     if (warp == 0) {
         if (CG == 1) tc::tmem_alloc<COLS>(&tslot);
         else {
@@ -58,11 +59,15 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long *c
             for (int k = 0; k < 4; ++k) {
                 const uint64_t ad = tc::sw128_desc(a0 + 32 * k, 16, 1024), bd = tc::sw128_desc(b0 + 32 * k, 16, 1024);
                 const uint32_t acc = (it | k) ? 1u : 0u;
-                if (CG == 1) tc::umma_f16(tmem, ad, bd, idesc, acc);
-                else
-                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-                                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+#pragma unroll
+                for (int q = 0; q < NACC; ++q) {  // independent accumulators, interleaved
+                    const uint32_t d = tmem + q * N;
+                    if (CG == 1) tc::umma_f16(d, ad, bd, idesc, acc);
+                    else
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                                     "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                }
             }
         }
         if (CG == 1) tc::umma_commit(&done);
@@ -84,10 +89,10 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long *c
     }
 }
 
-template <int CG, int M, int N>
+template <int CG, int M, int N, int NACC = 1>
 void run(int iters) {
     constexpr int smem = 1024 + (M / CG + N / CG) * 128;
-    auto k = probe<CG, M, N>;
+    auto k = probe<CG, M, N, NACC>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     unsigned long long *dc;
     cudaMalloc(&dc, 8);
@@ -114,10 +119,10 @@ void run(int iters) {
     cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long cyc = 0;
     cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost);
-    const double macs_per_cta = (double)(M / CG) * N * 64 * iters;  // this CTA's rows
+    const double macs_per_cta = (double)(M / CG) * N * 64 * iters * NACC;  // this CTA's rows
     const double tflops = 2.0 * macs_per_cta * 148 / (ms * 1e-3) / 1e12;
     const double mac_per_cyc = macs_per_cta / (double)cyc;
-    printf("cg=%d M=%3d N=%3d smem/MMA/SM=%5d B: %8.3f ms  %7.1f TFLOP/s  %6.0f MAC/cyc/SM  %s\n", CG, M, N,
+    printf("cg=%d M=%3d N=%3d acc=%d smem/MMA/SM=%5d B: %8.3f ms  %7.1f TFLOP/s  %6.0f MAC/cyc/SM  %s\n", CG, M, N, NACC,
            (M / CG + N / CG) * 32, ms, tflops, mac_per_cyc, cudaGetErrorString(err));
     cudaFree(dc);
 }
@@ -132,5 +137,9 @@ int main() {
     run<2, 256, 256>(it);
     run<2, 128, 256>(it);
     run<2, 128, 128>(it);
+    run<1, 128, 64, 2>(it);
+    run<1, 128, 64, 4>(it);
+    run<2, 256, 64, 2>(it);
+    run<1, 128, 32, 4>(it);
     return 0;
 }
