@@ -203,6 +203,21 @@ int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_planes, int
 int ice_stem_im2col(const uint8_t *img, int32_t n, int32_t h, int32_t w, uint16_t *out,
                     void *stream);
 
+/* Fused stem forward, replacing ice_stem_im2col + the K = 64 GEMM on the training path: the
+ * first conv (3 -> 64, 3 x 3, model.py:64-76 on x = u8 / 255, train.py:63) straight from the
+ * u8 images, no im2col buffer.  wt bf16 [64][64] = W[co][(r*3+s)*3+c] (columns 27..63 zero,
+ * the ice_stem_im2col column order), bias fp32 [64]; y = ReLU(conv + bias) bf16 [n][h][w][64];
+ * relu_bits (optional) u32 [2][n*h*w]: bit j of word c = channel 32 c + j of y > 0. */
+int ice_stem_fprop(const uint8_t *img, int32_t n, int32_t h, int32_t w, const uint16_t *wt,
+                   const float *bias, uint16_t *y, uint32_t *relu_bits, void *stream);
+
+/* Fused stem weight gradient: dw[co][k] += sum_p dz[p][co] * x_col[p][k] with the im2col
+ * columns gathered from the u8 images (k < 27; columns 27..63 get nothing).  dz bf16
+ * [n][h][w][64], dw fp32 [64][64].  Per-CTA partial slices in scratch, added in CTA order
+ * (deterministic; deferrable, see ice_finish_defer). */
+int ice_stem_wgrad(const uint8_t *img, int32_t n, int32_t h, int32_t w, const uint16_t *dz, float *dw,
+                   void *scratch, uint64_t *scratch_bytes, void *stream);
+
 /* Same stem from an fp32 NHWC image already in [0, 1] (UNet.forward on float input). */
 int ice_stem_im2col_f32(const float *img, int32_t n, int32_t h, int32_t w, uint16_t *out,
                         void *stream);

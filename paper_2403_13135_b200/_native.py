@@ -70,6 +70,8 @@ SIGNATURES = {
     "ice_halve_dgrad": [_V, _I32, _I32, _I32, _I32, _V, _I32, _V, _V, _V, _V, *_S, _V],
     "ice_halve_wgrad": [_V, _I32, _V, _I32, _I32, _I32, _I32, _V, *_S, _V],
     "ice_stem_im2col": [_V, _I32, _I32, _I32, _V, _V],
+    "ice_stem_fprop": [_V, _I32, _I32, _I32, _V, _V, _V, _V, _V],
+    "ice_stem_wgrad": [_V, _I32, _I32, _I32, _V, _V, *_S, _V],
     "ice_stem_im2col_f32": [_V, _I32, _I32, _I32, _V, _V],
     "ice_pad_weights": [_V, _I32, _I32, _V, _I32, _V],
     "ice_halve_prep": [_V, _I32, _I32, _V, _V],

@@ -206,7 +206,8 @@ class _Acts:
         e = lambda *shape: torch.empty(shape, dtype=torch.bfloat16, device=device)  # noqa: E731
         lv = lambda L, c, n=B: e(n, H >> L, W >> L, c)  # noqa: E731  (level-L tensor)
         self.B, self.H, self.W = B, H, W
-        self.stem = e(B, H, W, 64)
+        self.stem = None    # im2col buffer, only for float input / the unfused stem (lazy)
+        self.images = None  # u8 input of the fused stem (its weight gradient re-reads it)
         self.a1 = [lv(i, cp[i]) for i in range(d)]
         self.a2 = [lv(i, cp[i]) for i in range(d)]
         self.pool = [lv(i + 1, cp[i]) for i in range(d)]
@@ -357,17 +358,26 @@ class UNetEngine:
         B, H, W = images.shape[0], images.shape[1], images.shape[2]
         A = self.ensure(B, H, W)
         st = _native.stream_handle()
-        if float_input:
-            _native.call("ice_stem_im2col_f32", images.data_ptr(), B, H, W, A.stem.data_ptr(), st)
-        else:
-            _native.call("ice_stem_im2col", images.data_ptr(), B, H, W, A.stem.data_ptr(), st)
+        fused = self.fused_stem and not float_input
+        if fused:
+            images = images.contiguous()
+        A.images = images if fused else None
+        if not fused:
+            if A.stem is None:
+                A.stem = torch.empty((B, H, W, 64), dtype=torch.bfloat16, device=self.device)
+            fn = "ice_stem_im2col_f32" if float_input else "ice_stem_im2col"
+            _native.call(fn, images.data_ptr(), B, H, W, A.stem.data_ptr(), st)
         self._drop_masks(A, seed, train)
         dr = A.drop.get
         x = A.stem
         for i in range(d):
             n0, n2 = f"down.{i}.block.0", f"down.{i}.block.2"
-            ops.conv_fprop(x, self.wb16(n0), self.b(n0), relu=True, ksize=1 if i == 0 else 3, out=A.a1[i],
-                           relu_bits=A.a1_bits[i])
+            if i == 0 and fused:  # stem straight from the u8 images (csrc/stem.cu)
+                _native.call("ice_stem_fprop", _native.ptr(images), B, H, W, self.wb16(n0).data_ptr(),
+                             self.b(n0).data_ptr(), A.a1[0].data_ptr(), A.a1_bits[0].data_ptr(), st)
+            else:
+                ops.conv_fprop(x, self.wb16(n0), self.b(n0), relu=True, ksize=1 if i == 0 else 3, out=A.a1[i],
+                               relu_bits=A.a1_bits[i])
             ops.conv_fprop(A.a1[i], self.wb16(n2), self.b(n2), relu=True, drop=dr(f"down.{i}"), out=A.a2[i])
             a2 = A.a2[i]
             _native.call("ice_maxpool_fwd", a2.data_ptr(), B, a2.shape[1], a2.shape[2], a2.shape[3],
@@ -423,7 +433,10 @@ class UNetEngine:
     # Deferred finishing (ice_finish_defer): the ~50 fixed-order finishers of the weight / bias
     # gradient reductions run as ONE kernel per flush instead of one launch each (bit-identical
     # results); every backward call then gets its own scratch slice (bump mode).
-    defer_finish = True
+    defer_finish = os.environ.get("ICE_DEFER_FINISH", "1") != "0"  # A/B switch, read once
+    # The first conv straight from the u8 images (ice_stem_fprop / ice_stem_wgrad) instead of
+    # a bf16 im2col buffer + GEMMs; float input always takes the im2col path.
+    fused_stem = os.environ.get("ICE_FUSED_STEM", "1") != "0"  # A/B switch, read once
 
     def backward(self, A: _Acts, dz, on_layer_done=None) -> None:
         """Accumulate parameter gradients into self.grads (dz: dZ of up.{d-1}.block.2).
@@ -500,7 +513,10 @@ class UNetEngine:
             dz1 = A.dz_b[i]
             ops.conv_dgrad(dz2, self.wb16(n2), A.a1[i].shape[3], out1=dz1, **self._relu(A.a1[i], A.a1_bits[i]), db1=self.b(n0, G))
             done(n2)
-            if i == 0:
+            if i == 0 and A.images is not None:
+                _native.call("ice_stem_wgrad", A.images.data_ptr(), B, A.H, A.W, dz1.data_ptr(),
+                             self.w(n0, G).data_ptr(), st)
+            elif i == 0:
                 ops.conv_wgrad(A.stem, dz1, self.w(n0, G), ksize=1)
             else:
                 ops.conv_wgrad(A.pool[i - 1], dz1, self.w(n0, G))

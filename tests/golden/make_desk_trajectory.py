@@ -12,6 +12,7 @@ the last 50 step losses, final whole-corpus eval loss) to the reference's own sp
 Run in the build container (/root/reference present; ~25 min on 8 cores):
 
     python tests/golden/make_desk_trajectory.py [--spread N]
+    python tests/golden/make_desk_trajectory.py --extend 32   # more perturbed runs, appended
 """
 import hashlib
 import os
@@ -73,8 +74,29 @@ def run(x, y, perturb_seed=None):
     return losses, tot / y.numel()
 
 
+def extend(total: int) -> None:
+    """Append perturbed reference runs (seeds 1000 + k, k = len(existing) .. total - 1) to the
+    existing golden, saving after every run: more samples of the reference's own spread make
+    the late-training comparison a proper two-sample test."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "desk_trajectory.pt")
+    gold = torch.load(path)
+    x_u8, y = reference_corpus()
+    assert sha(x_u8) == gold["tiles_sha"] and sha(y) == gold["labels_sha"]
+    x = torch.from_numpy(x_u8).permute(0, 3, 1, 2).float() / 255.0
+    yt = torch.from_numpy(y.astype(np.int64))
+    while len(gold["perturbed"]) < total:
+        k = len(gold["perturbed"])
+        losses, ev = run(x, yt, perturb_seed=1000 + k)
+        gold["perturbed"].append(losses)
+        gold["perturbed_eval"].append(ev)
+        torch.save(gold, path)
+        print(f"run {k}: last {losses[-1]:.4f} late median {float(np.median(losses[-50:])):.4f}", flush=True)
+
+
 def main():
     torch.set_num_threads(os.cpu_count())
+    if "--extend" in sys.argv:
+        return extend(int(sys.argv[sys.argv.index("--extend") + 1]))
     spread = int(sys.argv[sys.argv.index("--spread") + 1]) if "--spread" in sys.argv else 8
     x_u8, y = reference_corpus()
     x = torch.from_numpy(x_u8).permute(0, 3, 1, 2).float() / 255.0

@@ -254,3 +254,50 @@ def test_stem_im2col(shape):
     want = torch.zeros(n * h * w, 64, dtype=torch.bfloat16, device="cuda")
     want[:, :27] = ref.to(torch.bfloat16)
     assert torch.equal(out.view(torch.bfloat16), want)
+
+
+def _stem_ref(img, wt, bias):
+    """fp32 reference of the stem on the kernel's exact operands: bf16(x / 255) and bf16 weights."""
+    x = (img.float() / 255.0).to(torch.bfloat16).float().permute(0, 3, 1, 2)
+    w27 = wt[:, :27].float().view(64, 3, 3, 3).permute(0, 3, 1, 2)  # [co][(r*3+s)*3+c] -> OIHW
+    return F.conv2d(x, w27, bias, padding=1)
+
+
+@pytest.mark.parametrize("shape", [(3, 8, 16), (2, 5, 7), (2, 256, 256), (4, 33, 64), (1, 64, 32)], ids=str)
+def test_stem_fused_fprop_and_wgrad(shape):
+    """ice_stem_fprop / ice_stem_wgrad (the first conv straight from u8 pixels, mma.sync with
+    gathered im2col fragments) against torch fp32 on the same bf16 operands; the ReLU mask
+    words agree with the stored activations bit for bit."""
+    from paper_2403_13135_b200 import _native
+    n, h, w = shape
+    g = torch.Generator().manual_seed(11)
+    img = torch.randint(0, 256, (n, h, w, 3), generator=g, dtype=torch.uint8).cuda()
+    wt = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
+    wt[:, :27] = (torch.randn(64, 27, generator=g) * 0.3).to(torch.bfloat16).cuda()
+    bias = (torch.randn(64, generator=g) * 0.1).cuda()
+    y = torch.empty(n, h, w, 64, dtype=torch.bfloat16, device="cuda")
+    bits = torch.zeros(2, n * h * w, dtype=torch.int32, device="cuda")
+    st = _native.stream_handle()
+    _native.call("ice_stem_fprop", img.data_ptr(), n, h, w, wt.data_ptr(), bias.data_ptr(), y.data_ptr(),
+                 bits.data_ptr(), st)
+    torch.cuda.synchronize()
+    ref = torch.relu(_stem_ref(img, wt, bias)).permute(0, 2, 3, 1)
+    assert rel(y, ref) < 4e-3
+    pos = (y.view(-1, 64).float() > 0).to(torch.int64)
+    want = torch.stack([(pos[:, 32 * c:32 * c + 32] << torch.arange(32, device="cuda")).sum(1) for c in range(2)])
+    assert torch.equal(bits.to(torch.int64) & 0xffffffff, want & 0xffffffff)
+    # weight gradient: dW[co][k] = sum_p dz[p][co] col[p][k]; columns 27..63 untouched
+    dz = rnd(n, h, w, 64, scale=0.5)
+    dw = torch.full((64, 64), 0.25, device="cuda")
+    _native.call("ice_stem_wgrad", img.data_ptr(), n, h, w, dz.data_ptr(), dw.data_ptr(), st)
+    torch.cuda.synchronize()
+    x = (img.float() / 255.0).to(torch.bfloat16).float().permute(0, 3, 1, 2)
+    cols = F.unfold(x, 3, padding=1).view(n, 3, 9, h * w).permute(0, 3, 2, 1).reshape(n * h * w, 27)
+    want_w = dz.view(-1, 64).float().t() @ cols
+    assert rel(dw[:, :27] - 0.25, want_w) < 1e-4
+    assert torch.equal(dw[:, 27:], torch.full((64, 37), 0.25, device="cuda"))
+    # the same, deterministic: a second call adds bit-identical partial sums
+    dw2 = torch.full((64, 64), 0.25, device="cuda")
+    _native.call("ice_stem_wgrad", img.data_ptr(), n, h, w, dz.data_ptr(), dw2.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert torch.equal(dw, dw2)
