@@ -265,10 +265,11 @@ int ice_dropout_scale(int32_t count, float p, uint64_t seed, const int64_t *step
                       void *stream);
 
 /* torch.optim.Adam step (defaults of train.py:149: no weight decay, no amsgrad) over flat
- * fp32 buffers, fused with the bf16 working-copy write and zeroing of g.  The step t is
+ * fp32 buffers, fused with the bf16 working-copy write and zeroing of g.  Hyper-parameters are
+ * doubles (torch forms 1 - beta and the bias corrections from Python floats).  The step t is
  * `step`, or *step_dev when step_dev is non-NULL (bias corrections computed on the device). */
 int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64_t step,
-             const int64_t *step_dev, float lr, float beta1, float beta2, float eps,
+             const int64_t *step_dev, double lr, double beta1, double beta2, double eps,
              uint16_t *out_bf16, void *stream);
 
 /* *counter += delta on the device (the step counter advanced inside CUDA graphs). */

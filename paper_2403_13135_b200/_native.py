@@ -40,6 +40,7 @@ _V = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
 _F32 = ctypes.c_float
+_F64 = ctypes.c_double
 _U64P = ctypes.POINTER(ctypes.c_uint64)
 _S = [_V, _U64P]  # (scratch, scratch_bytes) before the stream: see include/icelabel_b200.h
 
@@ -80,7 +81,7 @@ SIGNATURES = {
     "ice_head_ce": [_V, _I64, _I32, _V, _V, _V, _V, _F32, _V, _V, _V, _V, _V, _V, *_S, _V],
     "ice_bias_grad": [_V, _I64, _I32, _V, *_S, _V],
     "ice_dropout_scale": [_I32, _F32, ctypes.c_uint64, _V, _V, _V],
-    "ice_adam": [_V, _V, _V, _V, _I64, _I64, _V, _F32, _F32, _F32, _F32, _V, _V],
+    "ice_adam": [_V, _V, _V, _V, _I64, _I64, _V, _F64, _F64, _F64, _F64, _V, _V],
     "ice_counter_add": [_V, _I64, _V],
     "ice_cast_bf16": [_V, _I64, _V, _V],
     "ice_fill_f32": [_V, _I64, _F32, _V],

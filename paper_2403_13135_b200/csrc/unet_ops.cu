@@ -483,12 +483,13 @@ __global__ void dropout_scale_kernel(int count, float p, unsigned long long seed
 // ---- fused Adam (torch.optim.Adam defaults, train.py:149): one pass over p, g, m, v;
 // writes the bf16 working copy and zeroes the gradient for the next step ---------------
 __global__ void adam_kernel(float *__restrict__ p, float *__restrict__ g, float *__restrict__ m, float *__restrict__ v,
-                            long long n, float lr_corr, float b1, float b2, float eps, float bc2_sqrt,
-                            uint16_t *__restrict__ out_bf16, const long long *__restrict__ step_dev, float lr) {
+                            long long n, float lr_corr, float omb1, float b2, float omb2, float eps, float bc2_sqrt,
+                            uint16_t *__restrict__ out_bf16, const long long *__restrict__ step_dev, double lr,
+                            double b1d, double b2d) {
     if (step_dev) {  // bias corrections from the device step counter (CUDA-graph replays)
         const double t = (double)*step_dev;
-        lr_corr = (float)((double)lr / (1.0 - pow((double)b1, t)));
-        bc2_sqrt = (float)sqrt(1.0 - pow((double)b2, t));
+        lr_corr = (float)(lr / (1.0 - pow(b1d, t)));
+        bc2_sqrt = (float)sqrt(1.0 - pow(b2d, t));
     }
     const long long n4 = n / 4;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
@@ -499,8 +500,8 @@ __global__ void adam_kernel(float *__restrict__ p, float *__restrict__ g, float 
         float *pe = &pp.x, *ge = &gg.x, *me = &mm.x, *ve = &vv.x;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            me[e] = me[e] + (1.f - b1) * (ge[e] - me[e]);
-            ve[e] = ve[e] * b2 + (1.f - b2) * ge[e] * ge[e];
+            me[e] = me[e] + omb1 * (ge[e] - me[e]);
+            ve[e] = ve[e] * b2 + omb2 * ge[e] * ge[e];
             const float denom = sqrtf(ve[e]) / bc2_sqrt + eps;
             pe[e] = pe[e] - lr_corr * (me[e] / denom);
         }
@@ -518,8 +519,8 @@ __global__ void adam_kernel(float *__restrict__ p, float *__restrict__ g, float 
     // tail
     for (long long i = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const float ge = g[i];
-        const float me = m[i] + (1.f - b1) * (ge - m[i]);
-        const float ve = v[i] * b2 + (1.f - b2) * ge * ge;
+        const float me = m[i] + omb1 * (ge - m[i]);
+        const float ve = v[i] * b2 + omb2 * ge * ge;
         const float pe = p[i] - lr_corr * (me / (sqrtf(ve) / bc2_sqrt + eps));
         m[i] = me;
         v[i] = ve;
@@ -672,16 +673,20 @@ extern "C" int ice_dropout_scale(int32_t count, float p, uint64_t seed, const in
 }
 
 extern "C" int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64_t step, const int64_t *step_dev,
-                        float lr, float beta1, float beta2, float eps, uint16_t *out_bf16, void *stream) {
+                        double lr, double beta1, double beta2, double eps, uint16_t *out_bf16, void *stream) {
     if (!p || !g || !m || !v || n < 0 || (step < 1 && !step_dev)) return ICE_EINVAL;
     if (n == 0) return ICE_OK;
-    // torch.optim.Adam (_single_tensor_adam): step_size = lr / (1 - b1^t), denom = sqrt(v)/sqrt(1 - b2^t) + eps
+    // torch.optim.Adam (_single_tensor_adam): exp_avg.lerp_(g, 1 - b1); exp_avg_sq.mul_(b2)
+    // .addcmul_(g, g, value=1 - b2); step_size = lr / (1 - b1^t), denom = sqrt(v)/sqrt(1 - b2^t)
+    // + eps.  The scalars are formed in double from the caller's (Python) values, then used as
+    // fp32 like torch's fp32 kernels do (1 - 0.999 in double is 0.001; in fp32 from 0.999f it
+    // would be 0.00099999 -- a 1.3e-5 relative bias in the second moment).
     const double t = step < 1 ? 1.0 : (double)step;
-    const double bc1 = 1.0 - pow((double)beta1, t);
-    const double bc2 = 1.0 - pow((double)beta2, t);
+    const double bc1 = 1.0 - pow(beta1, t);
+    const double bc2 = 1.0 - pow(beta2, t);
     adam_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, (cudaStream_t)stream>>>(
-        p, g, m, v, n, (float)(lr / bc1), beta1, beta2, eps, (float)sqrt(bc2), out_bf16,
-        reinterpret_cast<const long long *>(step_dev), lr);
+        p, g, m, v, n, (float)(lr / bc1), (float)(1.0 - beta1), (float)beta2, (float)(1.0 - beta2), (float)eps,
+        (float)sqrt(bc2), out_bf16, reinterpret_cast<const long long *>(step_dev), lr, beta1, beta2);
     ice::count_launch();
     LAUNCH_CHECK();
 }
