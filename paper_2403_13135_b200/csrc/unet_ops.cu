@@ -147,17 +147,18 @@ __global__ void halve_prep_kernel(const float *__restrict__ w, int cout, int c, 
 // ---- max-pool 2x2 / 2 (model.py:102,125 nn.MaxPool2d(2)) ----------------------------
 // 8 channels per thread (16-byte vectors)
 __global__ void maxpool_fwd_kernel(const uint16_t *__restrict__ x, int n, int h, int w, int c, uint16_t *__restrict__ y) {
+    // 32-bit index math (the host guarantees 4 x total < 2^31): 64-bit division made the
+    // level-0 passes instruction-bound
     const int ho = h / 2, wo = w / 2, cv = c / 8;
-    const long long total = (long long)n * ho * wo * cv;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-        const int cg = (int)(i % cv);
-        long long p = i / cv;
-        const int xo = (int)(p % wo);
-        const int yo = (int)((p / wo) % ho);
-        const long long img = p / ((long long)wo * ho);
+    const int total = n * ho * wo * cv;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int cg = i % cv;
+        const int p = i / cv;
+        const int xo = p % wo, q = p / wo;
+        const int yo = q % ho, img = q / ho;
         const uint4 *src = reinterpret_cast<const uint4 *>(x);
-        const long long r0 = ((img * h + 2 * yo) * w + 2 * xo) * cv + cg;
-        uint4 a = src[r0], b = src[r0 + cv], cc = src[r0 + (long long)w * cv], d = src[r0 + (long long)w * cv + cv];
+        const int r0 = ((img * h + 2 * yo) * w + 2 * xo) * cv + cg;
+        uint4 a = src[r0], b = src[r0 + cv], cc = src[r0 + w * cv], d = src[r0 + w * cv + cv];
         const uint16_t *pa = reinterpret_cast<const uint16_t *>(&a), *pb = reinterpret_cast<const uint16_t *>(&b);
         const uint16_t *pc = reinterpret_cast<const uint16_t *>(&cc), *pd = reinterpret_cast<const uint16_t *>(&d);
         uint4 o;
@@ -184,18 +185,19 @@ __global__ void maxpool_fwd_kernel(const uint16_t *__restrict__ x, int n, int h,
 __global__ void maxpool_bwd_kernel(const uint16_t *__restrict__ x, const uint16_t *__restrict__ dpool,
                                    const uint16_t *__restrict__ add, const float *__restrict__ drop, int n, int h, int w,
                                    int c, uint16_t *__restrict__ dz, float *__restrict__ bpart) {
-    const int ho = h / 2, wo = w / 2, cv = c / 8;
-    const long long total = (long long)n * ho * wo * cv;
+    // 32-bit index math (the host guarantees 4 x total < 2^31); cv is a power of two and the
+    // grid-stride a multiple of it, so the thread's channel group is fixed
+    const int ho = h / 2, wo = w / 2, cv = c / 8, lcv = __ffs(cv) - 1;
+    const int total = n * ho * wo * cv;
     float bsum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const long long stride = (long long)gridDim.x * blockDim.x;  // multiple of cv (host)
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += stride) {
-        const int cg = (int)(i % cv);
-        long long p = i / cv;
-        const int xo = (int)(p % wo);
-        const int yo = (int)((p / wo) % ho);
-        const long long img = p / ((long long)wo * ho);
-        const long long r[4] = {((img * h + 2 * yo) * w + 2 * xo) * cv + cg, 0, 0, 0};
-        const long long idx[4] = {r[0], r[0] + cv, r[0] + (long long)w * cv, r[0] + (long long)w * cv + cv};
+    const int stride = gridDim.x * blockDim.x;  // multiple of cv (host)
+    const int cg = (blockIdx.x * blockDim.x + threadIdx.x) & (cv - 1);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int p = i >> lcv;
+        const int xo = p % wo, q = p / wo;
+        const int yo = q % ho, img = q / ho;
+        const int r0 = ((img * h + 2 * yo) * w + 2 * xo) * cv + cg;
+        const int idx[4] = {r0, r0 + cv, r0 + w * cv, r0 + w * cv + cv};
         uint4 xv[4], av[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -575,6 +577,7 @@ extern "C" int ice_halve_prep(const float *w, int32_t cout, int32_t c, uint16_t 
 extern "C" int ice_maxpool_fwd(const uint16_t *x, int32_t n, int32_t h, int32_t w, int32_t c, uint16_t *y,
                                void *stream) {
     if (!x || !y || n < 1 || h < 2 || w < 2 || (h | w) & 1 || c % 8) return ICE_EINVAL;
+    if ((long long)n * h * w * (c / 8) >= (1LL << 31)) return ICE_ETOOBIG;
     maxpool_fwd_kernel<<<grid_for((long long)n * (h / 2) * (w / 2) * (c / 8), 256), 256, 0, (cudaStream_t)stream>>>(
         x, n, h, w, c, y);
     ice::count_launch();
@@ -596,6 +599,7 @@ extern "C" int ice_maxpool_bwd(const uint16_t *x, const uint16_t *dpool, const u
     const int cv = c / 8, threads = 256;
     // grid * threads must be a multiple of cv (fixed channels per thread for the bias sums)
     if (cv > threads || threads % cv) return ICE_EINVAL;  // c <= 2048, power-of-two channel groups
+    if ((long long)n * h * w * cv >= (1LL << 31)) return ICE_ETOOBIG;
     long long blocks = (total + threads - 1) / threads;
     // one wave of resident blocks (72 registers: 3 per SM, not 4 -- a 4th would run as a tail)
     static int resident = 0;
