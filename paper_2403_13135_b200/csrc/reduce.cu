@@ -3,6 +3,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -392,6 +394,13 @@ extern "C" int ice_finish_flush(void *stream) {
     std::vector<FItem> v;
     v.swap(g_def.items);
     cudaStream_t st = (cudaStream_t)stream;
+    static const bool dbg = getenv("ICE_FLUSH_DEBUG") != nullptr;
+    if (dbg)
+        for (const FItem &f : v)
+            fprintf(stderr, "flush item kind %d blocks %d rows %d cols %d nsplit %d n %zu bytes %.1f MB\n", f.kind,
+                    f.blocks, f.rows, f.cols, f.nsplit, f.n,
+                    f.kind == F_COLSUM ? (double)f.rows * f.ld * 4 / 1e6
+                                       : (double)f.nsplit * f.n * (f.kind == F_SEQ1 ? 4 : 16) / 1e6);
     // batches of <= MAXF items whose destinations do not overlap (items touching the same
     // gradient keep their recorded order across batches)
     size_t lo = 0;
