@@ -57,31 +57,38 @@ __global__ void __launch_bounds__(1024) colsum_kernel(const float *__restrict__ 
     }
 }
 
-// few slices: one thread per float4, the slices' loads issued together, added in order
-template <int MAXZ>
+// slices added in z order, then dst += (one thread per float4; loads issued 4 at a time)
+__device__ __forceinline__ void seq_sum4(const float4 *__restrict__ ws, int nsplit, size_t stride4, size_t i,
+                                         float4 *__restrict__ dst) {
+    float4 a = __ldcg(ws + i);
+    for (int z0 = 1; z0 < nsplit; z0 += 4) {
+        float4 v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (z0 + q < nsplit) v[q] = __ldcg(ws + (z0 + q) * stride4 + i);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (z0 + q < nsplit) {
+                a.x += v[q].x;
+                a.y += v[q].y;
+                a.z += v[q].z;
+                a.w += v[q].w;
+            }
+    }
+    float4 d = dst[i];
+    d.x += a.x;
+    d.y += a.y;
+    d.z += a.z;
+    d.w += a.w;
+    dst[i] = d;
+}
+
+// up to SEQ_MAX slices: one thread per float4
+constexpr int SEQ_MAX = 64;
 __global__ void splitsum_kernel4(const float4 *__restrict__ ws, int nsplit, size_t stride4, size_t n4,
                                  float4 *__restrict__ dst) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
-        float4 v[MAXZ];
-#pragma unroll
-        for (int z = 0; z < MAXZ; ++z)
-            if (z < nsplit) v[z] = __ldcg(ws + z * stride4 + i);
-        float4 a = v[0];
-#pragma unroll
-        for (int z = 1; z < MAXZ; ++z)
-            if (z < nsplit) {
-                a.x += v[z].x;
-                a.y += v[z].y;
-                a.z += v[z].z;
-                a.w += v[z].w;
-            }
-        float4 d = dst[i];
-        d.x += a.x;
-        d.y += a.y;
-        d.z += a.z;
-        d.w += a.w;
-        dst[i] = d;
-    }
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+        seq_sum4(ws, nsplit, stride4, i, dst);
 }
 
 // many slices (the halo weight gradients split pixels 50-150 ways): block = 32 float4 columns
@@ -149,13 +156,14 @@ struct FItem {
     size_t stride, n;    // in float4 (F_SEQ4 / F_WIDE4) or float (F_SEQ1) units
     float *dst;
 };
-constexpr int MAXF = 40;
+constexpr int MAXF = 96;
 struct FBatch {
     int n;
     int start[MAXF + 1];
     FItem it[MAXF];
 };
 constexpr int FNT = 1024;
+static_assert(sizeof(FBatch) <= 32000, "kernel parameter space (32 KB)");
 
 __global__ void __launch_bounds__(FNT) flush_kernel(const __grid_constant__ FBatch b) {
     __shared__ float4 red4[32][33];
@@ -234,33 +242,10 @@ __global__ void __launch_bounds__(FNT) flush_kernel(const __grid_constant__ FBat
             o.w += t.w;
             *d = o;
         }
-    } else if (f.kind == F_SEQ4) {  // == splitsum_kernel4: slices added in z order, then dst +=
-        const float4 *ws = reinterpret_cast<const float4 *>(f.src);
+    } else if (f.kind == F_SEQ4) {  // == splitsum_kernel4
         const size_t j = (size_t)lb * FNT + threadIdx.x;
-        if (j < f.n) {
-            float4 a = __ldcg(ws + j);
-            for (int z0 = 1; z0 < f.nsplit; z0 += 4) {
-                float4 v[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (z0 + q < f.nsplit) v[q] = __ldcg(ws + (z0 + q) * f.stride + j);
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (z0 + q < f.nsplit) {
-                        a.x += v[q].x;
-                        a.y += v[q].y;
-                        a.z += v[q].z;
-                        a.w += v[q].w;
-                    }
-            }
-            float4 *d = reinterpret_cast<float4 *>(f.dst) + j;
-            float4 o = *d;
-            o.x += a.x;
-            o.y += a.y;
-            o.z += a.z;
-            o.w += a.w;
-            *d = o;
-        }
+        if (j < f.n)
+            seq_sum4(reinterpret_cast<const float4 *>(f.src), f.nsplit, f.stride, j, reinterpret_cast<float4 *>(f.dst));
     } else {  // F_SEQ1 == splitsum_kernel1
         const size_t j = (size_t)lb * FNT + threadIdx.x;
         if (j < f.n) {
@@ -356,7 +341,7 @@ int splitsum_finish(const float *ws, int nsplit, size_t stride, size_t n, float 
             f.n = n;
             f.blocks = (int)((n + FNT - 1) / FNT);
         } else {
-            f.kind = nsplit <= 16 ? F_SEQ4 : F_WIDE4;
+            f.kind = nsplit <= SEQ_MAX ? F_SEQ4 : F_WIDE4;
             f.stride = stride / 4;
             f.n = n / 4;
             f.blocks = (int)(f.kind == F_SEQ4 ? (f.n + FNT - 1) / FNT : (f.n + 31) / 32);
@@ -365,10 +350,8 @@ int splitsum_finish(const float *ws, int nsplit, size_t stride, size_t n, float 
     }
     if (!v4)
         splitsum_kernel1<<<grid(n), 256, 0, st>>>(ws, nsplit, stride, n, dst);
-    else if (nsplit <= 4)
-        splitsum_kernel4<4><<<grid(n / 4), 256, 0, st>>>(w4, nsplit, stride / 4, n / 4, d4);
-    else if (nsplit <= 16)
-        splitsum_kernel4<16><<<grid(n / 4), 256, 0, st>>>(w4, nsplit, stride / 4, n / 4, d4);
+    else if (nsplit <= SEQ_MAX)
+        splitsum_kernel4<<<grid(n / 4), 256, 0, st>>>(w4, nsplit, stride / 4, n / 4, d4);
     else
         splitsum_wide_kernel<<<(unsigned)((n / 4 + 31) / 32), 1024, 0, st>>>(w4, nsplit, stride / 4, n / 4, d4);
     count_launch();
