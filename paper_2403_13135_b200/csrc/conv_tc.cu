@@ -1445,9 +1445,14 @@ struct HWgrad {
 // HALVE variant (2x2 halving conv, model.py:79-88): dW[(a,b), c] accumulates, for each of
 // the 4 sub-pixel classes (cy, cx), x[p + ((cy+a)/2, (cx+b)/2)] (x) dY_cls[p]; the halo is
 // 2 rows x 65 pixels and the dY segment comes as 4 class planes.
+// KR: output rows per K-block.  The 3x3 variant takes two output rows (128 pixels) per K-block
+// from one 4-row halo slab: every x row is fetched twice instead of three times, and each
+// barrier wait feeds twice the MMAs (the 1-row form was L2-bound: 58 KB per K-block of 64
+// pixels at cin 128, ~17 TB/s of L2 reads at the MMA rate).
 template <bool HALVE>
 struct HWGeom {
-    static constexpr int ROWS = HALVE ? 2 : 3, COLS = HALVE ? 65 : 66;
+    static constexpr int KR = HALVE ? 1 : 2;
+    static constexpr int ROWS = HALVE ? 2 : 4, COLS = HALVE ? 65 : 66;
     static constexpr int TX = ROWS * COLS * 128;
     static constexpr int BYTES = (TX + 1023) / 1024 * 1024;
     static constexpr int TAPS = HALVE ? 4 : 9;
@@ -1456,7 +1461,7 @@ struct HWGeom {
 
 template <int COUT, int NCH, int STAGES, bool HALVE>
 constexpr int hw_stage_bytes() {
-    return NCH * HWGeom<HALVE>::BYTES + HWGeom<HALVE>::CLASSES * (COUT / 64) * 8192;
+    return NCH * HWGeom<HALVE>::BYTES + HWGeom<HALVE>::CLASSES * (COUT / 64) * 8192 * HWGeom<HALVE>::KR;
 }
 template <int COUT, int NCH, int STAGES, bool HALVE>
 constexpr int hw_smem_bytes() {
@@ -1476,7 +1481,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int STAGE = hw_stage_bytes<COUT, NCH, STAGES, HALVE>();
-    constexpr int DY_BYTES = (COUT / 64) * 8192;
+    constexpr int DY_BYTES = (COUT / 64) * 8192 * G::KR;  // [cout block][KR rows][64 px][64 ch]
     constexpr int TX = NCH * G::TX + G::CLASSES * DY_BYTES;
     constexpr int NBLK = G::TAPS * NCH;  // M blocks: (tap, chunk), tap-major
     constexpr int TCOLS = 512;
@@ -1519,7 +1524,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                     tc::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     tc::mbar_expect_tx(&full[s], TX);
                     const int seg = kb & (segs - 1), row = kb >> lg2(segs);  // W, H powers of two
-                    const int h = row & (p.H - 1), n = row >> lg2(p.H), w0 = seg * 64;
+                    const int hk = p.H / G::KR;  // K-block rows per image
+                    const int h = (row & (hk - 1)) * G::KR, n = row >> lg2(hk), w0 = seg * 64;
                     uint8_t *st = base + s * STAGE;
 #pragma unroll
                     for (int c = 0; c < NCH; ++c)
@@ -1562,12 +1568,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                             const bool sw = a1 < a0;
                             const uint32_t lo = sw ? a1 : a0, dl = sw ? a0 - a1 : a1 - a0;
                             const uint32_t d = tmem + (mt - mt0) * COUT;
-                            const uint64_t ad = tc::sw128_desc(lo, dl, 1024);
-                            const uint64_t bd = tc::sw128_desc(bbase, 8192, 1024);
 #pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                tc::umma_f16(d, ad + 128 * k, bd + 128 * k, idesc,
-                                             (kb > kb0 || cls > 0 || k > 0) ? 1u : 0u);
+                            for (int orow = 0; orow < G::KR; ++orow) {  // output row orow: halo rows + orow
+                                const uint64_t ad = tc::sw128_desc(lo + orow * G::COLS * 128, dl, 1024);
+                                const uint64_t bd = tc::sw128_desc(bbase + orow * 8192, 8192 * G::KR, 1024);
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    tc::umma_f16(d, ad + 128 * k, bd + 128 * k, idesc,
+                                                 (kb > kb0 || cls > 0 || orow > 0 || k > 0) ? 1u : 0u);
+                            }
                         }
                     }
                     tc::umma_commit(&empty[s]);
@@ -2083,15 +2092,17 @@ int try_hwgrad(const uint16_t *x1, int c1, const uint16_t *x2, int c2, const uin
     HWgrad p;
     memset(&p, 0, sizeof p);
     p.N = n; p.H = h; p.W = w; p.ct = c1 + c2; p.cout = cout; p.nchx = nch; p.dw = dw;
-    p.total_kb = n * h * (w / 64);
+    const int kr = halve ? 1 : 2;  // output rows per K-block (HWGeom::KR)
+    if (h % kr) return 1;
+    p.total_kb = n * (h / kr) * (w / 64);
     for (int c = 0; c < nch; ++c) {
         const int cc = c * 64;
-        const int cols = halve ? 65 : 66, rows = halve ? 2 : 3;
+        const int cols = halve ? 65 : 66, rows = halve ? 2 : 4;
         const bool ok = cc < c1 ? map_halo_box(&p.xm[c], x1, n, h, w, c1, cc, cols, rows)
                                 : map_halo_box(&p.xm[c], x2, n, h, w, c2, cc - c1, cols, rows);
         if (!ok) return ICE_EINVAL;
     }
-    PixTile seg{64, 1, 1, w / 64, h, (halve ? 4 : 1) * n};
+    PixTile seg{64, kr, 1, w / 64, h / kr, (halve ? 4 : 1) * n};
     if (!map_act_nb(&p.dym, dy, (halve ? 4 : 1) * n, h, w, cout, seg, cout / 64)) return ICE_EINVAL;
     // work split: M tile groups (G x cout <= 512 TMEM columns) x pixel splits
     p.total_mt = ((halve ? 4 : 9) * nch + 1) / 2;
@@ -2107,10 +2118,10 @@ int try_hwgrad(const uint16_t *x1, int c1, const uint16_t *x2, int c2, const uin
     const int grid = persist_grid(units);
     int rc;
     if (halve) rc = nch == 1 ? launch_hwgrad<64, 1, 3, true>(p, grid, st) : launch_hwgrad<64, 2, 3, true>(p, grid, st);
-    else if (cout == 64 && nch == 1) rc = launch_hwgrad<64, 1, 6, false>(p, grid, st);
-    else if (cout == 64) rc = launch_hwgrad<64, 2, 3, false>(p, grid, st);
-    else if (nch == 1) rc = launch_hwgrad<128, 1, 5, false>(p, grid, st);
-    else rc = launch_hwgrad<128, 2, 3, false>(p, grid, st);
+    else if (cout == 64 && nch == 1) rc = launch_hwgrad<64, 1, 4, false>(p, grid, st);
+    else if (cout == 64) rc = launch_hwgrad<64, 2, 2, false>(p, grid, st);
+    else if (nch == 1) rc = launch_hwgrad<128, 1, 3, false>(p, grid, st);
+    else rc = launch_hwgrad<128, 2, 2, false>(p, grid, st);
     if (rc || splits == 1) return rc;
     return ice::splitsum_finish(p.ws, splits - 1, p.wsize, p.wsize, dw, st);
 }

@@ -23,7 +23,7 @@ cap adam "adam_kernel" 2
 cap wgrad_m2 "conv_gemm_m2<.int.256, .int.3, .*WgradProb" 40
 cap halo_fp64 "halo_gemm<.int.64, .int.1, .bool.1, .*FpropProb" 2
 cap halo_dg64 "halo_gemm<.int.64, .int.1, .bool.1, .*DgradProb" 2
-cap hwgrad64 "hwgrad_kernel<.int.64, .int.2, .int.3, .bool.0" 2
+cap hwgrad64 "hwgrad_kernel<.int.64, .int.2, .int.2, .bool.0" 2
 cap fprop256 "conv_gemm<.int.256, .int.4, .*FpropProb" 20
 [ -z "$ONLY" ] && timeout 600 $F -k "regex:autolabel256" -s 1 -c 1 -o gpurun_out/r02f_autolabel256 -f python tools/profile_autolabel.py --reps 1 > gpurun_out/r02f_al.log 2>&1
 ls -la gpurun_out/*.ncu-rep
