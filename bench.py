@@ -19,6 +19,7 @@ Under torchrun each rank drives one GPU (NCCL); rank 0 prints.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import subprocess
@@ -113,7 +114,7 @@ def _scene512_chunk(args):
 
 def config5_bench(dev, dist, world, rank, steps: int = 10, warmup: int = 3, count: int = 64):
     """BASELINE config 5 geometry on this job's GPUs: the paper U-Net on 512 x 512 tiles
-    (generate_corpus(101, 64, 0.3, size=512) with the generator's truth labels), batch 16 per
+    (generate_corpus(101, 64, 0.3, size=512) labelled by K1 at 512^2), batch 16 per
     GPU, device-timed like the headline.  Returns a dict for the JSON line."""
     import multiprocessing as mp
     from paper_2403_13135_b200.icetrain import Adam, UNet, UNetSpec
@@ -122,7 +123,18 @@ def config5_bench(dev, dist, world, rank, steps: int = 10, warmup: int = 3, coun
     with mp.get_context("fork").Pool(8) as pool:
         parts = pool.map(_scene512_chunk, [(101, count, 0.3, int(bounds[i]), int(bounds[i + 1])) for i in range(8)])
     x_all = torch.from_numpy(np.concatenate([p[0] for p in parts])).to(dev)
-    y_all = torch.from_numpy(np.concatenate([p[1] for p in parts])).to(dev)
+    # labels by K1 at 512^2 (the multi-CTA region path, ice_autolabel_scene), timed on its own
+    from paper_2403_13135_b200 import icelabel as il
+    lab = il.autolabel(x_all)
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(5):
+        il.autolabel(x_all, out=lab)
+    a1.record()
+    torch.cuda.synchronize()
+    al_ms = a0.elapsed_time(a1) / 5
+    y_all = lab["label"].clone()
     batch = 16
     torch.manual_seed(0)
     model = UNet(UNetSpec(input_size=512), dev)
@@ -162,7 +174,10 @@ def config5_bench(dev, dist, world, rank, steps: int = 10, warmup: int = 3, coun
             "value": round(value, 2), "unit": UNIT, "ms_per_step": round(ms / steps, 3), "steps": steps,
             "warmup": warmup, "n_gpus": world, "global_batch": union,
             "tflops": round(1622.4e9 * union / (ms / steps / 1000.0) / 1e12, 1),
-            "data": "synthetic generate_corpus(101, 64, 0.3, size=512) tiles, generator truth labels"}
+            "data": "synthetic generate_corpus(101, 64, 0.3, size=512) tiles, labels by K1 on GPU (512^2 region path)",
+            "autolabel_512": {"value": round(count * 512 * 512 / (al_ms / 1000.0) / 1e6, 1), "unit": "Mpixel/s",
+                              "ms": round(al_ms, 3), "tiles": count,
+                              "path": "ice_autolabel_scene region path (3 x 3 cores of <= 230^2 + halo per tile)"}}
 
 
 def config0_bench():
@@ -546,6 +561,19 @@ def main():
                 al_traffic = tj["ice_autolabel_bytes_per_tile"] * n_tiles
         except Exception:
             pass
+        al_compute = None  # K1's integer-pipe utilisation, from the committed ncu full capture
+        try:
+            for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "r0*_ncu_full_summary.json")), reverse=True):
+                hit = [k for k in json.load(open(fn)) if "autolabel256" in k.get("kernel", "")]
+                if hit:
+                    k = hit[0]
+                    num = lambda v: float(str(v).split()[0])  # noqa: E731
+                    al_compute = {"bound": "int-alu", "alu_pipe_pct": num(k["alu_pipe_pct"]),
+                                  "fma_pipe_pct": num(k.get("fma_pipe_pct", 0)), "dram_pct": num(k["dram_pct"]),
+                                  "source": os.path.relpath(fn, ROOT) + " (ncu --set full, one K1 launch, T-gray)"}
+                    break
+        except Exception:
+            pass
         variants = {}
         for name, make in (("t_tint", lambda: tint_corpus(corpus)), ("t_rand", lambda: rand_corpus(len(corpus)))):
             vdev = torch.from_numpy(make()).to(dev)
@@ -564,7 +592,8 @@ def main():
                      "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
                                   "frac": round(gbs / hbm, 4), "traffic": al_traffic,
                                   "note": "7 B/px algorithmic (RGB in, filtered + label out); "
-                                          "the 21x21 medians make K1 integer-ALU-bound (SWAR kernel)"},
+                                          "the 21x21 medians make K1 integer-ALU-bound (SWAR kernel)",
+                                  "compute": al_compute},
                      "segment_only": {"metric": "label-only (K1s, icelabel label) Mpixel/s",
                                       "value": round(px / (seg_ms / 1000.0) / 1e6, 1), "unit": "Mpixel/s",
                                       "ms": round(seg_ms, 3),
