@@ -242,10 +242,35 @@ __global__ void __launch_bounds__(FNT) flush_kernel(const __grid_constant__ FBat
             o.w += t.w;
             *d = o;
         }
-    } else if (f.kind == F_SEQ4) {  // == splitsum_kernel4
-        const size_t j = (size_t)lb * FNT + threadIdx.x;
-        if (j < f.n)
-            seq_sum4(reinterpret_cast<const float4 *>(f.src), f.nsplit, f.stride, j, reinterpret_cast<float4 *>(f.dst));
+    } else if (f.kind == F_SEQ4) {  // == splitsum_kernel4, two float4 columns per thread (loads of both in flight)
+        const size_t j0 = (size_t)lb * 2 * FNT + threadIdx.x, j1 = j0 + FNT;
+        const float4 *ws = reinterpret_cast<const float4 *>(f.src);
+        float4 *dst = reinterpret_cast<float4 *>(f.dst);
+        if (j1 < f.n) {
+            float4 a = __ldcg(ws + j0), b = __ldcg(ws + j1);
+            for (int z0 = 1; z0 < f.nsplit; z0 += 4) {
+                float4 va[4], vb[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (z0 + q < f.nsplit) {
+                        va[q] = __ldcg(ws + (z0 + q) * f.stride + j0);
+                        vb[q] = __ldcg(ws + (z0 + q) * f.stride + j1);
+                    }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (z0 + q < f.nsplit) {
+                        a.x += va[q].x; a.y += va[q].y; a.z += va[q].z; a.w += va[q].w;
+                        b.x += vb[q].x; b.y += vb[q].y; b.z += vb[q].z; b.w += vb[q].w;
+                    }
+            }
+            float4 d = dst[j0], e = dst[j1];
+            d.x += a.x; d.y += a.y; d.z += a.z; d.w += a.w;
+            e.x += b.x; e.y += b.y; e.z += b.z; e.w += b.w;
+            dst[j0] = d;
+            dst[j1] = e;
+        } else if (j0 < f.n) {
+            seq_sum4(ws, f.nsplit, f.stride, j0, dst);
+        }
     } else {  // F_SEQ1 == splitsum_kernel1
         const size_t j = (size_t)lb * FNT + threadIdx.x;
         if (j < f.n) {
@@ -344,7 +369,7 @@ int splitsum_finish(const float *ws, int nsplit, size_t stride, size_t n, float 
             f.kind = nsplit <= SEQ_MAX ? F_SEQ4 : F_WIDE4;
             f.stride = stride / 4;
             f.n = n / 4;
-            f.blocks = (int)(f.kind == F_SEQ4 ? (f.n + FNT - 1) / FNT : (f.n + 31) / 32);
+            f.blocks = (int)(f.kind == F_SEQ4 ? (f.n + 2 * FNT - 1) / (2 * FNT) : (f.n + 31) / 32);
         }
         return push_or_launch(f);
     }
