@@ -19,7 +19,6 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
-#include <cstdio>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -137,16 +136,16 @@ struct FpropProb {
         if (c2) tc::tma_prefetch_desc(&xb);
         tc::tma_prefetch_desc(&wm);
     }
-    template <int BN, bool PAIR = false>
+    template <int BN>
     __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int z) const {
         const Taps &tp = taps[z];
         const int cch = (c1 + c2) / BK;
         const int t = kb / cch, c = (kb % cch) * BK;
         int n0, h0, w0;
         pt.origin(mt, n0, h0, w0);
-        if (c < c1) tc::tma_load_4d<PAIR>(sa, &xa, bar, c, w0 + tp.dx[t], h0 + tp.dy[t], n0);
-        else tc::tma_load_4d<PAIR>(sa, &xb, bar, c - c1, w0 + tp.dx[t], h0 + tp.dy[t], n0);
-        tc::tma_load_3d<PAIR>(sb, &wm, bar, c, tp.wt[t], nt * BN);
+        if (c < c1) tc::tma_load_4d(sa, &xa, bar, c, w0 + tp.dx[t], h0 + tp.dy[t], n0);
+        else tc::tma_load_4d(sa, &xb, bar, c - c1, w0 + tp.dx[t], h0 + tp.dy[t], n0);
+        tc::tma_load_3d(sb, &wm, bar, c, tp.wt[t], nt * BN);
     }
     // 256-row tile mt = pixel tiles 2 mt and 2 mt + 1 over one 256-column weight block
     template <int BN>
@@ -559,7 +558,6 @@ struct WgradProb {
     float *dw;  // [cout][taps][c1+c2]
     float *ws;  // partials of splits 1.. [splits - 1][cout][taps][c1+c2] (scratch) when splits > 1
     size_t wsize;
-    int pair;   // host: run on CTA pairs (conv_gemm_2sm, loads through load<BN, true>)
 
     __device__ void kb_range(int z, int &kb0, int &nkb) const {
         kb0 = z * kb_per_split;
@@ -571,7 +569,6 @@ struct WgradProb {
         if (c2) tc::tma_prefetch_desc(&xb);
     }
     // one 64-channel x 64-pixel box of x for the 64-wide (tap, cin) block starting at col
-    template <bool PAIR = false>
     __device__ __forceinline__ void load_x(uint8_t *dst, uint64_t *bar, int col, int cls, int n0, int h0,
                                            int w0) const {
         const int ct = c1 + c2;
@@ -583,30 +580,29 @@ struct WgradProb {
             sx = ((cls & 1) + (t & 1)) >> 1;
         }
         if (nbx == 1) {
-            if (c < c1) tc::tma_load_4d<PAIR>(dst, &xa, bar, c, w0 + sx, h0 + sy, n0);
-            else tc::tma_load_4d<PAIR>(dst, &xb, bar, c - c1, w0 + sx, h0 + sy, n0);
+            if (c < c1) tc::tma_load_4d(dst, &xa, bar, c, w0 + sx, h0 + sy, n0);
+            else tc::tma_load_4d(dst, &xb, bar, c - c1, w0 + sx, h0 + sy, n0);
         } else {
-            if (c < c1) tc::tma_load_5d<PAIR>(dst, &xa, bar, 0, w0 + sx, h0 + sy, n0, c >> 6);
-            else tc::tma_load_5d<PAIR>(dst, &xb, bar, 0, w0 + sx, h0 + sy, n0, (c - c1) >> 6);
+            if (c < c1) tc::tma_load_5d(dst, &xa, bar, 0, w0 + sx, h0 + sy, n0, c >> 6);
+            else tc::tma_load_5d(dst, &xb, bar, 0, w0 + sx, h0 + sy, n0, (c - c1) >> 6);
         }
     }
-    template <bool PAIR = false>
     __device__ __forceinline__ void load_dy(uint8_t *dst, uint64_t *bar, int c0, int cls, int n0, int h0,
                                             int w0) const {
         const int img = halve ? cls * N + n0 : n0;  // sub-pixel planes [4][N] flatten to 4N images
-        if (nby == 1) tc::tma_load_4d<PAIR>(dst, &dym, bar, c0, w0, h0, img);
-        else tc::tma_load_5d<PAIR>(dst, &dym, bar, 0, w0, h0, img, c0 >> 6);
+        if (nby == 1) tc::tma_load_4d(dst, &dym, bar, c0, w0, h0, img);
+        else tc::tma_load_5d(dst, &dym, bar, 0, w0, h0, img, c0 >> 6);
     }
-    template <int BN, bool PAIR = false>
+    template <int BN>
     __device__ void load(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
-        load_rows<BN, 2, PAIR>(kb, sa, sb, bar, mt * BM, nt);
+        load_rows<BN, 2>(kb, sa, sb, bar, mt * BM, nt);
     }
     template <int BN>
     __device__ void load_m2(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int mt, int nt, int) const {
         load_rows<BN, 4>(kb, sa, sb, bar, mt * 2 * BM, nt);
     }
     // MB 64-row blocks of the M operand starting at row m0 (MB = 4: the 256-row tiles of conv_gemm_m2)
-    template <int BN, int MB, bool PAIR = false>
+    template <int BN, int MB>
     __device__ void load_rows(int kb, uint8_t *sa, uint8_t *sb, uint64_t *bar, int m0, int nt) const {
         int n0, h0, w0, cls = 0;
         if (halve) {
@@ -618,11 +614,11 @@ struct WgradProb {
         // one TMA box carries nb consecutive 64-channel blocks ([block][pixel][64 ch] in smem)
         const int bx = nbx, by = nby;
         if (!trans) {
-            for (int j = 0; j < MB; j += by) load_dy<PAIR>(sa + j * 8192, bar, m0 + j * 64, cls, n0, h0, w0);
-            for (int j = 0; j < BN / 64; j += bx) load_x<PAIR>(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
+            for (int j = 0; j < MB; j += by) load_dy(sa + j * 8192, bar, m0 + j * 64, cls, n0, h0, w0);
+            for (int j = 0; j < BN / 64; j += bx) load_x(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
         } else {
-            for (int j = 0; j < MB; j += bx) load_x<PAIR>(sa + j * 8192, bar, m0 + j * 64, cls, n0, h0, w0);
-            for (int j = 0; j < BN / 64; j += by) load_dy<PAIR>(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
+            for (int j = 0; j < MB; j += bx) load_x(sa + j * 8192, bar, m0 + j * 64, cls, n0, h0, w0);
+            for (int j = 0; j < BN / 64; j += by) load_dy(sb + j * 8192, bar, nt * BN + j * 64, cls, n0, h0, w0);
         }
     }
     struct Pre {};
@@ -1800,7 +1796,6 @@ const int8_t HALVE_DX[9] = {0, 0, 1, 0, 0, 0, 1, 0, 1};
 struct Knobs {
     bool no_dual, no_stage, no_splitk, no_wgrad_trans256, no_ref_tma, no_halo_wgrad, no_halve_merge;
     int conv_m2, wg_m2;  // -1 = automatic, 0 / 1 forced
-    int pair2sm;         // 256 x 256 tiles on CTA pairs (conv_gemm_2sm) instead of conv_gemm_m2
 };
 const Knobs &knobs() {
     static const Knobs k = [] {
@@ -1819,7 +1814,6 @@ const Knobs &knobs() {
         r.no_halve_merge = flag("ICE_NO_HALVE_MERGE");
         r.conv_m2 = tri("ICE_CONV_M2");
         r.wg_m2 = tri("ICE_WG_M2");
-        r.pair2sm = tri("ICE_2SM") == 1 ? 1 : 0;
         return r;
     }();
     return k;
@@ -1887,173 +1881,6 @@ int run_halo(const P &p, const HaloPlan &h, int ncols, cudaStream_t st) {
 }
 
 bool use_halo(int ksize, int w) { return ksize == 3 && w >= 128 && w % 128 == 0; }
-
-// 256 x 256 tiles on a CTA PAIR (cta_group::2): each CTA of the cluster holds one 128-row M
-// half of A and one 128-column half of B; the leader's single thread issues
-// tcgen05.mma.cta_group::2 (M = 256, N = 256), which reads both CTAs' shared memory, and each
-// CTA's TMEM receives its 128 rows x 256 columns.  Against conv_gemm_m2 (both halves on one
-// SM) every SM moves half the operand bytes per MAC through TMA, L2 and the tensor-core
-// shared-memory reads (the 256-row wgrad measured 65% of the MMA peak there: 160 KB of smem
-// traffic per 1024 MMA cycles per K-block), and each CTA's accumulator takes only 256 TMEM
-// columns, so two of them double-buffer and the epilogue overlaps the next tile again.
-// Loads: both CTAs' TMA complete_tx on the leader's full barrier (cta_group::2 form); the
-// leader's MMA commits multicast to both CTAs' empty / tmem-full barriers; both CTAs'
-// epilogue warps arrive on the leader's tmem-empty barrier.
-template <int STAGES>
-constexpr int sm2_smem_bytes() {
-    return 1024 + STAGES * (A_BYTES + 128 * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16 +
-           BIAS_SLOTS * 256 * 4;
-}
-
-template <int STAGES, class P>
-__global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_2sm(const __grid_constant__ P p, const TileGrid g) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    constexpr int BN = 256, BH = 128, B_BYTES = BH * BK * 2;
-    uint8_t *sa = base;
-    uint8_t *sb = base + STAGES * A_BYTES;
-    uint8_t *sst = sb + STAGES * B_BYTES;
-    uint64_t *full = reinterpret_cast<uint64_t *>(sst + EPI_WARPS * STAGE_BYTES);
-    uint64_t *empty = full + STAGES;
-    uint64_t *tfull = empty + STAGES;  // [2]
-    uint64_t *tempty = tfull + 2;      // [2] (the leader's count both CTAs' epilogue warps)
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
-    float *sbias = reinterpret_cast<float *>(tslot + 4);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = tc::cluster_ctarank();
-    const int pair0 = (int)(blockIdx.x >> 1), npairs = (int)(gridDim.x >> 1);
-    const int ntiles = g.count();
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&empty[s], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            tc::mbar_init(&tfull[a], 1);
-            tc::mbar_init(&tempty[a], 2 * EPI_WARPS);
-        }
-        tc::fence_barrier_init();
-    }
-    if (warp == 0 && lane == 0) p.prefetch();
-    if (warp == 1) tc::tmem_alloc_cg2<2 * BN>(tslot);
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::cluster_sync();  // both CTAs' barriers initialised before any cross-CTA arrive / TMA
-    tc::tc_fence_after();
-    const uint32_t tmem = *tslot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            int it = 0;
-            for (int t = pair0; t < ntiles; t += npairs) {
-                int mt, nt, z, kb0, nkb;
-                g.coords(t, mt, nt, z);
-                p.kb_range(z, kb0, nkb);
-                for (int i = 0; i < nkb; ++i, ++it) {
-                    const int s = it % STAGES;
-                    tc::mbar_wait_cl(&empty[s], ((it / STAGES) & 1) ^ 1);  // released by the leader's MMA commit
-                    if (rank == 0) tc::mbar_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
-                    p.template load<BH, true>(kb0 + i, sa + s * A_BYTES, sb + s * B_BYTES, &full[s], 2 * mt + (int)rank,
-                                              2 * nt + (int)rank, z);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
-            constexpr uint32_t idesc = tc::idesc_bf16(2 * BM, BN, P::A_MN, P::B_MN);
-            int it = 0, local = 0;
-            for (int t = pair0; t < ntiles; t += npairs, ++local) {
-                int mt, nt, z, kb0, nkb;
-                g.coords(t, mt, nt, z);
-                p.kb_range(z, kb0, nkb);
-                const int acc = local & 1;
-                tc::mbar_wait_cl(&tempty[acc], ((local >> 1) & 1) ^ 1);  // both CTAs drained it
-                tc::tc_fence_after();
-                const uint32_t d = tmem + acc * BN;
-                for (int i = 0; i < nkb; ++i, ++it) {
-                    const int s = it % STAGES;
-                    tc::mbar_wait_cl(&full[s], (it / STAGES) & 1);  // both CTAs' bytes landed
-                    tc::tc_fence_after();
-                    const uint64_t ad = tc::sw128_desc(tc::smem_u32(sa + s * A_BYTES), P::A_MN ? 8192 : 16, 1024);
-                    const uint64_t bd = tc::sw128_desc(tc::smem_u32(sb + s * B_BYTES), P::B_MN ? 8192 : 16, 1024);
-#pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)
-                        tc::umma_f16_cg2(d, ad + (P::A_MN ? 128 : 2) * k, bd + (P::B_MN ? 128 : 2) * k, idesc,
-                                         (i | k) != 0 ? 1u : 0u);
-                    tc::umma_commit_pair(&empty[s]);
-                }
-                tc::umma_commit_pair(&tfull[acc]);
-            }
-        }
-        __syncwarp();
-    } else {
-        const int sub = warp & 3, half = (warp - 2) >> 2;  // TMEM lane quarter, column half
-        constexpr int NCH = BN / 32, PER = NCH / 2;
-        const int cc0 = half * PER, cc1 = cc0 + PER;
-        const int row = sub * 32 + lane;
-        float bacc[4] = {0.f, 0.f, 0.f, 0.f};
-        int local = 0;
-        const uint32_t tempty_leader = tc::mapa(tc::smem_u32(&tempty[0]), 0);
-        for (int t = pair0; t < ntiles; t += npairs, ++local) {
-            int mt, nt, z;
-            g.coords(t, mt, nt, z);
-            const int mh = 2 * mt + (int)rank;  // this CTA's 128-row M tile
-            typename P::Pre pre;
-            p.template pre_load<BN>(pre, row, mh, nt, z, cc0, cc1);
-            const int acc = local & 1;
-            tc::mbar_wait_cl(&tfull[acc], (local >> 1) & 1);
-            tc::tc_fence_after();
-            p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), row, mh, nt, z, cc0, cc1, bacc, pre,
-                                    sst + (warp - 2) * STAGE_BYTES);
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive_cluster(tempty_leader + acc * 8);
-        }
-        if (lane == 0) tc::bulk_wait<0>();  // staged stores complete before the CTA ends
-    }
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::cluster_sync();  // the peer no longer uses the pair's TMEM / barriers
-    if (warp == 1) tc::tmem_dealloc_cg2<2 * BN>(tmem);
-    (void)sbias;
-}
-
-template <int STAGES, class P>
-int launch_2sm(const P &p, dim3 tiles, cudaStream_t st) {
-    constexpr int smem = sm2_smem_bytes<STAGES>();
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(conv_gemm_2sm<STAGES, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return (int)e;
-        attr = true;
-    }
-    const TileGrid g = tile_grid(tiles);
-    const long long total = (long long)tiles.x * tiles.y * tiles.z;
-    const long long pairs = total < num_sms() / 2 ? total : num_sms() / 2;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * pairs));
-    cfg.blockDim = dim3(NTHREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    static const bool dbg = getenv("ICE_2SM_DEBUG") != nullptr;
-    if (dbg) {
-        int ncl = -1;
-        const cudaError_t qe = cudaOccupancyMaxActiveClusters(&ncl, conv_gemm_2sm<STAGES, P>, &cfg);
-        fprintf(stderr, "2sm: stages %d smem %d grid %u max active clusters %d (%s)\n", STAGES, smem,
-                cfg.gridDim.x, ncl, cudaGetErrorString(qe));
-    }
-    cudaError_t e = cudaLaunchKernelEx(&cfg, conv_gemm_2sm<STAGES, P>, p, g);
-    ice::count_launch();
-    return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
-}
 
 template <int BN, int STAGES, class P>
 int launch(const P &p, dim3 tiles, cudaStream_t st) {
@@ -2204,8 +2031,8 @@ bool wgrad_m2(int mtiles, int bn, int total_kb) {
 // beyond the first writes a partial slice of the weight gradient (fixed-order reduction,
 // reduce.cuh), so the GEMM path caps the units at one round: its layers' weights are MBs and
 // 80-split slices cost GBs of traffic; the halo path's weights are 0.15-0.6 MB.
-int split_k(int total_kb, long long tiles, long long max_units = 8LL * 148, long long slots = 0) {
-    const long long sms = slots > 0 ? slots : num_sms();  // concurrent units (CTA pairs: SMs / 2)
+int split_k(int total_kb, long long tiles, long long max_units = 8LL * 148) {
+    const long long sms = num_sms();
     int best = 1;
     double best_eff = -1.0;
     for (int s = 1; s <= total_kb; ++s) {
@@ -2308,7 +2135,7 @@ int run_wgrad(WgradProb &p, int ncols, int mtiles, int ntiles, int bn, bool m2, 
     p.ws = splits > 1 ? ar.take<float>((size_t)(splits - 1) * p.wsize * 4) : nullptr;
     ICE_SETTLE(ar);
     dim3 grid((unsigned)mtiles, (unsigned)ntiles, (unsigned)splits);
-    const int rc = p.pair ? launch_2sm<5>(p, grid, st) : m2 ? launch_m2<256, 3>(p, grid, st) : launch_bn(p, bn, grid, st);
+    const int rc = m2 ? launch_m2<256, 3>(p, grid, st) : launch_bn(p, bn, grid, st);
     if (rc || splits == 1) return rc;
     return ice::splitsum_finish(p.ws, splits - 1, p.wsize, p.wsize, p.dw, st);
 }
@@ -2425,14 +2252,8 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
         return (int)cudaGetLastError();
     }
     ICE_SETTLE(ar);
-    if (conv_m2(mtiles, cout, bn, splits, total_kb)) {
-        if (bn == 256 && knobs().pair2sm) {  // CTA pairs: each loads 128 pixel rows + 128 weight rows
-            if (!map_wgt(&p.wm, wgt, cout, p.taps[0].n, c1 + c2, 128)) return ICE_EINVAL;
-            return getenv("ICE_2SM_S3") ? launch_2sm<3>(p, dim3((unsigned)(mtiles / 2), cout / bn, 1), st)
-                                        : launch_2sm<5>(p, dim3((unsigned)(mtiles / 2), cout / bn, 1), st);
-        }
+    if (conv_m2(mtiles, cout, bn, splits, total_kb))
         return launch_bn_m2(p, bn, dim3((unsigned)(mtiles / 2), cout / bn, 1), st);
-    }
     return launch_bn(p, bn, dim3((unsigned)mtiles, cout / bn, 1), st);
 }
 
@@ -2555,11 +2376,8 @@ extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2
     p.total_kb = p.pk.tw * p.pk.th * p.pk.tn;
     const bool m2 = wgrad_m2(mtiles, bn, p.total_kb);
     if (m2) mtiles /= 2;
-    p.pair = m2 && knobs().pair2sm;  // each CTA of a pair loads 128 rows + 128 columns
-    p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles, p.pair ? num_sms() / 2 : num_sms(),
-                             p.pair ? num_sms() / 2 : 0);
-    if (p.pair) wgrad_boxes(p, false, 128);
-    else wgrad_boxes(p, m2, bn);
+    p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles, num_sms());
+    wgrad_boxes(p, m2, bn);
     if (!map_act_nb(&p.dym, dy, n, h, w, cout, p.pk, p.nby)) return ICE_EINVAL;
     if (!map_act_nb(&p.xa, x1, n, h, w, c1, p.pk, p.nbx)) return ICE_EINVAL;
     if (c2 && !map_act_nb(&p.xb, x2, n, h, w, c2, p.pk, p.nbx)) return ICE_EINVAL;
@@ -2691,11 +2509,8 @@ extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_
     p.total_kb = 4 * p.pk.tw * p.pk.th * p.pk.tn;
     const bool m2 = wgrad_m2(mtiles, bn, p.total_kb);
     if (m2) mtiles /= 2;
-    p.pair = m2 && knobs().pair2sm;  // each CTA of a pair loads 128 rows + 128 columns
-    p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles, p.pair ? num_sms() / 2 : num_sms(),
-                             p.pair ? num_sms() / 2 : 0);
-    if (p.pair) wgrad_boxes(p, false, 128);
-    else wgrad_boxes(p, m2, bn);
+    p.kb_per_split = split_k(p.total_kb, (long long)mtiles * ntiles, num_sms());
+    wgrad_boxes(p, m2, bn);
     if (!map_act_nb(&p.dym, dy_planes, 4 * n, h, w, cout, p.pk, p.nby)) return ICE_EINVAL;
     if (!map_act_nb(&p.xa, x, n, h, w, c, p.pk, p.nbx)) return ICE_EINVAL;
     return run_wgrad(p, ncols, mtiles, ntiles, bn, m2, ar, scratch_bytes, st);
