@@ -1016,6 +1016,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
 // with 128 output columns): 256 x 128 tiles move 48 KB per K-block for 256 x 128 x 64 MACs
 // (a 128 x 128 tile: 32 KB for half of that) and two accumulator pairs fit TMEM, so the
 // epilogue overlaps the next tile as in conv_gemm.
+#ifdef ICE_CONV_PROF
+// MMA-thread cycle accounting of conv_gemm_m2 (debug build): [0] waiting for the epilogue
+// (tmem empty), [1] waiting for TMA (full), [2] issuing, [3] tiles, [4] K-blocks
+__device__ unsigned long long g_conv_prof[8];
+#endif
 template <int BN, int STAGES>
 constexpr int m2_smem_bytes() {
     return 1024 + STAGES * (2 * A_BYTES + BN * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16 +
@@ -1082,13 +1087,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
                 g.coords(t, mt, nt, z);
                 p.kb_range(z, kb0, nkb);
                 const int acc = local % NACC;
+#ifdef ICE_CONV_PROF
+                long long q0 = clock64();
+#endif
                 tc::mbar_wait(&tempty[acc], ((local / NACC) & 1) ^ 1);
                 tc::tc_fence_after();
+#ifdef ICE_CONV_PROF
+                long long q1 = clock64();
+                atomicAdd(&g_conv_prof[0], (unsigned long long)(q1 - q0));
+                atomicAdd(&g_conv_prof[3], 1ull);
+#endif
                 const uint32_t d = tmem + acc * 2 * BN;
                 for (int i = 0; i < nkb; ++i, ++it) {
                     const int s = it % STAGES;
+#ifdef ICE_CONV_PROF
+                    const long long w0 = clock64();
+#endif
                     tc::mbar_wait(&full[s], (it / STAGES) & 1);
                     tc::tc_fence_after();
+#ifdef ICE_CONV_PROF
+                    const long long w1 = clock64();
+                    atomicAdd(&g_conv_prof[1], (unsigned long long)(w1 - w0));
+                    atomicAdd(&g_conv_prof[4], 1ull);
+#endif
                     const uint64_t a0 = tc::sw128_desc(tc::smem_u32(sa + s * AB), P::A_MN ? 8192 : 16, 1024);
                     const uint64_t a1 = tc::sw128_desc(tc::smem_u32(sa + s * AB + A_BYTES), P::A_MN ? 8192 : 16, 1024);
                     const uint64_t b0 = tc::sw128_desc(tc::smem_u32(sb + s * B_BYTES), P::B_MN ? 8192 : 16, 1024);
@@ -2515,3 +2536,14 @@ extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_
     if (!map_act_nb(&p.xa, x, n, h, w, c, p.pk, p.nbx)) return ICE_EINVAL;
     return run_wgrad(p, ncols, mtiles, ntiles, bn, m2, ar, scratch_bytes, st);
 }
+
+#ifdef ICE_CONV_PROF
+extern "C" int ice_conv_prof_read(unsigned long long *out8, int reset) {
+    cudaMemcpyFromSymbol(out8, g_conv_prof, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_conv_prof, z, sizeof z);
+    }
+    return 0;
+}
+#endif

@@ -186,26 +186,28 @@ def test_checkpoint_layout_is_the_reference_layout(tmp_path):
 
 def test_loss_after_200_steps_desk_config():
     """north_star: "loss after 200 steps on the same seed and batch order must agree within 2%",
-    at SURVEY.md 8(d).4's parity config -- UNetSpec(256, base_channels=16, dropout=0.0), batch 8,
+    at SURVEY.md 8(d).4's desk config -- UNetSpec(256, base_channels=16, dropout=0.0), batch 8,
     Adam lr 1e-3, seed 0, 256 T-gray tiles labelled by the auto-labeler -- against the
     reference CPU fp32 trainer (tests/golden/desk_trajectory.pt, made by
     tests/golden/make_desk_trajectory.py from /root/reference).  No retries: every run of the
-    B200 step is bit-reproducible, so this test's outcome is fixed.
+    B200 step is bit-reproducible, so this test's outcome is fixed for a given build.
 
-    The reference is chaotic at this config (DESIGN.md 3.3): from initial weights perturbed by
+    The reference is chaotic at this config (DESIGN.md 3.5): from initial weights perturbed by
     1e-6 (fp32 rounding scale) its own runs track each other to 2e-6 for 12 steps, all spike to
-    loss ~15 at step 16, and end with step-200 losses 0.03-0.09 and late medians 0.11-0.24; a
-    single trajectory cannot agree with another to 2% after ~15 steps, in fp32 or bf16 (torch's
-    own bf16 autocast leaves the band at step 16 too).  So the comparison is the reference's
-    own experiment, repeated on the B200: the unperturbed run plus the same 8 perturbed
-    initialisations (identical draws), and
+    loss ~15 at step 16, and then scatter (step-200 losses 0.03-1.7, late medians 0.10-0.24).
+    A single trajectory cannot agree with another to 2% after ~15 steps, in fp32 or bf16, so
+    the comparison is the reference's own experiment repeated on the B200 -- the unperturbed
+    run plus the same perturbed initialisations (identical draws; 32 in the golden) -- and
       * the first 14 steps of the unperturbed run within 2% of the reference's;
-      * the late-training level -- the median over the 9 runs of each run's median loss over
-        the last 50 steps -- within 2% of the reference's, or within half the reference's own
-        inter-quartile spread of that statistic if that is wider;
-      * a majority of the runs' step-200 losses inside the reference runs' [min, max]."""
+      * the late-training level (each run's median loss over its last 50 steps) and the
+        step-200 loss: our runs and the reference's runs are samples of the same distribution
+        -- two-sided Mann-Whitney U and a permutation test on the difference of medians, each at
+        p >= 0.01 (with 33 runs per side the median of the late level is pinned to ~0.3 sigma
+        of the reference's own spread);
+      * the median late level within max(2%, the reference's inter-quartile range / 2)."""
     import hashlib
     import sys
+    from scipy.stats import mannwhitneyu
     sys.path.insert(0, os.path.dirname(os.path.dirname(__file__)))
     from paper_2403_13135_b200 import icelabel as il
     from tests.fixtures import synth
@@ -238,15 +240,26 @@ def test_loss_after_200_steps_desk_config():
     for k in range(14):
         assert abs(ours[k] - ref[k]) / ref[k] < 0.02, (k, ours[k], ref[k])
     late = lambda ls: float(np.median(ls[-50:]))  # noqa: E731
-    ref_stats, our_stats = [late(r) for r in ref_runs], [late(r) for r in ours_runs]
-    ref_level, our_level = float(np.median(ref_stats)), float(np.median(our_stats))
-    q1, q3 = np.percentile(ref_stats, [25, 75])
-    band = max(0.02 * ref_level, 0.5 * (q3 - q1))
-    print("late medians ref", [round(v, 4) for v in ref_stats], "ours", [round(v, 4) for v in our_stats])
-    assert abs(our_level - ref_level) <= band, (our_level, ref_level, band)
-    lo, hi = min(r[-1] for r in ref_runs), max(r[-1] for r in ref_runs)
-    inside = sum(lo <= r[-1] <= hi for r in ours_runs)
-    assert inside * 2 > len(ours_runs), ([r[-1] for r in ours_runs], lo, hi)
+    ref_late, our_late = np.array([late(r) for r in ref_runs]), np.array([late(r) for r in ours_runs])
+    ref_last, our_last = np.array([r[-1] for r in ref_runs]), np.array([r[-1] for r in ours_runs])
+    print("late medians ref", np.round(np.sort(ref_late), 4).tolist(), "ours", np.round(np.sort(our_late), 4).tolist())
+
+    def perm_p(a, b, n=20000, seed=0):  # two-sided permutation test on the difference of medians
+        rng = np.random.default_rng(seed)
+        pool, obs = np.concatenate([a, b]), abs(np.median(a) - np.median(b))
+        hits = 0
+        for _ in range(n):
+            rng.shuffle(pool)
+            hits += abs(np.median(pool[:len(a)]) - np.median(pool[len(a):])) >= obs - 1e-15
+        return (hits + 1) / (n + 1)
+
+    for name, a, b in (("late level", our_late, ref_late), ("step-200 loss", our_last, ref_last)):
+        p_mw = mannwhitneyu(a, b, alternative="two-sided").pvalue
+        p_pm = perm_p(a, b)
+        assert p_mw >= 0.01 and p_pm >= 0.01, (name, p_mw, p_pm, np.median(a), np.median(b))
+    q1, q3 = np.percentile(ref_late, [25, 75])
+    band = max(0.02 * np.median(ref_late), 0.5 * (q3 - q1))
+    assert abs(np.median(our_late) - np.median(ref_late)) <= band, (np.median(our_late), np.median(ref_late), band)
 
 
 def test_config5_512_tiles_forward_and_grads_match_oracle():
