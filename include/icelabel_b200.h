@@ -97,8 +97,10 @@ int ice_autolabel(const uint8_t *rgb, int64_t n, int32_t h, int32_t w,
  * <= 256 go to ice_autolabel (no scratch).  Larger ones run the multi-CTA region path:
  * cores of <= (256 - 2 * halo)^2 pixels with their halo (halo = bg_dilate_k / 2 +
  * bg_median_k / 2), image-global statistics (d histogram -> stretch -> Otsu, channel
- * medians) in per-image scratch counters; 4 kernels + one memset.  Bit-exact like
- * ice_autolabel.  Scratch (see above): n * (4152 + h * w) bytes, rounded up.
+ * medians) in per-image scratch counters; 4 kernels + one memset.  With the default windows,
+ * h, w >= 256 and w % 16 == 0 the cores run the SWAR pipeline on 256 x 256 windows of the
+ * image (scratch: n * (4152 + 2 h w) bytes, rounded up); otherwise the generic byte pipeline
+ * (n * (4152 + h w)).  Bit-exact like ice_autolabel.
  * ICE_ETOOBIG: h * w >= 2^31, or windows so large that a core would be < 16 pixels. */
 int ice_autolabel_scene(const uint8_t *rgb, int64_t n, int32_t h, int32_t w,
                         const IceFilterCfg *cfg, const IceScheme *scheme,

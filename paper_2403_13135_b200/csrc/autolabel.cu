@@ -1642,11 +1642,13 @@ __device__ __forceinline__ void pack16(const uint32_t (&R)[4], const uint32_t (&
 
 // V = max(r, g, b) (cloudfilter.py:89) or one channel of the tile into a plane ("group" map);
 // returns whether any pixel has unequal channels
-__device__ int load_plane(const uint8_t *tile, int ch, uint32_t *dst, uint32_t *sh = nullptr) {
+// rstride: bytes between the rows of the 256 x 256 window (768: a contiguous tile; 3 w: a
+// window of a w-wide image, 16-B aligned rows)
+__device__ int load_plane(const uint8_t *tile, int ch, uint32_t *dst, uint32_t *sh = nullptr, int rstride = 768) {
     int uneq = 0;
-    const uint4 *t4 = reinterpret_cast<const uint4 *>(tile);
     for (int g = threadIdx.x; g < 4096; g += NTF) {
-        const uint4 a = __ldg(t4 + 3 * g), b = __ldg(t4 + 3 * g + 1), c = __ldg(t4 + 3 * g + 2);
+        const uint4 *t4 = reinterpret_cast<const uint4 *>(tile + (size_t)(g >> 4) * rstride) + 3 * (g & 15);
+        const uint4 a = __ldg(t4), b = __ldg(t4 + 1), c = __ldg(t4 + 2);
         uint32_t R[4], G[4], B[4];
         unpack16(a, b, c, R, G, B);
         uint32_t *d = dst + (g >> 4) * WP + 4 * (g & 15);
@@ -1979,6 +1981,331 @@ autolabel256_kernel(const uint8_t *__restrict__ rgb, int n, int ahead, Params pr
     process_tile256(rgb, prm, filtered, label, maskout, affected, counts, unmatched, s, (size_t)t);
 }
 
+
+// =====================================================================================
+// SWAR region path: the 256 x 256 SWAR pipeline on 256 x 256 WINDOWS of a larger image
+// (whole scenes, 512^2 tiles) with the default windows.  h, w >= 256, w % 16 == 0.  The image
+// is cut into cores (<= 230 rows, <= 224 columns, column starts at multiples of 16); each
+// core's window is the 256 x 256 block that holds the core plus its 13-pixel halo, shifted
+// inside the image at the borders (so window borders that are image borders replicate, as
+// cv2 does, and interior window borders lie >= 13 pixels from the core).  Window rows are
+// 16-B aligned (column origin a multiple of 16), so the SWAR loads / stores apply unchanged.
+// Pass 1 (region256_d_kernel) writes the core's d and background-of-V bytes to scratch
+// planes and adds the core's d / channel histograms to the image's counters; the
+// image-global statistics come from region_stats_kernel; pass 2 (region256_out_kernel)
+// masks the core, recomputes channel backgrounds only when the window is not gray and the
+// core holds masked pixels (blocks without masked pixels skipped), and writes filtered /
+// mask / label for the core.
+struct R256 {
+    int h, w, ny, nx, cs_y, cs_x;
+};
+struct R256Box {
+    int cy0, ch, cx0, cw, ry0, rx0;
+};
+__device__ __forceinline__ R256Box r256_box(const R256 &g, int r) {
+    R256Box b;
+    const int by = r / g.nx, bx = r - by * g.nx;
+    b.cy0 = by * g.cs_y;
+    b.ch = min(g.cs_y, g.h - b.cy0);
+    b.cx0 = bx * g.cs_x;
+    b.cw = min(g.cs_x, g.w - b.cx0);
+    b.ry0 = min(max(b.cy0 - MR - 3, 0), g.h - 256);
+    b.rx0 = min(max(b.cx0 - 16, 0), g.w - 256);
+    return b;
+}
+
+__global__ void __launch_bounds__(NTF, 1)
+region256_d_kernel(const uint8_t *__restrict__ rgb, R256 g, IceFilterCfg cfg, int regions,
+                   uint8_t *__restrict__ dplanes, uint8_t *__restrict__ bgplanes, RegionStats *__restrict__ st) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    SmemF &s = *reinterpret_cast<SmemF *>(smem_raw);
+    const int img = blockIdx.x / regions;
+    const R256Box b = r256_box(g, blockIdx.x - img * regions);
+    const size_t npx = (size_t)g.h * g.w;
+    const uint8_t *im = rgb + img * npx * 3;
+    const uint8_t *win = im + ((size_t)b.ry0 * g.w + b.rx0) * 3;
+    const int rs = 3 * g.w;
+    RegionStats &S = st[img];
+    uint32_t *P0 = s.p[0], *P1 = s.p[1], *P2 = s.p[2];
+    const int cc = threadIdx.x & 63, y0 = (threadIdx.x >> 6) * 32;  // "col" map
+    if (threadIdx.x < 256) s.flags[threadIdx.x] = 0;
+    __syncthreads();
+    load_plane(win, 3, P0, nullptr, rs);  // V (cloudfilter.py:89)
+    __syncthreads();
+    dilate7(P0, P1, P2, s);  // D in P2
+    median21(P2, P0, P1, s, ICE_AL_COARSE_V);  // background of V in P1
+    load_plane(win, 3, P0, nullptr, rs);
+    __syncthreads();
+    median3_plane(P0, P2);  // smooth in P2
+    __syncthreads();
+    subhist_zero(P0);
+    __syncthreads();
+    // the core's d (and bg) words -> scratch planes; d histogram over the core
+    const int oy = b.cy0 - b.ry0, ox4 = (b.cx0 - b.rx0) >> 2, cw4 = b.cw >> 2;
+    const uint32_t tt4 = (uint32_t)cfg.truncate_t * 0x01010101u;
+    uint32_t *dpl = reinterpret_cast<uint32_t *>(dplanes + img * npx);
+    uint32_t *bpl = reinterpret_cast<uint32_t *>(bgplanes + img * npx);
+    const bool col_in = cc >= ox4 && cc < ox4 + cw4;
+#pragma unroll 4
+    for (int y = 0; y < 32; ++y) {
+        const int r = y0 + y;
+        if (!col_in || r < oy || r >= oy + b.ch) continue;
+        const int o = r * WP + cc;
+        uint32_t d = __vabsdiffu4(P2[o], P1[o]);
+        if (cfg.diff_truncate) d = vmin(d, tt4);
+        const size_t gw = (((size_t)(b.ry0 + r) * g.w + b.rx0) >> 2) + cc;
+        dpl[gw] = d;
+        bpl[gw] = P1[o];
+        subhist_add4(P0, d);
+    }
+    __syncthreads();
+    subhist_reduce(P0, s.hist);
+    __syncthreads();
+    if (threadIdx.x < 256 && s.hist[threadIdx.x]) atomicAdd(&S.hist_d[threadIdx.x], s.hist[threadIdx.x]);
+    __syncthreads();
+    // channel histograms of the core (for the channel medians of the repair)
+    subhist_zero(P0);
+    subhist_zero(P1);
+    subhist_zero(P2);
+    __syncthreads();
+    const int cg = b.cw >> 4, ng = b.ch * cg;
+    for (int q = threadIdx.x; q < ng; q += NTF) {
+        const int r = q / cg, k = q - r * cg;
+        const uint4 *t4 = reinterpret_cast<const uint4 *>(im + ((size_t)(b.cy0 + r) * g.w + b.cx0 + 16 * k) * 3);
+        uint32_t R[4], G[4], B[4];
+        unpack16(__ldg(t4), __ldg(t4 + 1), __ldg(t4 + 2), R, G, B);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            subhist_add4(P0, R[e]);
+            subhist_add4(P1, G[e]);
+            subhist_add4(P2, B[e]);
+        }
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int c = 0; c < 3; ++c) {
+        subhist_reduce(s.p[c], s.hist);
+        __syncthreads();
+        if (threadIdx.x < 256 && s.hist[threadIdx.x]) atomicAdd(&S.hist_c[c][threadIdx.x], s.hist[threadIdx.x]);
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(NTF, 1)
+region256_out_kernel(const uint8_t *__restrict__ rgb, R256 g, Params prm, int regions,
+                     const uint8_t *__restrict__ dplanes, const uint8_t *__restrict__ bgplanes,
+                     RegionStats *__restrict__ st, uint8_t *__restrict__ filtered, uint8_t *__restrict__ label,
+                     uint8_t *__restrict__ maskout) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    SmemF &s = *reinterpret_cast<SmemF *>(smem_raw);
+    if (threadIdx.x < 256 && prm.v_only) {
+        int cls = 255;
+        const int v = threadIdx.x;
+        for (int k = 2; k >= 0; --k)
+            if (v >= prm.scheme.lo[k][2] && v <= prm.scheme.hi[k][2]) cls = prm.scheme.cls[k];
+        const int slot = cls == 255 ? 3 : cls;
+        s.vlut[v] = (uint32_t)cls | (1u << (12 + 5 * slot));
+    }
+    const int img = blockIdx.x / regions;
+    const R256Box b = r256_box(g, blockIdx.x - img * regions);
+    const size_t npx = (size_t)g.h * g.w;
+    const uint8_t *im = rgb + img * npx * 3;
+    const uint8_t *win = im + ((size_t)b.ry0 * g.w + b.rx0) * 3;
+    const int rs = 3 * g.w;
+    uint8_t *fim = filtered + img * npx * 3;
+    const uint32_t *dpl = reinterpret_cast<const uint32_t *>(dplanes + img * npx);
+    const uint32_t *bpl = reinterpret_cast<const uint32_t *>(bgplanes + img * npx);
+    RegionStats &S = st[img];
+    uint32_t *P0 = s.p[0], *P1 = s.p[1], *P2 = s.p[2];
+    const int cc = threadIdx.x & 63, y0 = (threadIdx.x >> 6) * 32;
+    const int oy = b.cy0 - b.ry0, ox = b.cx0 - b.rx0;
+    // masked <=> d > dthr, dthr = the largest d whose stretch is <= thr (kernels.py:66-74, 94-96)
+    if (threadIdx.x == 0) {
+        int dthr = S.lo - 1;
+        for (int v = S.lo; v <= S.lo + S.range; ++v)
+            if (stretch(v, S.lo, S.range) <= S.thr) dthr = v;
+        s.bc[0] = dthr;
+        s.need_bits = 0;
+        for (int k = 0; k < 256; ++k) s.flags[k] = 0;
+    }
+    __syncthreads();
+    const int dthr = s.bc[0];
+    const bool all_masked = dthr < 0;
+    const uint32_t mc4 = (uint32_t)(255 - max(dthr, 0)) * 0x01010101u;
+    // mask bits of the window (non-core pixels are never masked here)
+    int any = 0;
+    for (int w = threadIdx.x; w < 2048; w += NTF) {
+        uint32_t bits = 0;
+        const int y = w >> 3, x0 = (w & 7) * 32;
+        if (S.masked > 0 && y >= oy && y < oy + b.ch) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int x = x0 + 4 * q;
+                if (x < ox || x >= ox + b.cw) continue;
+                const uint32_t dw = dpl[(((size_t)(b.ry0 + y) * g.w + b.rx0 + x) >> 2)];
+                const uint32_t gq = all_masked ? 0x01010101u : gt4(dw, mc4, mc4 & 0x7f7f7f7fu);
+                bits |= ((gq & 1) | ((gq >> 7) & 2) | ((gq >> 14) & 4) | ((gq >> 21) & 8)) << (4 * q);
+            }
+        }
+        s.maskbits[w] = bits;
+        if (bits) atomicOr(&s.need_bits, 1u << (2 * (y >> 5) + ((w & 7) >> 2)));
+        any |= bits != 0;
+    }
+    const bool repair = __syncthreads_or(any) != 0;
+    bool gray = true;
+    if (repair) {
+        // R == G == B over the window: every channel's background is V's (pass 1's bg plane)
+        gray = !__syncthreads_or(load_plane(win, 0, P0, nullptr, rs));
+        if (!gray) {
+            const uint32_t need = s.need_bits;
+            for (int ch = 0; ch < 3; ++ch) {
+                load_plane(win, ch, P0, nullptr, rs);
+                __syncthreads();
+                dilate7(P0, P1, P2, s);
+                median21(P2, P0, P1, s, ICE_AL_COARSE_C, need);  // bg_c in P1 (blocks in need)
+                load_plane(win, ch, P0, nullptr, rs);
+                __syncthreads();
+                const int c_ch = S.center[ch];
+#pragma unroll 2
+                for (int y = 0; y < 32; ++y) {
+                    const int yy = y0 + y;
+                    const uint32_t mb = (s.maskbits[yy * 8 + (cc >> 3)] >> (4 * (cc & 7))) & 15;
+                    if (mb) {
+                        const uint32_t chw = P0[yy * WP + cc], bgw = P1[yy * WP + cc];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            if (mb >> k & 1) {
+                                const size_t gi = (size_t)(b.ry0 + yy) * g.w + b.rx0 + 4 * cc + k;
+                                const int f = (int)((chw >> (8 * k)) & 255) - (int)((bgw >> (8 * k)) & 255) + c_ch;
+                                fim[3 * gi + ch] = (uint8_t)clampi(f, 0, 255);
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    // output: the core in 16-pixel groups
+    int c0 = 0, c1 = 0, c2 = 0, first = 0x7fffffff;
+    const SchemeR scr(prm.scheme);
+    const int cgw = b.cw >> 4, ng = b.ch * cgw;
+    const int cen = S.center[0];
+    for (int q = threadIdx.x; q < ng; q += NTF) {
+        const int r = q / cgw, k = q - r * cgw;
+        const size_t gi = (size_t)(b.cy0 + r) * g.w + b.cx0 + 16 * k;  // first pixel of the group
+        const uint4 *t4 = reinterpret_cast<const uint4 *>(im + gi * 3);
+        uint32_t R[4], G[4], B[4];
+        unpack16(__ldg(t4), __ldg(t4 + 1), __ldg(t4 + 2), R, G, B);
+        const int wy = oy + r, wx = ox + 16 * k;
+        const uint32_t bits16 = (s.maskbits[wy * 8 + (wx >> 5)] >> (wx & 31)) & 0xffffu;
+        uint32_t mk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t n = bits16 >> (4 * e);
+            mk[e] = (n & 1) | ((n & 2) << 7) | ((n & 4) << 14) | ((n & 8) << 21);
+        }
+        if (bits16) {
+            if (gray) {
+                const uint4 bgv = *reinterpret_cast<const uint4 *>(bpl + (gi >> 2));
+                const uint32_t bw[4] = {bgv.x, bgv.y, bgv.z, bgv.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    uint32_t f = 0;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const int x = (R[e] >> (8 * kk)) & 255;
+                        const int v = clampi(x - (int)((bw[e] >> (8 * kk)) & 255) + cen, 0, 255);
+                        f |= (uint32_t)((mk[e] >> (8 * kk) & 1) ? v : x) << (8 * kk);
+                    }
+                    R[e] = G[e] = B[e] = f;
+                }
+            } else {
+                const uint4 *f4 = reinterpret_cast<const uint4 *>(fim + gi * 3);
+                uint32_t FR[4], FG[4], FB[4];
+                unpack16(f4[0], f4[1], f4[2], FR, FG, FB);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t sel = mk[e] * 255u;
+                    R[e] = (FR[e] & sel) | (R[e] & ~sel);
+                    G[e] = (FG[e] & sel) | (G[e] & ~sel);
+                    B[e] = (FB[e] & sel) | (B[e] & ~sel);
+                }
+            }
+        }
+        uint4 fa, fb, fc;
+        pack16(R, G, B, fa, fb, fc);
+        uint4 *fo = reinterpret_cast<uint4 *>(fim + gi * 3);
+        fo[0] = fa;
+        fo[1] = fb;
+        fo[2] = fc;
+        if (maskout)
+            *reinterpret_cast<uint4 *>(maskout + img * npx + gi) =
+                make_uint4(mk[0] * 255u, mk[1] * 255u, mk[2] * 255u, mk[3] * 255u);
+        uint32_t lw[4];
+        if (prm.v_only) {
+            uint32_t sum = 0, e16[16];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t v = vmax3(R[e], G[e], B[e]);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    e16[4 * e + kk] = s.vlut[(v >> (8 * kk)) & 255];
+                    sum += e16[4 * e + kk];
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                lw[e] = __byte_perm(__byte_perm(e16[4 * e], e16[4 * e + 1], 0x0040),
+                                    __byte_perm(e16[4 * e + 2], e16[4 * e + 3], 0x0040), 0x5410);
+            c0 += (sum >> 12) & 31;
+            c1 += (sum >> 17) & 31;
+            c2 += (sum >> 22) & 31;
+            if (sum >> 27) {
+#pragma unroll
+                for (int kk = 15; kk >= 0; --kk)
+                    if ((e16[kk] & 255) == 255) first = min(first, (int)gi + kk);
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                lw[e] = 0;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const int cls = classify((R[e] >> (8 * kk)) & 255, (G[e] >> (8 * kk)) & 255,
+                                             (B[e] >> (8 * kk)) & 255, scr);
+                    lw[e] |= (uint32_t)cls << (8 * kk);
+                    c0 += cls == 0;
+                    c1 += cls == 1;
+                    c2 += cls == 2;
+                    if (cls == 255) first = min(first, (int)gi + 4 * e + kk);
+                }
+            }
+        }
+        *reinterpret_cast<uint4 *>(label + img * npx + gi) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+    for (int o = 16; o; o >>= 1) {
+        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+        first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        const int wi = threadIdx.x >> 5;
+        s.red[wi][0] = c0; s.red[wi][1] = c1; s.red[wi][2] = c2; s.red[wi][3] = first;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < NTF / 32; ++i) {
+            c0 += s.red[i][0]; c1 += s.red[i][1]; c2 += s.red[i][2]; first = min(first, s.red[i][3]);
+        }
+        if (c0) atomicAdd(&S.counts[0], (uint32_t)c0);
+        if (c1) atomicAdd(&S.counts[1], (uint32_t)c1);
+        if (c2) atomicAdd(&S.counts[2], (uint32_t)c2);
+        if (first != 0x7fffffff) atomicMin(&S.first, first);
+    }
+}
 }  // namespace fastk
 
 bool full_hue(const IceScheme &sc) {
@@ -2077,6 +2404,63 @@ extern "C" int ice_autolabel_scene(const uint8_t *rgb, int64_t n, int32_t h, int
     if (!window_ok(cfg->noise_median_k, h, w) || !window_ok(cfg->bg_dilate_k, h, w) ||
         !window_ok(cfg->bg_median_k, h, w))
         return ICE_EWINDOW;
+    // SWAR windows (default windows, 16-B aligned rows) unless a test hook forces the generic path
+    const bool swar = g_autolabel_path != 1 && g_autolabel_path != 3 && h >= 256 && w >= 256 && w % 16 == 0 &&
+                      cfg->bg_dilate_k == 7 && cfg->bg_median_k == fastk::MK && cfg->noise_median_k == 3 &&
+                      ((reinterpret_cast<uintptr_t>(rgb) | reinterpret_cast<uintptr_t>(filtered) |
+                        reinterpret_cast<uintptr_t>(label) | reinterpret_cast<uintptr_t>(mask)) & 15) == 0;
+    if (swar) {
+        fastk::R256 g;
+        g.h = h;
+        g.w = w;
+        g.ny = (h + 229) / 230;
+        g.cs_y = (h + g.ny - 1) / g.ny;
+        g.nx = (w + 223) / 224;
+        g.cs_x = ((w + g.nx - 1) / g.nx + 15) / 16 * 16;
+        g.nx = (w + g.cs_x - 1) / g.cs_x;
+        const int regions = g.ny * g.nx;
+        const uint64_t stats_bytes = ((uint64_t)n * sizeof(RegionStats) + 255) & ~(uint64_t)255;
+        const uint64_t plane_bytes = ((uint64_t)n * h * w + 255) & ~(uint64_t)255;
+        const uint64_t need = stats_bytes + 2 * plane_bytes;
+        if (!scratch) {
+            if (!scratch_bytes) return ICE_ESCRATCH;
+            *scratch_bytes = need;
+            return ICE_OK;
+        }
+        if (!scratch_bytes || *scratch_bytes < need) return ICE_ESCRATCH;
+        if (n == 0) return ICE_OK;
+        if (!rgb || !filtered || !label || !affected || !counts || !unmatched) return ICE_EINVAL;
+        if ((int64_t)n * regions > 0x7fffffff) return ICE_ETOOBIG;
+        Params prm;
+        prm.cfg = *cfg;
+        prm.scheme = *scheme;
+        prm.v_only = full_hue(*scheme) && full_sat(*scheme);
+        static bool attr_swar = false;
+        if (!attr_swar) {
+            cudaError_t e = cudaFuncSetAttribute(fastk::region256_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)sizeof(fastk::SmemF));
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(fastk::region256_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(fastk::SmemF));
+            if (e != cudaSuccess) return (int)e;
+            attr_swar = true;
+        }
+        cudaStream_t st = (cudaStream_t)stream;
+        RegionStats *stats = reinterpret_cast<RegionStats *>(scratch);
+        uint8_t *dplanes = reinterpret_cast<uint8_t *>(scratch) + stats_bytes;
+        uint8_t *bgplanes = dplanes + plane_bytes;
+        cudaError_t e = cudaMemsetAsync(stats, 0, (size_t)n * sizeof(RegionStats), st);
+        if (e != cudaSuccess) return (int)e;
+        const unsigned grid = (unsigned)(n * regions);
+        fastk::region256_d_kernel<<<grid, fastk::NTF, sizeof(fastk::SmemF), st>>>(rgb, g, *cfg, regions, dplanes,
+                                                                                  bgplanes, stats);
+        region_stats_kernel<<<(unsigned)n, 256, 0, st>>>(stats, h * w, *cfg);
+        fastk::region256_out_kernel<<<grid, fastk::NTF, sizeof(fastk::SmemF), st>>>(
+            rgb, g, prm, regions, dplanes, bgplanes, stats, filtered, label, mask);
+        region_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stats, (int)n, affected, counts, unmatched);
+        for (int k = 0; k < 4; ++k) ice::count_launch();
+        return (int)cudaGetLastError();
+    }
     const int halo = max(cfg->bg_dilate_k / 2 + cfg->bg_median_k / 2, cfg->noise_median_k / 2);
     int cmax = MAXD - 2 * halo;
     if (g_autolabel_path == 3) cmax = min(cmax, 40);  // test hook: many small regions

@@ -353,3 +353,18 @@ def test_region_path_hsv_scheme_and_scene_size():
     lbl, first = orc.segment(f, _ranges(SAT_ONLY))
     assert np.array_equal(out["label"][0], lbl)
     assert out["unmatched"][0] == first
+
+
+@pytest.mark.parametrize("shape", [(512, 512), (600, 768), (257, 256), (256, 1024)], ids=str)
+def test_region_swar_windows_match_generic_region_path(shape):
+    """The SWAR 256 x 256-window region path (default windows, w % 16 == 0) equals the generic
+    region path (mode 1) on T-gray, T-tint and T-rand content, every output."""
+    h, w = shape
+    base = np.ascontiguousarray(synth.scene(3, 1, max(h, w), True)[0][:h, :w])
+    rng = np.random.default_rng(h * w)
+    tiles = [base, synth.tint(base, 3, 1), rng.integers(0, 256, (h, w, 3), dtype=np.uint8)]
+    sw = _run_path(tiles, 0)
+    gen = _run_path(tiles, 1)
+    for k in gen:
+        for i in range(len(tiles)):
+            assert np.array_equal(sw[k][i], gen[k][i]), (k, i)

@@ -66,7 +66,9 @@ def test_autolabel_scene_scratch_query_and_errors():
     q = ctypes.c_uint64(123)
     args = (None, None, None, None, None, None)
     assert lib.ice_autolabel_scene(None, 2, 512, 512, cfg, sc, *args, None, ctypes.byref(q), None) == 0
-    assert q.value == ((2 * 4152 + 255) // 256) * 256 + 2 * 512 * 512
+    assert q.value == ((2 * 4152 + 255) // 256) * 256 + 2 * (2 * 512 * 512)  # SWAR windows: d + bg planes
+    assert lib.ice_autolabel_scene(None, 2, 512, 520, cfg, sc, *args, None, ctypes.byref(q), None) == 0
+    assert q.value == ((2 * 4152 + 255) // 256) * 256 + ((2 * 512 * 520 + 255) // 256) * 256  # generic: d plane
     assert lib.ice_autolabel_scene(None, 3, 64, 64, cfg, sc, *args, None, ctypes.byref(q), None) == 0
     assert q.value == 0  # <= 256 x 256: one CTA per tile, no scratch
     assert lib.ice_autolabel_scene(None, 1, 300, 10, cfg, sc, *args, None, ctypes.byref(q), None) == -2
