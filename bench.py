@@ -177,7 +177,7 @@ def config5_bench(dev, dist, world, rank, steps: int = 10, warmup: int = 3, coun
             "data": "synthetic generate_corpus(101, 64, 0.3, size=512) tiles, labels by K1 on GPU (512^2 region path)",
             "autolabel_512": {"value": round(count * 512 * 512 / (al_ms / 1000.0) / 1e6, 1), "unit": "Mpixel/s",
                               "ms": round(al_ms, 3), "tiles": count,
-                              "path": "ice_autolabel_scene region path (3 x 3 cores of <= 230^2 + halo per tile)"}}
+                              "path": "ice_autolabel_scene region path: 3 x 3 cores per tile, each on a SWAR 256^2 window"}}
 
 
 def config0_bench():
