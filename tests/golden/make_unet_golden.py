@@ -43,11 +43,18 @@ def digest(sd):
 
 
 def compact(tensors, full):
-    """full tensors for the desk spec; norms + leading 256 values otherwise (size cap)."""
+    """full tensors for the desk spec; otherwise (size cap) norms, the leading 256 values, and
+    the values at 1024 seeded random positions of each tensor ("idx" / "sample": an unbiased
+    element sample, so a per-tensor relative error is measured on the whole tensor)."""
     if full:
         return {k: v.detach().clone() for k, v in tensors.items()}
-    return {k: {"norm": float(v.norm()), "head": v.detach().reshape(-1)[:256].clone()}
-            for k, v in tensors.items()}
+    out = {}
+    for pos, (k, v) in enumerate(tensors.items()):
+        flat = v.detach().reshape(-1)
+        idx = torch.randperm(flat.numel(), generator=torch.Generator().manual_seed(1000 + pos))[:1024]
+        out[k] = {"norm": float(v.norm()), "head": flat[:256].clone(), "idx": idx.to(torch.int32),
+                  "sample": flat[idx].clone()}
+    return out
 
 
 def main():

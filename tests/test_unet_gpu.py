@@ -53,7 +53,9 @@ def test_logits_match_reference(name):
 @pytest.mark.parametrize("name", ["desk", "deep"])
 def test_loss_and_grads_match_reference(name):
     """Golden gradients of the reference itself; same per-tensor rule as the paper-spec
-    test (2e-2, or 2x torch's bf16-autocast error; on average within 1.5x of torch)."""
+    test (2e-2, or 2x torch's bf16-autocast error; on average within 1.5x of torch).  The deep
+    spec's golden keeps, per tensor, the norm and 1024 seeded random elements (an unbiased
+    sample of the whole tensor: tests/golden/make_unet_golden.py)."""
     g = GOLD[name]
     spec = UNetSpec(**g["spec"])
     torch.manual_seed(0)
@@ -65,9 +67,13 @@ def test_loss_and_grads_match_reference(name):
     errs, floors = [], []
     for k, v in grads.items():
         ref = g["grads"][k]
-        if isinstance(ref, dict):
-            err = abs(float(v.norm()) - ref["norm"]) / max(ref["norm"], 1e-30)
-            floor = abs(float(base[k].norm()) - ref["norm"]) / max(ref["norm"], 1e-30)
+        if isinstance(ref, dict):  # deep spec: 1024 seeded random elements of each tensor + its norm
+            idx = ref["idx"].long()
+            err = rel(v.reshape(-1)[idx], ref["sample"])
+            floor = rel(base[k].reshape(-1)[idx], ref["sample"])
+            n_err = abs(float(v.norm()) - ref["norm"]) / max(ref["norm"], 1e-30)
+            n_floor = abs(float(base[k].norm()) - ref["norm"]) / max(ref["norm"], 1e-30)
+            assert n_err < max(TOL, 2 * n_floor), (k, "norm", n_err, n_floor)
         else:
             err, floor = rel(v, ref), rel(base[k], ref)
         errs.append(err)
