@@ -62,3 +62,35 @@ def test_two_ranks_equal_union_batch_step():
         assert abs(a - c) <= 1e-5 * abs(c) + 1e-6
     rel = float((p0 - m.engine.params.cpu()).norm() / m.engine.params.cpu().norm())
     assert rel < 1e-5
+
+
+def _al_rank(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2403_13135_b200 import icelabel as il
+    from tests.fixtures import synth
+    tiles = torch.from_numpy(__import__("numpy").stack([t for t, _ in synth.corpus(23, 7, 0.5)]))
+    res, (lo, hi), totals = il.autolabel_sharded(tiles)  # host corpus: each rank copies its shard
+    out[rank] = (lo, hi, res["label"].cpu() if res is not None else None, totals.cpu())
+    dist.destroy_process_group()
+
+
+def test_autolabel_sharded_two_ranks():
+    """BASELINE configs[3] layout on two ranks (one GPU, gloo): contiguous tile shards with no
+    data-path collective, the per-class / masked totals summed by ONE small all-reduce; the
+    shards' labels and the totals equal the single-process labeling of the whole corpus."""
+    import numpy as np
+    from paper_2403_13135_b200 import icelabel as il
+    from tests.fixtures import synth
+    out = mp.Manager().dict()
+    mp.spawn(_al_rank, args=(2, _port(), out), nprocs=2, join=True)
+    tiles = torch.from_numpy(np.stack([t for t, _ in synth.corpus(23, 7, 0.5)])).cuda()
+    ref = il.autolabel(tiles)
+    (lo0, hi0, lab0, tot0), (lo1, hi1, lab1, tot1) = out[0], out[1]
+    assert (lo0, hi0, lo1, hi1) == (0, 3, 3, 7)  # shard_bounds(7, 2, r)
+    assert torch.equal(torch.cat([lab0, lab1]), ref["label"].cpu())
+    assert torch.equal(tot0, tot1)
+    want = torch.tensor(ref["counts"].to(torch.int64).sum(0).tolist() + [int(ref["affected"].sum()),
+                                                                         int((ref["unmatched"] >= 0).sum())])
+    assert torch.equal(tot0, want)
