@@ -437,6 +437,7 @@ class UNetEngine:
     # The first conv straight from the u8 images (ice_stem_fprop / ice_stem_wgrad) instead of
     # a bf16 im2col buffer + GEMMs; float input always takes the im2col path.
     fused_stem = os.environ.get("ICE_FUSED_STEM", "1") != "0"  # A/B switch, read once
+    side_flush = os.environ.get("ICE_SIDE_FLUSH", "1") != "0"  # A/B switch, read once
 
     def backward(self, A: _Acts, dz, on_layer_done=None) -> None:
         """Accumulate parameter gradients into self.grads (dz: dZ of up.{d-1}.block.2).
@@ -446,16 +447,46 @@ class UNetEngine:
             return self._backward(A, dz, on_layer_done)
         _native.call("ice_finish_defer", 1)
         _native.scratch.begin_bump()
+        self._side_events = []
         try:
             self._backward(A, dz, on_layer_done)
             self.flush_deferred()
+            cur = torch.cuda.current_stream()
+            for ev in self._side_events:  # finishers flushed early on the side stream
+                cur.wait_event(ev)
         finally:
+            self._side_events = []
             _native.call("ice_finish_defer", 0)
             _native.scratch.end_bump()
 
     def flush_deferred(self, stream=None) -> None:
-        """Run the gradient finishers recorded so far (one launch; no-op when none)."""
+        """Run the gradient finishers recorded so far (one launch; no-op when none).  On the
+        current stream it also joins the finishers flushed early on the side stream, so every
+        gradient is complete after it in stream order (the bucketer relies on that)."""
+        if stream is None:
+            cur = torch.cuda.current_stream()
+            for ev in getattr(self, "_side_events", ()):
+                cur.wait_event(ev)
         _native.call("ice_finish_flush", _native.stream_handle(stream))
+
+    def _flush_side(self) -> None:
+        """Flush the finishers recorded so far on a side stream, so their (HBM-bound) slice
+        sums overlap the rest of the (tensor-bound) backward; backward() joins it before it
+        returns.  Their gradients are complete once their producers ran (ordered by the event);
+        no later kernel of the backward touches them, and bump-mode scratch keeps their
+        partial sums."""
+        if not self.defer_finish or not self.grads.is_cuda or not self.side_flush:
+            return
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        cur = torch.cuda.current_stream()
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        self._side.wait_event(ev)
+        self.flush_deferred(self._side)
+        done = torch.cuda.Event()
+        done.record(self._side)
+        self._side_events.append(done)
 
     def _backward(self, A: _Acts, dz, on_layer_done=None) -> None:
         d = self.spec.depth
@@ -492,6 +523,7 @@ class UNetEngine:
                          hl.cin_p, dz.data_ptr(), xprev.data_ptr(), _native.ptr(drop_prev),
                          self.b(prev_name, G).data_ptr(), st)
             done(hn)
+        self._flush_side()  # the up path's finishers overlap the bottleneck and down path
         # bottleneck
         ops.conv_wgrad(A.b1, dz, self.w("bottleneck.block.2", G))
         dz1 = A.dz_b[d]
