@@ -74,6 +74,15 @@ typedef struct {
 int ice_finish_defer(int32_t on);
 int ice_finish_flush(void *stream);
 
+/* Gradient overwrite mode.  ice_grad_overwrite(1): until ice_grad_overwrite(0), every gradient
+ * producer (ice_conv_wgrad, ice_halve_wgrad, ice_stem_wgrad, and the bias / head gradients of
+ * ice_conv_dgrad, ice_halve_dgrad, ice_maxpool_bwd, ice_head_ce, ice_bias_grad) STORES its
+ * contribution (dw = contribution) instead of adding it; each gradient element has exactly one
+ * producer per backward, so a backward in this mode writes every gradient without the buffer
+ * having been zeroed.  The optimizer step can then skip zeroing (ice_adam zero_grad = 0), and
+ * split-K weight gradients need not read the old value.  Process-wide; not thread-safe. */
+int ice_grad_overwrite(int32_t on);
+
 /* Fused auto-label kernel (K1): replaces engine.process_tile (engine.py:145-160) =
  * cloudfilter.apply_filter (cloudfilter.py:99-117) + segmentation.segment
  * (segmentation.py:118-128) over a batch of n tiles, plus per-class counts (new).
@@ -267,12 +276,13 @@ int ice_dropout_scale(int32_t count, float p, uint64_t seed, const int64_t *step
                       void *stream);
 
 /* torch.optim.Adam step (defaults of train.py:149: no weight decay, no amsgrad) over flat
- * fp32 buffers, fused with the bf16 working-copy write and zeroing of g.  Hyper-parameters are
+ * fp32 buffers, fused with the bf16 working-copy write and (zero_grad != 0) zeroing of g --
+ * skipped when the next backward runs in gradient overwrite mode.  Hyper-parameters are
  * doubles (torch forms 1 - beta and the bias corrections from Python floats).  The step t is
  * `step`, or *step_dev when step_dev is non-NULL (bias corrections computed on the device). */
 int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64_t step,
              const int64_t *step_dev, double lr, double beta1, double beta2, double eps,
-             uint16_t *out_bf16, void *stream);
+             int32_t zero_grad, uint16_t *out_bf16, void *stream);
 
 /* *counter += delta on the device (the step counter advanced inside CUDA graphs). */
 int ice_counter_add(int64_t *counter, int64_t delta, void *stream);

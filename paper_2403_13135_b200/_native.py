@@ -52,6 +52,7 @@ SIGNATURES = {
     "ice_autolabel_set_path": [_I32],
     "ice_finish_defer": [_I32],
     "ice_finish_flush": [_V],
+    "ice_grad_overwrite": [_I32],
     "ice_autolabel_scene": [_V, _I64, _I32, _I32, ctypes.POINTER(IceFilterCfg), ctypes.POINTER(IceScheme),
                             _V, _V, _V, _V, _V, _V, *_S, _V],
     "ice_cut_tiles": [_V, _I32, _I32, _I32, _I32, _V, _V],
@@ -81,7 +82,7 @@ SIGNATURES = {
     "ice_head_ce": [_V, _I64, _I32, _V, _V, _V, _V, _F32, _V, _V, _V, _V, _V, _V, *_S, _V],
     "ice_bias_grad": [_V, _I64, _I32, _V, *_S, _V],
     "ice_dropout_scale": [_I32, _F32, ctypes.c_uint64, _V, _V, _V],
-    "ice_adam": [_V, _V, _V, _V, _I64, _I64, _V, _F64, _F64, _F64, _F64, _V, _V],
+    "ice_adam": [_V, _V, _V, _V, _I64, _I64, _V, _F64, _F64, _F64, _F64, _I32, _V, _V],
     "ice_counter_add": [_V, _I64, _V],
     "ice_cast_bf16": [_V, _I64, _V, _V],
     "ice_fill_f32": [_V, _I64, _F32, _V],

@@ -558,6 +558,7 @@ struct WgradProb {
     float *dw;  // [cout][taps][c1+c2]
     float *ws;  // partials of splits 1.. [splits - 1][cout][taps][c1+c2] (scratch) when splits > 1
     size_t wsize;
+    int ow;     // gradient overwrite mode: split 0 stores instead of adding (ice_grad_overwrite)
 
     __device__ void kb_range(int z, int &kb0, int &nkb) const {
         kb0 = z * kb_per_split;
@@ -646,7 +647,7 @@ struct WgradProb {
             if (!trans) {
                 if (m >= cout) continue;
                 float *dst = base + (size_t)m * ld + nt * BN + cc * 32;
-                if (part) {
+                if (part || ow) {  // a slice, or the first gradient of the step (overwrite mode)
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
                         __stcg(reinterpret_cast<float4 *>(dst) + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
@@ -661,7 +662,7 @@ struct WgradProb {
                 for (int j = 0; j < 32; ++j) {
                     if (o0 + j >= cout) continue;
                     float *dst = base + (size_t)(o0 + j) * ld + m;
-                    if (part) __stcg(dst, v[j]);
+                    if (part || ow) __stcg(dst, v[j]);
                     else atomicAdd(dst, v[j]);  // RED, fire-and-forget; one contribution per element
                 }
             }
@@ -1461,6 +1462,7 @@ struct HWgrad {
     float *dw;  // [cout][9][ct]
     float *ws;  // partials of splits 1.. [splits - 1][cout][9][ct] (scratch)
     size_t wsize;
+    int ow;     // gradient overwrite mode: split 0 stores instead of adding
 };
 
 // HALVE variant (2x2 halving conv, model.py:79-88): dW[(a,b), c] accumulates, for each of
@@ -1640,7 +1642,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                     float v[32];
                     tc::tmem_ld32(tmem + (mt - mt0) * COUT + cc * 32 + ((uint32_t)(sub * 32) << 16), v);
                     if (!valid) continue;
-                    if (part) {
+                    if (part || p.ow) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) __stcg(dst + (size_t)(cc * 32 + j) * ld, v[j]);
                     } else {  // RED (fire-and-forget): the launch's one contribution per element
@@ -2113,6 +2115,7 @@ int try_hwgrad(const uint16_t *x1, int c1, const uint16_t *x2, int c2, const uin
     HWgrad p;
     memset(&p, 0, sizeof p);
     p.N = n; p.H = h; p.W = w; p.ct = c1 + c2; p.cout = cout; p.nchx = nch; p.dw = dw;
+    p.ow = ice::grad_overwrite() ? 1 : 0;
     const int kr = halve ? 1 : 2;  // output rows per K-block (HWGeom::KR)
     if (h % kr) return 1;
     p.total_kb = n * (h / kr) * (w / 64);
@@ -2183,7 +2186,8 @@ void take_bias_rows(DgradProb &p, const ice::RowSched &s, ice::Arena &ar) {
 }
 int finish_bias(const DgradProb &p, const ice::RowSched &s, cudaStream_t st) {
     if (!p.db1 && !p.db2) return 0;
-    const ice::ColSegs segs{{p.db1, p.db2, nullptr, nullptr}, {p.c1, p.c2, 0, 0}};
+    const int ow = ice::grad_overwrite() ? 1 : 0;
+    const ice::ColSegs segs{{p.db1, p.db2, nullptr, nullptr}, {p.c1, p.c2, 0, 0}, {ow, ow, 0, 0}};
     return ice::colsum_finish(p.bpart, s.G, p.c1 + p.c2, p.c1 + p.c2, segs, s, st);
 }
 }  // namespace
@@ -2360,7 +2364,8 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
         ice::count_launch();
         rc = (int)cudaGetLastError();
         if (rc || (!p.db1 && !p.db2)) return rc;
-        const ice::ColSegs segs{{p.db1, p.db2, nullptr, nullptr}, {c1, c2, 0, 0}};
+        const int ow = ice::grad_overwrite() ? 1 : 0;
+        const ice::ColSegs segs{{p.db1, p.db2, nullptr, nullptr}, {c1, c2, 0, 0}, {ow, ow, 0, 0}};
         return ice::colsum_finish(p.bpart, strips, ct, ct, segs, ice::RowSched{1, 1, 1, 1, 0}, st);
     }
     const bool m2 = conv_m2(mtiles, ct, bn, splits, total_kb);
@@ -2391,6 +2396,7 @@ extern "C" int ice_conv_wgrad(const uint16_t *x1, int32_t c1, const uint16_t *x2
     p.taps = make_taps(ksize);
     p.N = n; p.H = h; p.W = w; p.c1 = c1; p.c2 = c2; p.cout = cout;
     p.dw = dw;
+    p.ow = ice::grad_overwrite() ? 1 : 0;
     const int ncols = p.taps.n * (c1 + c2);
     int mtiles, ntiles, bn;
     wgrad_tiles(ncols, cout, p.trans, mtiles, ntiles, bn);
@@ -2524,6 +2530,7 @@ extern "C" int ice_halve_wgrad(const uint16_t *x, int32_t c, const uint16_t *dy_
     p.halve = 1;
     p.N = n; p.H = h; p.W = w; p.c1 = c; p.c2 = 0; p.cout = cout;
     p.dw = dw;
+    p.ow = ice::grad_overwrite() ? 1 : 0;
     const int ncols = 4 * c;
     int mtiles, ntiles, bn;
     wgrad_tiles(ncols, cout, p.trans, mtiles, ntiles, bn);

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(1024) colsum_kernel(const float *__restrict__ 
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if (c < segs.len[q]) {
-                if (segs.dst[q]) segs.dst[q][c] += t;
+                if (segs.dst[q]) segs.dst[q][c] = segs.ow[q] ? t : segs.dst[q][c] + t;
                 break;
             }
             c -= segs.len[q];
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(1024) colsum_kernel(const float *__restrict__ 
 
 // slices added in z order, then dst += (one thread per float4; loads issued 4 at a time)
 __device__ __forceinline__ void seq_sum4(const float4 *__restrict__ ws, int nsplit, size_t stride4, size_t i,
-                                         float4 *__restrict__ dst) {
+                                         float4 *__restrict__ dst, bool ow = false) {
     float4 a = __ldcg(ws + i);
     for (int z0 = 1; z0 < nsplit; z0 += 4) {
         float4 v[4];
@@ -75,6 +75,10 @@ __device__ __forceinline__ void seq_sum4(const float4 *__restrict__ ws, int nspl
                 a.w += v[q].w;
             }
     }
+    if (ow) {
+        dst[i] = a;
+        return;
+    }
     float4 d = dst[i];
     d.x += a.x;
     d.y += a.y;
@@ -86,16 +90,17 @@ __device__ __forceinline__ void seq_sum4(const float4 *__restrict__ ws, int nspl
 // up to SEQ_MAX slices: one thread per float4
 constexpr int SEQ_MAX = 64;
 __global__ void splitsum_kernel4(const float4 *__restrict__ ws, int nsplit, size_t stride4, size_t n4,
-                                 float4 *__restrict__ dst) {
+                                 float4 *__restrict__ dst, bool ow) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
-        seq_sum4(ws, nsplit, stride4, i, dst);
+        seq_sum4(ws, nsplit, stride4, i, dst, ow);
 }
 
 // many slices (the halo weight gradients split pixels 50-150 ways): block = 32 float4 columns
 // x 32 slice groups; thread (g, lane) adds slices g, g + 32, ... in order, then the group sums
 // are added in group order
 __global__ void __launch_bounds__(1024) splitsum_wide_kernel(const float4 *__restrict__ ws, int nsplit,
-                                                             size_t stride4, size_t n4, float4 *__restrict__ dst) {
+                                                             size_t stride4, size_t n4, float4 *__restrict__ dst,
+                                                             bool ow) {
     __shared__ float4 red[32][33];
     const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
     const size_t i = blockIdx.x * (size_t)32 + lane;
@@ -121,6 +126,10 @@ __global__ void __launch_bounds__(1024) splitsum_wide_kernel(const float4 *__res
             t.z += b.z;
             t.w += b.w;
         }
+        if (ow) {
+            dst[i] = t;
+            return;
+        }
         float4 d = dst[i];
         d.x += t.x;
         d.y += t.y;
@@ -131,11 +140,11 @@ __global__ void __launch_bounds__(1024) splitsum_wide_kernel(const float4 *__res
 }
 
 __global__ void splitsum_kernel1(const float *__restrict__ ws, int nsplit, size_t stride, size_t n,
-                                 float *__restrict__ dst) {
+                                 float *__restrict__ dst, bool ow) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         float a = __ldcg(ws + i);
         for (int z = 1; z < nsplit; ++z) a += __ldcg(ws + z * stride + i);
-        dst[i] += a;
+        dst[i] = ow ? a : dst[i] + a;
     }
 }
 
@@ -155,6 +164,7 @@ struct FItem {
     int nsplit;          // splitsum
     size_t stride, n;    // in float4 (F_SEQ4 / F_WIDE4) or float (F_SEQ1) units
     float *dst;
+    int ow;              // splitsum: dst = sum instead of dst += sum
 };
 constexpr int MAXF = 96;
 struct FBatch {
@@ -203,7 +213,7 @@ __global__ void __launch_bounds__(FNT) flush_kernel(const __grid_constant__ FBat
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 if (c < f.segs.len[q]) {
-                    if (f.segs.dst[q]) f.segs.dst[q][c] += t;
+                    if (f.segs.dst[q]) f.segs.dst[q][c] = f.segs.ow[q] ? t : f.segs.dst[q][c] + t;
                     break;
                 }
                 c -= f.segs.len[q];
@@ -235,12 +245,16 @@ __global__ void __launch_bounds__(FNT) flush_kernel(const __grid_constant__ FBat
                 t.w += v.w;
             }
             float4 *d = reinterpret_cast<float4 *>(f.dst) + j;
-            float4 o = *d;
-            o.x += t.x;
-            o.y += t.y;
-            o.z += t.z;
-            o.w += t.w;
-            *d = o;
+            if (f.ow) {
+                *d = t;
+            } else {
+                float4 o = *d;
+                o.x += t.x;
+                o.y += t.y;
+                o.z += t.z;
+                o.w += t.w;
+                *d = o;
+            }
         }
     } else if (f.kind == F_SEQ4) {  // == splitsum_kernel4, two float4 columns per thread (loads of both in flight)
         const size_t j0 = (size_t)lb * 2 * FNT + threadIdx.x, j1 = j0 + FNT;
@@ -263,20 +277,25 @@ __global__ void __launch_bounds__(FNT) flush_kernel(const __grid_constant__ FBat
                         b.x += vb[q].x; b.y += vb[q].y; b.z += vb[q].z; b.w += vb[q].w;
                     }
             }
-            float4 d = dst[j0], e = dst[j1];
-            d.x += a.x; d.y += a.y; d.z += a.z; d.w += a.w;
-            e.x += b.x; e.y += b.y; e.z += b.z; e.w += b.w;
-            dst[j0] = d;
-            dst[j1] = e;
+            if (f.ow) {
+                dst[j0] = a;
+                dst[j1] = b;
+            } else {
+                float4 d = dst[j0], e = dst[j1];
+                d.x += a.x; d.y += a.y; d.z += a.z; d.w += a.w;
+                e.x += b.x; e.y += b.y; e.z += b.z; e.w += b.w;
+                dst[j0] = d;
+                dst[j1] = e;
+            }
         } else if (j0 < f.n) {
-            seq_sum4(ws, f.nsplit, f.stride, j0, dst);
+            seq_sum4(ws, f.nsplit, f.stride, j0, dst, f.ow);
         }
     } else {  // F_SEQ1 == splitsum_kernel1
         const size_t j = (size_t)lb * FNT + threadIdx.x;
         if (j < f.n) {
             float a = __ldcg(f.src + j);
             for (int z = 1; z < f.nsplit; ++z) a += __ldcg(f.src + z * f.stride + j);
-            f.dst[j] += a;
+            f.dst[j] = f.ow ? a : f.dst[j] + a;
         }
     }
 }
@@ -324,6 +343,8 @@ int push_or_launch(const FItem &f) {
 }  // namespace
 
 static std::atomic<unsigned long long> g_launches{0};
+static bool g_grad_ow = false;
+bool grad_overwrite() { return g_grad_ow; }
 void count_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
 int colsum_finish(const float *P, int rows, int ld, int cols, const ColSegs &segs, const RowSched &sch,
@@ -346,7 +367,7 @@ int colsum_finish(const float *P, int rows, int ld, int cols, const ColSegs &seg
     return (int)cudaGetLastError();
 }
 
-int splitsum_finish(const float *ws, int nsplit, size_t stride, size_t n, float *dst, cudaStream_t st) {
+int splitsum_finish(const float *ws, int nsplit, size_t stride, size_t n, float *dst, cudaStream_t st, bool ow) {
     if (n == 0 || nsplit <= 0) return 0;
     const bool v4 = (stride % 4 == 0) && (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(ws) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
     auto grid = [](size_t work) {
@@ -360,6 +381,7 @@ int splitsum_finish(const float *ws, int nsplit, size_t stride, size_t n, float 
         f.src = ws;
         f.dst = dst;
         f.nsplit = nsplit;
+        f.ow = ow ? 1 : 0;
         if (!v4) {
             f.kind = F_SEQ1;
             f.stride = stride;
@@ -374,11 +396,11 @@ int splitsum_finish(const float *ws, int nsplit, size_t stride, size_t n, float 
         return push_or_launch(f);
     }
     if (!v4)
-        splitsum_kernel1<<<grid(n), 256, 0, st>>>(ws, nsplit, stride, n, dst);
+        splitsum_kernel1<<<grid(n), 256, 0, st>>>(ws, nsplit, stride, n, dst, ow);
     else if (nsplit <= SEQ_MAX)
-        splitsum_kernel4<<<grid(n / 4), 256, 0, st>>>(w4, nsplit, stride / 4, n / 4, d4);
+        splitsum_kernel4<<<grid(n / 4), 256, 0, st>>>(w4, nsplit, stride / 4, n / 4, d4, ow);
     else
-        splitsum_wide_kernel<<<(unsigned)((n / 4 + 31) / 32), 1024, 0, st>>>(w4, nsplit, stride / 4, n / 4, d4);
+        splitsum_wide_kernel<<<(unsigned)((n / 4 + 31) / 32), 1024, 0, st>>>(w4, nsplit, stride / 4, n / 4, d4, ow);
     count_launch();
     return (int)cudaGetLastError();
 }
@@ -429,4 +451,11 @@ extern "C" int ice_finish_flush(void *stream) {
         seen.insert(seen.end(), mine.begin(), mine.end());
     }
     return v.size() > lo ? launch_batch(v, lo, v.size(), st) : 0;
+}
+
+// Gradient overwrite mode (see include/icelabel_b200.h).
+extern "C" int ice_grad_overwrite(int32_t on) {
+    if (on != 0 && on != 1) return -1;
+    ice::g_grad_ow = on != 0;
+    return 0;
 }

@@ -48,7 +48,12 @@ struct Arena {
 struct ColSegs {
     float *dst[4];
     int len[4];
+    int ow[4];  // 1: dst = sum (the first gradient of a step after a non-zeroing optimizer step)
 };
+
+// Gradient overwrite mode (ice_grad_overwrite): while on, every gradient producer STORES its
+// contribution instead of adding it, so the optimizer step need not zero the gradients.
+bool grad_overwrite();
 
 // Which partial rows a column adds.  bn == 0: all rows.  Otherwise row b is the column sums
 // of CTA b of a persistent GEMM with G CTAs walking tiles t = b, b + G, ... (tile t ->
@@ -67,7 +72,8 @@ void count_launch(int n = 1);
 int colsum_finish(const float *P, int rows, int ld, int cols, const ColSegs &segs, const RowSched &sch,
                   cudaStream_t st);
 
-// dst[i] += sum_{z < nsplit} ws[z * stride + i] (in z order), i < n.
-int splitsum_finish(const float *ws, int nsplit, size_t stride, size_t n, float *dst, cudaStream_t st);
+// dst[i] += sum_{z < nsplit} ws[z * stride + i] (in z order), i < n  (ow: dst[i] = sum).
+int splitsum_finish(const float *ws, int nsplit, size_t stride, size_t n, float *dst, cudaStream_t st,
+                    bool ow = false);
 
 }  // namespace ice

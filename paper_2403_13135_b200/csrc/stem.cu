@@ -342,5 +342,5 @@ extern "C" int ice_stem_wgrad(const uint8_t *img, int32_t n, int32_t h, int32_t 
     ice::count_launch();
     const int rc = (int)cudaGetLastError();
     if (rc) return rc;
-    return ice::splitsum_finish(part, ctas, 4096, 4096, dw, st);
+    return ice::splitsum_finish(part, ctas, 4096, 4096, dw, st, ice::grad_overwrite());
 }

@@ -487,7 +487,7 @@ __global__ void dropout_scale_kernel(int count, float p, unsigned long long seed
 __global__ void adam_kernel(float *__restrict__ p, float *__restrict__ g, float *__restrict__ m, float *__restrict__ v,
                             long long n, float lr_corr, float omb1, float b2, float omb2, float eps, float bc2_sqrt,
                             uint16_t *__restrict__ out_bf16, const long long *__restrict__ step_dev, double lr,
-                            double b1d, double b2d) {
+                            double b1d, double b2d, bool zero_g) {
     if (step_dev) {  // bias corrections from the device step counter (CUDA-graph replays)
         const double t = (double)*step_dev;
         lr_corr = (float)(lr / (1.0 - pow(b1d, t)));
@@ -510,7 +510,7 @@ __global__ void adam_kernel(float *__restrict__ p, float *__restrict__ g, float 
         reinterpret_cast<float4 *>(p)[i] = pp;
         reinterpret_cast<float4 *>(m)[i] = mm;
         reinterpret_cast<float4 *>(v)[i] = vv;
-        reinterpret_cast<float4 *>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (zero_g) reinterpret_cast<float4 *>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (out_bf16) {
             uint2 o;
             o.x = (uint32_t)to_bf(pp.x) | ((uint32_t)to_bf(pp.y) << 16);
@@ -527,7 +527,7 @@ __global__ void adam_kernel(float *__restrict__ p, float *__restrict__ g, float 
         m[i] = me;
         v[i] = ve;
         p[i] = pe;
-        g[i] = 0.f;
+        if (zero_g) g[i] = 0.f;
         if (out_bf16) out_bf16[i] = to_bf(pe);
     }
 }
@@ -619,7 +619,8 @@ extern "C" int ice_maxpool_bwd(const uint16_t *x, const uint16_t *dpool, const u
     ice::count_launch();
     const int rc = (int)cudaGetLastError();
     if (rc || !dbias) return rc;
-    return ice::colsum_finish(part, (int)blocks, c, c, ice::ColSegs{{dbias, nullptr, nullptr, nullptr}, {c, 0, 0, 0}},
+    const int ow = ice::grad_overwrite() ? 1 : 0;
+    return ice::colsum_finish(part, (int)blocks, c, c, ice::ColSegs{{dbias, nullptr, nullptr, nullptr}, {c, 0, 0, 0}, {ow, 0, 0, 0}},
                               ice::RowSched{1, 1, 1, 1, 0}, st);
 }
 
@@ -642,7 +643,8 @@ extern "C" int ice_head_ce(const uint16_t *h, int64_t npx, int32_t hw, const uin
     ice::count_launch();
     const int rc = (int)cudaGetLastError();
     if (rc || !need) return rc;
-    const ice::ColSegs segs{{dw, db, zsum ? dzbias : nullptr, stats}, {3 * HC, 3, HC, 2}};
+    const int ow = ice::grad_overwrite() ? 1 : 0;  // gradients only: the loss statistics accumulate
+    const ice::ColSegs segs{{dw, db, zsum ? dzbias : nullptr, stats}, {3 * HC, 3, HC, 2}, {ow, ow, ow, 0}};
     return ice::colsum_finish(part, (int)blocks, HEAD_LD, HEAD_COLS, segs, ice::RowSched{1, 1, 1, 1, 0}, st);
 }
 
@@ -662,7 +664,8 @@ extern "C" int ice_bias_grad(const uint16_t *dz, int64_t rows, int32_t c, float 
     ice::count_launch();
     const int rc = (int)cudaGetLastError();
     if (rc) return rc;
-    return ice::colsum_finish(part, (int)blocks, c, c, ice::ColSegs{{db, nullptr, nullptr, nullptr}, {c, 0, 0, 0}},
+    const int ow = ice::grad_overwrite() ? 1 : 0;
+    return ice::colsum_finish(part, (int)blocks, c, c, ice::ColSegs{{db, nullptr, nullptr, nullptr}, {c, 0, 0, 0}, {ow, 0, 0, 0}},
                               ice::RowSched{1, 1, 1, 1, 0}, st);
 }
 
@@ -677,7 +680,8 @@ extern "C" int ice_dropout_scale(int32_t count, float p, uint64_t seed, const in
 }
 
 extern "C" int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64_t step, const int64_t *step_dev,
-                        double lr, double beta1, double beta2, double eps, uint16_t *out_bf16, void *stream) {
+                        double lr, double beta1, double beta2, double eps, int32_t zero_grad, uint16_t *out_bf16,
+                        void *stream) {
     if (!p || !g || !m || !v || n < 0 || (step < 1 && !step_dev)) return ICE_EINVAL;
     if (n == 0) return ICE_OK;
     // torch.optim.Adam (_single_tensor_adam): exp_avg.lerp_(g, 1 - b1); exp_avg_sq.mul_(b2)
@@ -690,7 +694,7 @@ extern "C" int ice_adam(float *p, float *g, float *m, float *v, int64_t n, int64
     const double bc2 = 1.0 - pow(beta2, t);
     adam_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, (cudaStream_t)stream>>>(
         p, g, m, v, n, (float)(lr / bc1), (float)(1.0 - beta1), (float)beta2, (float)(1.0 - beta2), (float)eps,
-        (float)sqrt(bc2), out_bf16, reinterpret_cast<const long long *>(step_dev), lr, beta1, beta2);
+        (float)sqrt(bc2), out_bf16, reinterpret_cast<const long long *>(step_dev), lr, beta1, beta2, zero_grad != 0);
     ice::count_launch();
     LAUNCH_CHECK();
 }

@@ -409,13 +409,20 @@ class UNetEngine:
         B, hw = h.shape[0], h.shape[1] * h.shape[2]
         st = _native.stream_handle()
         dz = A.dz_a[0] if train else None
-        _native.call("ice_head_ce", h.data_ptr(), B * hw, hw, labels.data_ptr(),
-                     self.w("out").data_ptr(), self.b("out").data_ptr(),
-                     _native.ptr(A.drop.get(f"up.{d - 1}")) if train else None, float(grad_scale),
-                     _native.ptr(dz), _native.ptr(self.w("out", self.grads)) if train else None,
-                     _native.ptr(self.b("out", self.grads)) if train else None, A.stats.data_ptr(),
-                     _native.ptr(logits), _native.ptr(self.b(f"up.{d - 1}.block.2", self.grads)) if train else None,
-                     st)
+        overwrite = train and self.grads_stale  # the head's gradients open the backward (see backward)
+        if overwrite:
+            _native.call("ice_grad_overwrite", 1)
+        try:
+            _native.call("ice_head_ce", h.data_ptr(), B * hw, hw, labels.data_ptr(),
+                         self.w("out").data_ptr(), self.b("out").data_ptr(),
+                         _native.ptr(A.drop.get(f"up.{d - 1}")) if train else None, float(grad_scale),
+                         _native.ptr(dz), _native.ptr(self.w("out", self.grads)) if train else None,
+                         _native.ptr(self.b("out", self.grads)) if train else None, A.stats.data_ptr(),
+                         _native.ptr(logits),
+                         _native.ptr(self.b(f"up.{d - 1}.block.2", self.grads)) if train else None, st)
+        finally:
+            if overwrite:
+                _native.call("ice_grad_overwrite", 0)
         return dz
 
     # ---- backward -----------------------------------------------------------------------
@@ -438,13 +445,30 @@ class UNetEngine:
     # a bf16 im2col buffer + GEMMs; float input always takes the im2col path.
     fused_stem = os.environ.get("ICE_FUSED_STEM", "1") != "0"  # A/B switch, read once
     side_flush = os.environ.get("ICE_SIDE_FLUSH", "1") != "0"  # A/B switch, read once
+    # The fused Adam leaves the gradients unzeroed ("stale"); the next backward then runs in
+    # gradient overwrite mode (every producer stores instead of adding): 4 B/param less for Adam
+    # and no read of the old value by the split-0 weight-gradient epilogues.
+    lazy_zero = os.environ.get("ICE_LAZY_ZERO", "1") != "0"  # A/B switch, read once
+    grads_stale = False
 
     def backward(self, A: _Acts, dz, on_layer_done=None) -> None:
         """Accumulate parameter gradients into self.grads (dz: dZ of up.{d-1}.block.2).
         on_layer_done(name) fires after each layer's gradient is complete (DP buckets); a
         callback that reads gradients before backward returns calls flush_deferred() first."""
-        if not self.defer_finish:
-            return self._backward(A, dz, on_layer_done)
+        overwrite = self.grads_stale  # the optimizer step left the gradients logically zero
+        self.grads_stale = False
+        if overwrite:
+            _native.call("ice_grad_overwrite", 1)
+        try:
+            if self.defer_finish:
+                self._backward_deferred(A, dz, on_layer_done)
+            else:
+                self._backward(A, dz, on_layer_done)
+        finally:
+            if overwrite:
+                _native.call("ice_grad_overwrite", 0)
+
+    def _backward_deferred(self, A: _Acts, dz, on_layer_done=None) -> None:
         _native.call("ice_finish_defer", 1)
         _native.scratch.begin_bump()
         self._side_events = []
@@ -567,16 +591,21 @@ class UNetEngine:
 
     def adam_slice(self, start: int, stop: int, step: int, lr: float, betas=(0.9, 0.999), eps: float = 1e-8,
                    stream=None) -> None:
-        """Fused Adam on flat elements [start, stop) (a gradient bucket); 4-element aligned."""
+        """Fused Adam on flat elements [start, stop) (a gradient bucket); 4-element aligned.
+        With lazy_zero the gradients are not zeroed: they become logically zero ("stale") and
+        the next backward writes them in overwrite mode (ice_grad_overwrite)."""
         st = _native.stream_handle(stream)
         off4, off2 = start * 4, start * 2
         _native.call("ice_adam", self.params.data_ptr() + off4, self.grads.data_ptr() + off4,
                      self.exp_avg.data_ptr() + off4, self.exp_avg_sq.data_ptr() + off4, stop - start, int(step),
                      self.step_dev.data_ptr(), float(lr), float(betas[0]), float(betas[1]), float(eps),
-                     self.wbf16.data_ptr() + off2, st)
+                     0 if self.lazy_zero else 1, self.wbf16.data_ptr() + off2, st)
+        if self.lazy_zero:
+            self.grads_stale = True
 
     def zero_grad(self) -> None:
         _native.call("ice_fill_f32", self.grads.data_ptr(), self.numel, 0.0, _native.stream_handle())
+        self.grads_stale = False
 
     def layer_slice(self, name):
         """(start, stop) of a layer's weight+bias in the flat buffers."""

@@ -126,7 +126,7 @@ def test_adam_matches_torch_optim():
         grad = (torch.randn(n, generator=g) * 10 ** (-step)).cuda()
         gk = grad.clone()
         _native.call("ice_adam", p.data_ptr(), gk.data_ptr(), m.data_ptr(), v.data_ptr(), n, step, None, 1e-3, 0.9,
-                     0.999, 1e-8, wb.data_ptr(), _native.stream_handle())
+                     0.999, 1e-8, 1, wb.data_ptr(), _native.stream_handle())
         ref.grad = grad
         opt.step()
         torch.cuda.synchronize()
