@@ -434,10 +434,29 @@ struct DgradProb {
         asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
     }
     // (register prefetch of the next tile's ReLU-reference rows measured slower: the
-    // extra in-flight loads contend with the epilogue's stores)
-    struct Pre {};
+    // extra in-flight loads contend with the epilogue's stores).  The packed ReLU-mask words
+    // (4 B per row and 32 channels) are prefetched for the next tile ahead of its accumulator
+    // wait, so the epilogue does not stall on their global-load latency.
+    struct Pre {
+        uint32_t b[4];
+    };
     template <int BN>
-    __device__ void pre_load(Pre &, int, int, int, int, int, int) const {}
+    __device__ void pre_load(Pre &pr, int row, int mt, int nt, int, int cc0, int cc1) const {
+#pragma unroll
+        for (int ci = 0; ci < 4; ++ci) pr.b[ci] = 0xffffffffu;
+        if (!rbits1) return;
+        int n0, h0, w0, n, h, w;
+        pt.origin(mt, n0, h0, w0);
+        pt.pixel(row, n0, h0, w0, n, h, w);
+        if (n >= N) return;
+        const size_t pix = ((size_t)n * H + h) * W + w;
+        constexpr int NCH = BN / 32, PER = (NCH + 1) / 2;
+#pragma unroll
+        for (int ci = 0; ci < PER && ci < 4; ++ci) {
+            const int cc = cc0 + ci, col = nt * BN + cc * 32;
+            if (cc < cc1 && col < c1) pr.b[ci] = __ldg(rbits1 + (size_t)(col >> 5) * ((size_t)N * H * W) + pix);
+        }
+    }
     template <int BN>
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int, int cc0, int cc1, float *bacc,
                              const Pre &pr, uint8_t *stage = nullptr, const uint8_t *ref_smem = nullptr) const {
@@ -482,7 +501,7 @@ struct DgradProb {
                     }
                 }
                 if (rbits1 && out == out1) {  // the forward's packed ReLU mask: 4 B instead of 64 B per row
-                    const uint32_t b = __ldg(rbits1 + (size_t)(col >> 5) * ((size_t)N * H * W) + pix);
+                    const uint32_t b = pr.b[ci];  // prefetched (pre_load)
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
                         if (!((b >> e) & 1u)) v[e] = 0.f;
