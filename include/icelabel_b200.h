@@ -197,7 +197,7 @@ int ice_halve_fprop(const uint16_t *x, int32_t c, int32_t n, int32_t h, int32_t 
  * dbias (may be NULL) += column sums of dx (fused bias gradient). */
 int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t n, int32_t h, int32_t w,
                     const uint16_t *wc, int32_t c, uint16_t *dx, const uint16_t *relu_ref,
-                    const float *drop_scale, float *dbias, void *scratch,
+                    const uint32_t *relu_bits, const float *drop_scale, float *dbias, void *scratch,
                     uint64_t *scratch_bytes, void *stream);
 
 /* Halving conv weight gradient: dw[cout][2][2][c] (fp32, caller-zeroed) +=

@@ -69,7 +69,7 @@ SIGNATURES = {
     "ice_conv_dgrad": [_V, _I32, _I32, _I32, _I32, _I32, _V, _I32, _I32, _V, _V, _V, _V, _V, _V, _V, _V, _I32,
                        _V, _V, _V, *_S, _V],
     "ice_halve_fprop": [_V, _I32, _I32, _I32, _I32, _V, _V, _I32, _V, *_S, _V],
-    "ice_halve_dgrad": [_V, _I32, _I32, _I32, _I32, _V, _I32, _V, _V, _V, _V, *_S, _V],
+    "ice_halve_dgrad": [_V, _I32, _I32, _I32, _I32, _V, _I32, _V, _V, _V, _V, _V, *_S, _V],
     "ice_halve_wgrad": [_V, _I32, _V, _I32, _I32, _I32, _I32, _V, *_S, _V],
     "ice_stem_im2col": [_V, _I32, _I32, _I32, _V, _V],
     "ice_stem_fprop": [_V, _I32, _I32, _I32, _V, _V, _V, _V, _V],

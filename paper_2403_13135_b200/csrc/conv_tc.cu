@@ -2495,8 +2495,8 @@ extern "C" int ice_halve_fprop(const uint16_t *x, int32_t c, int32_t n, int32_t 
 
 extern "C" int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t n, int32_t h, int32_t w,
                                const uint16_t *wc, int32_t c, uint16_t *dx, const uint16_t *relu_ref,
-                               const float *drop_scale, float *dbias, void *scratch, uint64_t *scratch_bytes,
-                               void *stream) {
+                               const uint32_t *relu_bits, const float *drop_scale, float *dbias, void *scratch,
+                               uint64_t *scratch_bytes, void *stream) {
     if (!encode_fn()) return ICE_ENODRIVER;
     if (!dy_planes || !wc || !dx || c <= 0 || c % 64 || cout <= 0 || cout % 64 || !shape_ok(n, h, w))
         return ICE_EINVAL;
@@ -2515,6 +2515,7 @@ extern "C" int ice_halve_dgrad(const uint16_t *dy_planes, int32_t cout, int32_t 
     p.N = n; p.H = h; p.W = w; p.c1 = c; p.c2 = 0; p.cout = cout;
     p.out1 = reinterpret_cast<bf16 *>(dx);
     p.ref1 = reinterpret_cast<const bf16 *>(relu_ref);
+    p.rbits1 = relu_bits;  // packed ReLU mask (4 B per 32 channels) instead of the bf16 reference
     p.drop1 = drop_scale;
     p.db1 = dbias;
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;

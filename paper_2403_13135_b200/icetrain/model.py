@@ -228,6 +228,8 @@ class _Acts:
         self.a1_bits = [bits(i, cp[i]) for i in range(d)]
         self.b1_bits = bits(d, cp[d])
         self.u1_bits = [bits(d - 1 - j, cp[d - 1 - j]) for j in range(d)]
+        # ... and of the up-block outputs that feed the next halving conv (its dgrad's ReLU mask)
+        self.u2_bits = [bits(d - 1 - j, cp[d - 1 - j]) for j in range(d - 1)]
         self.labels = torch.empty((B, H, W), dtype=torch.uint8, device=device)
         self.drop = {}  # block name -> fp32 [B][c_p] Dropout2d scales (train mode, p > 0)
 
@@ -397,7 +399,8 @@ class UNetEngine:
             n0, n2 = f"up.{j}.block.0", f"up.{j}.block.2"
             ops.conv_fprop(A.a2[L], self.wb16(n0), self.b(n0), x2=A.hv[j], relu=True, out=A.u1[j],
                            relu_bits=A.u1_bits[j])
-            ops.conv_fprop(A.u1[j], self.wb16(n2), self.b(n2), relu=True, drop=dr(f"up.{j}"), out=A.u2[j])
+            ops.conv_fprop(A.u1[j], self.wb16(n2), self.b(n2), relu=True, drop=dr(f"up.{j}"), out=A.u2[j],
+                           relu_bits=A.u2_bits[j] if j < d - 1 else None)
             x = A.u2[j]
         return A
 
@@ -543,8 +546,9 @@ class UNetEngine:
             dz = A.dz_a[L + 1]
             drop_prev = A.drop.get("bottleneck" if j == 0 else f"up.{j - 1}")
             prev_name = "bottleneck.block.2" if j == 0 else f"up.{j - 1}.block.2"
+            bits_prev = A.u2_bits[j - 1] if j > 0 else None  # (the bottleneck output keeps split-K: no bits)
             _native.call("ice_halve_dgrad", A.dhv[L].data_ptr(), hl.cout_p, B, s, s, self.halve_wc[hn].data_ptr(),
-                         hl.cin_p, dz.data_ptr(), xprev.data_ptr(), _native.ptr(drop_prev),
+                         hl.cin_p, dz.data_ptr(), xprev.data_ptr(), _native.ptr(bits_prev), _native.ptr(drop_prev),
                          self.b(prev_name, G).data_ptr(), st)
             done(hn)
         self._flush_side()  # the up path's finishers overlap the bottleneck and down path

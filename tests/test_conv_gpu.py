@@ -154,7 +154,18 @@ def test_halve_fprop_dgrad_wgrad(shape):
     dyp = _planes(dy)
     dbx = torch.zeros(c, device="cuda")
     _native.call("ice_halve_dgrad", dyp.data_ptr(), cout, n, h, w, wc.data_ptr(), c, dx.data_ptr(),
-                 ref_relu.data_ptr(), None, dbx.data_ptr(), st)
+                 ref_relu.data_ptr(), None, None, dbx.data_ptr(), st)
+    # the same through the packed ReLU mask (bit j of word k = channel 32 k + j > 0): identical
+    pos = (ref_relu.view(-1, c).float() > 0).to(torch.int64)
+    words = torch.stack([(pos[:, 32 * k:32 * k + 32] << torch.arange(32, device="cuda")).sum(1)
+                         for k in range(c // 32)])
+    bits = ((words + 2 ** 31) % 2 ** 32 - 2 ** 31).to(torch.int32).contiguous()
+    dx_b = torch.empty_like(dx)
+    dbx_b = torch.zeros(c, device="cuda")
+    _native.call("ice_halve_dgrad", dyp.data_ptr(), cout, n, h, w, wc.data_ptr(), c, dx_b.data_ptr(),
+                 None, bits.data_ptr(), None, dbx_b.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert torch.equal(dx_b, dx) and torch.equal(dbx_b, dbx)
     dw = torch.zeros(cout, 2, 2, c, device="cuda")
     _native.call("ice_halve_wgrad", x.data_ptr(), c, dyp.data_ptr(), cout, n, h, w, dw.data_ptr(), st)
     xin = nchw(x).requires_grad_(True)
