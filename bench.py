@@ -599,7 +599,7 @@ def main():
                                       "ms": round(seg_ms, 3),
                                       "roofline": {"bound": "hbm", "achieved": round(seg_gbs, 1), "peak": hbm,
                                                    "unit": "GB/s", "frac": round(seg_gbs / hbm, 4),
-                                                   "traffic": None, "note": "4 B/px (RGB in, label out)"}},
+                                                   "traffic": None, "note": "4 B/px (RGB in, label out); a 3:1 read-dominated stream can exceed the copy-measured peak (read+write of b.copy_(a))"}},
                      "corpus": "T-gray (headline); T-tint / T-rand below (SURVEY.md 8(d)), tile i = corpus[i mod 4224]",
                      **variants}
 

@@ -4,15 +4,16 @@
 # the round-2 kernels (deferred finisher batch, fused stem, max-pool backward) and K1.
 #   gpurun --timeout 3600 -- 'bash tools/gpu_profiles_r02.sh'
 mkdir -p gpurun_out
+P=${P:-r02f}
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
-[ -z "$ONLY" ] && timeout 900 ncu --metrics $M --clock-control none -c 3000 --csv --log-file gpurun_out/r02f_launches.csv \
-  python tools/profile_step.py --steps 3 > gpurun_out/r02f_launches.log 2>&1
-[ -z "$ONLY" ] && timeout 600 ncu --metrics $M --clock-control none -c 50 --csv --log-file gpurun_out/r02f_launches_al.csv \
-  python tools/profile_autolabel.py > gpurun_out/r02f_launches_al.log 2>&1
+[ -z "$ONLY" ] && timeout 900 ncu --metrics $M --clock-control none -c 3000 --csv --log-file gpurun_out/${P}_launches.csv \
+  python tools/profile_step.py --steps 3 > gpurun_out/${P}_launches.log 2>&1
+[ -z "$ONLY" ] && timeout 600 ncu --metrics $M --clock-control none -c 50 --csv --log-file gpurun_out/${P}_launches_al.csv \
+  python tools/profile_autolabel.py > gpurun_out/${P}_launches_al.log 2>&1
 F="ncu --set full --clock-control none --import-source on --kernel-name-base demangled"
 cap() {  # name regex skip   (ONLY="a b": just those captures)
   if [ -n "$ONLY" ] && [[ " $ONLY " != *" $1 "* ]]; then return; fi
-  timeout 600 $F -k "regex:$2" -s $3 -c 1 -o gpurun_out/r02f_$1 -f python tools/profile_step.py --steps 3 > gpurun_out/r02f_$1.log 2>&1
+  timeout 600 $F -k "regex:$2" -s $3 -c 1 -o gpurun_out/${P}_$1 -f python tools/profile_step.py --steps 3 > gpurun_out/${P}_$1.log 2>&1
 }
 cap flush "flush_kernel" 2
 cap stem_fprop "stem_fprop_kernel" 2
@@ -25,5 +26,5 @@ cap halo_fp64 "halo_gemm<.int.64, .int.1, .bool.1, .*FpropProb" 2
 cap halo_dg64 "halo_gemm<.int.64, .int.1, .bool.1, .*DgradProb" 2
 cap hwgrad64 "hwgrad_kernel<.int.64, .int.2, .int.2, .bool.0" 2
 cap fprop256 "conv_gemm<.int.256, .int.4, .*FpropProb" 20
-[ -z "$ONLY" ] && timeout 600 $F -k "regex:autolabel256" -s 1 -c 1 -o gpurun_out/r02f_autolabel256 -f python tools/profile_autolabel.py --reps 1 > gpurun_out/r02f_al.log 2>&1
+[ -z "$ONLY" ] && timeout 600 $F -k "regex:autolabel256" -s 1 -c 1 -o gpurun_out/${P}_autolabel256 -f python tools/profile_autolabel.py --reps 1 > gpurun_out/${P}_al.log 2>&1
 ls -la gpurun_out/*.ncu-rep

@@ -18,6 +18,8 @@ ap.add_argument("csv")
 ap.add_argument("--steps", type=int, default=0, help="0: count head_ce_kernel launches (one per step)")
 ap.add_argument("--out", default=None)
 ap.add_argument("--traffic", default=None)
+ap.add_argument("--after", default="adam_kernel",
+                help="count only launches after the first launch whose name contains this (skips setup + step 1)")
 ap.add_argument("--al-tiles", type=int, default=1024, help="tiles per autolabel256 launch (bench --corpus)")
 a = ap.parse_args()
 
@@ -43,6 +45,11 @@ def short(n):
     return n.split("(")[0] if "(" in n and "<" not in n.split("(")[0][-2:] else n[: n.find(">(") + 1] if ">(" in n else n[:60]
 
 
+if a.after:
+    names = [d["name"] for d in launch.values()]
+    first = next((i for i, n in enumerate(names) if a.after in n), None)
+    if first is not None:
+        launch = collections.OrderedDict(list(launch.items())[first + 1:])
 if a.steps <= 0:
     a.steps = max(1, sum(1 for d in launch.values() if "head_ce_kernel" in d["name"]))
 agg = collections.OrderedDict()
@@ -60,7 +67,7 @@ for k, g in sorted(agg.items(), key=lambda kv: -kv[1]["ns"]):
     print(f"{g['launches'] / a.steps:6.1f} x {g['ns'] / 1e6 / a.steps:8.3f} ms {100 * g['ns'] / tot:5.1f}%  "
           f"{g['dram_bytes'] / g['launches'] / 1e6:9.1f} MB/launch  {k}")
 if a.out:
-    json.dump({"source": a.csv, "steps": a.steps, "kernels": rows}, open(a.out, "w"), indent=1)
+    json.dump({"source": a.csv, "steps": a.steps, "after_first": a.after, "kernels": rows}, open(a.out, "w"), indent=1)
 wg = [g for k, g in agg.items() if "WgradProb" in k or "hwgrad_kernel" in k]
 if a.traffic and wg and any(g["dram_bytes"] for g in wg):
     n = sum(g["launches"] for g in wg)
