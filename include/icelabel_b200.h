@@ -83,6 +83,11 @@ int ice_finish_flush(void *stream);
  * split-K weight gradients need not read the old value.  Process-wide; not thread-safe. */
 int ice_grad_overwrite(int32_t on);
 
+/* Re-read the convolution tiling switches (ICE_CONV_M2, ICE_WG_M2, ICE_NO_SPLITK, ... -- tuning
+ * and test hooks; the defaults are the measured-best tilings) from the environment.  They are
+ * read once when the library loads; a test that sets them calls this before and after. */
+int ice_conv_reload_knobs(void);
+
 /* Fused auto-label kernel (K1): replaces engine.process_tile (engine.py:145-160) =
  * cloudfilter.apply_filter (cloudfilter.py:99-117) + segmentation.segment
  * (segmentation.py:118-128) over a batch of n tiles, plus per-class counts (new).

@@ -53,6 +53,7 @@ SIGNATURES = {
     "ice_finish_defer": [_I32],
     "ice_finish_flush": [_V],
     "ice_grad_overwrite": [_I32],
+    "ice_conv_reload_knobs": [],
     "ice_autolabel_scene": [_V, _I64, _I32, _I32, ctypes.POINTER(IceFilterCfg), ctypes.POINTER(IceScheme),
                             _V, _V, _V, _V, _V, _V, *_S, _V],
     "ice_cut_tiles": [_V, _I32, _I32, _I32, _I32, _V, _V],

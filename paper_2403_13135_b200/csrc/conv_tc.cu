@@ -1833,33 +1833,32 @@ const int8_t HALVE_CLS[9] = {0, 1, 1, 2, 2, 3, 3, 3, 3};
 const int8_t HALVE_DY[9] = {0, 0, 0, 0, 1, 0, 0, 1, 1};
 const int8_t HALVE_DX[9] = {0, 0, 1, 0, 0, 0, 1, 0, 1};
 
-// A/B switches of the tiling heuristics (test / tuning hooks), read once when the library is
-// first used; the defaults are the measured-best choices.
+// A/B switches of the tiling heuristics (test / tuning hooks), read when the library is first
+// used and again on ice_conv_reload_knobs(); the defaults are the measured-best choices.
 struct Knobs {
     bool no_dual, no_stage, no_splitk, no_wgrad_trans256, no_ref_tma, no_halo_wgrad, no_halve_merge;
     int conv_m2, wg_m2;  // -1 = automatic, 0 / 1 forced
 };
-const Knobs &knobs() {
-    static const Knobs k = [] {
-        auto flag = [](const char *n) { return getenv(n) != nullptr; };
-        auto tri = [](const char *n) {
-            const char *e = getenv(n);
-            return e ? (atoi(e) != 0 ? 1 : 0) : -1;
-        };
-        Knobs r;
-        r.no_dual = flag("ICE_NO_DUAL");
-        r.no_stage = flag("ICE_NO_STAGE");
-        r.no_splitk = flag("ICE_NO_SPLITK");
-        r.no_wgrad_trans256 = flag("ICE_NO_WGRAD_TRANS256");
-        r.no_ref_tma = flag("ICE_NO_REF_TMA");
-        r.no_halo_wgrad = flag("ICE_NO_HALO_WGRAD");
-        r.no_halve_merge = flag("ICE_NO_HALVE_MERGE");
-        r.conv_m2 = tri("ICE_CONV_M2");
-        r.wg_m2 = tri("ICE_WG_M2");
-        return r;
-    }();
-    return k;
+Knobs read_knobs() {
+    auto flag = [](const char *n) { return getenv(n) != nullptr; };
+    auto tri = [](const char *n) {
+        const char *e = getenv(n);
+        return e ? (atoi(e) != 0 ? 1 : 0) : -1;
+    };
+    Knobs r;
+    r.no_dual = flag("ICE_NO_DUAL");
+    r.no_stage = flag("ICE_NO_STAGE");
+    r.no_splitk = flag("ICE_NO_SPLITK");
+    r.no_wgrad_trans256 = flag("ICE_NO_WGRAD_TRANS256");
+    r.no_ref_tma = flag("ICE_NO_REF_TMA");
+    r.no_halo_wgrad = flag("ICE_NO_HALO_WGRAD");
+    r.no_halve_merge = flag("ICE_NO_HALVE_MERGE");
+    r.conv_m2 = tri("ICE_CONV_M2");
+    r.wg_m2 = tri("ICE_WG_M2");
+    return r;
 }
+Knobs g_knobs = read_knobs();
+const Knobs &knobs() { return g_knobs; }
 
 // (settle the scratch arena: answer a size query or reject a too-small buffer before any launch)
 #define ICE_SETTLE(ar)                                           \
@@ -2210,6 +2209,11 @@ int finish_bias(const DgradProb &p, const ice::RowSched &s, cudaStream_t st) {
     return ice::colsum_finish(p.bpart, s.G, p.c1 + p.c2, p.c1 + p.c2, segs, s, st);
 }
 }  // namespace
+
+extern "C" int ice_conv_reload_knobs(void) {
+    g_knobs = read_knobs();
+    return ICE_OK;
+}
 
 // merged halving-conv weights wm[(cls * cout + co)][t][ci] (t = 2 dy + dx) from the 9 combined
 // slabs wc[co][slab][ci] (ice_halve_prep); taps a class does not use are zero

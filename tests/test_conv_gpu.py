@@ -92,11 +92,25 @@ M2_SHAPES = [(33, 8, 8, 128, 128, 512, 3), (8, 8, 8, 256, 256, 512, 3), (6, 16, 
              (3, 32, 32, 128, 0, 256, 3), (5, 16, 16, 512, 512, 512, 3)]
 
 
+@pytest.fixture
+def conv_knobs(monkeypatch):
+    """Set tiling switches (read by the library at load and on ice_conv_reload_knobs) for one
+    test; the defaults come back afterwards."""
+    from paper_2403_13135_b200 import _native
+
+    def set_knobs(**kv):
+        for k, v in kv.items():
+            monkeypatch.setenv(k, v)
+        _native.call("ice_conv_reload_knobs")
+
+    yield set_knobs
+    monkeypatch.undo()
+    _native.call("ice_conv_reload_knobs")
+
+
 @pytest.mark.parametrize("shape", M2_SHAPES, ids=str)
-def test_m2_tiles_forced(shape, monkeypatch):
-    monkeypatch.setenv("ICE_CONV_M2", "1")
-    monkeypatch.setenv("ICE_WG_M2", "1")
-    monkeypatch.setenv("ICE_NO_SPLITK", "1")  # the 256-row path runs unsplit
+def test_m2_tiles_forced(shape, conv_knobs):
+    conv_knobs(ICE_CONV_M2="1", ICE_WG_M2="1", ICE_NO_SPLITK="1")  # the 256-row path runs unsplit
     test_fprop(shape)
     test_dgrad(shape)
     test_wgrad(shape)
@@ -240,11 +254,27 @@ def test_relu_bits_roundtrip(shape):
     assert rel(db_a, db_b) < 1e-5
 
 
+# every tiling switch off in turn (the alternate paths they select stay correct): a halo shape
+# with a concat input, a 256-wide GEMM shape that splits K, a (tap, cin) width of 1152, and
+# a halving conv on the merged-class tiling
+KNOBS = ["ICE_NO_DUAL", "ICE_NO_STAGE", "ICE_NO_SPLITK", "ICE_NO_WGRAD_TRANS256", "ICE_NO_REF_TMA",
+         "ICE_NO_HALO_WGRAD", "ICE_NO_HALVE_MERGE"]
+
+
+@pytest.mark.parametrize("knob", KNOBS)
+def test_tiling_switches(knob, conv_knobs):
+    conv_knobs(**{knob: "1"})
+    for shape in [(1, 4, 256, 64, 64, 64, 3), (8, 8, 8, 256, 256, 512, 3), (2, 16, 16, 128, 0, 256, 3)]:
+        test_fprop(shape)
+        test_dgrad(shape)
+        test_wgrad(shape)
+    test_halve_fprop_dgrad_wgrad((2, 64, 64, 128, 64))
+
+
 @pytest.mark.parametrize("shape", [(32, 32, 32, 512, 256), (32, 64, 64, 128, 64), (16, 16, 16, 1024, 512)], ids=str)
-def test_halve_m2_tiles_forced(shape, monkeypatch):
+def test_halve_m2_tiles_forced(shape, conv_knobs):
     """Halving conv with 256-row tiles forced on (256x256 and 256x128 dgrad tiles, 256-row wgrad)."""
-    monkeypatch.setenv("ICE_CONV_M2", "1")
-    monkeypatch.setenv("ICE_WG_M2", "1")
+    conv_knobs(ICE_CONV_M2="1", ICE_WG_M2="1")
     test_halve_fprop_dgrad_wgrad(shape)
 
 
