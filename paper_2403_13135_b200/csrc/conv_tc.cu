@@ -946,7 +946,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (tc::issuer(lane)) {
             constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, P::A_MN, P::B_MN);
             int it = 0, local = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
@@ -969,11 +969,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
                     const uint64_t bd0 = tc::sw128_desc(tc::smem_u32(sb + s * B_BYTES), P::B_MN ? 8192 : 16, 1024);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        tc::umma_f16(d, ad0 + (P::A_MN ? 128 : 2) * k, bd0 + (P::B_MN ? 128 : 2) * k, idesc,
+                        tc::mma(d, ad0 + (P::A_MN ? 128 : 2) * k, bd0 + (P::B_MN ? 128 : 2) * k, idesc,
                                      (i | k) != 0 ? 1u : 0u);
-                    tc::umma_commit(&empty[s]);
+                    tc::mma_commit(&empty[s]);
                 }
-                tc::umma_commit(&tfull[acc]);
+                tc::mma_commit(&tfull[acc]);
             }
         }
         __syncwarp();
@@ -1099,7 +1099,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (tc::issuer(lane)) {
             constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, P::A_MN, P::B_MN);
             int it = 0, local = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
@@ -1114,8 +1114,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
                 tc::tc_fence_after();
 #ifdef ICE_CONV_PROF
                 long long q1 = clock64();
-                atomicAdd(&g_conv_prof[0], (unsigned long long)(q1 - q0));
-                atomicAdd(&g_conv_prof[3], 1ull);
+                if (lane == 0) {
+                    atomicAdd(&g_conv_prof[0], (unsigned long long)(q1 - q0));
+                    atomicAdd(&g_conv_prof[3], 1ull);
+                }
 #endif
                 const uint32_t d = tmem + acc * 2 * BN;
                 for (int i = 0; i < nkb; ++i, ++it) {
@@ -1127,8 +1129,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
                     tc::tc_fence_after();
 #ifdef ICE_CONV_PROF
                     const long long w1 = clock64();
-                    atomicAdd(&g_conv_prof[1], (unsigned long long)(w1 - w0));
-                    atomicAdd(&g_conv_prof[4], 1ull);
+                    if (lane == 0) {
+                        atomicAdd(&g_conv_prof[1], (unsigned long long)(w1 - w0));
+                        atomicAdd(&g_conv_prof[4], 1ull);
+                    }
 #endif
                     const uint64_t a0 = tc::sw128_desc(tc::smem_u32(sa + s * AB), P::A_MN ? 8192 : 16, 1024);
                     const uint64_t a1 = tc::sw128_desc(tc::smem_u32(sa + s * AB + A_BYTES), P::A_MN ? 8192 : 16, 1024);
@@ -1136,12 +1140,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
                         const uint64_t bk = b0 + (P::B_MN ? 128 : 2) * k;
-                        tc::umma_f16(d, a0 + (P::A_MN ? 128 : 2) * k, bk, idesc, (i | k) != 0 ? 1u : 0u);
-                        tc::umma_f16(d + BN, a1 + (P::A_MN ? 128 : 2) * k, bk, idesc, (i | k) != 0 ? 1u : 0u);
+                        tc::mma(d, a0 + (P::A_MN ? 128 : 2) * k, bk, idesc, (i | k) != 0 ? 1u : 0u);
+                        tc::mma(d + BN, a1 + (P::A_MN ? 128 : 2) * k, bk, idesc, (i | k) != 0 ? 1u : 0u);
                     }
-                    tc::umma_commit(&empty[s]);
+                    tc::mma_commit(&empty[s]);
                 }
-                tc::umma_commit(&tfull[acc]);
+                tc::mma_commit(&tfull[acc]);
             }
         }
         __syncwarp();
@@ -1313,7 +1317,7 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
         // MMA only when the previous one is nearly done, so an issuer's per-tile barrier waits
         // and bookkeeping would idle it; issuer i owns the CTA's tiles j = i mod 2 together
         // with A slot i and accumulator i, and the other issuer's MMAs fill its gaps.
-        if (lane == 0) {
+        if (tc::issuer(lane)) {
             constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, false, P::B_MN);
             const int iss = warp == 1 ? 0 : 1;
             uint32_t voff[9];
@@ -1335,15 +1339,15 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
                     const uint64_t bd = bdesc + tap * (B_TAP >> 4);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        tc::umma_f16(d, ad + 2 * k, bd + (P::B_MN ? 128 : 2) * k, idesc, (tap | k) != 0 ? 1u : 0u);
+                        tc::mma(d, ad + 2 * k, bd + (P::B_MN ? 128 : 2) * k, idesc, (tap | k) != 0 ? 1u : 0u);
                 }
-                tc::umma_commit(&aempty[iss]);
-                tc::umma_commit(&tfull[iss]);
+                tc::mma_commit(&aempty[iss]);
+                tc::mma_commit(&tfull[iss]);
             }
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (tc::issuer(lane)) {
             constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, false, P::B_MN);
             // per-tap window offsets in descriptor units (128 B halo rows), hoisted out of the
             // tile loop: a constant-bank load chain per tap would stall every tap's first MMA
@@ -1388,21 +1392,21 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
                             const uint64_t bd = bdesc + q * (B_TAP >> 4);
 #pragma unroll
                             for (int k = 0; k < BK / 16; ++k)
-                                tc::umma_f16(d, ad + 2 * k, bd + (P::B_MN ? 128 : 2) * k, idesc,
+                                tc::mma(d, ad + 2 * k, bd + (P::B_MN ? 128 : 2) * k, idesc,
                                              (ch | tap | k) != 0 ? 1u : 0u);
                         }
                         if (!RES) {
-                            tc::umma_commit(&bempty[bs]);
+                            tc::mma_commit(&bempty[bs]);
                             ++bit;
                         }
                     }
-                    tc::umma_commit(&aempty[as]);
+                    tc::mma_commit(&aempty[as]);
                 }
-                tc::umma_commit(&tfull[acc]);
+                tc::mma_commit(&tfull[acc]);
                 if (RES) {  // last tile of this column run: release the resident weights
                     int nmt, nnt = -1, nz;
                     if (t + (int)gridDim.x < ntiles) g.coords(t + gridDim.x, nmt, nnt, nz);
-                    if (nnt != nt) tc::umma_commit(&bempty[0]);
+                    if (nnt != nt) tc::mma_commit(&bempty[0]);
                 }
             }
         }
@@ -1584,7 +1588,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (tc::issuer(lane)) {
             constexpr uint32_t idesc = tc::idesc_bf16(BM, COUT, true, true);
             int it = 0, local = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++local) {
@@ -1616,14 +1620,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) hwgrad_kernel(const __grid_consta
                                 const uint64_t bd = tc::sw128_desc(bbase + orow * 8192, 8192 * G::KR, 1024);
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
-                                    tc::umma_f16(d, ad + 128 * k, bd + 128 * k, idesc,
+                                    tc::mma(d, ad + 128 * k, bd + 128 * k, idesc,
                                                  (kb > kb0 || cls > 0 || orow > 0 || k > 0) ? 1u : 0u);
                             }
                         }
                     }
-                    tc::umma_commit(&empty[s]);
+                    tc::mma_commit(&empty[s]);
                 }
-                tc::umma_commit(tfull);
+                tc::mma_commit(tfull);
             }
         }
         __syncwarp();

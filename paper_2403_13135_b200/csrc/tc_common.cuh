@@ -99,6 +99,40 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
                  : "memory");
 }
 
+// MMA issue from a whole warp.  A chain issued by lane 0 inside a divergent `if (lane == 0)`
+// gets every tcgen05.mma wrapped in an ELECT / BRA.U.ANY waterfall with its operands moved
+// through R2UR: 60 cycles per 128x64x16 MMA with per-MMA descriptor math against 48 when the
+// whole warp runs the loop in uniform control flow and elect.sync picks the issuing lane
+// (tools/probe/issue_probe.cu; N >= 128 MMAs are tensor-bound either way).
+#ifndef ICE_WARP_ISSUE
+#define ICE_WARP_ISSUE 1
+#endif
+constexpr bool WARP_ISSUE = ICE_WARP_ISSUE;
+__device__ __forceinline__ bool issuer(int lane) { return WARP_ISSUE || lane == 0; }
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                    uint32_t accumulate) {
+    if (WARP_ISSUE) {
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+    } else {
+        umma_f16(tmem_d, adesc, bdesc, idesc, accumulate);
+    }
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    if (WARP_ISSUE) {
+        asm volatile(
+            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+            : "memory");
+    } else {
+        umma_commit(bar);
+    }
+}
+
 // 32 lanes x 32 consecutive fp32 columns (one row per thread)
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
