@@ -1205,11 +1205,24 @@ constexpr int HALO_TX = HALO_ROWS * 128;        // bytes a halo load delivers
 constexpr int HALO_BYTES = (HALO_TX + 1023) / 1024 * 1024;
 
 constexpr int TAPS_PER_SLOT = 3;
+// PAIR tiles: two 128-pixel tiles of consecutive rows (same columns) share every weight stage.
+// Their halo is ONE 4 x 130-pixel slab (rows h0-1 .. h0+2; sub-tile s reads windows s rows
+// lower), so per 256 pixels the weights are streamed once instead of twice and the halo is
+// 4 rows instead of 6: for the 128-wide streamed-weight tiles the shared-memory traffic per
+// MAC (operand reads + TMA writes + staged stores) drops ~16%, and that traffic is what bounds
+// them.  Weights then stream one tap per stage (the two halo buffers take 130 KB).
+constexpr int HALO4_TX = 4 * 130 * 128;
+// first 128-pixel tile (row tile index of PixTile: w fastest, then h, then n) of pair tile u:
+// rows 2k and 2k + 1 of an image are tiles t0 and t0 + tw
+__device__ __forceinline__ int pair_first(int u, const PixTile &pt) {
+    return ((u >> lg2(pt.tw)) << (lg2(pt.tw) + 1)) | (u & (pt.tw - 1));
+}
+constexpr int HALO4_BYTES = (HALO4_TX + 1023) / 1024 * 1024;
 constexpr int REF_BYTES = 128 * 128;  // staged ReLU-reference tile: 128 px x 64 ch bf16  // one kernel row per weight stage: 12 MMAs per barrier wait
 
-template <int BN, int BSTAGES, bool RES>
+template <int BN, int BSTAGES, bool RES, bool PAIR = false>
 constexpr int halo_smem_bytes(bool refs = false) {
-    return 1024 + 2 * HALO_BYTES + (RES ? 9 : BSTAGES * TAPS_PER_SLOT) * BN * BK * 2 +
+    return 1024 + 2 * (PAIR ? HALO4_BYTES : HALO_BYTES) + (RES ? 9 : BSTAGES * (PAIR ? 1 : TAPS_PER_SLOT)) * BN * BK * 2 +
            (((BN == 64 && RES) || BN == 128) ? EPI_WARPS * STAGE_BUFS * STAGE_BYTES : 0) +
            ((BN == 64 && RES && refs) ? 2 * REF_BYTES : 0) +
            (2 * 2 + 2 * BSTAGES + 6 + 4) * 8 + 16 + BIAS_SLOTS * BN * 4;
@@ -1218,18 +1231,22 @@ constexpr int halo_smem_bytes(bool refs = false) {
 // RES (resident weights): single-chunk problems (64 input channels) keep all 9 weight taps
 // of the current column tile in smem; they are reloaded only when the persistent CTA moves
 // to another column tile, so the MMA thread waits once per tile (36 MMAs per wait).
-template <int BN, int BSTAGES, bool RES, class P, bool DUAL>
+template <int BN, int BSTAGES, bool RES, class P, bool DUAL, bool PAIR = false>
 __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const __grid_constant__ P p, const TileGrid g) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    static_assert(!PAIR || (!RES && !DUAL), "pair tiles stream their weights");
+    constexpr int NSUB = PAIR ? 2 : 1;                 // 128-pixel sub-tiles per tile
+    constexpr int TPS = PAIR ? 1 : TAPS_PER_SLOT;      // weight taps per stage
+    constexpr int HB = PAIR ? HALO4_BYTES : HALO_BYTES, HTX = PAIR ? HALO4_TX : HALO_TX;
     constexpr int B_TAP = BN * BK * 2;
-    constexpr int B_BYTES = RES ? 9 * B_TAP : TAPS_PER_SLOT * B_TAP;
+    constexpr int B_BYTES = RES ? 9 * B_TAP : TPS * B_TAP;
     constexpr int NBS = RES ? 1 : BSTAGES;
     // BN = 64 resident-weight tiles stage each warp's 32 x 32 output box in shared memory and
     // write it with a TMA store (per-lane 64-B row stores were the epilogue's bottleneck)
     constexpr bool STAGE = (BN == 64 && RES) || BN == 128;
-    uint8_t *sa = base;                    // [2][HALO_BYTES]
-    uint8_t *sb = base + 2 * HALO_BYTES;   // [NBS][B_BYTES]
+    uint8_t *sa = base;            // [2][HB]
+    uint8_t *sb = base + 2 * HB;   // [NBS][B_BYTES]
     uint8_t *sst = sb + NBS * B_BYTES;     // [EPI_WARPS][STAGE_BUFS][STAGE_BYTES] when STAGE
     // ... and TMA-stage the tile's ReLU reference (dgrad) for the epilogue
     constexpr bool REFS = BN == 64 && RES && P::STAGE_REF;
@@ -1266,7 +1283,7 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
         tc::fence_barrier_init();
     }
     if (warp == 0 && lane == 0) p.prefetch();
-    if (warp == 1) tc::tmem_alloc<2 * BN>(tslot);
+    if (warp == 1) tc::tmem_alloc<2 * BN * NSUB>(tslot);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
@@ -1297,16 +1314,16 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
 #ifdef ICE_EXP_NOTMA
                     tc::mbar_arrive(&afull[as]);
 #else
-                    tc::mbar_expect_tx(&afull[as], HALO_TX);
-                    p.load_halo(ch, sa + as * HALO_BYTES, &afull[as], mt);
+                    tc::mbar_expect_tx(&afull[as], HTX);
+                    p.load_halo(ch, sa + as * HB, &afull[as], PAIR ? pair_first(mt, p.pt) : mt);
 #endif
                     if (RES) continue;
-                    for (int r = 0; r < 9 / TAPS_PER_SLOT; ++r, ++bit) {
+                    for (int r = 0; r < 9 / TPS; ++r, ++bit) {
                         const int bs = bit % BSTAGES;
                         tc::mbar_wait(&bempty[bs], ((bit / BSTAGES) & 1) ^ 1);
                         tc::mbar_expect_tx(&bfull[bs], B_BYTES);
-                        for (int q = 0; q < TAPS_PER_SLOT; ++q)
-                            p.template load_tap_b<BN>(r * TAPS_PER_SLOT + q, ch, sb + bs * B_BYTES + q * B_TAP,
+                        for (int q = 0; q < TPS; ++q)
+                            p.template load_tap_b<BN>(r * TPS + q, ch, sb + bs * B_BYTES + q * B_TAP,
                                                       &bfull[bs], nt);
                     }
                 }
@@ -1323,7 +1340,7 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
             uint32_t voff[9];
 #pragma unroll
             for (int tap = 0; tap < 9; ++tap) voff[tap] = p.view_row(tap) * 8;
-            const uint64_t adesc = tc::sw128_desc(tc::smem_u32(sa + iss * HALO_BYTES), 16, 1024);
+            const uint64_t adesc = tc::sw128_desc(tc::smem_u32(sa + iss * HB), 16, 1024);
             const uint64_t bdesc = tc::sw128_desc(tc::smem_u32(sb), P::B_MN ? 8192 : 16, 1024);
             const uint32_t d = tmem + iss * BN;
             tc::mbar_wait(&bfull[0], 0);
@@ -1366,18 +1383,18 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
                 const int acc = local & 1;
                 tc::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
                 tc::tc_fence_after();
-                const uint32_t d = tmem + acc * BN;
+                const uint32_t d = tmem + acc * BN * NSUB;
                 for (int ch = 0; ch < nch; ++ch, ++ait) {
                     const int as = ait & 1;
                     tc::mbar_wait(&afull[as], (ait >> 1) & 1);
                     tc::tc_fence_after();
-                    const uint64_t adesc = tc::sw128_desc(tc::smem_u32(sa + as * HALO_BYTES), 16, 1024);
+                    const uint64_t adesc = tc::sw128_desc(tc::smem_u32(sa + as * HB), 16, 1024);
 #pragma unroll
-                    for (int r = 0; r < 9 / TAPS_PER_SLOT; ++r) {
+                    for (int r = 0; r < 9 / TPS; ++r) {
                         int bs = 0;
                         uint32_t bslot;
                         if (RES) {
-                            bslot = tc::smem_u32(sb + r * TAPS_PER_SLOT * B_TAP);
+                            bslot = tc::smem_u32(sb + r * TPS * B_TAP);
                         } else {
                             bs = bit % BSTAGES;
                             tc::mbar_wait(&bfull[bs], (bit / BSTAGES) & 1);
@@ -1386,14 +1403,17 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
                         }
                         const uint64_t bdesc = tc::sw128_desc(bslot, P::B_MN ? 8192 : 16, 1024);
 #pragma unroll
-                        for (int q = 0; q < TAPS_PER_SLOT; ++q) {
-                            const int tap = r * TAPS_PER_SLOT + q;
-                            const uint64_t ad = adesc + voff[tap];
+                        for (int q = 0; q < TPS; ++q) {
+                            const int tap = r * TPS + q;
                             const uint64_t bd = bdesc + q * (B_TAP >> 4);
 #pragma unroll
-                            for (int k = 0; k < BK / 16; ++k)
-                                tc::mma(d, ad + 2 * k, bd + (P::B_MN ? 128 : 2) * k, idesc,
-                                             (ch | tap | k) != 0 ? 1u : 0u);
+                            for (int sub = 0; sub < NSUB; ++sub) {  // sub-tile sub: windows sub rows lower
+                                const uint64_t ad = adesc + voff[tap] + sub * 130 * 8;
+#pragma unroll
+                                for (int k = 0; k < BK / 16; ++k)
+                                    tc::mma(d + sub * BN, ad + 2 * k, bd + (P::B_MN ? 128 : 2) * k, idesc,
+                                            (ch | tap | k) != 0 ? 1u : 0u);
+                            }
                         }
                         if (!RES) {
                             tc::mma_commit(&bempty[bs]);
@@ -1422,7 +1442,7 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
         if (blockIdx.x < (unsigned)ntiles) {
             int mt, nt, z;
             g.coords(blockIdx.x, mt, nt, z);
-            p.template pre_load<BN>(pre, sub * 32 + lane, mt, nt, z, cc0, cc1);
+            p.template pre_load<BN>(pre, sub * 32 + lane, PAIR ? pair_first(mt, p.pt) : mt, nt, z, cc0, cc1);
         }
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
             int mt, nt, z;
@@ -1434,22 +1454,31 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
                 }
                 cur_nt = nt;
             }
-            const typename P::Pre cur = pre;
-            if (t + (int)gridDim.x < ntiles) {  // next tile's epilogue operands, ahead of the wait
-                int mt2, nt2, z2;
-                g.coords(t + gridDim.x, mt2, nt2, z2);
-                p.template pre_load<BN>(pre, sub * 32 + lane, mt2, nt2, z2, cc0, cc1);
-            }
             const int acc = local & 1;
-            tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
-            tc::tc_fence_after();
-            if (REFS && stage_ref) tc::mbar_wait(&rfull[acc], (local >> 1) & 1);
+            const int m0 = PAIR ? pair_first(mt, p.pt) : mt;
+#pragma unroll
+            for (int s2 = 0; s2 < NSUB; ++s2) {
+                const typename P::Pre cur = pre;
+                // the next sub-tile's epilogue operands, ahead of the accumulator wait
+                if (s2 + 1 < NSUB) {
+                    p.template pre_load<BN>(pre, sub * 32 + lane, m0 + p.pt.tw, nt, z, cc0, cc1);
+                } else if (t + (int)gridDim.x < ntiles) {
+                    int mt2, nt2, z2;
+                    g.coords(t + gridDim.x, mt2, nt2, z2);
+                    p.template pre_load<BN>(pre, sub * 32 + lane, PAIR ? pair_first(mt2, p.pt) : mt2, nt2, z2, cc0, cc1);
+                }
+                if (s2 == 0) {
+                    tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
+                    tc::tc_fence_after();
+                    if (REFS && stage_ref) tc::mbar_wait(&rfull[acc], (local >> 1) & 1);
+                }
 #ifndef ICE_EXP_NOEPI
-            p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z, cc0,
-                                    cc1, bacc, cur,
-                                    STAGE ? sst + ((warp - 2) * STAGE_BUFS + acc % STAGE_BUFS) * STAGE_BYTES : nullptr,
-                                    (REFS && stage_ref) ? sref + acc * REF_BYTES : nullptr);
+                p.template epilogue<BN>(tmem + (acc * NSUB + s2) * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane,
+                                        m0 + s2 * p.pt.tw, nt, z, cc0, cc1, bacc, cur,
+                                        STAGE ? sst + ((warp - 2) * STAGE_BUFS + acc % STAGE_BUFS) * STAGE_BYTES : nullptr,
+                                        (REFS && stage_ref) ? sref + acc * REF_BYTES : nullptr);
 #endif
+            }
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -1465,7 +1494,7 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_dealloc<2 * BN>(tmem);
+    if (warp == 1) tc::tmem_dealloc<2 * BN * NSUB>(tmem);
 }
 
 // Row-halo weight gradient for 3x3 convs with narrow outputs (cout 64/128) on wide images
@@ -1754,10 +1783,10 @@ bool map_out32(CUtensorMap *m, const void *ptr, int N, int H, int W, int C) {
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool map_halo(CUtensorMap *m, const void *ptr, int N, int H, int W, int C) {
+bool map_halo(CUtensorMap *m, const void *ptr, int N, int H, int W, int C, int rows = 3) {
     cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
     cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-    cuuint32_t box[4] = {64, 130, 3, 1};
+    cuuint32_t box[4] = {64, 130, (cuuint32_t)rows, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(ptr), dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1840,7 +1869,7 @@ const int8_t HALVE_DX[9] = {0, 0, 1, 0, 0, 0, 1, 0, 1};
 // A/B switches of the tiling heuristics (test / tuning hooks), read when the library is first
 // used and again on ice_conv_reload_knobs(); the defaults are the measured-best choices.
 struct Knobs {
-    bool no_dual, no_stage, no_splitk, no_wgrad_trans256, no_ref_tma, no_halo_wgrad, no_halve_merge;
+    bool no_dual, no_stage, no_splitk, no_wgrad_trans256, no_ref_tma, no_halo_wgrad, no_halve_merge, no_pair;
     int conv_m2, wg_m2;  // -1 = automatic, 0 / 1 forced
 };
 Knobs read_knobs() {
@@ -1857,6 +1886,7 @@ Knobs read_knobs() {
     r.no_ref_tma = flag("ICE_NO_REF_TMA");
     r.no_halo_wgrad = flag("ICE_NO_HALO_WGRAD");
     r.no_halve_merge = flag("ICE_NO_HALVE_MERGE");
+    r.no_pair = flag("ICE_NO_PAIR");
     r.conv_m2 = tri("ICE_CONV_M2");
     r.wg_m2 = tri("ICE_WG_M2");
     return r;
@@ -1879,20 +1909,20 @@ ice::RowSched sched(dim3 tiles, int bn, int slots) {
     return ice::RowSched{persist_grid(total), slots, (int)tiles.x, (int)total, bn};
 }
 
-template <int BN, int BSTAGES, bool RES, class P, bool DUAL = false>
+template <int BN, int BSTAGES, bool RES, class P, bool DUAL = false, bool PAIR = false>
 int launch_halo(const P &p, dim3 tiles, cudaStream_t st) {
-    constexpr int smem = halo_smem_bytes<BN, BSTAGES, RES>(P::STAGE_REF);
+    constexpr int smem = halo_smem_bytes<BN, BSTAGES, RES, PAIR>(P::STAGE_REF);
     static_assert(smem <= 232448, "halo kernel smem");
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(halo_gemm<BN, BSTAGES, RES, P, DUAL>,
+        cudaError_t e = cudaFuncSetAttribute(halo_gemm<BN, BSTAGES, RES, P, DUAL, PAIR>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }
     const TileGrid g = tile_grid(tiles);
     const long long total = (long long)tiles.x * tiles.y * tiles.z;
-    halo_gemm<BN, BSTAGES, RES, P, DUAL><<<persist_grid(total), NTHREADS + (DUAL ? 32 : 0), smem, st>>>(p, g);
+    halo_gemm<BN, BSTAGES, RES, P, DUAL, PAIR><<<persist_grid(total), NTHREADS + (DUAL ? 32 : 0), smem, st>>>(p, g);
     ice::count_launch();
     return (int)cudaGetLastError();
 }
@@ -1905,14 +1935,17 @@ int halo_bn(int nch, int ncols) { return ncols % 128 == 0 ? 128 : 64; }
 struct HaloPlan {
     int kind;  // 0: BN 64, resident weights (dual issuers when ncols == 64); 1: BN 128; 2: BN 64 streamed
     int bn;
+    bool pair;  // kind 1 on row pairs (pair tiles: 2 x 128 pixels, one 4-row halo slab)
     dim3 tiles;
+    int halo_rows() const { return pair ? 4 : 3; }
 };
-HaloPlan halo_plan(int nch, int ncols, unsigned mtiles) {
-    HaloPlan h;
-    h.bn = halo_bn(nch, ncols);
-    h.kind = (h.bn == 64 && nch == 1) ? 0 : (h.bn == 128 ? 1 : 2);
-    h.tiles = dim3(mtiles, ncols / h.bn, 1);
-    return h;
+HaloPlan halo_plan(int nch, int ncols, unsigned mtiles, int h) {
+    HaloPlan hp;
+    hp.bn = halo_bn(nch, ncols);
+    hp.kind = (hp.bn == 64 && nch == 1) ? 0 : (hp.bn == 128 ? 1 : 2);
+    hp.pair = hp.kind == 1 && h % 2 == 0 && !knobs().no_pair;
+    hp.tiles = dim3(hp.pair ? mtiles / 2 : mtiles, ncols / hp.bn, 1);
+    return hp;
 }
 
 template <class P>
@@ -1921,6 +1954,7 @@ int run_halo(const P &p, const HaloPlan &h, int ncols, cudaStream_t st) {
         if (ncols == 64 && !knobs().no_dual) return launch_halo<64, 1, true, P, true>(p, h.tiles, st);
         return launch_halo<64, 1, true>(p, h.tiles, st);
     }
+    if (h.kind == 1 && h.pair) return launch_halo<128, 4, false, P, false, true>(p, h.tiles, st);
     if (h.kind == 1) return launch_halo<128, 2, false>(p, h.tiles, st);
     return launch_halo<64, 5, false>(p, h.tiles, st);
 }
@@ -2270,9 +2304,9 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     if (use_halo(ksize, w)) {
         const int nch = (c1 + c2) / 64;
-        const HaloPlan hp = halo_plan(nch, cout, (unsigned)mtiles);
-        if (!map_halo(&p.xa, x1, n, h, w, c1)) return ICE_EINVAL;
-        if (c2 && !map_halo(&p.xb, x2, n, h, w, c2)) return ICE_EINVAL;
+        const HaloPlan hp = halo_plan(nch, cout, (unsigned)mtiles, h);
+        if (!map_halo(&p.xa, x1, n, h, w, c1, hp.halo_rows())) return ICE_EINVAL;
+        if (c2 && !map_halo(&p.xb, x2, n, h, w, c2, hp.halo_rows())) return ICE_EINVAL;
         if (!map_wgt(&p.wm, wgt, cout, 9, c1 + c2, hp.bn)) return ICE_EINVAL;
         if (((nch == 1 && cout == 64) || hp.bn == 128) && !knobs().no_stage) {  // staged TMA stores
             if (!map_out32(&p.ym, y, n, h, w, cout)) return ICE_EINVAL;
@@ -2337,8 +2371,8 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
     const int ct = c1 + c2;
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     if (use_halo(ksize, w)) {  // the epilogue picks dx1/dx2 (and the plane layout) per 32-column chunk
-        const HaloPlan hp = halo_plan(cout / 64, ct, (unsigned)mtiles);
-        if (!map_halo(&p.dym, dy, n, h, w, cout)) return ICE_EINVAL;
+        const HaloPlan hp = halo_plan(cout / 64, ct, (unsigned)mtiles, h);
+        if (!map_halo(&p.dym, dy, n, h, w, cout, hp.halo_rows())) return ICE_EINVAL;
         if (!map_wgt(&p.wm, wgt, cout, 9, ct, 64)) return ICE_EINVAL;
         const bool res64 = cout == 64 && ct == 64 && c2 == 0;  // resident-weight BN = 64 tiles
         if ((res64 || hp.bn == 128) && dx1 && !knobs().no_stage) {  // staged TMA stores

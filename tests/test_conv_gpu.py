@@ -46,6 +46,8 @@ SHAPES = [  # n, h, w, c1, c2, cout, ksize
     (3, 128, 128, 64, 0, 64, 3),
     (32, 8, 8, 1024, 0, 2048, 3),    # bottleneck: 256-wide tiles; dgrad splits K (64 tiles)
     (8, 8, 8, 256, 256, 512, 3),     # 8 tiles: fprop and dgrad both split K, concat input
+    (3, 8, 256, 128, 128, 128, 3),   # row-pair halo tiles (128-wide), concat input, 2 tiles per row
+    (2, 1, 128, 64, 64, 128, 3),     # one-row images: 128-wide halo tiles without pairing
 ]
 
 
@@ -258,7 +260,7 @@ def test_relu_bits_roundtrip(shape):
 # with a concat input, a 256-wide GEMM shape that splits K, a (tap, cin) width of 1152, and
 # a halving conv on the merged-class tiling
 KNOBS = ["ICE_NO_DUAL", "ICE_NO_STAGE", "ICE_NO_SPLITK", "ICE_NO_WGRAD_TRANS256", "ICE_NO_REF_TMA",
-         "ICE_NO_HALO_WGRAD", "ICE_NO_HALVE_MERGE"]
+         "ICE_NO_HALO_WGRAD", "ICE_NO_HALVE_MERGE", "ICE_NO_PAIR"]
 
 
 @pytest.mark.parametrize("knob", KNOBS)

@@ -1,0 +1,6 @@
+for rep in 1 2; do
+for args in "dgrad 32 256 256 64 64 64" "fprop 32 128 128 128 128 128" "dgrad 32 128 128 128 128 128" "fprop 32 128 128 128 0 128" "dgrad 32 128 128 128 0 128" "fprop 32 128 128 64 0 128"; do
+  a=$(python tools/time_conv.py $args 2>&1 | tail -1)
+  b=$(ICE_NO_PAIR=1 python tools/time_conv.py $args 2>&1 | tail -1)
+  echo "$args | pair: $a | nopair: $b"
+done; done
