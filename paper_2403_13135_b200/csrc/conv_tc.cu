@@ -1935,15 +1935,18 @@ int halo_bn(int nch, int ncols) { return ncols % 128 == 0 ? 128 : 64; }
 struct HaloPlan {
     int kind;  // 0: BN 64, resident weights (dual issuers when ncols == 64); 1: BN 128; 2: BN 64 streamed
     int bn;
-    bool pair;  // kind 1 on row pairs (pair tiles: 2 x 128 pixels, one 4-row halo slab)
+    bool pair;  // streamed-weight kinds on row pairs (pair tiles: 2 x 128 pixels, one 4-row halo slab)
     dim3 tiles;
     int halo_rows() const { return pair ? 4 : 3; }
 };
-HaloPlan halo_plan(int nch, int ncols, unsigned mtiles, int h) {
+// Row pairs are taken where they measured faster (tools/pair_ab.sh): every streamed-weight
+// fprop (+5% at 64 columns, +13-15% at 128) and the 128-wide dgrads with K >= 128 (+7-9%);
+// the K = 64 dgrads are bound by their epilogue and lose ~1% with the coarser accumulators.
+HaloPlan halo_plan(int nch, int ncols, unsigned mtiles, int h, bool dgrad) {
     HaloPlan hp;
     hp.bn = halo_bn(nch, ncols);
     hp.kind = (hp.bn == 64 && nch == 1) ? 0 : (hp.bn == 128 ? 1 : 2);
-    hp.pair = hp.kind == 1 && h % 2 == 0 && !knobs().no_pair;
+    hp.pair = (dgrad ? hp.kind == 1 && nch >= 2 : hp.kind != 0) && h % 2 == 0 && !knobs().no_pair;
     hp.tiles = dim3(hp.pair ? mtiles / 2 : mtiles, ncols / hp.bn, 1);
     return hp;
 }
@@ -1956,6 +1959,7 @@ int run_halo(const P &p, const HaloPlan &h, int ncols, cudaStream_t st) {
     }
     if (h.kind == 1 && h.pair) return launch_halo<128, 4, false, P, false, true>(p, h.tiles, st);
     if (h.kind == 1) return launch_halo<128, 2, false>(p, h.tiles, st);
+    if (h.pair) return launch_halo<64, 6, false, P, false, true>(p, h.tiles, st);
     return launch_halo<64, 5, false>(p, h.tiles, st);
 }
 
@@ -2304,7 +2308,7 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     if (use_halo(ksize, w)) {
         const int nch = (c1 + c2) / 64;
-        const HaloPlan hp = halo_plan(nch, cout, (unsigned)mtiles, h);
+        const HaloPlan hp = halo_plan(nch, cout, (unsigned)mtiles, h, false);
         if (!map_halo(&p.xa, x1, n, h, w, c1, hp.halo_rows())) return ICE_EINVAL;
         if (c2 && !map_halo(&p.xb, x2, n, h, w, c2, hp.halo_rows())) return ICE_EINVAL;
         if (!map_wgt(&p.wm, wgt, cout, 9, c1 + c2, hp.bn)) return ICE_EINVAL;
@@ -2371,7 +2375,7 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
     const int ct = c1 + c2;
     const long long mtiles = (long long)p.pt.tw * p.pt.th * p.pt.tn;
     if (use_halo(ksize, w)) {  // the epilogue picks dx1/dx2 (and the plane layout) per 32-column chunk
-        const HaloPlan hp = halo_plan(cout / 64, ct, (unsigned)mtiles, h);
+        const HaloPlan hp = halo_plan(cout / 64, ct, (unsigned)mtiles, h, true);
         if (!map_halo(&p.dym, dy, n, h, w, cout, hp.halo_rows())) return ICE_EINVAL;
         if (!map_wgt(&p.wm, wgt, cout, 9, ct, 64)) return ICE_EINVAL;
         const bool res64 = cout == 64 && ct == 64 && c2 == 0;  // resident-weight BN = 64 tiles
