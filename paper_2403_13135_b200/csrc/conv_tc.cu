@@ -350,6 +350,8 @@ struct DgradProb {
     int bslots;
     CUtensorMap o1m;   // dx1 as (c1, W, H, N), box 32 ch x 32 px, SWIZZLE_64B (staged stores)
     int o1_tma;
+    CUtensorMap o2m;   // dx2 planes as (c2, W/2, H/2, N, 4), box 32 ch x 16 px (row tiles, staged stores)
+    int o2_tma;
 
     __device__ void kb_range(int, int &kb0, int &nkb) const {
         kb0 = 0;
@@ -541,6 +543,24 @@ struct DgradProb {
                     __syncwarp();
                     if (lane == 0) {
                         tc::tma_store_4d(&o1m, stage, col, w, h, n);  // lane 0's pixel starts the box
+                        tc::bulk_commit();
+                    }
+                } else if (stage && o2_tma && out == out2) {
+                    // sub-pixel planes: the warp's 32 pixels of one row split by column parity into
+                    // two 16-pixel runs of planes 2 (h & 1) and 2 (h & 1) + 1 -- staged as rows
+                    // 0-15 (even lanes) and 16-31 (odd lanes), written by two TMA stores
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) pk[e] = tc::pack_bf16(v[2 * e], v[2 * e + 1]);
+                    if (lane == 0) tc::bulk_wait_read<STAGE_BUFS - 1>();
+                    __syncwarp();
+                    tc::stage_row64_at(stage, (lane & 1) * 16 + (lane >> 1), pk);
+                    tc::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {  // lane 0's pixel (w even) starts both runs
+                        const int cls = 2 * (h & 1);
+                        tc::tma_store_5d(&o2m, stage, col, w >> 1, h >> 1, n, cls);
+                        tc::tma_store_5d(&o2m, stage + 16 * 64, col, w >> 1, h >> 1, n, cls + 1);
                         tc::bulk_commit();
                     }
                 } else {
@@ -1223,7 +1243,7 @@ constexpr int REF_BYTES = 128 * 128;  // staged ReLU-reference tile: 128 px x 64
 template <int BN, int BSTAGES, bool RES, bool PAIR = false>
 constexpr int halo_smem_bytes(bool refs = false) {
     return 1024 + 2 * (PAIR ? HALO4_BYTES : HALO_BYTES) + (RES ? 9 : BSTAGES * (PAIR ? 1 : TAPS_PER_SLOT)) * BN * BK * 2 +
-           (((BN == 64 && RES) || BN == 128) ? EPI_WARPS * STAGE_BUFS * STAGE_BYTES : 0) +
+           (((BN == 64 && (RES || PAIR)) || BN == 128) ? EPI_WARPS * STAGE_BUFS * STAGE_BYTES : 0) +
            ((BN == 64 && RES && refs) ? 2 * REF_BYTES : 0) +
            (2 * 2 + 2 * BSTAGES + 6 + 4) * 8 + 16 + BIAS_SLOTS * BN * 4;
 }
@@ -1244,7 +1264,7 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
     constexpr int NBS = RES ? 1 : BSTAGES;
     // BN = 64 resident-weight tiles stage each warp's 32 x 32 output box in shared memory and
     // write it with a TMA store (per-lane 64-B row stores were the epilogue's bottleneck)
-    constexpr bool STAGE = (BN == 64 && RES) || BN == 128;
+    constexpr bool STAGE = (BN == 64 && (RES || PAIR)) || BN == 128;
     uint8_t *sa = base;            // [2][HB]
     uint8_t *sb = base + 2 * HB;   // [NBS][B_BYTES]
     uint8_t *sst = sb + NBS * B_BYTES;     // [EPI_WARPS][STAGE_BUFS][STAGE_BYTES] when STAGE
@@ -2312,7 +2332,7 @@ extern "C" int ice_conv_fprop(const uint16_t *x1, int32_t c1, const uint16_t *x2
         if (!map_halo(&p.xa, x1, n, h, w, c1, hp.halo_rows())) return ICE_EINVAL;
         if (c2 && !map_halo(&p.xb, x2, n, h, w, c2, hp.halo_rows())) return ICE_EINVAL;
         if (!map_wgt(&p.wm, wgt, cout, 9, c1 + c2, hp.bn)) return ICE_EINVAL;
-        if (((nch == 1 && cout == 64) || hp.bn == 128) && !knobs().no_stage) {  // staged TMA stores
+        if (((nch == 1 && cout == 64) || hp.bn == 128 || hp.pair) && !knobs().no_stage) {  // staged TMA stores
             if (!map_out32(&p.ym, y, n, h, w, cout)) return ICE_EINVAL;
             p.y_tma = 1;
         }
@@ -2382,6 +2402,18 @@ extern "C" int ice_conv_dgrad(const uint16_t *dy, int32_t cout, int32_t n, int32
         if ((res64 || hp.bn == 128) && dx1 && !knobs().no_stage) {  // staged TMA stores
             if (!map_out32(&p.o1m, dx1, n, h, w, c1)) return ICE_EINVAL;
             p.o1_tma = 1;
+        }
+        if (hp.bn == 128 && dx2 && dx2_planes && !knobs().no_stage) {  // staged plane stores
+            cuuint64_t dims[5] = {(cuuint64_t)c2, (cuuint64_t)(w / 2), (cuuint64_t)(h / 2), (cuuint64_t)n, 4};
+            cuuint64_t strides[4] = {(cuuint64_t)c2 * 2, (cuuint64_t)(w / 2) * c2 * 2, (cuuint64_t)(h / 2) * (w / 2) * c2 * 2,
+                                     (cuuint64_t)n * (h / 2) * (w / 2) * c2 * 2};
+            cuuint32_t box[5] = {32, 16, 1, 1, 1};
+            cuuint32_t es[5] = {1, 1, 1, 1, 1};
+            if (encode_fn()(&p.o2m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, dx2, dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return ICE_EINVAL;
+            p.o2_tma = 1;
         }
         if (res64 && dx1 && !knobs().no_stage && relu_ref1 && !relu_bits1 && !knobs().no_ref_tma) {
             // ReLU reference staged by the producer

@@ -184,6 +184,13 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap *m, const void *s
                  "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                  : "memory");
 }
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap *m, const void *src, int c0, int c1, int c2, int c3,
+                                             int c4) {
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
@@ -197,6 +204,14 @@ __device__ __forceinline__ void stage_row64(uint8_t *stage, int lane, const uint
 #pragma unroll
     for (int q = 0; q < 4; ++q)
         *reinterpret_cast<uint4 *>(stage + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+}
+
+// The same 64-B row written at staging row r (the SWIZZLE_64B pattern is address-based).
+__device__ __forceinline__ void stage_row64_at(uint8_t *stage, int r, const uint32_t (&pk)[16]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4 *>(stage + r * 64 + ((q ^ ((r >> 1) & 3)) << 4)) =
             make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
 }
 

@@ -192,10 +192,13 @@ def test_halve_fprop_dgrad_wgrad(shape):
     assert rel(dw.permute(0, 3, 1, 2), wref.grad) < 1e-2
 
 
-def test_dgrad_split_k_planes_and_both_outputs():
-    """Split-K dgrad finisher: dx1 / dx2 split at c1, sub-pixel planes for dx2, gradient sums,
-    ReLU-backward masks, Dropout2d scales and both bias gradients."""
-    n, h, w, c1, c2, cout = 4, 8, 8, 256, 256, 512
+@pytest.mark.parametrize("shape", [(4, 8, 8, 256, 256, 512), (2, 4, 256, 64, 64, 64), (2, 4, 128, 128, 128, 128)],
+                         ids=str)
+def test_dgrad_split_k_planes_and_both_outputs(shape):
+    """dx1 / dx2 split at c1, sub-pixel planes for dx2, gradient sums, ReLU-backward masks,
+    Dropout2d scales and both bias gradients: through the split-K finisher (8x8) and the
+    128-wide halo tiles with staged plane stores (unpaired K = 64, row pairs K = 128)."""
+    n, h, w, c1, c2, cout = shape
     torch.manual_seed(7)
     dy = rnd(n, h, w, cout)
     wt = rnd(cout, 3, 3, c1 + c2, scale=0.05)
