@@ -24,7 +24,16 @@ cap adam "adam_kernel" 2
 cap wgrad_m2 "conv_gemm_m2<.int.256, .int.3, .*WgradProb" 40
 cap halo_fp64 "halo_gemm<.int.64, .int.1, .bool.1, .*FpropProb" 2
 cap halo_dg64 "halo_gemm<.int.64, .int.1, .bool.1, .*DgradProb" 2
+cap halo_dg128 "halo_gemm<.int.128, .int.2, .bool.0, .*DgradProb" 2
+cap halo_fp128 "halo_gemm<.int.128, .int.2, .bool.0, .*FpropProb" 6
 cap hwgrad64 "hwgrad_kernel<.int.64, .int.2, .int.2, .bool.0" 2
 cap fprop256 "conv_gemm<.int.256, .int.4, .*FpropProb" 20
 [ -z "$ONLY" ] && timeout 600 $F -k "regex:autolabel256" -s 1 -c 1 -o gpurun_out/${P}_autolabel256 -f python tools/profile_autolabel.py --reps 1 > gpurun_out/${P}_al.log 2>&1
-ls -la gpurun_out/*.ncu-rep
+# summarise on the box and drop the reports (gpurun copies back at most 64 MiB); KEEP="a b"
+# keeps those captures' .ncu-rep files
+python tools/summarize_ncu_full.py gpurun_out/${P}_ncu_full_summary.json gpurun_out/${P}_*.ncu-rep > gpurun_out/${P}_summary.log 2>&1
+for f in gpurun_out/${P}_*.ncu-rep; do
+  n=${f#gpurun_out/${P}_}; n=${n%.ncu-rep}
+  [[ " $KEEP " == *" $n "* ]] || rm -f "$f"
+done
+ls -la gpurun_out/ | tail -30
