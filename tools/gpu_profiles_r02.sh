@@ -26,6 +26,9 @@ cap halo_fp64 "halo_gemm<.int.64, .int.1, .bool.1, .*FpropProb" 2
 cap halo_dg64 "halo_gemm<.int.64, .int.1, .bool.1, .*DgradProb" 2
 cap halo_dg128 "halo_gemm<.int.128, .int.2, .bool.0, .*DgradProb" 2
 cap halo_fp128 "halo_gemm<.int.128, .int.2, .bool.0, .*FpropProb" 6
+cap halo_fp128p "halo_gemm<.int.128, .int.4, .bool.0, .*FpropProb" 4
+cap halo_dg128p "halo_gemm<.int.128, .int.4, .bool.0, .*DgradProb" 2
+cap halo_fp64p "halo_gemm<.int.64, .int.6, .bool.0, .*FpropProb" 2
 cap hwgrad64 "hwgrad_kernel<.int.64, .int.2, .int.2, .bool.0" 2
 cap fprop256 "conv_gemm<.int.256, .int.4, .*FpropProb" 20
 [ -z "$ONLY" ] && timeout 600 $F -k "regex:autolabel256" -s 1 -c 1 -o gpurun_out/${P}_autolabel256 -f python tools/profile_autolabel.py --reps 1 > gpurun_out/${P}_al.log 2>&1
