@@ -25,7 +25,7 @@ __device__ __forceinline__ void commit_elect(uint64_t *bar) {
         : "memory");
 }
 
-template <int N, bool WARP>
+template <int N, bool WARP, int M = 128>
 __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long *cycles) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long *c
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = tslot;
-    constexpr uint32_t idesc = tc::idesc_bf16(128, N, false, false);
+    constexpr uint32_t idesc = tc::idesc_bf16(M, N, false, false);
     const uint32_t a0 = tc::smem_u32(A), b0 = tc::smem_u32(B);
     if (warp == 1 && (WARP || lane == 0)) {
         long long t0 = clock64();
@@ -71,10 +71,10 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long *c
     if (warp == 0) tc::tmem_dealloc<2 * N>(tmem);
 }
 
-template <int N, bool WARP>
+template <int N, bool WARP, int M = 128>
 void run(int iters) {
     constexpr int smem = 1024 + 4 * 16384 + N * 128;
-    auto k = probe<N, WARP>;
+    auto k = probe<N, WARP, M>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     unsigned long long *dc;
     cudaMalloc(&dc, 8);
@@ -91,8 +91,8 @@ void run(int iters) {
     unsigned long long cyc = 0;
     cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost);
     const double mmas = 4.0 * iters;
-    const double tflops = 2.0 * 128 * N * 16 * mmas * 148 / (ms * 1e-3) / 1e12;
-    printf("N=%3d issue=%-11s %6.1f cycles/MMA  %7.1f TFLOP/s  %s\n", N, WARP ? "warp+elect" : "lane0", cyc / mmas, tflops,
+    const double tflops = 2.0 * M * N * 16 * mmas * 148 / (ms * 1e-3) / 1e12;
+    printf("M=%3d N=%3d issue=%-11s %6.1f cycles/MMA  %7.1f TFLOP/s  %s\n", M, N, WARP ? "warp+elect" : "lane0", cyc / mmas, tflops,
            cudaGetErrorString(err));
     cudaFree(dc);
 }
@@ -105,5 +105,8 @@ int main() {
     run<128, true>(it);
     run<256, false>(it);
     run<256, true>(it);
+    run<64, true, 64>(it);
+    run<128, true, 64>(it);
+    run<256, true, 64>(it);
     return 0;
 }
