@@ -237,8 +237,8 @@ def call(name: str, *args) -> None:
             rc = fn(*core, None, None, stream)
     else:
         rc = fn(*args)
-    if name == "ice_autolabel_set_path":
-        scratch.sizes.clear()  # the region path's scratch need depends on the mode
+    if name in ("ice_autolabel_set_path", "ice_conv_reload_knobs"):
+        scratch.sizes.clear()  # scratch needs depend on the path / the tiling switches
     if rc != ICE_OK:
         raise NativeError(name, rc)
     counter.launches += 1
