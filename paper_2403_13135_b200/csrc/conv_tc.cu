@@ -471,8 +471,12 @@ struct DgradProb {
             ((((size_t)((h & 1) * 2 + (w & 1)) * N + n) * (H >> 1) + (h >> 1)) * (W >> 1)) + (w >> 1);
         const int lane = threadIdx.x & 31;
         constexpr int NCH = BN / 32, PER = (NCH + 1) / 2;
-#pragma unroll
-        for (int ci = 0; ci < PER; ++ci) {  // compile-time index into bacc (no local memory)
+        // not unrolled: the body holds every output variant (add / mask / drop / staged dx1 /
+        // staged planes / direct), and one copy per chunk overflowed the instruction cache
+        // (ncu: 25% of the epilogue's stall samples were no_inst); bacc and the prefetched mask
+        // words are indexed through selects, so they stay in registers
+#pragma unroll 1
+        for (int ci = 0; ci < PER; ++ci) {
             const int cc = cc0 + ci;
             if (cc >= cc1) break;
             float v[32];
@@ -503,7 +507,7 @@ struct DgradProb {
                     }
                 }
                 if (rbits1 && out == out1) {  // the forward's packed ReLU mask: 4 B instead of 64 B per row
-                    const uint32_t b = pr.b[ci];  // prefetched (pre_load)
+                    const uint32_t b = ci == 0 ? pr.b[0] : ci == 1 ? pr.b[1] : ci == 2 ? pr.b[2] : pr.b[3];  // (pre_load)
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
                         if (!((b >> e) & 1u)) v[e] = 0.f;
@@ -577,7 +581,10 @@ struct DgradProb {
             }
             if (db) {  // warp-uniform: bias gradient = column sums of the (fp32) gradient
 
-                bacc[cc - cc0] += warp_col_sum32(v, lane);
+                const float cs = warp_col_sum32(v, lane);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k == ci) bacc[k] += cs;
             }
         }
     }
@@ -1476,8 +1483,8 @@ __global__ void __launch_bounds__(NTHREADS + (DUAL ? 32 : 0), 1) halo_gemm(const
             }
             const int acc = local & 1;
             const int m0 = PAIR ? pair_first(mt, p.pt) : mt;
-#pragma unroll
-            for (int s2 = 0; s2 < NSUB; ++s2) {
+#pragma unroll 1
+            for (int s2 = 0; s2 < NSUB; ++s2) {  // (one copy of the epilogue: instruction cache)
                 const typename P::Pre cur = pre;
                 // the next sub-tile's epilogue operands, ahead of the accumulator wait
                 if (s2 + 1 < NSUB) {
