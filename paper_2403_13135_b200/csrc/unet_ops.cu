@@ -488,10 +488,16 @@ __global__ void adam_kernel(float *__restrict__ p, float *__restrict__ g, float 
                             long long n, float lr_corr, float omb1, float b2, float omb2, float eps, float bc2_sqrt,
                             uint16_t *__restrict__ out_bf16, const long long *__restrict__ step_dev, double lr,
                             double b1d, double b2d, bool zero_g) {
-    if (step_dev) {  // bias corrections from the device step counter (CUDA-graph replays)
-        const double t = (double)*step_dev;
-        lr_corr = (float)(lr / (1.0 - pow(b1d, t)));
-        bc2_sqrt = (float)sqrt(1.0 - pow(b2d, t));
+    if (step_dev) {  // bias corrections from the device step counter (CUDA-graph replays):
+        __shared__ float corr[2];  // one thread per block evaluates the fp64 pows
+        if (threadIdx.x == 0) {
+            const double t = (double)*step_dev;
+            corr[0] = (float)(lr / (1.0 - pow(b1d, t)));
+            corr[1] = (float)sqrt(1.0 - pow(b2d, t));
+        }
+        __syncthreads();
+        lr_corr = corr[0];
+        bc2_sqrt = corr[1];
     }
     const long long n4 = n / 4;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
