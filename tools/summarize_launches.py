@@ -68,14 +68,19 @@ for k, g in sorted(agg.items(), key=lambda kv: -kv[1]["ns"]):
           f"{g['dram_bytes'] / g['launches'] / 1e6:9.1f} MB/launch  {k}")
 if a.out:
     json.dump({"source": a.csv, "steps": a.steps, "after_first": a.after, "kernels": rows}, open(a.out, "w"), indent=1)
-wg = [g for k, g in agg.items() if "WgradProb" in k or "hwgrad_kernel" in k]
-if a.traffic and wg and any(g["dram_bytes"] for g in wg):
-    n = sum(g["launches"] for g in wg)
-    tr = {"ice_conv_wgrad": round(sum(g["dram_bytes"] for g in wg) / n),
-          "_note": "DRAM read+write bytes per launch, average over the wgrad family (conv_gemm<..,WgradProb> "
-                   "+ hwgrad_kernel) of one train step, from " + a.csv}
+fams = {"ice_conv_wgrad": lambda k: "WgradProb" in k or "hwgrad_kernel" in k,
+        "ice_conv_dgrad": lambda k: "DgradProb" in k,
+        "ice_conv_fprop": lambda k: "FpropProb" in k}
+if a.traffic and any(g["dram_bytes"] for g in agg.values()):
     old = json.load(open(a.traffic)) if os.path.exists(a.traffic) else {}
-    old.update(tr)
+    for fam, sel in fams.items():
+        gs = [g for k, g in agg.items() if sel(k)]
+        n = sum(g["launches"] for g in gs)
+        if n:
+            old[fam] = round(sum(g["dram_bytes"] for g in gs) / n)
+    old["_note"] = ("DRAM read+write bytes per launch, averaged over each convolution family's kernels of the warm "
+                    "steps (FpropProb / DgradProb / WgradProb + hwgrad template instances; the halving conv's "
+                    "launches are included in their family), from " + a.csv)
     al = [g for k, g in agg.items() if "autolabel256" in k]
     if al and al[0]["dram_bytes"]:
         old["ice_autolabel_bytes_per_tile"] = round(al[0]["dram_bytes"] / al[0]["launches"] / a.al_tiles)
