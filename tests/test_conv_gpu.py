@@ -48,6 +48,7 @@ SHAPES = [  # n, h, w, c1, c2, cout, ksize
     (8, 8, 8, 256, 256, 512, 3),     # 8 tiles: fprop and dgrad both split K, concat input
     (3, 8, 256, 128, 128, 128, 3),   # row-pair halo tiles (128-wide), concat input, 2 tiles per row
     (2, 1, 128, 64, 64, 128, 3),     # one-row images: 128-wide halo tiles without pairing
+    (3, 2, 256, 64, 64, 128, 3),     # one row pair per image column: pair slabs cover both borders
 ]
 
 
