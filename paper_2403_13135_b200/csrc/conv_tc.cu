@@ -110,6 +110,8 @@ __device__ __forceinline__ float warp_col_sum32(float (&v)[32], int lane) {
 // ------------------------------------------------------------------------------------
 struct FpropProb {
     static constexpr bool A_MN = false, B_MN = false;
+    static constexpr int EPI_STAGE = STAGE_BYTES;
+    static constexpr bool BIAS_ROWS = true;
     static constexpr bool STAGE_REF = false;
     static constexpr int ref_tma = 0;
     __device__ void load_ref(uint8_t *, uint64_t *, int, int) const {}
@@ -332,6 +334,8 @@ struct FpropProb {
 // ------------------------------------------------------------------------------------
 struct DgradProb {
     static constexpr bool A_MN = false, B_MN = true;
+    static constexpr int EPI_STAGE = STAGE_BYTES;
+    static constexpr bool BIAS_ROWS = true;
     static constexpr bool STAGE_REF = true;
     CUtensorMap dym, wm;  // dY (box 64 x pixel tile), weights (box 64 cin x 1 x 64 cout)
     CUtensorMap refm;     // ReLU reference of dx1, box 64 ch x 128 px (halo BN = 64 tiles)
@@ -593,6 +597,9 @@ struct DgradProb {
 // ------------------------------------------------------------------------------------
 struct WgradProb {
     static constexpr bool A_MN = true, B_MN = true;
+    // 256-row tiles: a 4 KB fp32 staging block per epilogue warp (transposed stores), no bias rows
+    static constexpr int EPI_STAGE = 4096;
+    static constexpr bool BIAS_ROWS = false;
     CUtensorMap dym, xa, xb;  // boxes of 64 channels x 64 pixels
     PixTile pk;               // the 64-pixel K-block geometry
     Taps taps;
@@ -681,7 +688,7 @@ struct WgradProb {
     // stores its partial tile into slice z - 1 of ws and splitsum_finish then adds the slices in
     // split order: dw = (dw + p0) + ((p1 + p2) + ...), a fixed association -> bit-reproducible
     __device__ void epilogue(uint32_t tmem, int row, int mt, int nt, int z, int cc0, int cc1, float *, const Pre &,
-                             uint8_t * = nullptr, const uint8_t * = nullptr) const {
+                             uint8_t *stage = nullptr, const uint8_t * = nullptr) const {
         const int m = mt * BM + row;
         const int ld = taps.n * (c1 + c2);
         const bool part = z > 0;
@@ -690,7 +697,29 @@ struct WgradProb {
         for (int cc = cc0; cc < cc1; ++cc) {
             float v[32];
             tc::tmem_ld32(tmem + cc * 32, v);
-            if (!trans) {
+            if (!trans && stage) {
+                // 256-row tiles drain with the mainloop stopped (TMEM holds one tile): a lane's
+                // 128-B row segment as 8 x 16-B stores touches 32 lines per warp instruction;
+                // through the warp's 4 KB staging block each instruction covers 4 full rows
+                // (lane l: row 4 i + l / 8, 16-B chunk l % 8), 8x fewer L2 requests
+                const int lane = threadIdx.x & 31;
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < 8; ++q)  // chunk q of row `lane` at q ^ (lane & 7): conflict-free
+                    *reinterpret_cast<float4 *>(stage + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                        make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                __syncwarp();
+                const int m0 = m - lane, q = lane & 7;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int r = 4 * i + (lane >> 3);
+                    const float4 u = *reinterpret_cast<const float4 *>(stage + r * 128 + ((q ^ (r & 7)) << 4));
+                    if (m0 + r >= cout) continue;
+                    float *dst = base + (size_t)(m0 + r) * ld + nt * BN + cc * 32 + 4 * q;
+                    if (part || ow) __stcg(reinterpret_cast<float4 *>(dst), u);
+                    else tc::red_add_v4(dst, u.x, u.y, u.z, u.w);
+                }
+            } else if (!trans) {
                 if (m >= cout) continue;
                 float *dst = base + (size_t)m * ld + nt * BN + cc * 32;
                 if (part || ow) {  // a slice, or the first gradient of the step (overwrite mode)
@@ -727,6 +756,8 @@ struct WgradProb {
 template <class P>
 struct SplitK {
     static constexpr bool A_MN = P::A_MN, B_MN = P::B_MN;
+    static constexpr int EPI_STAGE = STAGE_BYTES;
+    static constexpr bool BIAS_ROWS = true;
     P p;
     float *ws;
     size_t zstride;  // floats per split slice (pixels x ld)
@@ -1037,7 +1068,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
             tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
             tc::tc_fence_after();
             p.template epilogue<BN>(tmem + acc * BN + ((uint32_t)(sub * 32) << 16), sub * 32 + lane, mt, nt, z, cc0,
-                                    cc1, bacc, cur, sst + (warp - 2) * STAGE_BYTES);
+                                    cc1, bacc, cur, P::EPI_STAGE == STAGE_BYTES ? sst + (warp - 2) * STAGE_BYTES : nullptr);
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
@@ -1068,10 +1099,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm(const __grid_constant__
 // (tmem empty), [1] waiting for TMA (full), [2] issuing, [3] tiles, [4] K-blocks
 __device__ unsigned long long g_conv_prof[8];
 #endif
-template <int BN, int STAGES>
+template <int BN, int STAGES, class P>
 constexpr int m2_smem_bytes() {
-    return 1024 + STAGES * (2 * A_BYTES + BN * BK * 2) + EPI_WARPS * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16 +
-           BIAS_SLOTS * BN * 4;
+    return 1024 + STAGES * (2 * A_BYTES + BN * BK * 2) + EPI_WARPS * P::EPI_STAGE + (2 * STAGES + 4) * 8 + 16 +
+           (P::BIAS_ROWS ? BIAS_SLOTS * BN * 4 : 0);
 }
 
 template <int BN, int STAGES, class P>
@@ -1083,7 +1114,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
     uint8_t *sa = base;
     uint8_t *sb = base + STAGES * AB;
     uint8_t *sst = sb + STAGES * B_BYTES;
-    uint64_t *full = reinterpret_cast<uint64_t *>(sst + EPI_WARPS * STAGE_BYTES);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sst + EPI_WARPS * P::EPI_STAGE);
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;  // [2]
     uint64_t *tempty = tfull + 2;      // [2]
@@ -1180,7 +1211,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_gemm_m2(const __grid_constan
         const int sub = warp & 3, half = (warp - 2) >> 2;  // TMEM lane quarter, M half
         const int row = sub * 32 + lane;
         constexpr int NCH = BN / 32, PER = (NCH + 1) / 2;  // two passes of PER chunks
-        uint8_t *stage = sst + (warp - 2) * STAGE_BYTES;
+        uint8_t *stage = sst + (warp - 2) * P::EPI_STAGE;
         float bacc0[4] = {0.f, 0.f, 0.f, 0.f}, bacc1[4] = {0.f, 0.f, 0.f, 0.f};
         int cur_nt = -1, local = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
@@ -2009,7 +2040,8 @@ int launch(const P &p, dim3 tiles, cudaStream_t st) {
 
 template <int BN, int STAGES, class P>
 int launch_m2(const P &p, dim3 tiles, cudaStream_t st) {
-    constexpr int smem = m2_smem_bytes<BN, STAGES>();
+    constexpr int smem = m2_smem_bytes<BN, STAGES, P>();
+    static_assert(smem <= 232448, "conv_gemm_m2 smem");
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(conv_gemm_m2<BN, STAGES, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
